@@ -1,0 +1,153 @@
+/* migsim_b200.h — C ABI of the B200 Goodput-planner hot path.
+ *
+ * Plain C, POD structs, caller-owned host buffers, library-owned device state.
+ * This is the thin layer under the unchanged C++ planner API: the C++ drop-in
+ * (paper_2407_13126_b200/csrc/host/migsim/*.hpp) marshals a
+ * migsim::PlanContext into an mgs_problem and rethrows mgs_error as
+ * migsim::Error(code, message). Python (ctypes) and any other FFI bind the same
+ * symbols; see INTEGRATION.md.
+ *
+ * Reference interfaces each entry point replaces (paths relative to the
+ * reference root, proj/include/migsim/):
+ *   mgs_enumerate      engine::Space::build            space.hpp:126-210
+ *   mgs_precheck       precheck_scenario               solvers.hpp:27-69
+ *   mgs_goodput_table  solve_dp ub_suffix + incumbent  solvers.hpp:258-322
+ *   mgs_solve_window   solve_dp                        solvers.hpp:242-579
+ *   mgs_solve_batch    solve_dp over independent windows (the reference's
+ *                      per-scenario call in a host loop)
+ *   mgs_evaluate_batch evaluate_plan(verify=false)     evaluate.hpp:153-210
+ */
+#ifndef MIGSIM_B200_H
+#define MIGSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MGS_MAX_MODELS 4  /* engine::kMaxModels, space.hpp:17 */
+#define MGS_MAX_SLOTS 8   /* slots per configuration (gpc_count <= 8) */
+#define MGS_SIZES 8       /* tables indexed by instance size 0..7 (space.hpp:39-40) */
+#define MGS_FOREIGN_MASK 0xffffffffu /* engine::kForeignMask, space.hpp:303 */
+
+/* Status codes map 1:1 onto the reference's migsim::Error code strings
+ * (mgs_status_code() returns the string). */
+typedef enum {
+  MGS_OK = 0,
+  MGS_ERR_INPUT_SCENARIO = 1,          /* "input.scenario"   space.hpp:49-50 */
+  MGS_ERR_INPUT_CATALOG = 2,           /* "input.catalog"    space.hpp:65 */
+  MGS_ERR_INPUT_FORECAST = 3,          /* "input.forecast"   solvers.hpp:250-252 */
+  MGS_ERR_INPUT_ARRIVALS = 4,          /* "input.arrivals"   evaluate.hpp:166-167 */
+  MGS_ERR_DEPLOYMENT_FLOOR = 5,        /* "infeasible.deployment-floor" solvers.hpp:38,51 */
+  MGS_ERR_RETRAINING_WINDOW = 6,       /* "infeasible.retraining-window" solvers.hpp:44 */
+  MGS_ERR_NO_COEXISTENCE = 7,          /* "infeasible.no-coexistence-configuration" :62 */
+  MGS_ERR_INFEASIBLE_JOINT = 8,        /* "infeasible.joint" solvers.hpp:348,565 */
+  MGS_ERR_STATE_BUDGET = 9,            /* "planner.state-budget" solvers.hpp:539-542 */
+  MGS_ERR_PLAN_INFEASIBLE = 10,        /* "plan.infeasible" evaluate.hpp:165 */
+  MGS_ERR_CUDA = 11,                   /* device failure (no reference analogue) */
+  MGS_ERR_ARGUMENT = 12                /* null pointer / size out of range */
+} mgs_status;
+
+typedef struct {
+  int32_t code;        /* mgs_status */
+  int32_t step;        /* planner.state-budget: step s+1 of the overflow */
+  uint64_t frontier;   /* planner.state-budget: frontier size at that step */
+  int32_t model;       /* precheck: offending model index, -1 if none */
+  char message[320];   /* same text the reference puts in Error::what() */
+} mgs_error;
+
+/* The partition lattice: catalog configurations in file order, slots of each
+ * configuration sorted by slice_start (catalog.hpp:141-142). */
+typedef struct {
+  int32_t n_configs;
+  int32_t gpc_count;
+  const int32_t* slot_offset; /* [n_configs+1] */
+  const int32_t* slot_size;   /* [slot_offset[n_configs]] */
+  const int32_t* slot_start;  /* [slot_offset[n_configs]] */
+} mgs_lattice;
+
+/* Per-window tables (engine::Tables, space.hpp:32-86). cap 0 = no capability,
+ * rt -1 = undefined, exactly as Tables::build fills them. */
+typedef struct {
+  int32_t models; /* M, 1..4 */
+  int32_t steps;  /* S */
+  double cap_by_size[MGS_MAX_MODELS][MGS_SIZES];
+  int64_t rt_by_size[MGS_MAX_MODELS][MGS_SIZES];
+  int32_t floor_gpcs[MGS_MAX_MODELS];
+  double psi[MGS_MAX_MODELS];       /* loss fraction = min(psi, 1), plan_types.hpp:68 */
+  double acc_pre[MGS_MAX_MODELS];   /* accuracy of window w (PlanContext::accuracy_pre) */
+  double acc_post[MGS_MAX_MODELS];
+} mgs_tables;
+
+/* One planning window (PlanContext + ArrivalForecast + SolveOptions). */
+typedef struct {
+  mgs_lattice lattice;
+  mgs_tables tables;
+  const int64_t* forecast;            /* [models][forecast_len] row-major */
+  int32_t forecast_len;               /* must equal steps (input.forecast otherwise) */
+  int32_t has_initial;                /* PlanContext::initial present */
+  uint32_t init_mask[MGS_MAX_MODELS]; /* initial_masks(): universe bit masks */
+  uint64_t state_budget;              /* SolveOptions::state_budget (4,000,000) */
+  int32_t workers;                    /* accepted; results never depend on it */
+} mgs_problem;
+
+typedef struct {
+  uint64_t options;          /* |O|, Space::options.size() */
+  uint64_t candidates;       /* distinct (signature, inference-placement) pairs */
+  uint64_t transitions_ref;  /* reference inner-loop trips, solvers.hpp:424-469 */
+  uint64_t transitions;      /* (unit, candidate) pairs the GPU evaluated */
+  uint64_t frontier_total;   /* sum over steps of surviving states */
+  uint64_t frontier_peak;
+  double device_ms;          /* device time of the solve (CUDA events) */
+} mgs_stats;
+
+typedef struct mgs_ctx mgs_ctx;
+
+int mgs_open(int device, mgs_ctx** out);
+void mgs_close(mgs_ctx* ctx);
+const char* mgs_status_code(int status);
+const char* mgs_version(void);
+
+/* Candidate enumeration (Space::build). *n_options receives |O|. Optional
+ * host copies (pass NULL to skip) hold min(cap, |O|) options in lex order:
+ * config[i], labels[i*MGS_MAX_SLOTS + slot], infer_mask[i*4+m],
+ * infer_cap[i*4+m], retrain_size[i*4+m]. */
+int mgs_enumerate(mgs_ctx* ctx, const mgs_lattice* lattice, const mgs_tables* tables, int64_t* n_options,
+                  int64_t cap, int32_t* config, int8_t* labels, uint32_t* infer_mask, double* infer_cap,
+                  int8_t* retrain_size, mgs_error* err);
+
+/* Goodput table reductions used by solve_dp before the search: the
+ * optimistic per-step bound ub_suffix[0..S] (solvers.hpp:270-280) and the
+ * greedy incumbent (solvers.hpp:283-322; -inf when the greedy walk does not
+ * finish every retraining). greedy_option[s] = chosen option or -1. */
+int mgs_goodput_table(mgs_ctx* ctx, const mgs_problem* p, double* ub_suffix, double* incumbent,
+                      int32_t* greedy_option, mgs_error* err);
+
+/* solve_dp on one window. out_option[s] = option index (lex rank) chosen at
+ * step s; out_config[s] / out_labels[s*MGS_MAX_SLOTS+slot] its configuration
+ * and per-slot labels (0 unused, 1+2m inference m, 2+2m retraining m);
+ * *out_objective = evaluate_plan(...).total of that plan. Any output pointer
+ * may be NULL. */
+int mgs_solve_window(mgs_ctx* ctx, const mgs_problem* p, int32_t* out_option, int32_t* out_config,
+                     int8_t* out_labels, double* out_objective, mgs_stats* stats, mgs_error* err);
+
+/* n independent windows (different scenarios / traces) solved back to back on
+ * the device; per-problem outputs at out_option[i*S_max...], status[i],
+ * objective[i]. Returns MGS_OK if the call itself ran (per-problem errors are
+ * in status[]/errs[]). */
+int mgs_solve_batch(mgs_ctx* ctx, const mgs_problem* problems, int32_t n, int32_t s_max, int32_t* out_option,
+                    double* out_objective, int32_t* status, mgs_stats* stats, mgs_error* errs);
+
+/* evaluate_plan(verify_feasibility=false) for n_plans plans x n_traces traces
+ * sharing one window's tables: plans[i*S+s] = option index,
+ * arrivals[t*M*S + m*S + s]. total[i*n_traces+t] = objective;
+ * throughput (optional, [i][t][s][m]) = SLO-attained counts. */
+int mgs_evaluate_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* plans, int32_t n_plans,
+                       const int64_t* arrivals, int32_t n_traces, double* total, double* throughput,
+                       mgs_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,191 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// Driver around the UNMODIFIED reference planner (header-only C++20 under
+// /root/reference/proj/include, compiled in place by oracle/Makefile into
+// oracle/_ref/). It is the ground truth the CPU restatement and the GPU path
+// are pinned against, and the CPU baseline arm of bench.py.
+//
+//   migref solve <scenario.scn> [window] [--workers N] [--budget B] [--chain] [--bf]
+//       load_scenario (workload.hpp:337) -> solve_dp (solvers.hpp:242) [and
+//       solve_bruteforce (:143)] -> evaluate_plan (evaluate.hpp:153); prints
+//       one JSON object: plan encoding (space.hpp:231), objective bits, per-(s,m)
+//       SLO-attained throughput bits, wall time, or the Error code.
+//       --chain re-plans with initial = final_ranges(first plan)
+//       (solver_test.cpp:130-147 semantics).
+//   migref gen-random <seed> <count> <outdir> [--no-drop]
+//       the reference's own randomized oracle corpus generator
+//       (tests/test_util.hpp:104-181), written to files with
+//       write_scenario_files (workload.hpp:422) so other implementations
+//       read identical inputs.
+//
+// The shared-library build exports migref_solve_file() for bench.py.
+#include <chrono>
+#include <cinttypes>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#ifndef MIGSIM_DATA_DIR
+#define MIGSIM_DATA_DIR "/nonexistent"
+#endif
+#include "migsim/solvers.hpp"
+#include "test_util.hpp"  // reference tests/test_util.hpp (via -I)
+
+using namespace migsim;
+
+namespace {
+
+std::string hexbits(double v) {
+  uint64_t b;
+  std::memcpy(&b, &v, 8);
+  char buf[32];
+  std::snprintf(buf, sizeof buf, "%016" PRIx64, b);
+  return buf;
+}
+
+std::string json_str(const std::string& s) {
+  std::string o = "\"";
+  for (char c : s) {
+    if (c == '"' || c == '\\') { o += '\\'; o += c; }
+    else if (c == '\n') o += "\\n";
+    else o += c;
+  }
+  return o + "\"";
+}
+
+ArrivalForecast window_forecast(const Scenario& sc, int w) {
+  ArrivalForecast fc;
+  for (size_t m = 0; m < sc.models.size(); ++m) fc.counts.push_back(sc.window_arrivals(static_cast<int>(m), w));
+  return fc;
+}
+
+std::string plan_json(const PlanContext& ctx, const AllocationSequence& seq, const ArrivalForecast& fc) {
+  engine::Space sp = engine::Space::build(ctx);
+  auto enc = sp.encode(seq);
+  PlanScore sc = evaluate_plan(ctx, seq, fc.counts);
+  std::string o = "{\"encode\":[";
+  for (size_t i = 0; i < enc.size(); ++i) o += (i ? "," : "") + std::to_string(enc[i]);
+  o += "],\"obj\":\"" + hexbits(sc.total) + "\",\"objective\":" + fmt_real(sc.total) + ",\"thr\":[";
+  for (size_t i = 0; i < sc.breakdown.size(); ++i) o += std::string(i ? "," : "") + "\"" + hexbits(sc.breakdown[i].throughput) + "\"";
+  o += "]}";
+  return o;
+}
+
+std::string initial_json(const std::map<TaskId, std::set<SlotRange>>& init) {
+  std::string o = "[";
+  bool first = true;
+  for (const auto& [task, ranges] : init)
+    for (const auto& [start, size] : ranges) {
+      o += std::string(first ? "" : ",") + "[" + json_str(task.model) + "," +
+           (task.kind == TaskKind::Inference ? "\"i\"" : "\"r\"") + "," + std::to_string(start) + "," +
+           std::to_string(size) + "]";
+      first = false;
+    }
+  return o + "]";
+}
+
+template <class F>
+std::string guarded(F&& f) {
+  try {
+    return f();
+  } catch (const Error& e) {
+    return "{\"error\":" + json_str(e.code()) + ",\"message\":" + json_str(e.what()) + "}";
+  }
+}
+
+int cmd_solve(int argc, char** argv) {
+  if (argc < 3) return 2;
+  std::string path = argv[2];
+  int window = 0;
+  SolveOptions opt;
+  bool chain = false, bf = false;
+  for (int i = 3; i < argc; ++i) {
+    std::string a = argv[i];
+    if (a == "--workers") opt.workers = std::atoi(argv[++i]);
+    else if (a == "--budget") opt.state_budget = std::strtoull(argv[++i], nullptr, 10);
+    else if (a == "--chain") chain = true;
+    else if (a == "--bf") bf = true;
+    else window = std::atoi(a.c_str());
+  }
+  std::string out = guarded([&] {
+    Scenario sc = load_scenario(path);
+    PlanContext ctx{&sc, window, std::nullopt};
+    ArrivalForecast fc = window_forecast(sc, window);
+    auto t0 = std::chrono::steady_clock::now();
+    AllocationSequence dp = solve_dp(ctx, fc, opt);
+    double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::string o = "{\"dp\":" + plan_json(ctx, dp, fc) + ",\"seconds\":" + fmt_real(secs) +
+                    ",\"options\":" + std::to_string(engine::Space::build(ctx).options.size());
+    if (bf) o += ",\"bf\":" + guarded([&] { return plan_json(ctx, solve_bruteforce(ctx, fc, opt), fc); });
+    if (chain) {
+      PlanContext chained = ctx;
+      chained.initial = final_ranges(sc, dp);
+      o += ",\"chain\":{\"initial\":" + initial_json(*chained.initial) +
+           ",\"dp\":" + guarded([&] { return plan_json(chained, solve_dp(chained, fc, opt), fc); });
+      if (bf) o += ",\"bf\":" + guarded([&] { return plan_json(chained, solve_bruteforce(chained, fc, opt), fc); });
+      o += "}";
+    }
+    return o + "}";
+  });
+  std::printf("%s\n", out.c_str());
+  return 0;
+}
+
+int cmd_gen_random(int argc, char** argv) {
+  if (argc < 5) return 2;
+  unsigned seed = static_cast<unsigned>(std::strtoul(argv[2], nullptr, 10));
+  int count = std::atoi(argv[3]);
+  std::string dir = argv[4];
+  bool allow_drop = !(argc > 5 && std::string(argv[5]) == "--no-drop");
+  std::mt19937 rng(seed);
+  for (int i = 0; i < count; ++i) {
+    Scenario sc = testutil::random_oracle_scenario(rng, allow_drop);
+    std::string stem = "rnd_" + std::to_string(seed) + "_" + std::to_string(i);
+    write_scenario_files(sc, dir, stem);
+    std::printf("%s/%s.scn\n", dir.c_str(), stem.c_str());
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+// CPU baseline entry for bench.py: one solve_dp of window `window` of the
+// scenario file. Returns 0 on success, 1 on a migsim::Error (code copied).
+int migref_solve_file(const char* scn, int window, int workers, double* seconds, double* objective,
+                      int* encode, int encode_cap, int* encode_len, char* err_code, int err_cap) {
+  try {
+    Scenario sc = load_scenario(scn);
+    PlanContext ctx{&sc, window, std::nullopt};
+    ArrivalForecast fc = window_forecast(sc, window);
+    SolveOptions opt;
+    opt.workers = workers;
+    auto t0 = std::chrono::steady_clock::now();
+    AllocationSequence dp = solve_dp(ctx, fc, opt);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *objective = evaluate_plan(ctx, dp, fc.counts).total;
+    auto enc = engine::Space::build(ctx).encode(dp);
+    *encode_len = static_cast<int>(enc.size());
+    for (int i = 0; i < encode_cap && i < static_cast<int>(enc.size()); ++i) encode[i] = enc[i];
+    return 0;
+  } catch (const Error& e) {
+    if (err_cap > 0) std::snprintf(err_code, err_cap, "%s", e.code().c_str());
+    return 1;
+  }
+}
+}
+
+#ifndef MIGREF_NO_MAIN
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    std::fprintf(stderr, "usage: migref solve|gen-random ...\n");
+    return 2;
+  }
+  std::string cmd = argv[1];
+  if (cmd == "solve") return cmd_solve(argc, argv);
+  if (cmd == "gen-random") return cmd_gen_random(argc, argv);
+  std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
+  return 2;
+}
+#endif

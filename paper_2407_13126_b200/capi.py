@@ -1,0 +1,127 @@
+"""ctypes mirror of include/migsim_b200.h (the C ABI) and the product library loader.
+
+The product path is the CUDA library `lib/libmigsim_b200.so`; `load()` raises if it
+is missing — there is deliberately no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+MAX_MODELS = 4
+MAX_SLOTS = 8
+SIZES = 8
+FOREIGN_MASK = 0xFFFFFFFF
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(PKG_DIR, "lib")
+LIB_PATH = os.path.join(LIB_DIR, "libmigsim_b200.so")
+
+STATUS_CODES = {
+    0: "ok",
+    1: "input.scenario",
+    2: "input.catalog",
+    3: "input.forecast",
+    4: "input.arrivals",
+    5: "infeasible.deployment-floor",
+    6: "infeasible.retraining-window",
+    7: "infeasible.no-coexistence-configuration",
+    8: "infeasible.joint",
+    9: "planner.state-budget",
+    10: "plan.infeasible",
+    11: "device.cuda",
+    12: "input.argument",
+}
+
+
+class mgs_error(C.Structure):
+    _fields_ = [("code", C.c_int32), ("step", C.c_int32), ("frontier", C.c_uint64), ("model", C.c_int32),
+                ("message", C.c_char * 320)]
+
+
+class mgs_lattice(C.Structure):
+    _fields_ = [("n_configs", C.c_int32), ("gpc_count", C.c_int32), ("slot_offset", C.POINTER(C.c_int32)),
+                ("slot_size", C.POINTER(C.c_int32)), ("slot_start", C.POINTER(C.c_int32))]
+
+
+class mgs_tables(C.Structure):
+    _fields_ = [("models", C.c_int32), ("steps", C.c_int32),
+                ("cap_by_size", (C.c_double * SIZES) * MAX_MODELS),
+                ("rt_by_size", (C.c_int64 * SIZES) * MAX_MODELS),
+                ("floor_gpcs", C.c_int32 * MAX_MODELS), ("psi", C.c_double * MAX_MODELS),
+                ("acc_pre", C.c_double * MAX_MODELS), ("acc_post", C.c_double * MAX_MODELS)]
+
+
+class mgs_problem(C.Structure):
+    _fields_ = [("lattice", mgs_lattice), ("tables", mgs_tables), ("forecast", C.POINTER(C.c_int64)),
+                ("forecast_len", C.c_int32), ("has_initial", C.c_int32), ("init_mask", C.c_uint32 * MAX_MODELS),
+                ("state_budget", C.c_uint64), ("workers", C.c_int32)]
+
+
+class mgs_stats(C.Structure):
+    _fields_ = [("options", C.c_uint64), ("candidates", C.c_uint64), ("transitions_ref", C.c_uint64),
+                ("transitions", C.c_uint64), ("frontier_total", C.c_uint64), ("frontier_peak", C.c_uint64),
+                ("device_ms", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class PlannerError(RuntimeError):
+    """Mirror of migsim::Error: `.code` is the reference's stable code string."""
+
+    def __init__(self, status: int, err: mgs_error | None = None):
+        self.status = status
+        self.code = STATUS_CODES.get(status, "unknown")
+        self.message = err.message.decode(errors="replace") if err is not None else ""
+        self.step = err.step if err is not None else 0
+        self.frontier = err.frontier if err is not None else 0
+        super().__init__("%s: %s" % (self.code, self.message))
+
+
+def ptr(arr, ctype):
+    return arr.ctypes.data_as(C.POINTER(ctype))
+
+
+_LIB = None
+
+
+def load():
+    """Loads the CUDA product library; fails loudly when it is absent."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError("CUDA extension %s is missing: run __graft_entry__.build() (no CPU fallback exists)"
+                           % LIB_PATH)
+    lib = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    lib.mgs_open.argtypes = [C.c_int, P(C.c_void_p)]
+    lib.mgs_close.argtypes = [C.c_void_p]
+    lib.mgs_version.restype = C.c_char_p
+    lib.mgs_status_code.restype = C.c_char_p
+    lib.mgs_enumerate.argtypes = [C.c_void_p, P(mgs_lattice), P(mgs_tables), P(C.c_int64), C.c_int64,
+                                  P(C.c_int32), P(C.c_int8), P(C.c_uint32), P(C.c_double), P(C.c_int8),
+                                  P(mgs_error)]
+    lib.mgs_goodput_table.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_double), P(C.c_double), P(C.c_int32),
+                                      P(mgs_error)]
+    lib.mgs_solve_window.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_int32), P(C.c_int32), P(C.c_int8),
+                                     P(C.c_double), P(mgs_stats), P(mgs_error)]
+    lib.mgs_solve_batch.argtypes = [C.c_void_p, P(mgs_problem), C.c_int32, C.c_int32, P(C.c_int32),
+                                    P(C.c_double), P(C.c_int32), P(mgs_stats), P(mgs_error)]
+    lib.mgs_evaluate_batch.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_int32), C.c_int32, P(C.c_int64),
+                                       C.c_int32, P(C.c_double), P(C.c_double), P(mgs_error)]
+    _LIB = lib
+    return lib
+
+
+EXPORTED_SYMBOLS = ["mgs_open", "mgs_close", "mgs_status_code", "mgs_version", "mgs_enumerate",
+                    "mgs_goodput_table", "mgs_solve_window", "mgs_solve_batch", "mgs_evaluate_batch"]
+
+
+def empty_error():
+    e = mgs_error()
+    e.code = 0
+    return e

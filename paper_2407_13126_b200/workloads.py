@@ -1,0 +1,142 @@
+"""Synthetic planner inputs in the reference's file grammar.
+
+The reference ships no scenarios for the headline configurations, so this module
+writes them (SURVEY.md §8(d) "Concrete synthetic inputs").  Every number lands in
+the scenario / trace text exactly as the reference parser reads it
+(reference: proj/include/migsim/workload.hpp:99-148 trace CSV, :151-228 scenario
+sections), so the CPU reference, the CPU restatement and the GPU path all consume
+byte-identical inputs.  Arrivals are drawn with numpy's PCG64 (never
+std::poisson_distribution, which is not portable across standard libraries).
+"""
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+GOLDEN_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+A100_LATTICE = os.path.join(GOLDEN_DIR, "lattice_a100.catalog")
+
+
+@dataclass
+class Tenant:
+    name: str
+    per_gpc: float                  # capability[k] = k * per_gpc requests/step
+    acc_pre: list
+    acc_post: list
+    data_volume: int = 0            # rt_table derived as ceil(3*vol/cap[k]) when rt is None
+    rt: dict | None = None
+    psi: float = 0.5
+    floor: int = 1
+    gflops: float = 1.8
+    latency_full: float = 0.005
+    sizes: tuple = (1, 2, 3, 4, 5, 6, 7)
+
+
+@dataclass
+class ScenarioSpec:
+    tenants: list
+    window_size: int
+    window_count: int = 1
+    catalog_path: str = A100_LATTICE
+    counts: np.ndarray | None = field(default=None, repr=False)   # int64 [M][S*W]
+
+
+def fmt_real(v: float) -> str:
+    """%.9g, the reference's deterministic real formatting (common.hpp:114-118)."""
+    return "%.9g" % v
+
+
+def poisson_trace(lams, steps, seed):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return np.stack([rng.poisson(lam, size=steps) for lam in lams]).astype(np.int64)
+
+
+def mmpp_trace(per_gpc, steps, seed, lo=1.5, hi=5.0, p_switch=0.05):
+    """2-state MMPP per tenant (SURVEY.md §8(d) generator spec): rate lo*c or hi*c,
+    switch probability p per step, initial state low, counts ~ Poisson(rate)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    out = np.zeros((len(per_gpc), steps), dtype=np.int64)
+    for m, c in enumerate(per_gpc):
+        state = 0
+        flips = rng.random(steps) < p_switch
+        rates = np.empty(steps)
+        for s in range(steps):
+            rates[s] = (lo if state == 0 else hi) * c
+            if flips[s]:
+                state ^= 1
+        out[m] = rng.poisson(rates)
+    return out
+
+
+def scenario_text(spec: ScenarioSpec, catalog_file: str, trace_file: str) -> str:
+    lines = ["[windows]", "size %d" % spec.window_size, "count %d" % spec.window_count, "",
+             "[catalog]", "file %s" % catalog_file, "", "[models]"]
+    for t in spec.tenants:
+        lines.append("model %s" % t.name)
+        lines.append("gflops %s" % fmt_real(t.gflops))
+        lines.append("min_deploy_gpcs %d" % t.floor)
+        lines.append("latency_full %s" % fmt_real(t.latency_full))
+        lines.append("reconfig_overhead %s" % fmt_real(t.psi))
+        lines.append("capability " + " ".join("%d:%s" % (k, fmt_real(k * t.per_gpc)) for k in t.sizes))
+        if t.rt is not None:
+            lines.append("rt_table " + " ".join("%d:%d" % (k, v) for k, v in sorted(t.rt.items())))
+        else:
+            lines.append("data_volume %d" % t.data_volume)
+        lines.append("accuracy_pre " + " ".join(fmt_real(a) for a in t.acc_pre))
+        lines.append("accuracy_post " + " ".join(fmt_real(a) for a in t.acc_post))
+    lines += ["", "[trace]", "file %s" % trace_file, ""]
+    return "\n".join(lines)
+
+
+def trace_csv(names, counts) -> str:
+    out = ["second,model,count"]
+    for s in range(counts.shape[1]):
+        for m, n in enumerate(names):
+            out.append("%d,%s,%d" % (s, n, counts[m, s]))
+    return "\n".join(out) + "\n"
+
+
+def write_scenario(spec: ScenarioSpec, directory: str, stem: str) -> str:
+    """Writes <stem>.scn + <stem>.csv (catalog referenced by absolute-or-relative
+    path). Returns the .scn path."""
+    os.makedirs(directory, exist_ok=True)
+    cat = os.path.relpath(spec.catalog_path, directory)
+    names = [t.name for t in spec.tenants]
+    with open(os.path.join(directory, stem + ".csv"), "w") as f:
+        f.write(trace_csv(names, spec.counts))
+    scn = os.path.join(directory, stem + ".scn")
+    with open(scn, "w") as f:
+        f.write(scenario_text(spec, cat, stem + ".csv"))
+    return scn
+
+
+# --------------------------------------------------------------------------
+# BASELINE.json configurations
+
+def c1_spec(seed: int, steps: int = 200, data_volume: int = 3000, psi: float = 0.5,
+            lams=(120.0, 150.0)) -> ScenarioSpec:
+    """Config 1: two ResNet-18 tenants on the A100 lattice; cap[k] = 40k / 50k,
+    RT = ceil(3*vol/cap[k]), psi 0.5, acc 0.60->0.90 / 0.62->0.89, Poisson
+    lambda 120 / 150 (SURVEY.md §6.2 inputs)."""
+    tenants = [
+        Tenant("r18a", 40.0, [0.60], [0.90], data_volume=data_volume, psi=psi),
+        Tenant("r18b", 50.0, [0.62], [0.89], data_volume=data_volume, psi=psi),
+    ]
+    spec = ScenarioSpec(tenants, steps, 1)
+    spec.counts = poisson_trace(lams, steps, seed)
+    return spec
+
+
+def c2_spec(seed: int, steps: int = 200, windows: int = 3, tenants: int = 4) -> ScenarioSpec:
+    """Config 2 / 4 generator: ResNet-50 / MobileNetV2 / ViT-B / BERT-base with
+    c = 40/120/12/10 req/s/GPC, data_volume = 80c (RT = ceil(240/k)), psi 0.5,
+    explicit per-window accuracy lists, 2-state MMPP arrivals."""
+    table = [("resnet50", 40.0, 0.55, 0.85, 4.09), ("mobilenetv2", 120.0, 0.70, 0.80, 0.32),
+             ("vitb", 12.0, 0.60, 0.88, 17.56), ("bertbase", 10.0, 0.50, 0.83, 22.2)][:tenants]
+    ts = [Tenant(n, c, [pre] * windows, [post] * windows, data_volume=int(80 * c), gflops=g)
+          for (n, c, pre, post, g) in table]
+    spec = ScenarioSpec(ts, steps, windows)
+    spec.counts = mmpp_trace([t.per_gpc for t in ts], steps * windows, seed)
+    return spec
