@@ -26,6 +26,12 @@
 extern "C" {
 #endif
 
+#if defined(__GNUC__)
+#define MGS_API __attribute__((visibility("default")))
+#else
+#define MGS_API
+#endif
+
 #define MGS_MAX_MODELS 4  /* engine::kMaxModels, space.hpp:17 */
 #define MGS_MAX_SLOTS 8   /* slots per configuration (gpc_count <= 8) */
 #define MGS_SIZES 8       /* tables indexed by instance size 0..7 (space.hpp:39-40) */
@@ -104,16 +110,16 @@ typedef struct {
 
 typedef struct mgs_ctx mgs_ctx;
 
-int mgs_open(int device, mgs_ctx** out);
-void mgs_close(mgs_ctx* ctx);
-const char* mgs_status_code(int status);
-const char* mgs_version(void);
+MGS_API int mgs_open(int device, mgs_ctx** out);
+MGS_API void mgs_close(mgs_ctx* ctx);
+MGS_API const char* mgs_status_code(int status);
+MGS_API const char* mgs_version(void);
 
 /* Candidate enumeration (Space::build). *n_options receives |O|. Optional
  * host copies (pass NULL to skip) hold min(cap, |O|) options in lex order:
  * config[i], labels[i*MGS_MAX_SLOTS + slot], infer_mask[i*4+m],
  * infer_cap[i*4+m], retrain_size[i*4+m]. */
-int mgs_enumerate(mgs_ctx* ctx, const mgs_lattice* lattice, const mgs_tables* tables, int64_t* n_options,
+MGS_API int mgs_enumerate(mgs_ctx* ctx, const mgs_lattice* lattice, const mgs_tables* tables, int64_t* n_options,
                   int64_t cap, int32_t* config, int8_t* labels, uint32_t* infer_mask, double* infer_cap,
                   int8_t* retrain_size, mgs_error* err);
 
@@ -121,7 +127,7 @@ int mgs_enumerate(mgs_ctx* ctx, const mgs_lattice* lattice, const mgs_tables* ta
  * optimistic per-step bound ub_suffix[0..S] (solvers.hpp:270-280) and the
  * greedy incumbent (solvers.hpp:283-322; -inf when the greedy walk does not
  * finish every retraining). greedy_option[s] = chosen option or -1. */
-int mgs_goodput_table(mgs_ctx* ctx, const mgs_problem* p, double* ub_suffix, double* incumbent,
+MGS_API int mgs_goodput_table(mgs_ctx* ctx, const mgs_problem* p, double* ub_suffix, double* incumbent,
                       int32_t* greedy_option, mgs_error* err);
 
 /* solve_dp on one window. out_option[s] = option index (lex rank) chosen at
@@ -129,21 +135,21 @@ int mgs_goodput_table(mgs_ctx* ctx, const mgs_problem* p, double* ub_suffix, dou
  * and per-slot labels (0 unused, 1+2m inference m, 2+2m retraining m);
  * *out_objective = evaluate_plan(...).total of that plan. Any output pointer
  * may be NULL. */
-int mgs_solve_window(mgs_ctx* ctx, const mgs_problem* p, int32_t* out_option, int32_t* out_config,
+MGS_API int mgs_solve_window(mgs_ctx* ctx, const mgs_problem* p, int32_t* out_option, int32_t* out_config,
                      int8_t* out_labels, double* out_objective, mgs_stats* stats, mgs_error* err);
 
 /* n independent windows (different scenarios / traces) solved back to back on
  * the device; per-problem outputs at out_option[i*S_max...], status[i],
  * objective[i]. Returns MGS_OK if the call itself ran (per-problem errors are
  * in status[]/errs[]). */
-int mgs_solve_batch(mgs_ctx* ctx, const mgs_problem* problems, int32_t n, int32_t s_max, int32_t* out_option,
+MGS_API int mgs_solve_batch(mgs_ctx* ctx, const mgs_problem* problems, int32_t n, int32_t s_max, int32_t* out_option,
                     double* out_objective, int32_t* status, mgs_stats* stats, mgs_error* errs);
 
 /* evaluate_plan(verify_feasibility=false) for n_plans plans x n_traces traces
  * sharing one window's tables: plans[i*S+s] = option index,
  * arrivals[t*M*S + m*S + s]. total[i*n_traces+t] = objective;
  * throughput (optional, [i][t][s][m]) = SLO-attained counts. */
-int mgs_evaluate_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* plans, int32_t n_plans,
+MGS_API int mgs_evaluate_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* plans, int32_t n_plans,
                        const int64_t* arrivals, int32_t n_traces, double* total, double* throughput,
                        mgs_error* err);
 

@@ -18,6 +18,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -404,8 +405,11 @@ std::vector<int> solve(const mgs_problem& p, mgs_stats* stats) {
   using SubKey = std::array<uint32_t, KM>;
   uint64_t tr_ref = 0, tr = 0, ftot = 0, fpeak = 0;
 
+  const bool trace = std::getenv("MGS_ORACLE_TRACE") != nullptr;
   for (int s = 0; s < S; ++s) {
     const auto& cur = F[s];
+    size_t n_units_step = 0;
+    uint64_t tr_before = tr;
     if (cur.empty()) throw Fail{MGS_ERR_INFEASIBLE_JOINT, "no feasible allocation sequence exists for this window"};  // :348
     const bool charge = s > 0 || p.has_initial;
     std::unordered_map<uint64_t, std::vector<int>> groups;  // :351-353
@@ -462,6 +466,7 @@ std::vector<int> solve(const mgs_problem& p, mgs_stats* stats) {
       };
       rec(rec, 0);
       // transitions (:420-471)
+      n_units_step += units.size();
       for (auto& [packed, olist] : units) {
         tr_ref += olist->size();
         tr += cand_per_sig[P.opts[olist->front()].sig];
@@ -514,6 +519,7 @@ std::vector<int> solve(const mgs_problem& p, mgs_stats* stats) {
     std::vector<State> next;
     next.reserve(merged.size());
     for (auto& [k, st] : merged) next.push_back(st);
+    size_t n_merged = next.size();
     {  // band (:499-511)
       std::unordered_map<uint64_t, double> best;
       for (const auto& st : next) {
@@ -557,6 +563,14 @@ std::vector<int> solve(const mgs_problem& p, mgs_stats* stats) {
     for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
     std::sort(order.begin(), order.end(), [&](int a, int b) { return next[a].lex < next[b].lex; });
     for (size_t r = 0; r < order.size(); ++r) next[order[r]].rank = static_cast<uint32_t>(r);
+    if (trace) {
+      size_t gmax = 0;
+      for (auto& [st_, idxs] : groups) gmax = std::max(gmax, idxs.size());
+      std::unordered_map<uint64_t, int> ns_count;
+      for (auto& st_ : next) ns_count[st_.status]++;
+      std::fprintf(stderr, "step %d frontier %zu groups %zu gmax %zu units %zu tr %llu merged %zu kept %zu nsgroups %zu\n", s,
+                   cur.size(), groups.size(), gmax, n_units_step, (unsigned long long)(tr - tr_before), n_merged, next.size(), ns_count.size());
+    }
     ftot += next.size();
     fpeak = std::max<uint64_t>(fpeak, next.size());
     F[s + 1] = std::move(next);

@@ -1,0 +1,278 @@
+// C ABI (include/migsim_b200.h): thin POD layer over the device planner.
+// Every entry point catches planner / CUDA failures and maps them to the
+// reference's error codes; nothing here falls back to a CPU computation.
+#include <cmath>
+#include <cstdio>
+#include <new>
+
+#include "ctx.cuh"
+
+struct mgs_ctx {
+  mgs::Ctx c;
+};
+
+namespace mgs {
+void evaluate_batch(Ctx& c, const Prepared& pr, const DevSpace& sp, const int32_t* d_plans, int n_plans,
+                    const int64_t* d_arr, int n_traces, double* d_total, double* d_thr);
+}
+
+namespace {
+
+using mgs::Ctx;
+using mgs::PlanFail;
+
+void fill_err(mgs_error* e, int code, const std::string& msg, int step = 0, uint64_t frontier = 0, int model = -1) {
+  if (!e) return;
+  e->code = code;
+  e->step = step;
+  e->frontier = frontier;
+  e->model = model;
+  std::snprintf(e->message, sizeof e->message, "%s", msg.c_str());
+}
+
+template <class F>
+int guarded(mgs_error* err, F&& f) {
+  if (err) fill_err(err, MGS_OK, "");
+  try {
+    f();
+    return MGS_OK;
+  } catch (const PlanFail& pf) {
+    fill_err(err, pf.code, pf.msg, pf.step, pf.frontier, pf.model);
+    return pf.code;
+  } catch (const mgs::CudaFail& cf) {
+    fill_err(err, MGS_ERR_CUDA,
+             std::string("CUDA error ") + cudaGetErrorString(cf.err) + " at " + cf.what + ":" + std::to_string(cf.line));
+    return MGS_ERR_CUDA;
+  } catch (const std::bad_alloc&) {
+    fill_err(err, MGS_ERR_CUDA, "host allocation failed");
+    return MGS_ERR_CUDA;
+  }
+}
+
+mgs::Prepared prepare_problem(const mgs_problem& p) {
+  mgs::Prepared pr = mgs::prepare_tables(p.lattice, p.tables);
+  pr.has_initial = p.has_initial ? 1 : 0;
+  for (int m = 0; m < MGS_MAX_MODELS; ++m) pr.init_mask[m] = p.has_initial ? p.init_mask[m] : 0u;
+  return pr;
+}
+
+__global__ void k_to_double(const int64_t* in, double* out, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = static_cast<double>(in[i]);
+}
+
+// forecast [M][forecast_len] -> device doubles [M][S]
+double* upload_forecast(Ctx& c, const mgs_problem& p, int M, int S) {
+  if (!p.forecast) throw PlanFail{MGS_ERR_ARGUMENT, "forecast is null"};
+  int64_t* d_i = c.buf<int64_t>("forecast_i64", static_cast<size_t>(M) * S);
+  double* d_f = c.buf<double>("forecast_f64", static_cast<size_t>(M) * S);
+  if (p.forecast_len == S) {
+    MGS_CUDA_OK(cudaMemcpyAsync(d_i, p.forecast, static_cast<size_t>(M) * S * 8, cudaMemcpyHostToDevice, c.stream));
+  } else {
+    MGS_CUDA_OK(cudaMemcpy2DAsync(d_i, S * 8, p.forecast, p.forecast_len * 8, static_cast<size_t>(S) * 8, M,
+                                  cudaMemcpyHostToDevice, c.stream));
+  }
+  k_to_double<<<mgs::ceil_div(M * S, 256), 256, 0, c.stream>>>(d_i, d_f, M * S);
+  return d_f;
+}
+
+void solve_one(Ctx& c, const mgs_problem& p, int32_t* out_option, int32_t* out_config, int8_t* out_labels,
+               double* out_objective, mgs_stats* stats) {
+  MGS_CUDA_OK(cudaEventRecord(c.ev0, c.stream));
+  mgs::Prepared pr = prepare_problem(p);
+  mgs::DevSpace sp;
+  mgs::build_space(c, p.lattice, pr, sp);
+  mgs::precheck_space(c, p.lattice, pr, sp);  // throw_if_infeasible(precheck_scenario) first (solvers.hpp:245)
+  const int M = pr.t.M, S = pr.t.S;
+  if (p.forecast_len != S) throw PlanFail{MGS_ERR_INPUT_FORECAST, "forecast horizon != window size"};  // :250-252
+  double* d_recv = upload_forecast(c, p, M, S);
+  double* d_ub = c.buf<double>("ub_suffix", S + 1);
+  double* d_inc = c.buf<double>("incumbent", 1);
+  int32_t* d_greedy = c.buf<int32_t>("greedy", S);
+  mgs::goodput_reductions(c, pr, sp, d_recv, d_ub, d_inc, d_greedy);
+  mgs::SolveOut out;
+  mgs::solve_dp(c, p, pr, sp, d_recv, d_ub, d_inc, out);
+  // objective = evaluate_plan(...).total of the chosen plan, on the device
+  int32_t* d_plan = c.buf<int32_t>("plan_eval", S);
+  double* d_total = c.buf<double>("plan_total", 1);
+  MGS_CUDA_OK(cudaMemcpyAsync(d_plan, out.options.data(), S * 4, cudaMemcpyHostToDevice, c.stream));
+  int64_t* d_arr = c.buf<int64_t>("forecast_i64", static_cast<size_t>(M) * S);
+  mgs::evaluate_batch(c, pr, sp, d_plan, 1, d_arr, 1, d_total, nullptr);
+  double total = 0.0;
+  MGS_CUDA_OK(cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, c.stream));
+  if (out_config || out_labels) {
+    std::vector<int32_t> cfg(sp.n_opt);
+    std::vector<int8_t> lab(static_cast<size_t>(sp.n_opt) * MGS_MAX_SLOTS);
+    MGS_CUDA_OK(cudaMemcpyAsync(cfg.data(), sp.opt_config, sp.n_opt * 4, cudaMemcpyDeviceToHost, c.stream));
+    MGS_CUDA_OK(cudaMemcpyAsync(lab.data(), sp.opt_labels, lab.size(), cudaMemcpyDeviceToHost, c.stream));
+    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+    for (int s = 0; s < S; ++s) {
+      const int o = out.options[s];
+      if (out_config) out_config[s] = cfg[o];
+      if (out_labels)
+        for (int k = 0; k < MGS_MAX_SLOTS; ++k) out_labels[s * MGS_MAX_SLOTS + k] = lab[static_cast<size_t>(o) * MGS_MAX_SLOTS + k];
+    }
+  }
+  MGS_CUDA_OK(cudaEventRecord(c.ev1, c.stream));
+  MGS_CUDA_OK(cudaEventSynchronize(c.ev1));
+  float ms = 0.f;
+  MGS_CUDA_OK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+  out.stats.device_ms = ms;
+  if (out_option)
+    for (int s = 0; s < S; ++s) out_option[s] = out.options[s];
+  if (out_objective) *out_objective = total;
+  if (stats) *stats = out.stats;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mgs_version(void) { return "paper_2407_13126_b200 0.1 (sm_100a)"; }
+
+const char* mgs_status_code(int status) {
+  switch (status) {
+    case MGS_OK: return "ok";
+    case MGS_ERR_INPUT_SCENARIO: return "input.scenario";
+    case MGS_ERR_INPUT_CATALOG: return "input.catalog";
+    case MGS_ERR_INPUT_FORECAST: return "input.forecast";
+    case MGS_ERR_INPUT_ARRIVALS: return "input.arrivals";
+    case MGS_ERR_DEPLOYMENT_FLOOR: return "infeasible.deployment-floor";
+    case MGS_ERR_RETRAINING_WINDOW: return "infeasible.retraining-window";
+    case MGS_ERR_NO_COEXISTENCE: return "infeasible.no-coexistence-configuration";
+    case MGS_ERR_INFEASIBLE_JOINT: return "infeasible.joint";
+    case MGS_ERR_STATE_BUDGET: return "planner.state-budget";
+    case MGS_ERR_PLAN_INFEASIBLE: return "plan.infeasible";
+    case MGS_ERR_CUDA: return "device.cuda";
+    case MGS_ERR_ARGUMENT: return "input.argument";
+    default: return "unknown";
+  }
+}
+
+int mgs_open(int device, mgs_ctx** out) {
+  if (!out) return MGS_ERR_ARGUMENT;
+  *out = nullptr;
+  return guarded(nullptr, [&] {
+    int n = 0;
+    MGS_CUDA_OK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw PlanFail{MGS_ERR_ARGUMENT, "no such CUDA device"};
+    MGS_CUDA_OK(cudaSetDevice(device));
+    auto* h = new mgs_ctx();
+    h->c.device = device;
+    MGS_CUDA_OK(cudaDeviceGetAttribute(&h->c.sm_count, cudaDevAttrMultiProcessorCount, device));
+    MGS_CUDA_OK(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
+    MGS_CUDA_OK(cudaEventCreate(&h->c.ev0));
+    MGS_CUDA_OK(cudaEventCreate(&h->c.ev1));
+    *out = h;
+  });
+}
+
+void mgs_close(mgs_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->c.device);
+  delete ctx;
+}
+
+int mgs_enumerate(mgs_ctx* ctx, const mgs_lattice* lattice, const mgs_tables* tables, int64_t* n_options, int64_t cap,
+                  int32_t* config, int8_t* labels, uint32_t* infer_mask, double* infer_cap, int8_t* retrain_size,
+                  mgs_error* err) {
+  if (!ctx || !lattice || !tables || !n_options) return MGS_ERR_ARGUMENT;
+  return guarded(err, [&] {
+    Ctx& c = ctx->c;
+    MGS_CUDA_OK(cudaSetDevice(c.device));
+    mgs::Prepared pr = mgs::prepare_tables(*lattice, *tables);
+    mgs::DevSpace sp;
+    mgs::build_space(c, *lattice, pr, sp);
+    *n_options = sp.n_opt;
+    const int64_t n = std::min<int64_t>(cap, sp.n_opt);
+    if (n > 0) {
+      if (config) MGS_CUDA_OK(cudaMemcpyAsync(config, sp.opt_config, n * 4, cudaMemcpyDeviceToHost, c.stream));
+      if (labels) MGS_CUDA_OK(cudaMemcpyAsync(labels, sp.opt_labels, n * MGS_MAX_SLOTS, cudaMemcpyDeviceToHost, c.stream));
+      if (infer_mask) MGS_CUDA_OK(cudaMemcpyAsync(infer_mask, sp.opt_mask, n * 16, cudaMemcpyDeviceToHost, c.stream));
+      if (infer_cap) MGS_CUDA_OK(cudaMemcpyAsync(infer_cap, sp.opt_cap, n * 32, cudaMemcpyDeviceToHost, c.stream));
+      if (retrain_size) MGS_CUDA_OK(cudaMemcpyAsync(retrain_size, sp.opt_rsize, n * 4, cudaMemcpyDeviceToHost, c.stream));
+    }
+    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int mgs_goodput_table(mgs_ctx* ctx, const mgs_problem* p, double* ub_suffix, double* incumbent, int32_t* greedy_option,
+                      mgs_error* err) {
+  if (!ctx || !p) return MGS_ERR_ARGUMENT;
+  return guarded(err, [&] {
+    Ctx& c = ctx->c;
+    MGS_CUDA_OK(cudaSetDevice(c.device));
+    mgs::Prepared pr = prepare_problem(*p);
+    mgs::DevSpace sp;
+    mgs::build_space(c, p->lattice, pr, sp);
+    const int M = pr.t.M, S = pr.t.S;
+    if (p->forecast_len < S) throw PlanFail{MGS_ERR_INPUT_FORECAST, "forecast horizon != window size"};
+    if (sp.n_opt == 0) throw PlanFail{MGS_ERR_DEPLOYMENT_FLOOR, "no options"};
+    double* d_recv = upload_forecast(c, *p, M, S);
+    double* d_ub = c.buf<double>("ub_suffix", S + 1);
+    double* d_inc = c.buf<double>("incumbent", 1);
+    int32_t* d_greedy = c.buf<int32_t>("greedy", S);
+    mgs::goodput_reductions(c, pr, sp, d_recv, d_ub, d_inc, d_greedy);
+    if (ub_suffix) MGS_CUDA_OK(cudaMemcpyAsync(ub_suffix, d_ub, (S + 1) * 8, cudaMemcpyDeviceToHost, c.stream));
+    if (incumbent) MGS_CUDA_OK(cudaMemcpyAsync(incumbent, d_inc, 8, cudaMemcpyDeviceToHost, c.stream));
+    if (greedy_option) MGS_CUDA_OK(cudaMemcpyAsync(greedy_option, d_greedy, S * 4, cudaMemcpyDeviceToHost, c.stream));
+    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int mgs_solve_window(mgs_ctx* ctx, const mgs_problem* p, int32_t* out_option, int32_t* out_config, int8_t* out_labels,
+                     double* out_objective, mgs_stats* stats, mgs_error* err) {
+  if (!ctx || !p) return MGS_ERR_ARGUMENT;
+  return guarded(err, [&] {
+    MGS_CUDA_OK(cudaSetDevice(ctx->c.device));
+    solve_one(ctx->c, *p, out_option, out_config, out_labels, out_objective, stats);
+  });
+}
+
+int mgs_solve_batch(mgs_ctx* ctx, const mgs_problem* problems, int32_t n, int32_t s_max, int32_t* out_option,
+                    double* out_objective, int32_t* status, mgs_stats* stats, mgs_error* errs) {
+  if (!ctx || (!problems && n > 0) || n < 0) return MGS_ERR_ARGUMENT;
+  return guarded(nullptr, [&] {
+    MGS_CUDA_OK(cudaSetDevice(ctx->c.device));
+    for (int i = 0; i < n; ++i) {
+      mgs_error e{};
+      int st = guarded(&e, [&] {
+        if (problems[i].tables.steps > s_max) throw PlanFail{MGS_ERR_ARGUMENT, "window longer than s_max"};
+        solve_one(ctx->c, problems[i], out_option ? out_option + static_cast<size_t>(i) * s_max : nullptr, nullptr,
+                  nullptr, out_objective ? out_objective + i : nullptr, stats ? stats + i : nullptr);
+      });
+      if (status) status[i] = st;
+      if (errs) errs[i] = e;
+    }
+  });
+}
+
+int mgs_evaluate_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* plans, int32_t n_plans,
+                       const int64_t* arrivals, int32_t n_traces, double* total, double* throughput, mgs_error* err) {
+  if (!ctx || !p || !plans || !arrivals || !total || n_plans < 0 || n_traces < 0) return MGS_ERR_ARGUMENT;
+  return guarded(err, [&] {
+    Ctx& c = ctx->c;
+    MGS_CUDA_OK(cudaSetDevice(c.device));
+    mgs::Prepared pr = prepare_problem(*p);
+    mgs::DevSpace sp;
+    mgs::build_space(c, p->lattice, pr, sp);
+    const int M = pr.t.M, S = pr.t.S;
+    for (long long k = 0; k < static_cast<long long>(n_plans) * S; ++k)
+      if (plans[k] < 0 || plans[k] >= sp.n_opt) throw PlanFail{MGS_ERR_PLAN_INFEASIBLE, "plan names an unknown option"};
+    if (n_plans == 0 || n_traces == 0) return;
+    int32_t* d_plans = c.buf<int32_t>("eval_plans", static_cast<size_t>(n_plans) * S);
+    int64_t* d_arr = c.buf<int64_t>("eval_arr", static_cast<size_t>(n_traces) * M * S);
+    double* d_total = c.buf<double>("eval_total", static_cast<size_t>(n_plans) * n_traces);
+    double* d_thr = throughput ? c.buf<double>("eval_thr", static_cast<size_t>(n_plans) * n_traces * S * M) : nullptr;
+    MGS_CUDA_OK(cudaMemcpyAsync(d_plans, plans, static_cast<size_t>(n_plans) * S * 4, cudaMemcpyHostToDevice, c.stream));
+    MGS_CUDA_OK(cudaMemcpyAsync(d_arr, arrivals, static_cast<size_t>(n_traces) * M * S * 8, cudaMemcpyHostToDevice, c.stream));
+    mgs::evaluate_batch(c, pr, sp, d_plans, n_plans, d_arr, n_traces, d_total, d_thr);
+    MGS_CUDA_OK(cudaMemcpyAsync(total, d_total, static_cast<size_t>(n_plans) * n_traces * 8, cudaMemcpyDeviceToHost, c.stream));
+    if (throughput)
+      MGS_CUDA_OK(cudaMemcpyAsync(throughput, d_thr, static_cast<size_t>(n_plans) * n_traces * S * M * 8,
+                                  cudaMemcpyDeviceToHost, c.stream));
+    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+}  // extern "C"

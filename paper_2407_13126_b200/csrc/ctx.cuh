@@ -1,0 +1,165 @@
+// Library context: one device, one stream, grow-only scratch pools.
+#pragma once
+
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mgs {
+
+// Grow-only device allocation; contents are NOT preserved on growth.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T>
+  T* get(size_t n) {
+    size_t bytes = n * sizeof(T);
+    if (bytes == 0) bytes = sizeof(T);
+    if (bytes > cap) {
+      if (p) MGS_CUDA_OK(cudaFree(p));
+      size_t want = bytes + bytes / 4 + 256;
+      MGS_CUDA_OK(cudaMalloc(&p, want));
+      cap = want;
+    }
+    return static_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// Pinned host staging for small device->host reads.
+struct HostPinned {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T>
+  T* get(size_t n) {
+    size_t bytes = n * sizeof(T);
+    if (bytes > cap) {
+      if (p) cudaFreeHost(p);
+      MGS_CUDA_OK(cudaMallocHost(&p, bytes));
+      cap = bytes;
+    }
+    return static_cast<T*>(p);
+  }
+};
+
+// Planner failure carrying the reference's error code (mgs_status) and text.
+struct PlanFail {
+  int code;
+  std::string msg;
+  int step = 0;
+  uint64_t frontier = 0;
+  int model = -1;
+};
+
+// History arena: per-step (parent, option) arrays kept for the backtrack;
+// chunks are reused across solves.
+struct History {
+  std::vector<void*> chunks;
+  std::vector<size_t> chunk_cap;  // int32 entries
+  size_t cur = 0, used = 0;
+  std::vector<int32_t*> parent, option;
+  void reset() {
+    cur = 0;
+    used = 0;
+    parent.clear();
+    option.clear();
+  }
+  void take(size_t n, int32_t** p, int32_t** o) {
+    const size_t need = 2 * n + 64;
+    while (cur < chunks.size() && used + need > chunk_cap[cur]) {
+      ++cur;
+      used = 0;
+    }
+    if (cur == chunks.size()) {
+      const size_t cap = need > (size_t(64) << 20) ? need : (size_t(64) << 20);
+      void* ptr = nullptr;
+      MGS_CUDA_OK(cudaMalloc(&ptr, cap * 4));
+      chunks.push_back(ptr);
+      chunk_cap.push_back(cap);
+      used = 0;
+    }
+    int32_t* base = static_cast<int32_t*>(chunks[cur]) + used;
+    *p = base;
+    *o = base + n;
+    used += need;
+    parent.push_back(*p);
+    option.push_back(*o);
+  }
+  void release() {
+    for (void* q : chunks) cudaFree(q);
+    chunks.clear();
+    chunk_cap.clear();
+    reset();
+  }
+};
+
+struct Ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::map<std::string, DevBuf> bufs;
+  HostPinned pinned;
+  uint64_t kernel_launches = 0;
+  History history;
+
+  template <class T>
+  T* buf(const char* name, size_t n) {
+    return bufs[name].get<T>(n);
+  }
+  ~Ctx() {
+    for (auto& kv : bufs) kv.second.release();
+    history.release();
+    if (pinned.p) cudaFreeHost(pinned.p);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+// Host-side derived inputs of one window (engine::Tables + initial masks).
+struct Prepared {
+  HostTables t;
+  std::vector<int> slot_uid;        // universe id per flat slot
+  int n_universe = 0;
+  int has_initial = 0;
+  uint32_t init_mask[KM] = {0, 0, 0, 0};
+};
+
+// space.cu
+Prepared prepare_tables(const mgs_lattice& lat, const mgs_tables& tab);
+void build_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, DevSpace& sp);
+void precheck_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, const DevSpace& sp);
+// goodput.cu
+void goodput_reductions(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* d_recv, double* d_ub,
+                        double* d_incumbent, int32_t* d_greedy);
+// dp.cu
+struct SolveOut {
+  std::vector<int32_t> options;
+  mgs_stats stats{};
+};
+void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& sp, const double* d_recv,
+              const double* d_ub, const double* d_incumbent, SolveOut& out);
+
+// small device helpers (scan.cu)
+void exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int n);  // out has n+1 entries
+void exclusive_scan_u32(Ctx& c, const uint32_t* in, uint32_t* out, int n);
+
+template <class T>
+inline T read_scalar(Ctx& c, const T* dptr) {
+  T* h = c.pinned.get<T>(1);
+  MGS_CUDA_OK(cudaMemcpyAsync(h, dptr, sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+  MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+  return *h;
+}
+
+inline unsigned ceil_div(long long a, long long b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+}  // namespace mgs

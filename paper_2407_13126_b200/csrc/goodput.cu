@@ -1,0 +1,221 @@
+// The Goodput table: per slot x candidate x tenant SLO-attained counts
+// weighted by accuracy, reduced the two ways solve_dp consumes it before the
+// search, plus batched plan scoring.
+//
+//   k_ub_best / k_ub_suffix   ub_suffix (solvers.hpp:258-280): per step the max
+//                             over candidates of sum_m acc_max*min(recv, cap),
+//                             then a suffix sum in descending step order.
+//   k_greedy                  the greedy incumbent (solvers.hpp:282-322): a
+//                             sequential walk, each step a block-wide first-max
+//                             over the candidates compatible with the status.
+//   k_evaluate                evaluate_plan(verify=false) (evaluate.hpp:153-210)
+//                             for plans x traces, one thread per pair, folding
+//                             step-major / model-minor exactly like the reference.
+//
+// Candidates are the distinct (signature, placement) pairs: every option of a
+// pair has the same capabilities and masks, hence the same cell values, and the
+// first-max rule picks its smallest option index — the candidate's index.
+#include <cfloat>
+
+#include "ctx.cuh"
+
+namespace mgs {
+namespace {
+
+struct Recv {
+  const double* v;  // [M][S] forecast as double (static_cast in the reference)
+  int S;
+  __device__ double operator()(int m, int s) const { return v[m * S + s]; }
+};
+
+__global__ void k_ub_best(DevSpace sp, HostTables t, Recv recv, double* best_out) {
+  const int s = blockIdx.x;
+  double acc_max[KM];
+  for (int m = 0; m < KM; ++m) acc_max[m] = t.pre[m] > t.post[m] ? t.pre[m] : t.post[m];
+  double best = 0.0;  // reference starts at 0.0 and uses std::max
+  for (int p = threadIdx.x; p < sp.P; p += blockDim.x) {
+    double v = 0.0;
+    for (int m = 0; m < t.M; ++m) v = dadd(v, dmul(acc_max[m], thr_of(recv(m, s), sp.pl_cap[p * KM + m])));
+    best = v > best ? v : best;
+  }
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    double x = __shfl_down_sync(0xffffffffu, best, o);
+    best = x > best ? x : best;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    best = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      double x = __shfl_down_sync(0xffffffffu, best, o);
+      best = x > best ? x : best;
+    }
+    if (threadIdx.x == 0) best_out[s] = best;
+  }
+}
+
+__global__ void k_ub_suffix(const double* best, int S, double* ub) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  ub[S] = 0.0;
+  for (int s = S - 1; s >= 0; --s) ub[s] = dadd(ub[s + 1], best[s]);
+}
+
+// Single-CTA sequential greedy walk.
+__global__ void __launch_bounds__(1024) k_greedy(DevSpace sp, HostTables t, Recv recv, int has_initial,
+                                                 double* incumbent, int32_t* greedy) {
+  __shared__ double s_v[32];
+  __shared__ int s_oi[32], s_ci[32];
+  __shared__ int s_state[KM];
+  __shared__ uint64_t s_ids;
+  __shared__ double s_value;
+  __shared__ int s_alive, s_best_ci;
+  const Codec codec{t.S};
+  if (threadIdx.x == 0) {
+    for (int m = 0; m < KM; ++m) s_state[m] = 0;
+    s_ids = sp.pl_ids[sp.root_pid];
+    s_value = 0.0;
+    s_alive = 1;
+  }
+  __syncthreads();
+  for (int s = 0; s < t.S; ++s) {
+    const bool charge = s > 0 || has_initial;
+    const double value = s_value;
+    const uint64_t cur_ids = s_ids;
+    int st[KM];
+    for (int m = 0; m < KM; ++m) st[m] = s_state[m];
+    double bv = -DBL_MAX;
+    int boi = INT_MAX, bci = -1;
+    for (int ci = threadIdx.x; ci < sp.n_cand; ci += blockDim.x) {
+      const int sig = sp.cand_sig[ci];
+      bool ok = true;
+      for (int m = 0; m < t.M && ok; ++m) {
+        const int ns = codec.advance(t.rt[m], st[m], (sig >> (3 * m)) & 7, s);
+        ok = ns >= 0 && !(ns == 0 && (t.min_rt[m] < 0 || s + 1 + t.min_rt[m] > t.S));
+      }
+      if (!ok) continue;
+      const int p = sp.cand_pid[ci];
+      const uint64_t ids = sp.pl_ids[p];
+      double v = value;
+      for (int m = 0; m < t.M; ++m) {
+        const double acc = st[m] == Codec::done() ? t.post[m] : t.pre[m];
+        const bool changed = charge && field16(cur_ids, m) != field16(ids, m);
+        const double eff = eff_cap(sp.pl_cap[p * KM + m], changed ? t.loss[m] : 0.0);
+        v = dadd(v, dmul(thr_of(recv(m, s), eff), acc));
+      }
+      const int oi = sp.cand_oi[ci];
+      if (bci < 0 || v > bv || (v == bv && oi < boi)) {
+        bv = v;
+        boi = oi;
+        bci = ci;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_down_sync(0xffffffffu, bv, o);
+      int ooi = __shfl_down_sync(0xffffffffu, boi, o);
+      int oci = __shfl_down_sync(0xffffffffu, bci, o);
+      if (oci >= 0 && (bci < 0 || ov > bv || (ov == bv && ooi < boi))) {
+        bv = ov;
+        boi = ooi;
+        bci = oci;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_v[threadIdx.x >> 5] = bv;
+      s_oi[threadIdx.x >> 5] = boi;
+      s_ci[threadIdx.x >> 5] = bci;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double v = -DBL_MAX;
+      int oi = INT_MAX, ci = -1;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        if (s_ci[w] >= 0 && (ci < 0 || s_v[w] > v || (s_v[w] == v && s_oi[w] < oi))) {
+          v = s_v[w];
+          oi = s_oi[w];
+          ci = s_ci[w];
+        }
+      }
+      s_best_ci = ci;
+      if (ci < 0) {
+        s_alive = 0;
+        greedy[s] = -1;
+      } else {
+        greedy[s] = oi;
+        s_value = v;
+        const int sig = sp.cand_sig[ci];
+        for (int m = 0; m < t.M; ++m) s_state[m] = codec.advance(t.rt[m], s_state[m], (sig >> (3 * m)) & 7, s);
+        s_ids = sp.pl_ids[sp.cand_pid[ci]];
+      }
+    }
+    __syncthreads();
+    if (!s_alive) break;
+  }
+  if (threadIdx.x == 0) {
+    bool all_done = s_alive != 0;
+    for (int m = 0; m < t.M; ++m) all_done = all_done && s_state[m] == Codec::done();
+    *incumbent = all_done ? s_value : -INFINITY;
+  }
+}
+
+}  // namespace
+
+void goodput_reductions(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* d_recv, double* d_ub,
+                        double* d_incumbent, int32_t* d_greedy) {
+  const HostTables& t = pr.t;
+  Recv recv{d_recv, t.S};
+  double* best = c.buf<double>("ub_best", t.S);
+  k_ub_best<<<t.S, 256, 0, c.stream>>>(sp, t, recv, best);
+  k_ub_suffix<<<1, 32, 0, c.stream>>>(best, t.S, d_ub);
+  k_greedy<<<1, 1024, 0, c.stream>>>(sp, t, recv, pr.has_initial, d_incumbent, d_greedy);
+  c.kernel_launches += 3;
+  MGS_CUDA_OK(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// evaluate_plan(verify=false) batch: thread per (plan, trace).
+__global__ void k_evaluate(DevSpace sp, HostTables t, const int32_t* plans, int n_plans, const int64_t* arrivals,
+                           int n_traces, int has_initial, uint4 init_lo, double* total, double* thr_out) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)n_plans * n_traces) return;
+  const int i = static_cast<int>(idx / n_traces), j = static_cast<int>(idx % n_traces);
+  const int S = t.S, M = t.M;
+  const int32_t* plan = plans + (size_t)i * S;
+  const int64_t* arr = arrivals + (size_t)j * M * S;
+  const uint32_t init[KM] = {init_lo.x, init_lo.y, init_lo.z, init_lo.w};
+  int finish_after[KM];
+  for (int m = 0; m < M; ++m) {  // Eq-12: finished strictly before step s (evaluate.hpp:174-179)
+    finish_after[m] = INT_MAX;
+    for (int s = S - 1; s >= 0; --s)
+      if (sp.opt_rsize[plan[s] * KM + m] > 0) {
+        finish_after[m] = s + 1;
+        break;
+      }
+  }
+  double tot = 0.0;
+  for (int s = 0; s < S; ++s) {
+    const int o = plan[s];
+    for (int m = 0; m < M; ++m) {
+      const uint32_t mask = sp.opt_mask[o * KM + m];
+      const bool changed = s == 0 ? (has_initial && mask != init[m]) : (mask != sp.opt_mask[plan[s - 1] * KM + m]);
+      const double eff = eff_cap(sp.opt_cap[o * KM + m], changed ? t.loss[m] : 0.0);
+      const double thr = thr_of(static_cast<double>(arr[m * S + s]), eff);
+      const double acc = s >= finish_after[m] ? t.post[m] : t.pre[m];
+      tot = dadd(tot, dmul(thr, acc));
+      if (thr_out) thr_out[(idx * S + s) * M + m] = thr;
+    }
+  }
+  total[idx] = tot;
+}
+
+void evaluate_batch(Ctx& c, const Prepared& pr, const DevSpace& sp, const int32_t* d_plans, int n_plans,
+                    const int64_t* d_arr, int n_traces, double* d_total, double* d_thr) {
+  const long long n = (long long)n_plans * n_traces;
+  uint4 init{pr.init_mask[0], pr.init_mask[1], pr.init_mask[2], pr.init_mask[3]};
+  k_evaluate<<<ceil_div(n, 128), 128, 0, c.stream>>>(sp, pr.t, d_plans, n_plans, d_arr, n_traces, pr.has_initial,
+                                                     init, d_total, d_thr);
+  c.kernel_launches += 1;
+  MGS_CUDA_OK(cudaGetLastError());
+}
+
+}  // namespace mgs

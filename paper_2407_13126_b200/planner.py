@@ -1,0 +1,131 @@
+"""Python host API over the C ABI — the same operations as the reference's C++
+planner API (solve_dp, evaluate_plan, Space::build, ...), on B200.
+
+Every call goes through lib/libmigsim_b200.so (CUDA). There is no CPU path: if
+the library or a GPU is missing the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import capi
+from .scenario import Problem
+
+
+class Planner:
+    """One device context (mgs_open). Not shared across threads."""
+
+    def __init__(self, device: int = 0):
+        self.lib = capi.load()
+        h = C.c_void_p()
+        st = self.lib.mgs_open(device, C.byref(h))
+        if st != 0:
+            raise capi.PlannerError(st)
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            self.lib.mgs_close(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- engine::Space::build -------------------------------------------------
+    def enumerate(self, problem: Problem):
+        n = C.c_int64()
+        err = capi.empty_error()
+        lat, tab = C.byref(problem.c.lattice), C.byref(problem.c.tables)
+        st = self.lib.mgs_enumerate(self.h, lat, tab, C.byref(n), 0, None, None, None, None, None, C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        N = n.value
+        out = dict(config=np.zeros(N, np.int32), labels=np.zeros((N, capi.MAX_SLOTS), np.int8),
+                   mask=np.zeros((N, 4), np.uint32), cap=np.zeros((N, 4), np.float64),
+                   rsize=np.zeros((N, 4), np.int8))
+        st = self.lib.mgs_enumerate(self.h, lat, tab, C.byref(n), N, capi.ptr(out["config"], C.c_int32),
+                                    capi.ptr(out["labels"], C.c_int8), capi.ptr(out["mask"], C.c_uint32),
+                                    capi.ptr(out["cap"], C.c_double), capi.ptr(out["rsize"], C.c_int8), C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        return out
+
+    # -- ub_suffix + greedy incumbent ------------------------------------------
+    def goodput_table(self, problem: Problem):
+        ub = np.zeros(problem.S + 1, np.float64)
+        inc = C.c_double()
+        greedy = np.zeros(problem.S, np.int32)
+        err = capi.empty_error()
+        st = self.lib.mgs_goodput_table(self.h, problem.byref(), capi.ptr(ub, C.c_double), C.byref(inc),
+                                        capi.ptr(greedy, C.c_int32), C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        return ub, inc.value, greedy
+
+    # -- solve_dp ---------------------------------------------------------------
+    def solve_window(self, problem: Problem):
+        """Returns (options[S], config[S], labels[S][8], objective, stats)."""
+        S = problem.S
+        opt = np.zeros(S, np.int32)
+        cfg = np.zeros(S, np.int32)
+        lab = np.zeros((S, capi.MAX_SLOTS), np.int8)
+        obj = C.c_double()
+        stats = capi.mgs_stats()
+        err = capi.empty_error()
+        st = self.lib.mgs_solve_window(self.h, problem.byref(), capi.ptr(opt, C.c_int32), capi.ptr(cfg, C.c_int32),
+                                       capi.ptr(lab, C.c_int8), C.byref(obj), C.byref(stats), C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        return opt, cfg, lab, obj.value, stats.as_dict()
+
+    def solve_batch(self, problems):
+        n = len(problems)
+        s_max = max(p.S for p in problems)
+        arr = (capi.mgs_problem * n)(*[p.c for p in problems])
+        opts = np.full((n, s_max), -1, np.int32)
+        obj = np.zeros(n, np.float64)
+        status = np.zeros(n, np.int32)
+        stats = (capi.mgs_stats * n)()
+        errs = (capi.mgs_error * n)()
+        st = self.lib.mgs_solve_batch(self.h, arr, n, s_max, capi.ptr(opts, C.c_int32), capi.ptr(obj, C.c_double),
+                                      capi.ptr(status, C.c_int32), stats, errs)
+        if st:
+            raise capi.PlannerError(st)
+        return opts, obj, status, [s.as_dict() for s in stats], errs
+
+    # -- evaluate_plan(verify=false) batch ---------------------------------------
+    def evaluate_batch(self, problem: Problem, plans, arrivals, with_throughput=False):
+        plans = np.ascontiguousarray(plans, dtype=np.int32).reshape(-1, problem.S)
+        arrivals = np.ascontiguousarray(arrivals, dtype=np.int64).reshape(-1, problem.M, problem.S)
+        n_p, n_t = plans.shape[0], arrivals.shape[0]
+        total = np.zeros((n_p, n_t), np.float64)
+        thr = np.zeros((n_p, n_t, problem.S, problem.M), np.float64) if with_throughput else None
+        err = capi.empty_error()
+        st = self.lib.mgs_evaluate_batch(self.h, problem.byref(), capi.ptr(plans, C.c_int32), n_p,
+                                         capi.ptr(arrivals, C.c_int64), n_t, capi.ptr(total, C.c_double),
+                                         capi.ptr(thr, C.c_double) if thr is not None else None, C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        return (total, thr) if with_throughput else total
+
+
+def encode(config, labels, nslots):
+    """Space::encode (space.hpp:231-251): per step the configuration index then
+    that configuration's per-slot labels."""
+    out = []
+    for c, lab in zip(config, labels):
+        out.append(int(c))
+        out += [int(x) for x in lab[:nslots[int(c)]]]
+    return out

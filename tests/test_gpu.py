@@ -1,0 +1,180 @@
+"""GPU parity: the sm_100a planner (through the C ABI) against the reference.
+
+Bar (BASELINE.json north_star): bit-exact plans, option / placement indices and
+SLO-attained counts; objective Goodput bit-exact here (tolerance stated by the
+spec: 1e-6 relative — we require equality of the IEEE bits, which is stricter).
+"""
+import numpy as np
+import pytest
+
+import binding as B
+from golden_util import bits, nslots
+from paper_2407_13126_b200 import capi, planner
+from paper_2407_13126_b200 import scenario as SC
+
+pytestmark = pytest.mark.gpu
+
+OBJ_RTOL = 1e-6  # north_star tolerance; the checks below are stricter (bitwise)
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    with planner.Planner(0) as pl:
+        yield pl
+
+
+def gpu_solve(pl, path, initial=None, budget=4_000_000):
+    sc = SC.load_scenario(path)
+    p = SC.Problem(sc, 0, initial=initial, state_budget=budget)
+    opt, cfg, lab, obj, stats = pl.solve_window(p)
+    enc = planner.encode(cfg, lab, nslots(sc))
+    total, thr = pl.evaluate_batch(p, opt[None, :], p.forecast[None], with_throughput=True)
+    return p, opt, enc, obj, thr[0, 0].reshape(-1), stats, total[0, 0]
+
+
+def check(golden_plan, enc, obj, thr):
+    assert enc == golden_plan["encode"]
+    assert bits(obj) == golden_plan["obj"]
+    assert abs(obj - float(golden_plan["objective"])) <= OBJ_RTOL * max(1.0, abs(obj))
+    assert [bits(x) for x in thr] == golden_plan["thr"]
+
+
+def test_library_loads_and_reports_version():
+    lib = capi.load()
+    assert b"sm_100a" in lib.mgs_version()
+
+
+def test_enumeration_matches_oracle(gpu, golden_dir):
+    cases = golden_dir["random"][:40] + golden_dir["c1"] + golden_dir["kat"]
+    for stem, path, g in cases:
+        sc = SC.load_scenario(path)
+        p = SC.Problem(sc, 0)
+        try:
+            want = B.enumerate_options(p)
+        except capi.PlannerError:
+            continue
+        got = gpu.enumerate(p)
+        for k in ("config", "labels", "mask", "rsize"):
+            assert np.array_equal(got[k], want[k]), (stem, k)
+        assert got["cap"].tobytes() == want["cap"].tobytes(), stem
+
+
+def test_goodput_table_matches_oracle(gpu, golden_dir):
+    for stem, path, g in golden_dir["random"][:60] + golden_dir["c1"]:
+        sc = SC.load_scenario(path)
+        for initial in (None, [tuple(x) for x in g.get("chain", {}).get("initial", [])] or None):
+            p = SC.Problem(sc, 0, initial=initial)
+            ub, inc, greedy = gpu.goodput_table(p)
+            ub_o, inc_o, greedy_o = B.goodput_table(p)
+            assert ub.tobytes() == ub_o.tobytes(), stem
+            assert bits(inc) == bits(inc_o), stem
+            if np.isfinite(inc_o):
+                assert np.array_equal(greedy, greedy_o), stem
+
+
+def test_solve_random_corpus(gpu, golden_dir):
+    for stem, path, g in golden_dir["random"]:
+        p, opt, enc, obj, thr, stats, total = gpu_solve(gpu, path)
+        check(g["dp"], enc, obj, thr)
+        assert bits(total) == bits(obj)
+
+
+def test_solve_random_corpus_chained(gpu, golden_dir):
+    for stem, path, g in golden_dir["random"]:
+        ch = g["chain"]
+        init = [tuple(x) for x in ch["initial"]]
+        if "error" in ch["dp"]:
+            with pytest.raises(capi.PlannerError) as e:
+                gpu_solve(gpu, path, initial=init)
+            assert e.value.code == ch["dp"]["error"]
+            continue
+        p, opt, enc, obj, thr, stats, total = gpu_solve(gpu, path, initial=init)
+        check(ch["dp"], enc, obj, thr)
+
+
+def test_solve_c1_fixtures(gpu, golden_dir):
+    for stem, path, g in golden_dir["c1"]:
+        p, opt, enc, obj, thr, stats, total = gpu_solve(gpu, path)
+        check(g["dp"], enc, obj, thr)
+        assert stats["options"] == g["options"]
+        if "chain" in g:
+            init = [tuple(x) for x in g["chain"]["initial"]]
+            _, _, enc2, obj2, thr2, _, _ = gpu_solve(gpu, path, initial=init)
+            check(g["chain"]["dp"], enc2, obj2, thr2)
+
+
+def test_c1_counters_match_oracle(gpu, golden_dir):
+    """Work counters (transitions, frontier sizes) equal the restatement's."""
+    for stem, path, g in golden_dir["c1"]:
+        if int(stem.split("_")[1][1:]) > 60:
+            continue
+        sc = SC.load_scenario(path)
+        p = SC.Problem(sc, 0)
+        _, _, _, _, stats = gpu.solve_window(p)
+        _, _, ostats = B.solve_window(p)
+        for k in ("options", "candidates", "transitions_ref", "transitions", "frontier_total", "frontier_peak"):
+            assert stats[k] == ostats[k], (stem, k, stats[k], ostats[k])
+
+
+def test_known_answers_and_errors(gpu, golden_dir):
+    kat = {stem: (path, g) for stem, path, g in golden_dir["kat"]}
+    _, _, enc, obj, _, _, _ = gpu_solve(gpu, kat["worked_example"][0])
+    assert obj == 12.5 and enc == kat["worked_example"][1]["dp"]["encode"]
+    _, _, _, obj, _, _, _ = gpu_solve(gpu, kat["zero_trace"][0])
+    assert obj == 0.0
+    _, _, enc, _, _, _, _ = gpu_solve(gpu, kat["forced"][0])
+    assert enc == kat["forced"][1]["dp"]["encode"]
+    _, _, enc, obj, thr, _, _ = gpu_solve(gpu, kat["small_two_model"][0])
+    check(kat["small_two_model"][1]["dp"], enc, obj, thr)
+    for name in ("no_coexistence", "deployment_floor"):
+        with pytest.raises(capi.PlannerError) as e:
+            gpu_solve(gpu, kat[name][0])
+        assert e.value.code == kat[name][1]["expect_error"]
+    with pytest.raises(capi.PlannerError) as e:
+        gpu_solve(gpu, kat["small_two_model"][0], budget=1)
+    assert e.value.code == "planner.state-budget"
+    assert "states" in e.value.message
+    assert e.value.message == kat["small_two_model"][1]["budget1"]["message"]
+
+
+def test_forecast_length_error(gpu, golden_dir):
+    stem, path, g = golden_dir["kat"][0]
+    sc = SC.load_scenario(golden_dir["c1"][0][1])
+    p = SC.Problem(sc, 0, forecast=np.zeros((2, sc.window_size + 1), np.int64))
+    with pytest.raises(capi.PlannerError) as e:
+        gpu.solve_window(p)
+    assert e.value.code == "input.forecast"
+
+
+def test_evaluate_batch_matches_oracle(gpu, golden_dir):
+    rng = np.random.default_rng(7)
+    for stem, path, g in golden_dir["c1"][:2] + golden_dir["random"][:20]:
+        sc = SC.load_scenario(path)
+        p = SC.Problem(sc, 0)
+        n_opt = len(B.enumerate_options(p)["config"])
+        plans = rng.integers(0, n_opt, size=(5, p.S)).astype(np.int32)
+        traces = rng.integers(0, 300, size=(7, p.M, p.S)).astype(np.int64)
+        total, thr = gpu.evaluate_batch(p, plans, traces, with_throughput=True)
+        for i in range(plans.shape[0]):
+            for j in range(traces.shape[0]):
+                t_o, thr_o = B.evaluate(p, plans[i], traces[j])
+                assert bits(total[i, j]) == bits(t_o)
+                assert thr[i, j].reshape(-1).tobytes() == thr_o.tobytes()
+
+
+def test_solve_batch_equals_single(gpu, golden_dir):
+    cases = golden_dir["c1"][:3]
+    probs = [SC.Problem(SC.load_scenario(path), 0) for _, path, _ in cases]
+    opts, obj, status, stats, errs = gpu.solve_batch(probs)
+    for i, (stem, path, g) in enumerate(cases):
+        assert status[i] == 0
+        o1, _, _, obj1, _ = gpu.solve_window(probs[i])
+        assert np.array_equal(opts[i, :probs[i].S], o1)
+        assert bits(obj[i]) == bits(obj1) == g["dp"]["obj"]
+
+
+def test_deterministic_repeat(gpu, golden_dir):
+    stem, path, g = golden_dir["c1"][0]
+    a = gpu_solve(gpu, path)
+    b = gpu_solve(gpu, path)
+    assert a[2] == b[2] and bits(a[3]) == bits(b[3])
