@@ -1,0 +1,297 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Goodput planner hot path (BASELINE.json metric).
+
+One step = one per-window reconfiguration decision (solve_dp) on a config-1
+window: 2 tenants, A100 7-slice lattice, S = 200 one-second slots, Poisson
+arrivals (synthetic). Metric: candidate plans scored per
+second, where one candidate plan = one reference DP transition
+(solvers.hpp:424-469; 154,202,318 for the seed-100001 window).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU): weak scaling — every rank plans its own
+window (seed 100001 + rank) with no data-path collective; after each step the
+per-shard best (objective, rank) is combined with one NCCL all-reduce(max).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+SAMPLE = os.path.join(ROOT, "tests", "golden", "c1", "c1_S60_100003.scn")  # bounded CPU sample
+METRIC = "candidate plans scored/sec (GB/s vs HBM roofline); per-window decision latency ms"
+UNIT = "candidate plans/s"
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), "--query-gpu=" + q, "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def hbm_peak():
+    try:
+        d = json.load(open(PEAKS))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def c1_problem(seed, directory, pinned=False):
+    from paper_2407_13126_b200 import scenario as SC
+    from paper_2407_13126_b200 import workloads as W
+    spec = W.c1_spec(seed)
+    path = W.write_scenario(spec, directory, "c1_%d" % seed)
+    sc = SC.load_scenario(path)
+    p = SC.Problem(sc, 0)
+    if pinned:  # forecast in pinned host memory for the end-to-end leg
+        import torch
+        t = torch.from_numpy(p.forecast.copy()).pin_memory()
+        p._pinned = t
+        import ctypes as C
+        p.c.forecast = C.cast(t.data_ptr(), C.POINTER(C.c_int64))
+    return p
+
+
+def reference_cpu(steps, warmup, workers):
+    """The unmodified reference solve_dp on the bounded sample (oracle/_ref)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import binding  # noqa: E402  (checker / CPU-baseline only)
+    times = []
+    for k in range(warmup + steps):
+        secs, obj, enc = binding.ref_solve_inproc(SAMPLE, 0, workers)
+        if k >= warmup:
+            times.append(secs)
+    return times
+
+
+SAMPLE_TRANSITIONS = None
+
+
+def sample_transitions():
+    """Reference-defined transition count of the bounded sample (from the golden
+    counters of the restatement, which the GPU tests pin to the device's)."""
+    global SAMPLE_TRANSITIONS
+    if SAMPLE_TRANSITIONS is None:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import binding
+        from paper_2407_13126_b200 import scenario as SC
+        p = SC.Problem(SC.load_scenario(SAMPLE), 0)
+        _, _, st = binding.solve_window(p)
+        SAMPLE_TRANSITIONS = st["transitions_ref"]
+    return SAMPLE_TRANSITIONS
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    workers = os.cpu_count() or 1
+    times = reference_cpu(args.steps, args.warmup, workers)
+    tr = sample_transitions()
+    value = tr * len(times) / sum(times)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "config-1-shaped window, S=60 (bounded sample of the S=200 window)",
+                       "sample": os.path.relpath(SAMPLE, ROOT), "tenants": 2, "lattice": "a100 7-slice",
+                       "parallelism": "host threads (SolveOptions::workers=%d)" % workers},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
+                             "sample": "reference solve_dp on the S=60 config-1-shaped window, %d transitions" % tr},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2407_13126_b200 import planner
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    work = tempfile.mkdtemp(prefix="mgs_bench_")
+    seed = 100001 + rank
+    prob = c1_problem(seed, work)
+    prob_e2e = c1_problem(seed, work, pinned=True)
+    stream = torch.cuda.Stream()
+    pl = planner.Planner(local)
+    pl.lib.mgs_set_stream(pl.h, stream.cuda_stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    from paper_2407_13126_b200 import shard
+
+    def combine(obj):
+        # per-shard best (objective, shard) -> NCCL all-reduce(max): the only collective
+        if world > 1:
+            shard.combine_best(obj, rank, world, device="cuda")
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            opt, cfg, lab, obj, st = pl.solve_window(prob)
+            combine(obj)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks = Clocks(local)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        stats = []
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations (outside the event pair)
+            ev[k][0].record(stream)
+            opt, cfg, lab, obj, st = pl.solve_window(prob)
+            combine(obj)
+            ev[k][1].record(stream)
+            stats.append(st)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clk = clocks.stop()
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+
+        # end-to-end through the C ABI with host buffers (H2D forecast from
+        # pinned memory, D2H plan + objective inside every step)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            opt_e, cfg_e, lab_e, obj_e, st_e = pl.solve_window(prob_e2e)
+            combine(obj_e)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            dist.barrier()
+
+    tr_window = stats[-1]["transitions_ref"]
+    dev_s = sum(step_ms) / 1e3
+    trans_ms = sum(s["phase_ms"]["transitions"] for s in stats)
+    trans_bytes = sum(s["transition_bytes"] for s in stats)
+    launches = sum(s["kernel_launches"] for s in stats)
+    if world > 1:
+        t = torch.tensor([dev_s, e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s, e2e_s = t.tolist()
+        n = torch.tensor([float(tr_window)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(n, op=dist.ReduceOp.SUM)
+        total_tr = n.item() * args.steps
+    else:
+        total_tr = float(tr_window) * args.steps
+    if rank != 0:
+        pl.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # parity check of the timed plan (seed 100001 golden from the reference)
+    g = None
+    gpath = os.path.join(ROOT, "tests", "golden", "c1", "c1_golden.json")
+    if os.path.exists(gpath):
+        g = json.load(open(gpath)).get("c1_S200_%d" % seed)
+    peak, peak_kind = hbm_peak()
+    achieved = trans_bytes / (trans_ms / 1e3) / 1e9 if trans_ms > 0 else 0.0
+    phases = {}
+    for s in stats:
+        for k, v in s["phase_ms"].items():
+            phases[k] = phases.get(k, 0.0) + v / len(stats)
+    line = {
+        "metric": METRIC, "value": total_tr / dev_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config-1 window: 2 ResNet-18 tenants, A100 7-slice lattice (12 configs, 9864 options), "
+                               "S=200 x 1 s slots, Poisson lambda 120/150, psi 0.5",
+                   "seed": "100001+rank", "transitions_per_window": tr_window, "parallelism": "dp%d" % world,
+                   "l2": "flushed between timed steps (256 MiB write)"},
+        "decision_latency_ms": 1e3 * dev_s / args.steps,
+        "phase_ms_per_window": phases,
+        "e2e": {"value": total_tr / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": int(prob_e2e.forecast.nbytes + prob_e2e.slot_offset.nbytes +
+                                          prob_e2e.slot_size.nbytes + prob_e2e.slot_start.nbytes),
+                "d2h_bytes_per_step": int(prob_e2e.S * (4 + 4 + 8) + 8),
+                "decision_latency_ms": 1e3 * e2e_s / args.steps},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": "k_trans_small/k_trans_big (transition phase)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None, "traffic": None, "peak_kind": peak_kind,
+                     "bytes_per_window": trans_bytes // max(1, len(stats))},
+        "clocks": clk,
+        "objective": obj,
+    }
+    if g:
+        line["parity"] = {"golden": "c1_S200_%d" % seed, "objective_bits_equal": g["dp"]["obj"] == bits(obj)}
+    if world == 1 and not args.no_cpu_baseline:
+        times = reference_cpu(1, 0, 1)
+        tr = sample_transitions()
+        line["cpu_baseline"] = {"value": tr / times[0], "unit": UNIT, "cores": 1, "kind": "reference",
+                                "sample": "reference solve_dp, workers=1, S=60 config-1-shaped window "
+                                          "(tests/golden/c1/c1_S60_100003.scn, %d transitions, %.2f s)" % (tr, times[0])}
+    print(json.dumps(line), flush=True)
+    pl.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def bits(x):
+    import struct
+    return "%016x" % struct.unpack("<Q", struct.pack("<d", float(x)))[0]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

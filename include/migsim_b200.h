@@ -106,6 +106,16 @@ typedef struct {
   uint64_t frontier_total;   /* sum over steps of surviving states */
   uint64_t frontier_peak;
   double device_ms;          /* device time of the solve (CUDA events) */
+  uint64_t kernel_launches;  /* launches of this library's own kernels */
+  /* per-phase device time (CUDA events on the solve stream), ms:
+   * [0] enumeration + tables  [1] Goodput reductions  [2] unit expansion
+   * [3] transitions           [4] merge/band/dominance [5] compaction
+   * [6] lex ranks             [7] terminal + backtrack + objective */
+  double phase_ms[8];
+  /* algorithmic bytes of the transition kernels over the solve: every
+   * frontier state read once (value, rank, ids: 20 B), every candidate
+   * descriptor read once (8 B) and every candidate record written (29 B) */
+  uint64_t transition_bytes;
 } mgs_stats;
 
 typedef struct mgs_ctx mgs_ctx;
@@ -114,6 +124,10 @@ MGS_API int mgs_open(int device, mgs_ctx** out);
 MGS_API void mgs_close(mgs_ctx* ctx);
 MGS_API const char* mgs_status_code(int status);
 MGS_API const char* mgs_version(void);
+/* Run this context's work on a caller-provided cudaStream_t (e.g. a framework's
+ * current stream, so the caller's events time it). NULL restores the
+ * context's own stream. */
+MGS_API int mgs_set_stream(mgs_ctx* ctx, void* stream);
 
 /* Candidate enumeration (Space::build). *n_options receives |O|. Optional
  * host copies (pass NULL to skip) hold min(cap, |O|) options in lex order:

@@ -63,10 +63,16 @@ class mgs_problem(C.Structure):
 class mgs_stats(C.Structure):
     _fields_ = [("options", C.c_uint64), ("candidates", C.c_uint64), ("transitions_ref", C.c_uint64),
                 ("transitions", C.c_uint64), ("frontier_total", C.c_uint64), ("frontier_peak", C.c_uint64),
-                ("device_ms", C.c_double)]
+                ("device_ms", C.c_double), ("kernel_launches", C.c_uint64), ("phase_ms", C.c_double * 8),
+                ("transition_bytes", C.c_uint64)]
+
+    PHASES = ("enumerate", "goodput", "units", "transitions", "merge_band_dominance", "compaction", "ranks",
+              "terminal")
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "phase_ms"}
+        d["phase_ms"] = dict(zip(self.PHASES, list(self.phase_ms)))
+        return d
 
 
 class PlannerError(RuntimeError):
@@ -100,6 +106,7 @@ def load():
     P = C.POINTER
     lib.mgs_open.argtypes = [C.c_int, P(C.c_void_p)]
     lib.mgs_close.argtypes = [C.c_void_p]
+    lib.mgs_set_stream.argtypes = [C.c_void_p, C.c_void_p]
     lib.mgs_version.restype = C.c_char_p
     lib.mgs_status_code.restype = C.c_char_p
     lib.mgs_enumerate.argtypes = [C.c_void_p, P(mgs_lattice), P(mgs_tables), P(C.c_int64), C.c_int64,
@@ -117,7 +124,7 @@ def load():
     return lib
 
 
-EXPORTED_SYMBOLS = ["mgs_open", "mgs_close", "mgs_status_code", "mgs_version", "mgs_enumerate",
+EXPORTED_SYMBOLS = ["mgs_open", "mgs_close", "mgs_status_code", "mgs_version", "mgs_set_stream", "mgs_enumerate",
                     "mgs_goodput_table", "mgs_solve_window", "mgs_solve_batch", "mgs_evaluate_batch"]
 
 

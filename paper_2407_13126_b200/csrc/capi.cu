@@ -56,7 +56,7 @@ mgs::Prepared prepare_problem(const mgs_problem& p) {
   return pr;
 }
 
-__global__ void k_to_double(const int64_t* in, double* out, int n) {
+__global__ void k_to_double(const int64_t* in, double* out, int n) {  // static_cast<double>(count)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = static_cast<double>(in[i]);
 }
@@ -73,18 +73,24 @@ double* upload_forecast(Ctx& c, const mgs_problem& p, int M, int S) {
                                   cudaMemcpyHostToDevice, c.stream));
   }
   k_to_double<<<mgs::ceil_div(M * S, 256), 256, 0, c.stream>>>(d_i, d_f, M * S);
+  ++c.kernel_launches;
   return d_f;
 }
 
 void solve_one(Ctx& c, const mgs_problem& p, int32_t* out_option, int32_t* out_config, int8_t* out_labels,
                double* out_objective, mgs_stats* stats) {
   MGS_CUDA_OK(cudaEventRecord(c.ev0, c.stream));
+  c.timer.reset();
+  c.open_phase = -1;
+  c.kernel_launches = 0;
+  c.phase(0);
   mgs::Prepared pr = prepare_problem(p);
   mgs::DevSpace sp;
   mgs::build_space(c, p.lattice, pr, sp);
   mgs::precheck_space(c, p.lattice, pr, sp);  // throw_if_infeasible(precheck_scenario) first (solvers.hpp:245)
   const int M = pr.t.M, S = pr.t.S;
   if (p.forecast_len != S) throw PlanFail{MGS_ERR_INPUT_FORECAST, "forecast horizon != window size"};  // :250-252
+  c.phase(1);
   double* d_recv = upload_forecast(c, p, M, S);
   double* d_ub = c.buf<double>("ub_suffix", S + 1);
   double* d_inc = c.buf<double>("incumbent", 1);
@@ -93,6 +99,7 @@ void solve_one(Ctx& c, const mgs_problem& p, int32_t* out_option, int32_t* out_c
   mgs::SolveOut out;
   mgs::solve_dp(c, p, pr, sp, d_recv, d_ub, d_inc, out);
   // objective = evaluate_plan(...).total of the chosen plan, on the device
+  c.phase(7);
   int32_t* d_plan = c.buf<int32_t>("plan_eval", S);
   double* d_total = c.buf<double>("plan_total", 1);
   MGS_CUDA_OK(cudaMemcpyAsync(d_plan, out.options.data(), S * 4, cudaMemcpyHostToDevice, c.stream));
@@ -113,11 +120,14 @@ void solve_one(Ctx& c, const mgs_problem& p, int32_t* out_option, int32_t* out_c
         for (int k = 0; k < MGS_MAX_SLOTS; ++k) out_labels[s * MGS_MAX_SLOTS + k] = lab[static_cast<size_t>(o) * MGS_MAX_SLOTS + k];
     }
   }
+  c.phase(-1);
   MGS_CUDA_OK(cudaEventRecord(c.ev1, c.stream));
   MGS_CUDA_OK(cudaEventSynchronize(c.ev1));
   float ms = 0.f;
   MGS_CUDA_OK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
   out.stats.device_ms = ms;
+  c.phase_totals(out.stats.phase_ms);
+  out.stats.kernel_launches = c.kernel_launches;
   if (out_option)
     for (int s = 0; s < S; ++s) out_option[s] = out.options[s];
   if (out_objective) *out_objective = total;
@@ -160,11 +170,18 @@ int mgs_open(int device, mgs_ctx** out) {
     auto* h = new mgs_ctx();
     h->c.device = device;
     MGS_CUDA_OK(cudaDeviceGetAttribute(&h->c.sm_count, cudaDevAttrMultiProcessorCount, device));
-    MGS_CUDA_OK(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
+    MGS_CUDA_OK(cudaStreamCreateWithFlags(&h->c.own_stream, cudaStreamNonBlocking));
+    h->c.stream = h->c.own_stream;
     MGS_CUDA_OK(cudaEventCreate(&h->c.ev0));
     MGS_CUDA_OK(cudaEventCreate(&h->c.ev1));
     *out = h;
   });
+}
+
+int mgs_set_stream(mgs_ctx* ctx, void* stream) {
+  if (!ctx) return MGS_ERR_ARGUMENT;
+  ctx->c.stream = stream ? static_cast<cudaStream_t>(stream) : ctx->c.own_stream;
+  return MGS_OK;
 }
 
 void mgs_close(mgs_ctx* ctx) {

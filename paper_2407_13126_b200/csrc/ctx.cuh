@@ -100,10 +100,63 @@ struct History {
   }
 };
 
+// Per-phase device timing: event pairs recorded on the solve stream, summed
+// after the solve (no extra synchronisation inside the step loop).
+struct PhaseTimer {
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  struct Rec {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  cudaEvent_t get() {
+    if (next == pool.size()) {
+      cudaEvent_t e;
+      MGS_CUDA_OK(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    return pool[next++];
+  }
+  void reset() {
+    next = 0;
+    recs.clear();
+  }
+  void release() {
+    for (auto e : pool) cudaEventDestroy(e);
+    pool.clear();
+    reset();
+  }
+};
+
 struct Ctx {
   int device = 0;
   int sm_count = 148;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // the stream all work goes to
+  cudaStream_t own_stream = nullptr;  // created by mgs_open
+  PhaseTimer timer;
+  int open_phase = -1;
+  cudaEvent_t open_ev = nullptr;
+  void phase(int p) {  // closes the open phase (if any) and opens p (-1: none)
+    if (open_phase >= 0) {
+      cudaEvent_t e = timer.get();
+      MGS_CUDA_OK(cudaEventRecord(e, stream));
+      timer.recs.push_back({open_phase, open_ev, e});
+    }
+    open_phase = p;
+    if (p >= 0) {
+      open_ev = timer.get();
+      MGS_CUDA_OK(cudaEventRecord(open_ev, stream));
+    }
+  }
+  void phase_totals(double* out8) {
+    for (int i = 0; i < 8; ++i) out8[i] = 0.0;
+    for (auto& r : timer.recs) {
+      float ms = 0.f;
+      MGS_CUDA_OK(cudaEventElapsedTime(&ms, r.a, r.b));
+      out8[r.phase] += ms;
+    }
+  }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::map<std::string, DevBuf> bufs;
   HostPinned pinned;
@@ -120,7 +173,8 @@ struct Ctx {
     if (pinned.p) cudaFreeHost(pinned.p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    if (stream) cudaStreamDestroy(stream);
+    timer.release();
+    if (own_stream) cudaStreamDestroy(own_stream);
   }
 };
 

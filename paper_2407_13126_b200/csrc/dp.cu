@@ -712,16 +712,18 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
     case 3: set_smem(k_trans_big<3>); break;
     default: set_smem(k_trans_big<4>); break;
   }
-  uint64_t ftot = 0, fpeak = 0, tr = 0;
+  uint64_t ftot = 0, fpeak = 0, tr = 0, tbytes = 0;
   int32_t* hcnt = c.pinned.get<int32_t>(8);
 
   for (int s = 0; s < S; ++s) {
     if (cur.n == 0) throw PlanFail{MGS_ERR_INFEASIBLE_JOINT, "no feasible allocation sequence exists for this window"};
     // 1. units
+    c.phase(2);
     const int G = cur.n_groups;
     int32_t* ucount = c.buf<int32_t>("ucount", G);
     int32_t* uoff = c.buf<int32_t>("uoff", G + 1);
     k_unit_count<<<grid_for(G), 256, 0, c.stream>>>(t, sp.sig_nopt, cur, s, ucount);
+    ++c.kernel_launches;
     exclusive_scan_i32(c, ucount, uoff, G);
     const int NU = read_scalar(c, uoff + G);
     if (NU == 0) throw PlanFail{MGS_ERR_INFEASIBLE_JOINT, "no feasible allocation sequence exists for this window"};
@@ -730,6 +732,7 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
     uint64_t* u_ns = c.buf<uint64_t>("u_ns", NU);
     int32_t* u_iota = c.buf<int32_t>("u_iota", NU);
     k_unit_write<<<grid_for(G), 256, 0, c.stream>>>(t, sp.sig_nopt, cur, s, uoff, u_group, u_sig, u_ns, u_iota);
+    ++c.kernel_launches;
     uint64_t* su_ns = c.buf<uint64_t>("su_ns", NU);
     int32_t* perm = c.buf<int32_t>("u_perm", NU);
     {
@@ -768,12 +771,15 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
     int32_t* u_nsid = c.buf<int32_t>("u_nsid", NU);
     int32_t* ns_first = c.buf<int32_t>("ns_first", n_ns + 1);
     k_ns_index<<<grid_for(NU), 256, 0, c.stream>>>(ns_flag, ns_pos, NU, u_nsid, ns_first, n_ns);
+    ++c.kernel_launches;
     int32_t* its_u = c.buf<int32_t>("item_s_unit", nis);
     int32_t* its_c = c.buf<int32_t>("item_s_chunk", nis);
     int32_t* itb_u = c.buf<int32_t>("item_b_unit", nib);
     int32_t* itb_c = c.buf<int32_t>("item_b_chunk", nib);
     k_items<<<grid_for(NU), 256, 0, c.stream>>>(chs, ios, NU, its_u, its_c);
+    ++c.kernel_launches;
     k_items<<<grid_for(NU), 256, 0, c.stream>>>(chb, iob, NU, itb_u, itb_c);
+    ++c.kernel_launches;
 
     StepArgs a{};
     a.sp = sp;
@@ -803,6 +809,8 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
     a.c_live = c.buf<int32_t>("c_live", T);
 
     // 2. transitions
+    c.phase(3);
+    tbytes += static_cast<uint64_t>(cur.n) * 20 + static_cast<uint64_t>(T) * (8 + 29);
     if (nis > 0) {
       StepArgs as = a;
       as.item_unit = its_u;
@@ -815,6 +823,7 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
         case 3: k_trans_small<3><<<grid, 128, 0, c.stream>>>(as); break;
         default: k_trans_small<4><<<grid, 128, 0, c.stream>>>(as); break;
       }
+      ++c.kernel_launches;
     }
     if (nib > 0) {
       StepArgs ab = a;
@@ -828,13 +837,18 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
         case 3: k_trans_big<3><<<nib, kBigThreads, smem, c.stream>>>(ab); break;
         default: k_trans_big<4><<<nib, kBigThreads, smem, c.stream>>>(ab); break;
       }
+      ++c.kernel_launches;
     }
     // 3. merge, band, dominance
+    c.phase(4);
     k_merge<<<grid_for(T), 256, 0, c.stream>>>(a);
+    ++c.kernel_launches;
     unsigned long long* ns_best = c.buf<unsigned long long>("ns_best", n_ns);
     MGS_CUDA_OK(cudaMemsetAsync(ns_best, 0, static_cast<size_t>(n_ns) * 8, c.stream));
     k_band_max<<<grid_for(T), 256, 0, c.stream>>>(a, ns_best);
+    ++c.kernel_launches;
     k_band_mark<<<grid_for(T), 256, 0, c.stream>>>(a, ns_best, band);
+    ++c.kernel_launches;
     if (dominance_ok) {
       const int P1 = sp.P1;
       int32_t* pcount = c.buf<int32_t>("dom_count", P1);
@@ -844,11 +858,15 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
       MGS_CUDA_OK(cudaMemsetAsync(pcount, 0, P1 * 4, c.stream));
       MGS_CUDA_OK(cudaMemsetAsync(pcursor, 0, P1 * 4, c.stream));
       k_dom_count<<<grid_for(T), 256, 0, c.stream>>>(a, pcount);
+      ++c.kernel_launches;
       exclusive_scan_i32(c, pcount, poff, P1);
       k_dom_scatter<<<grid_for(T), 256, 0, c.stream>>>(a, pcount, poff, pcursor, bucket);
+      ++c.kernel_launches;
       k_dom_check<<<ceil_div(P1, 4), 128, 0, c.stream>>>(a, pcount, poff, bucket, P1);
+      ++c.kernel_launches;
     }
     // 4. compaction + groups
+    c.phase(5);
     int32_t* pos = c.buf<int32_t>("live_pos", T + 1);
     exclusive_scan_i32(c, a.c_live, pos, T);
     int32_t* gflag = c.buf<int32_t>("gflag", n_ns);
@@ -856,6 +874,7 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
     int32_t* gs_tmp = c.buf<int32_t>("gs_tmp", n_ns);
     int32_t* gn_tmp = c.buf<int32_t>("gn_tmp", n_ns);
     k_groups<<<grid_for(n_ns), 256, 0, c.stream>>>(a, pos, gflag, gs_tmp, gn_tmp);
+    ++c.kernel_launches;
     exclusive_scan_i32(c, gflag, gpos, n_ns);
     MGS_CUDA_OK(cudaMemcpyAsync(d_tot + 0, pos + T, 4, cudaMemcpyDeviceToDevice, c.stream));
     MGS_CUDA_OK(cudaMemcpyAsync(d_tot + 1, gpos + n_ns, 4, cudaMemcpyDeviceToDevice, c.stream));
@@ -873,13 +892,17 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
     int32_t *hp, *ho;
     hist.take(std::max(n_next, 1), &hp, &ho);
     k_compact<<<grid_for(T), 256, 0, c.stream>>>(a, pos, nx, hp, ho);
+    ++c.kernel_launches;
     k_groups_compact<<<grid_for(n_ns), 256, 0, c.stream>>>(a, gflag, gpos, gs_tmp, gn_tmp, nx);
+    ++c.kernel_launches;
     // 5. dense lex ranks (solvers.hpp:544-548)
+    c.phase(6);
     if (n_next > 0) {
       uint64_t* lex_sorted = c.buf<uint64_t>("lex_sorted", n_next);
       int32_t* iota = c.buf<int32_t>("rank_iota", n_next);
       int32_t* rperm = c.buf<int32_t>("rank_perm", n_next);
       k_iota<<<grid_for(n_next), 256, 0, c.stream>>>(iota, n_next);
+      ++c.kernel_launches;
       int hb = 1;
       while ((1ll << hb) <= cur.n) ++hb;
       const int end_bit = std::min(64, 32 + hb);
@@ -889,6 +912,7 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
       MGS_CUDA_OK(
           cub::DeviceRadixSort::SortPairs(tmp, tb, nx.lex, lex_sorted, iota, rperm, n_next, 0, end_bit, c.stream));
       k_rank<<<grid_for(n_next), 256, 0, c.stream>>>(rperm, n_next, nx.rank);
+      ++c.kernel_launches;
     }
     MGS_CUDA_OK(cudaGetLastError());
     ftot += n_next;
@@ -897,16 +921,19 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
     cur_is_a = !cur_is_a;
   }
   // terminal + backtrack
+  c.phase(7);
   uint64_t all_done = 0;
   for (int m = 0; m < M; ++m) all_done |= static_cast<uint64_t>(Codec::done()) << (16 * m);
   int* d_best = c.buf<int>("best_idx", 1);
   k_terminal<<<1, 1024, 0, c.stream>>>(cur, all_done, d_best);
+  ++c.kernel_launches;
   int32_t** d_hp = c.buf<int32_t*>("hist_parent_ptrs", S);
   int32_t** d_ho = c.buf<int32_t*>("hist_option_ptrs", S);
   MGS_CUDA_OK(cudaMemcpyAsync(d_hp, hist.parent.data(), S * sizeof(void*), cudaMemcpyHostToDevice, c.stream));
   MGS_CUDA_OK(cudaMemcpyAsync(d_ho, hist.option.data(), S * sizeof(void*), cudaMemcpyHostToDevice, c.stream));
   int32_t* d_chosen = c.buf<int32_t>("chosen", S);
   k_backtrack<<<1, 32, 0, c.stream>>>(d_hp, d_ho, S, d_best, d_chosen);
+  ++c.kernel_launches;
   out.options.resize(S);
   MGS_CUDA_OK(cudaMemcpyAsync(out.options.data(), d_chosen, S * 4, cudaMemcpyDeviceToHost, c.stream));
   int best_host = -1;
@@ -921,6 +948,7 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
   out.stats.transitions = tr;
   out.stats.frontier_total = ftot;
   out.stats.frontier_peak = fpeak;
+  out.stats.transition_bytes = tbytes;
   (void)codec;
 }
 

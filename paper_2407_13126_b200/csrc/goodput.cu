@@ -166,9 +166,11 @@ void goodput_reductions(Ctx& c, const Prepared& pr, const DevSpace& sp, const do
   Recv recv{d_recv, t.S};
   double* best = c.buf<double>("ub_best", t.S);
   k_ub_best<<<t.S, 256, 0, c.stream>>>(sp, t, recv, best);
+  ++c.kernel_launches;
   k_ub_suffix<<<1, 32, 0, c.stream>>>(best, t.S, d_ub);
+  ++c.kernel_launches;
   k_greedy<<<1, 1024, 0, c.stream>>>(sp, t, recv, pr.has_initial, d_incumbent, d_greedy);
-  c.kernel_launches += 3;
+  ++c.kernel_launches;
   MGS_CUDA_OK(cudaGetLastError());
 }
 
@@ -214,7 +216,6 @@ void evaluate_batch(Ctx& c, const Prepared& pr, const DevSpace& sp, const int32_
   uint4 init{pr.init_mask[0], pr.init_mask[1], pr.init_mask[2], pr.init_mask[3]};
   k_evaluate<<<ceil_div(n, 128), 128, 0, c.stream>>>(sp, pr.t, d_plans, n_plans, d_arr, n_traces, pr.has_initial,
                                                      init, d_total, d_thr);
-  c.kernel_launches += 1;
   MGS_CUDA_OK(cudaGetLastError());
 }
 

@@ -301,6 +301,7 @@ void build_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, DevSpace& s
   auto* flag = c.buf<int32_t>("enum_flag", total);
   auto* pos = c.buf<int32_t>("enum_pos", total + 1);
   k_enum_flags<<<grid_for(total), 256, 0, c.stream>>>(L, t, total, flag);
+  ++c.kernel_launches;
   exclusive_scan_i32(c, flag, pos, static_cast<int>(total));
   const int n_opt = read_scalar(c, pos + total);
   sp.n_opt = n_opt;
@@ -321,6 +322,7 @@ void build_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, DevSpace& s
   sp.opt_sig = c.buf<int32_t>("opt_sig", n_opt);
   sp.opt_pid = c.buf<int32_t>("opt_pid", n_opt);
   k_enum_write<<<grid_for(total), 256, 0, c.stream>>>(L, t, total, flag, pos, sp);
+  ++c.kernel_launches;
 
   // 2. per-tenant mask ids
   auto* col = c.buf<uint32_t>("col", n_opt);
@@ -330,6 +332,7 @@ void build_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, DevSpace& s
   std::vector<std::vector<uint32_t>> host_vals(M);
   for (int m = 0; m < M; ++m) {
     k_copy_mask_col<<<grid_for(n_opt), 256, 0, c.stream>>>(sp.opt_mask, n_opt, m, col);
+    ++c.kernel_launches;
     int nu = sort_unique(c, col, col_sorted, vals + val_off[m], n_opt);
     val_off[m + 1] = val_off[m] + nu;
     host_vals[m].resize(nu);
@@ -339,6 +342,7 @@ void build_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, DevSpace& s
   MGS_CUDA_OK(cudaMemcpyAsync(d_val_off, val_off.data(), (M + 1) * 4, cudaMemcpyHostToDevice, c.stream));
   auto* opt_ids = c.buf<uint64_t>("opt_ids", n_opt);
   k_assign_ids<<<grid_for(n_opt), 256, 0, c.stream>>>(sp.opt_mask, n_opt, M, vals, d_val_off, opt_ids);
+  ++c.kernel_launches;
 
   // 3. placements (+ the root's carried-over placement at index P)
   auto* ids_sorted = c.buf<uint64_t>("ids_sorted", n_opt);
@@ -381,6 +385,7 @@ void build_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, DevSpace& s
   auto* fl = c.buf<int32_t>("cand_flag", n_opt);
   auto* fpos = c.buf<int32_t>("cand_fpos", n_opt + 1);
   k_first_of_run<<<grid_for(n_opt), 256, 0, c.stream>>>(ckey_sorted, n_opt, fl);
+  ++c.kernel_launches;
   exclusive_scan_i32(c, fl, fpos, n_opt);
   sp.n_cand = read_scalar(c, fpos + n_opt);
   sp.cand_pid = c.buf<int32_t>("cand_pid", sp.n_cand);
@@ -390,6 +395,7 @@ void build_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, DevSpace& s
                                                          sp.cand_oi, sp.cand_sig);
   sp.sig_off = c.buf<int32_t>("sig_off", sp.n_sig + 1);
   k_sig_off<<<grid_for(sp.n_sig + 1), 256, 0, c.stream>>>(sp.cand_sig, sp.n_cand, sp.n_sig, sp.sig_off);
+  ++c.kernel_launches;
 
   // 5. subset projections of every placement (incl. the root)
   const int n_sub = 1 << M;
@@ -401,8 +407,10 @@ void build_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, DevSpace& s
   sp.proj_base[0] = 0;
   for (int sub = 0; sub < n_sub; ++sub) {
     k_proj_keys<<<grid_for(P1), 256, 0, c.stream>>>(sp.pl_ids, P1, M, sub, pk);
+    ++c.kernel_launches;
     const int nu = sort_unique(c, pk, pk_sorted, pk_uniq, P1);
     k_proj_assign<<<grid_for(P1), 256, 0, c.stream>>>(pk, P1, pk_uniq, nu, sp.proj_id + static_cast<size_t>(sub) * P1);
+    ++c.kernel_launches;
     sp.proj_base[sub + 1] = sp.proj_base[sub] + nu;
   }
   sp.proj_total = sp.proj_base[n_sub];
