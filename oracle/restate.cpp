@@ -564,6 +564,21 @@ std::vector<int> solve(const mgs_problem& p, mgs_stats* stats) {
     std::sort(order.begin(), order.end(), [&](int a, int b) { return next[a].lex < next[b].lex; });
     for (size_t r = 0; r < order.size(); ++r) next[order[r]].rank = static_cast<uint32_t>(r);
     if (trace) {
+      // detailed distribution stats for kernel design
+      size_t gh[4] = {0, 0, 0, 0};
+      for (auto& [st_, idxs] : groups) gh[idxs.size() <= 32 ? 0 : idxs.size() <= 128 ? 1 : idxs.size() <= 1024 ? 2 : 3]++;
+      std::unordered_map<int, int> kids;
+      for (auto& st_ : next) kids[st_.parent]++;
+      size_t kh[4] = {0, 0, 0, 0}; int kmax = 0;
+      for (auto& [p_, c_] : kids) { kh[c_ <= 1 ? 0 : c_ <= 32 ? 1 : c_ <= 256 ? 2 : 3]++; kmax = std::max(kmax, c_); }
+      std::unordered_map<SubKey, int, MaskHash> pc;
+      for (auto& st_ : next) pc[st_.mask]++;
+      size_t db = 0, dm = 0;
+      for (auto& [k_, c_] : pc) if (c_ >= 2 && c_ <= 64) { db++; dm += c_; }
+      std::fprintf(stderr, "  groups<=32:%zu <=128:%zu <=1024:%zu >1024:%zu | kids 1:%zu <=32:%zu <=256:%zu >256:%zu max %d | dom buckets %zu members %zu of %zu pids\n",
+                   gh[0], gh[1], gh[2], gh[3], kh[0], kh[1], kh[2], kh[3], kmax, db, dm, pc.size());
+    }
+    if (trace) {
       size_t gmax = 0;
       for (auto& [st_, idxs] : groups) gmax = std::max(gmax, idxs.size());
       std::unordered_map<uint64_t, int> ns_count;

@@ -12,6 +12,9 @@ struct mgs_ctx {
 };
 
 namespace mgs {
+bool solve_dp_v2_supported(const Prepared& pr, const DevSpace& sp);
+void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& sp, const double* d_recv,
+                 const double* d_ub, const double* d_incumbent, SolveOut& out);
 void evaluate_batch(Ctx& c, const Prepared& pr, const DevSpace& sp, const int32_t* d_plans, int n_plans,
                     const int64_t* d_arr, int n_traces, double* d_total, double* d_thr);
 }
@@ -97,7 +100,12 @@ void solve_one(Ctx& c, const mgs_problem& p, int32_t* out_option, int32_t* out_c
   int32_t* d_greedy = c.buf<int32_t>("greedy", S);
   mgs::goodput_reductions(c, pr, sp, d_recv, d_ub, d_inc, d_greedy);
   mgs::SolveOut out;
-  mgs::solve_dp(c, p, pr, sp, d_recv, d_ub, d_inc, out);
+  if (mgs::solve_dp_v2_supported(pr, sp)) {
+    c.phase(3);  // one persistent launch covers units..ranks
+    mgs::solve_dp_v2(c, p, pr, sp, d_recv, d_ub, d_inc, out);
+  } else {
+    mgs::solve_dp(c, p, pr, sp, d_recv, d_ub, d_inc, out);
+  }
   // objective = evaluate_plan(...).total of the chosen plan, on the device
   c.phase(7);
   int32_t* d_plan = c.buf<int32_t>("plan_eval", S);

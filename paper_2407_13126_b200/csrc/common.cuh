@@ -68,6 +68,61 @@ struct Codec {
   }
 };
 
+// status_dominates (solvers.hpp:128-134)
+__host__ __device__ inline bool status_dominates(const Codec& c, int x, int y) {
+  if (x == y) return true;
+  if (x == Codec::done()) return true;
+  if (Codec::is_running(x) && Codec::is_running(y) && c.run_size(x) == c.run_size(y)) return c.run_rem(x) <= c.run_rem(y);
+  return false;
+}
+
+// Successor units of one status group (solvers.hpp:379-411 with allowed_sizes
+// :79-97): every per-tenant retraining size the status allows, the cartesian
+// product as a signature, kept when every tenant's advance is legal, idle
+// not-started tenants can still start, and the signature has options.
+// f(sig, packed successor status) is called per unit; returns the count.
+template <class F>
+__device__ int for_each_unit(int M, int S, const long long (*rt)[8], const long long* min_rt,
+                             const int32_t* sig_nopt, uint64_t status, int s, F&& f) {
+  const Codec codec{S};
+  int st[KM], sizes[KM][9], cnt[KM];
+  for (int m = 0; m < M; ++m) {
+    st[m] = field16(status, m);
+    cnt[m] = 0;
+    if (Codec::is_running(st[m])) {
+      sizes[m][cnt[m]++] = codec.run_size(st[m]);
+    } else if (st[m] == Codec::done()) {
+      sizes[m][cnt[m]++] = 0;
+    } else {
+      if (min_rt[m] >= 0 && s + 1 + min_rt[m] <= S) sizes[m][cnt[m]++] = 0;
+      for (int k = 1; k <= 7; ++k)
+        if (rt[m][k] >= 1 && s + rt[m][k] <= S) sizes[m][cnt[m]++] = k;
+    }
+    if (cnt[m] == 0) return 0;
+  }
+  int pick[KM] = {0, 0, 0, 0};
+  int n = 0;
+  while (true) {
+    int sig = 0;
+    uint64_t ns = 0;
+    bool ok = true;
+    for (int m = M - 1; m >= 0; --m) sig = sig * 8 + sizes[m][pick[m]];
+    for (int m = 0; m < M && ok; ++m) {
+      const int a = codec.advance(rt[m], st[m], sizes[m][pick[m]], s);
+      ok = a >= 0 && !(a == 0 && (min_rt[m] < 0 || s + 1 + min_rt[m] > S));
+      ns |= static_cast<uint64_t>(a < 0 ? 0 : a) << (16 * m);
+    }
+    if (ok && sig_nopt[sig] > 0) {
+      f(sig, ns);
+      ++n;
+    }
+    int m = 0;  // odometer over the per-tenant choices
+    while (m < M && ++pick[m] == cnt[m]) pick[m++] = 0;
+    if (m == M) break;
+  }
+  return n;
+}
+
 // Device-resident, per-solve option space (Space::build output + the derived
 // candidate tables the DP consumes).
 struct DevSpace {

@@ -478,13 +478,6 @@ __global__ void k_dom_scatter(StepArgs a, const int32_t* pcount, const int32_t* 
   }
 }
 
-__device__ inline bool status_dominates(const Codec& c, int x, int y) {  // solvers.hpp:128-134
-  if (x == y) return true;
-  if (x == Codec::done()) return true;
-  if (Codec::is_running(x) && Codec::is_running(y) && c.run_size(x) == c.run_size(y)) return c.run_rem(x) <= c.run_rem(y);
-  return false;
-}
-
 __global__ void k_dom_check(StepArgs a, const int32_t* pcount, const int32_t* poff, const int32_t* bucket, int P1) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;

@@ -1,0 +1,1336 @@
+// Persistent single-launch DP engine (M <= 2): the whole per-window search of
+// solve_dp (solvers.hpp:242-579) as ONE cooperative kernel, 7 grid barriers per
+// slot, no host round trips, no sorts.
+//
+// Same procedure as the reference (and as the multi-launch engine in dp.cu):
+// subset representatives per status group, subset-candidate predecessor choice
+// + exact fold, strict bound test, equal-key merge, band, status dominance in
+// placement buckets of <= 64, state budget, dense lex ranks, terminal + parent
+// walk. What differs is only how the work is laid out on B200:
+//
+//   per slot s (F_s = current frontier, status groups contiguous in HBM)
+//   S1  units: thread per group enumerates (signature, successor status);
+//       successor statuses get ids from an open-addressing hash (no sort);
+//       per-id unit / candidate counters. Also: children per parent (ranks).
+//   S2  five decoupled-look-back scans in one pass (candidate and unit offsets
+//       per successor status, warp / CTA work items per unit, child offsets per
+//       parent).
+//   S3  placement: units get contiguous candidate ranges inside their status,
+//       work items are materialised, children are bucketed by parent.
+//   S4  dense lex ranks of F_s: rank = first child slot of the parent + rank of
+//       the option index inside the parent's bucket (lex = parent rank, option).
+//   S5  transitions: CTAs take big-group items (shared-memory subset tables
+//       built with a two-phase max-value / min-rank reduction), warps take
+//       small-group items (broadcast scan of the group's states).
+//   S6  per successor status: equal-key merge across its units, band, output
+//       of the surviving states straight into F_{s+1} (atomic segment
+//       allocation), history, dominance buckets.
+//   S7  status dominance per placement bucket (2..64 states); resets.
+//
+// Dead (dominated) states stay in F_{s+1} as holes flagged alive = 0 and are
+// skipped everywhere; ranks are dense over the live states only.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "ctx.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mgs {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kSmall = 128;         // groups up to this size: warp path
+constexpr int kChunkS = 32;         // targets per warp item
+constexpr int kChunkB = 512;        // targets per CTA item
+constexpr int kTile = kThreads * 8;  // scan tile
+constexpr int kBigNs = 1024;        // successor statuses with more candidates use the CTA path
+constexpr int kMergeWin = 2048;     // pid window of the CTA merge table
+constexpr int kSortCap = 4096;      // children buckets sorted in shared memory
+
+enum Err : int { kOk = 0, kOverflow = 100 };
+
+struct FrontierV2 {
+  uint32_t* status;
+  int32_t* pid;
+  double* value;
+  uint64_t* lex;
+  uint32_t* rank;
+  uint8_t* alive;
+  int32_t* group;
+  int32_t* g_start;
+  int32_t* g_size;
+  uint32_t* g_status;
+  int32_t* g_alive;
+};
+
+struct StepCounters {  // reset for the step after next (double buffered)
+  int n_units, n_ns, T, items_s, items_b, ticket, cur_big, cur_small, n_big_bucket, n_ns_big, n_ns_small,
+      cur_ns_big, cur_ns_small, cur_bucket, pad;
+};
+
+struct Ctl {
+  int err[2];
+  int err_code, err_step;
+  unsigned long long err_count;
+  long long need;
+  int need_what;
+  int n_store[2];   // storage size of F (incl. dead)
+  int n_groups[2];
+  int n_alive[2];
+  long long hist_top;  // history entries used
+  StepCounters sc[2];
+  unsigned long long tr_ref, tr, ftot, fpeak, tbytes;
+  unsigned long long best_vb, best_lex;
+  int best_idx;
+  int scan_total[5];
+};
+
+struct V2 {
+  DevSpace sp;
+  HostTables t;
+  int S;
+  int has_initial;
+  int dominance_ok;
+  double band;
+  uint64_t budget;
+  const double* recv;
+  const double* ub;
+  const double* incumbent;
+  FrontierV2 f[2];
+  int fcap, gcap;
+  int32_t* h_parent;
+  int32_t* h_oi;
+  long long hcap;
+  long long* hist_base;  // [S+1]
+  int32_t *u_group, *u_sig, *u_ns, *u_chs, *u_chb, *u_cbase, *u_sbase, *u_bbase;
+  int ucap;
+  unsigned long long* hash;
+  int hmask;
+  uint32_t* ns_key;
+  int32_t *ns_ucnt, *ns_ccnt, *ns_ubase, *ns_cbase, *ns_ucur, *ns_ccur, *ns_units, *ns_big, *ns_small;
+  int nscap;
+  int32_t *it_s_unit, *it_s_chunk, *it_b_unit, *it_b_chunk;
+  int itcap;
+  double* c_value;
+  uint64_t* c_lex;
+  int32_t* c_parent;
+  int32_t* c_pid;
+  uint8_t* c_ok;
+  uint8_t* c_live;
+  int ccap;
+  int32_t* kid_cnt[2];
+  int32_t* kid_cur[2];
+  int32_t* kid_base;
+  uint64_t* kid_items;
+  int32_t* big_bucket;
+  int32_t* pcnt;
+  int32_t* pbucket;
+  unsigned long long* scan_state;
+  int scan_cap;
+  int32_t* sig_len;  // [n_sig]
+  Ctl* ctl;
+  int32_t* chosen;
+  int n_partial;  // entries of the partial-subset tables (all subsets but the full one)
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+
+__device__ void raise_err(const V2& a, int phi, int code, int step = 0, unsigned long long count = 0, int what = 0,
+                          long long need = 0) {
+  if (atomicCAS(&a.ctl->err_code, 0, code) == 0) {
+    a.ctl->err_step = step;
+    a.ctl->err_count = count;
+    a.ctl->need_what = what;
+    a.ctl->need = need;
+  }
+  atomicExch(&a.ctl->err[phi & 1], 1);
+}
+
+// grid barrier + uniform error check (errors raised in phase phi become
+// visible to every CTA after the barrier that ends phi)
+__device__ __forceinline__ bool barrier(cg::grid_group& grid, const V2& a, int& phi) {
+  grid.sync();
+  const int e = ld_volatile(&a.ctl->err[phi & 1]);
+  ++phi;
+  return e != 0;
+}
+
+// ---------------------------------------------------------------------------
+// block-level exclusive scan of a tile (kThreads x 8 items)
+__device__ int block_scan_tile(const int32_t* in, int32_t* out, int n, int base, int* sm) {
+  const int tid = threadIdx.x;
+  int v[8];
+  int sum = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = base + tid * 8 + k;
+    v[k] = i < n ? in[i] : 0;
+    sum += v[k];
+  }
+  int x = sum;  // warp inclusive scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((tid & 31) >= o) x += y;
+  }
+  if ((tid & 31) == 31) sm[tid >> 5] = x;
+  __syncthreads();
+  if (tid < 32) {
+    int w = tid < kWarps ? sm[tid] : 0;
+    int z = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, z, o);
+      if (tid >= o) z += y;
+    }
+    if (tid < kWarps) sm[32 + tid] = z - w;  // exclusive warp offsets
+    if (tid == kWarps - 1) sm[64] = z;       // tile aggregate
+  }
+  __syncthreads();
+  int run = sm[32 + (tid >> 5)] + x - sum;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {  // exclusive within the tile
+    const int tmp = v[k];
+    v[k] = run;
+    run += tmp;
+  }
+  // store tile-relative exclusive values (offset added by the caller)
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = base + tid * 8 + k;
+    if (i < n) out[i] = v[k];
+  }
+  const int agg = sm[64];
+  __syncthreads();
+  return agg;
+}
+
+struct ScanJob {
+  const int32_t* in;
+  int32_t* out;
+  int n;
+};
+
+// Several exclusive scans in one pass: tiles are handed out by a ticket, so
+// every tile's predecessors are already owned by running CTAs (decoupled
+// look-back cannot deadlock in a cooperative launch).
+__device__ void multi_scan(const V2& a, const ScanJob* jobs, int njobs, int epoch, int* ticket, int* totals) {
+  __shared__ int sm[80];
+  __shared__ int s_tile, s_excl;
+  int tiles[5], tbase[6];
+  tbase[0] = 0;
+  for (int k = 0; k < njobs; ++k) {
+    tiles[k] = (jobs[k].n + kTile - 1) / kTile;
+    tbase[k + 1] = tbase[k] + tiles[k];
+  }
+  const int total_tiles = tbase[njobs];
+  while (true) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int t = s_tile;
+    __syncthreads();
+    if (t >= total_tiles) break;
+    int k = 0;
+    while (t >= tbase[k + 1]) ++k;
+    const int j = t - tbase[k];
+    const ScanJob& J = jobs[k];
+    const int agg = block_scan_tile(J.in, J.out, J.n, j * kTile, sm);
+    if (threadIdx.x == 0) {
+      unsigned long long* st = a.scan_state + t;
+      const unsigned long long ep = static_cast<unsigned long long>(epoch) << 34;
+      int excl = 0;
+      if (j == 0) {
+        __threadfence();
+        atomicExch(st, ep | (2ull << 32) | static_cast<uint32_t>(agg));
+      } else {
+        __threadfence();
+        atomicExch(st, ep | (1ull << 32) | static_cast<uint32_t>(agg));
+        int q = t - 1;
+        while (true) {
+          const unsigned long long w = ld_acquire(a.scan_state + q);
+          if ((w >> 34) != static_cast<unsigned long long>(epoch) || ((w >> 32) & 3) == 0) continue;
+          excl += static_cast<int>(w & 0xffffffffu);
+          if (((w >> 32) & 3) == 2) break;
+          --q;
+        }
+        __threadfence();
+        atomicExch(st, ep | (2ull << 32) | static_cast<uint32_t>(excl + agg));
+      }
+      s_excl = excl;
+      if (j == tiles[k] - 1) totals[k] = excl + agg;
+    }
+    __syncthreads();
+    const int excl = s_excl;
+    if (excl) {
+      for (int i = j * kTile + threadIdx.x; i < min(J.n, (j + 1) * kTile); i += kThreads) J.out[i] += excl;
+    }
+    __syncthreads();
+  }
+  for (int k = 0; k < njobs; ++k)
+    if (tiles[k] == 0 && blockIdx.x == 0 && threadIdx.x == 0) totals[k] = 0;
+}
+
+// ---------------------------------------------------------------------------
+__device__ int ns_get_id(const V2& a, StepCounters& sc, uint32_t key, int phi, int step) {
+  const unsigned long long want_hi = static_cast<unsigned long long>(key) + 1;
+  unsigned h = key * 2654435761u;
+  int reserved = -1;
+  for (int probe = 0; probe <= a.hmask; ++probe) {
+    const int slot = (h + probe) & a.hmask;
+    unsigned long long w = a.hash[slot];
+    while (true) {
+      if ((w >> 32) == want_hi) return static_cast<int>(w & 0xffffffffu);
+      if (w != 0) break;  // other key: next slot
+      if (reserved < 0) {
+        reserved = atomicAdd(&sc.n_ns, 1);
+        if (reserved >= a.nscap) {
+          raise_err(a, phi, kOverflow, step, 0, 1, reserved + 1);
+          return -1;
+        }
+      }
+      const unsigned long long mine = (want_hi << 32) | static_cast<unsigned>(reserved);
+      const unsigned long long prev = atomicCAS(&a.hash[slot], 0ull, mine);
+      if (prev == 0) {
+        a.ns_key[reserved] = key;
+        return reserved;
+      }
+      w = prev;  // lost the race: re-examine this slot
+    }
+  }
+  raise_err(a, phi, kOverflow, step, 0, 2, 0);
+  return -1;
+}
+
+// ---------------------------------------------------------------------------
+// S1: units of every live group + children per parent
+template <int M>
+__device__ void phase_units(const V2& a, int s, int phi) {
+  const int cur = s & 1;
+  StepCounters& sc = a.ctl->sc[s & 1];
+  const FrontierV2& F = a.f[cur];
+  const int G = a.ctl->n_groups[cur];
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  unsigned long long ref = 0;
+  for (int g = gtid; g < G; g += gstride) {
+    if (F.g_alive[g] <= 0) continue;
+    const int gsize = F.g_size[g];
+    for_each_unit(M, a.t.S, a.t.rt, a.t.min_rt, a.sp.sig_nopt, F.g_status[g], s, [&](int sig, uint64_t ns) {
+      const int u = atomicAdd(&sc.n_units, 1);
+      if (u >= a.ucap) {
+        raise_err(a, phi, kOverflow, s, 0, 3, u + 1);
+        return;
+      }
+      const int id = ns_get_id(a, sc, static_cast<uint32_t>(ns), phi, s);
+      if (id < 0) return;
+      const int L = a.sig_len[sig];
+      a.u_group[u] = g;
+      a.u_sig[u] = sig;
+      a.u_ns[u] = id;
+      const bool small = gsize <= kSmall;
+      a.u_chs[u] = small ? (L + kChunkS - 1) / kChunkS : 0;
+      a.u_chb[u] = small ? 0 : (L + kChunkB - 1) / kChunkB;
+      atomicAdd(&a.ns_ucnt[id], 1);
+      atomicAdd(&a.ns_ccnt[id], L);
+      ref += static_cast<unsigned long long>(a.sp.sig_nopt[sig]);
+    });
+  }
+  for (int o = 16; o > 0; o >>= 1) ref += __shfl_down_sync(0xffffffffu, ref, o);
+  if ((threadIdx.x & 31) == 0 && ref) atomicAdd(&a.ctl->tr_ref, ref);
+  // children per parent (rank buckets of F_s)
+  const int n = a.ctl->n_store[cur];
+  for (int i = gtid; i < n; i += gstride)
+    if (F.alive[i]) atomicAdd(&a.kid_cnt[cur][F.lex[i] >> 32], 1);
+}
+
+// S3: placement
+__device__ void phase_place(const V2& a, int s, int phi) {
+  const int cur = s & 1;
+  StepCounters& sc = a.ctl->sc[s & 1];
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  const int NU = sc.n_units, NS = sc.n_ns;
+  for (int u = gtid; u < NU; u += gstride) {
+    const int id = a.u_ns[u];
+    const int L = a.sig_len[a.u_sig[u]];
+    a.u_cbase[u] = a.ns_cbase[id] + atomicAdd(&a.ns_ccur[id], L);
+    a.ns_units[a.ns_ubase[id] + atomicAdd(&a.ns_ucur[id], 1)] = u;
+    for (int c = 0; c < a.u_chs[u]; ++c) {
+      a.it_s_unit[a.u_sbase[u] + c] = u;
+      a.it_s_chunk[a.u_sbase[u] + c] = c;
+    }
+    for (int c = 0; c < a.u_chb[u]; ++c) {
+      a.it_b_unit[a.u_bbase[u] + c] = u;
+      a.it_b_chunk[a.u_bbase[u] + c] = c;
+    }
+  }
+  for (int id = gtid; id < NS; id += gstride) {
+    if (a.ns_ucnt[id] == 0) continue;  // reserved id lost to a concurrent insert
+    const bool big = a.ns_ccnt[id] > kBigNs;
+    if (big) a.ns_big[atomicAdd(&sc.n_ns_big, 1)] = id;
+    else a.ns_small[atomicAdd(&sc.n_ns_small, 1)] = id;
+  }
+  const FrontierV2& F = a.f[cur];
+  const int n = a.ctl->n_store[cur];
+  for (int i = gtid; i < n; i += gstride) {
+    if (!F.alive[i]) continue;
+    const int pr = static_cast<int>(F.lex[i] >> 32);
+    const int q = atomicAdd(&a.kid_cur[cur][pr], 1);
+    a.kid_items[a.kid_base[pr] + q] = ((F.lex[i] & 0xffffffffull) << 32) | static_cast<uint32_t>(i);
+    if (q == 0 && a.kid_cnt[cur][pr] > 32) a.big_bucket[atomicAdd(&sc.n_big_bucket, 1)] = pr;
+  }
+}
+
+// S4: dense ranks of F_s = parent's child offset + position by option index
+__device__ void phase_ranks(const V2& a, int s, unsigned long long* sm64) {
+  const int cur = s & 1;
+  StepCounters& sc = a.ctl->sc[s & 1];
+  const FrontierV2& F = a.f[cur];
+  __shared__ int s_b;
+  // big buckets: CTA bitonic sort in shared memory
+  while (true) {
+    if (threadIdx.x == 0) s_b = atomicAdd(&sc.cur_bucket, 1);
+    __syncthreads();
+    const int b = s_b;
+    __syncthreads();
+    if (b >= sc.n_big_bucket) break;
+    const int pr = a.big_bucket[b];
+    const int base = a.kid_base[pr], c = a.kid_cnt[cur][pr];
+    if (c <= kSortCap) {
+      int n2 = 1;
+      while (n2 < c) n2 <<= 1;
+      for (int i = threadIdx.x; i < n2; i += kThreads) sm64[i] = i < c ? a.kid_items[base + i] : ~0ull;
+      __syncthreads();
+      for (int k = 2; k <= n2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int i = threadIdx.x; i < n2; i += kThreads) {
+            const int l = i ^ j;
+            if (l > i) {
+              const unsigned long long x = sm64[i], y = sm64[l];
+              const bool up = (i & k) == 0;
+              if ((x > y) == up) {
+                sm64[i] = y;
+                sm64[l] = x;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      for (int i = threadIdx.x; i < c; i += kThreads) F.rank[static_cast<uint32_t>(sm64[i])] = base + i;
+      __syncthreads();
+    } else {  // beyond shared memory: quadratic counting (rare, correct)
+      for (int i = threadIdx.x; i < c; i += kThreads) {
+        const unsigned long long me = a.kid_items[base + i];
+        int pos = 0;
+        for (int k = 0; k < c; ++k) pos += a.kid_items[base + k] < me;
+        F.rank[static_cast<uint32_t>(me)] = base + pos;
+      }
+      __syncthreads();
+    }
+  }
+  // small buckets: thread per state
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  const int n = a.ctl->n_store[cur];
+  for (int i = gtid; i < n; i += gstride) {
+    if (!F.alive[i]) continue;
+    const int pr = static_cast<int>(F.lex[i] >> 32);
+    const int c = a.kid_cnt[cur][pr];
+    if (c > 32) continue;
+    const int base = a.kid_base[pr];
+    const unsigned long long me = ((F.lex[i] & 0xffffffffull) << 32) | static_cast<uint32_t>(i);
+    int pos = 0;
+    for (int k = 0; k < c; ++k) pos += a.kid_items[base + k] < me;
+    F.rank[i] = base + pos;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// S5: transitions
+template <int M>
+struct BestT {
+  double v[1 << M];
+  uint32_t r[1 << M];
+  int i[1 << M];
+};
+
+template <int M>
+__device__ __forceinline__ void emit_target(const V2& a, int s, int charge, int unit, int t_idx, int gs,
+                                            const double* acc, int p, int oi, uint32_t ids_p, const BestT<M>& b,
+                                            const FrontierV2& F) {
+  const HostTables& t = a.t;
+  double cap[M], bonus[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {  // solvers.hpp:426-433
+    cap[m] = a.sp.pl_cap[p * KM + m];
+    const double recv = a.recv[m * t.S + s];
+    const double c_changed = dmul(thr_of(recv, eff_cap(cap[m], charge ? t.loss[m] : 0.0)), acc[m]);
+    bonus[m] = charge ? dsub(dmul(thr_of(recv, cap[m]), acc[m]), c_changed) : 0.0;
+  }
+  int chosen = -1;  // solvers.hpp:435-447
+  double cv = 0.0;
+  uint32_t cr = 0;
+#pragma unroll
+  for (int sub = 0; sub < (1 << M); ++sub) {
+    if (b.i[sub] < 0) continue;
+    double extra = 0.0;
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+      if ((sub >> m) & 1) extra = dadd(extra, bonus[m]);
+    const double cand = dadd(b.v[sub], extra);
+    if (chosen < 0 || better(cand, b.r[sub], cv, cr)) {
+      chosen = b.i[sub];
+      cv = cand;
+      cr = b.r[sub];
+    }
+  }
+  const int slot = a.u_cbase[unit] + t_idx;
+  if (chosen < 0) {  // group without live states cannot happen (units skip them); keep safe
+    a.c_ok[slot] = 0;
+    return;
+  }
+  const int pred = gs + chosen;
+  const uint32_t pids = static_cast<uint32_t>(a.sp.pl_ids[F.pid[pred]]);
+  double v = F.value[pred];  // exact fold (solvers.hpp:451-458)
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const bool changed = charge && ((pids >> (16 * m)) & 0xffff) != ((ids_p >> (16 * m)) & 0xffff);
+    const double eff = eff_cap(cap[m], changed ? t.loss[m] : 0.0);
+    v = dadd(v, dmul(thr_of(a.recv[m * t.S + s], eff), acc[m]));
+  }
+  const bool ok = !(dadd(v, a.ub[s + 1]) < *a.incumbent);  // solvers.hpp:459
+  a.c_value[slot] = v;
+  a.c_lex[slot] = (static_cast<uint64_t>(F.rank[pred]) << 32) | static_cast<uint32_t>(oi);
+  a.c_parent[slot] = pred;
+  a.c_pid[slot] = p;
+  a.c_ok[slot] = ok ? 1 : 0;
+}
+
+template <int M>
+__device__ __forceinline__ void group_acc(const V2& a, uint32_t gstat, double* acc) {
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+    acc[m] = static_cast<int>((gstat >> (16 * m)) & 0xffff) == Codec::done() ? a.t.post[m] : a.t.pre[m];
+}
+
+struct TransSmem {
+  unsigned long long* ex;  // [P1] (tag << 32) | idx of the group's state at that placement
+  unsigned long long* vb;  // [n_partial]
+  uint32_t* rk;
+  int32_t* ix;
+  uint32_t* tg;
+};
+
+template <int M>
+__device__ void phase_trans(const V2& a, int s, TransSmem& T, uint32_t& tag) {
+  const int cur = s & 1;
+  StepCounters& sc = a.ctl->sc[s & 1];
+  const FrontierV2& F = a.f[cur];
+  const int charge = (s > 0 || a.has_initial) ? 1 : 0;
+  const int P1 = a.sp.P1;
+  __shared__ int s_item;
+  // CTA items: big groups, shared-memory subset tables
+  while (true) {
+    if (threadIdx.x == 0) s_item = atomicAdd(&sc.cur_big, 1);
+    __syncthreads();
+    const int item = s_item;
+    __syncthreads();
+    if (item >= sc.items_b) break;
+    ++tag;
+    const int unit = a.it_b_unit[item], chunk = a.it_b_chunk[item];
+    const int g = a.u_group[unit], sig = a.u_sig[unit];
+    const int gs = F.g_start[g], gn = F.g_size[g];
+    double acc[M];
+    group_acc<M>(a, F.g_status[g], acc);
+    // phase 0: claim entries
+    for (int j = threadIdx.x; j < gn; j += kThreads) {
+      if (!F.alive[gs + j]) continue;
+      const int pj = F.pid[gs + j];
+      T.ex[pj] = (static_cast<unsigned long long>(tag) << 32) | static_cast<uint32_t>(j);
+#pragma unroll
+      for (int sub = 0; sub < (1 << M) - 1; ++sub) {
+        const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj];
+        T.tg[e] = tag;
+        T.vb[e] = 0ull;
+        T.rk[e] = 0xffffffffu;
+        T.ix[e] = -1;
+      }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < gn; j += kThreads) {
+      if (!F.alive[gs + j]) continue;
+      const int pj = F.pid[gs + j];
+      const unsigned long long vb = vbits(F.value[gs + j]);
+#pragma unroll
+      for (int sub = 0; sub < (1 << M) - 1; ++sub) atomicMax(&T.vb[a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj]], vb);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < gn; j += kThreads) {
+      if (!F.alive[gs + j]) continue;
+      const int pj = F.pid[gs + j];
+      const unsigned long long vb = vbits(F.value[gs + j]);
+      const uint32_t rj = F.rank[gs + j];
+#pragma unroll
+      for (int sub = 0; sub < (1 << M) - 1; ++sub) {
+        const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj];
+        if (T.vb[e] == vb) atomicMin(&T.rk[e], rj);
+      }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < gn; j += kThreads) {
+      if (!F.alive[gs + j]) continue;
+      const int pj = F.pid[gs + j];
+      const unsigned long long vb = vbits(F.value[gs + j]);
+      const uint32_t rj = F.rank[gs + j];
+#pragma unroll
+      for (int sub = 0; sub < (1 << M) - 1; ++sub) {
+        const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj];
+        if (T.vb[e] == vb && T.rk[e] == rj) T.ix[e] = j;
+      }
+    }
+    __syncthreads();
+    const int sb = a.sp.sig_off[sig], L = a.sp.sig_off[sig + 1] - sb;
+    const int t0 = chunk * kChunkB, t1 = min(L, t0 + kChunkB);
+    for (int ti = t0 + threadIdx.x; ti < t1; ti += kThreads) {
+      const int p = a.sp.cand_pid[sb + ti];
+      const int oi = a.sp.cand_oi[sb + ti];
+      BestT<M> b;
+#pragma unroll
+      for (int sub = 0; sub < (1 << M) - 1; ++sub) {
+        const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + p];
+        const bool hit = T.tg[e] == tag && T.ix[e] >= 0;
+        b.i[sub] = hit ? T.ix[e] : -1;
+        b.v[sub] = hit ? __longlong_as_double(static_cast<long long>(T.vb[e])) : 0.0;
+        b.r[sub] = hit ? T.rk[e] : 0u;
+      }
+      {
+        const unsigned long long w = T.ex[p];
+        const int full = (1 << M) - 1;
+        if ((w >> 32) == tag) {
+          const int j = static_cast<int>(w & 0xffffffffu);
+          b.i[full] = j;
+          b.v[full] = F.value[gs + j];
+          b.r[full] = F.rank[gs + j];
+        } else {
+          b.i[full] = -1;
+          b.v[full] = 0.0;
+          b.r[full] = 0u;
+        }
+      }
+      emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, static_cast<uint32_t>(a.sp.pl_ids[p]), b, F);
+    }
+    __syncthreads();
+  }
+  // warp items: small groups, broadcast scan
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(&sc.cur_small, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= sc.items_s) break;
+    const int unit = a.it_s_unit[item], chunk = a.it_s_chunk[item];
+    const int g = a.u_group[unit], sig = a.u_sig[unit];
+    const int gs = F.g_start[g], gn = F.g_size[g];
+    double acc[M];
+    group_acc<M>(a, F.g_status[g], acc);
+    const int sb = a.sp.sig_off[sig], L = a.sp.sig_off[sig + 1] - sb;
+    const int ti = chunk * kChunkS + lane;
+    if (ti >= L) continue;
+    const int p = a.sp.cand_pid[sb + ti];
+    const int oi = a.sp.cand_oi[sb + ti];
+    const uint32_t ids_p = static_cast<uint32_t>(a.sp.pl_ids[p]);
+    BestT<M> b;
+#pragma unroll
+    for (int k = 0; k < (1 << M); ++k) {
+      b.i[k] = -1;
+      b.v[k] = 0.0;
+      b.r[k] = 0xffffffffu;
+    }
+    for (int j = 0; j < gn; ++j) {
+      if (!F.alive[gs + j]) continue;
+      const double vj = F.value[gs + j];
+      const uint32_t rj = F.rank[gs + j];
+      const uint32_t idj = static_cast<uint32_t>(a.sp.pl_ids[F.pid[gs + j]]);
+      int mt = 0;
+#pragma unroll
+      for (int m = 0; m < M; ++m) mt |= (((idj ^ ids_p) >> (16 * m)) & 0xffff) == 0 ? (1 << m) : 0;
+#pragma unroll
+      for (int sub = 0; sub < (1 << M); ++sub) {
+        if ((sub & ~mt) != 0) continue;
+        if (b.i[sub] < 0 || better(vj, rj, b.v[sub], b.r[sub])) {
+          b.v[sub] = vj;
+          b.r[sub] = rj;
+          b.i[sub] = j;
+        }
+      }
+    }
+    emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, ids_p, b, F);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// S6: merge + band + output, per successor status
+// live after the equal-key merge (binary search in the other units' lists)
+__device__ bool merged_live(const V2& a, int ub, int uc, int k) {
+  if (!a.c_ok[k]) return false;
+  if (uc == 1) return true;
+  const int p = a.c_pid[k];
+  const double v = a.c_value[k];
+  const uint64_t lx = a.c_lex[k];
+  for (int q = 0; q < uc; ++q) {
+    const int u = a.ns_units[ub + q];
+    const int cb = a.u_cbase[u];
+    const int sig = a.u_sig[u];
+    const int b = a.sp.sig_off[sig], n = a.sp.sig_off[sig + 1] - b;
+    if (k >= cb && k < cb + n) continue;  // own unit
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (a.sp.cand_pid[b + mid] < p) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < n && a.sp.cand_pid[b + lo] == p) {
+      const int k2 = cb + lo;
+      if (a.c_ok[k2] && better(a.c_value[k2], a.c_lex[k2], v, lx)) return false;
+    }
+  }
+  return true;
+}
+
+__device__ __forceinline__ void write_state(const V2& a, int s, int nxt, int q, int gidx, uint32_t key, int k) {
+  const FrontierV2& N = a.f[nxt];
+  const int p = a.c_pid[k];
+  const uint64_t lx = a.c_lex[k];
+  N.status[q] = key;
+  N.pid[q] = p;
+  N.value[q] = a.c_value[k];
+  N.lex[q] = lx;
+  N.alive[q] = 1;
+  N.group[q] = gidx;
+  const long long h = a.hist_base[s + 1] + q;
+  a.h_parent[h] = a.c_parent[k];
+  a.h_oi[h] = static_cast<int32_t>(lx & 0xffffffffu);
+  if (a.dominance_ok) {
+    const int slot = atomicAdd(&a.pcnt[p], 1);
+    if (slot < 64) a.pbucket[p * 64 + slot] = q;
+  }
+}
+
+__device__ bool alloc_out(const V2& a, int s, int nxt, int count, int* q0, int* gidx, int phi) {
+  *q0 = atomicAdd(&a.ctl->n_store[nxt], count);
+  *gidx = atomicAdd(&a.ctl->n_groups[nxt], 1);
+  if (*q0 + count > a.fcap) {
+    raise_err(a, phi, kOverflow, s, 0, 4, static_cast<long long>(*q0) + count);
+    return false;
+  }
+  if (*gidx >= a.gcap) {
+    raise_err(a, phi, kOverflow, s, 0, 5, *gidx + 1);
+    return false;
+  }
+  if (a.hist_base[s + 1] + *q0 + count > a.hcap) {
+    raise_err(a, phi, kOverflow, s, 0, 6, a.hist_base[s + 1] + *q0 + count);
+    return false;
+  }
+  return true;
+}
+
+__device__ void phase_merge_out(const V2& a, int s, int phi, unsigned long long* mvb, unsigned long long* mlx) {
+  const int nxt = (s + 1) & 1;
+  StepCounters& sc = a.ctl->sc[s & 1];
+  const FrontierV2& N = a.f[nxt];
+  __shared__ int s_id, s_q0, s_g, s_cnt;
+  __shared__ unsigned long long s_max;
+  __shared__ int s_wsum[kWarps];
+  // CTA path: big successor statuses
+  while (true) {
+    if (threadIdx.x == 0) s_id = atomicAdd(&sc.cur_ns_big, 1);
+    __syncthreads();
+    const int w = s_id;
+    __syncthreads();
+    if (w >= sc.n_ns_big) break;
+    const int id = a.ns_big[w];
+    const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id], ub = a.ns_ubase[id], uc = a.ns_ucnt[id];
+    if (uc == 1) {
+      for (int k = cb + threadIdx.x; k < cb + cc; k += kThreads) a.c_live[k] = a.c_ok[k];
+    } else {
+      const int P1 = a.sp.P1;
+      for (int w0 = 0; w0 < P1; w0 += kMergeWin) {
+        for (int i = threadIdx.x; i < kMergeWin; i += kThreads) {
+          mvb[i] = 0ull;
+          mlx[i] = ~0ull;
+        }
+        __syncthreads();
+        for (int pass = 0; pass < 3; ++pass) {
+          for (int q = 0; q < uc; ++q) {
+            const int u = a.ns_units[ub + q];
+            const int sig = a.u_sig[u];
+            const int b = a.sp.sig_off[sig], n = a.sp.sig_off[sig + 1] - b;
+            const int cbu = a.u_cbase[u];
+            for (int t = threadIdx.x; t < n; t += kThreads) {
+              const int p = a.sp.cand_pid[b + t];
+              if (p < w0 || p >= w0 + kMergeWin) continue;
+              const int k = cbu + t;
+              if (!a.c_ok[k]) {
+                if (pass == 2) a.c_live[k] = 0;
+                continue;
+              }
+              const unsigned long long vb = vbits(a.c_value[k]);
+              if (pass == 0) atomicMax(&mvb[p - w0], vb);
+              else if (pass == 1) {
+                if (mvb[p - w0] == vb) atomicMin(&mlx[p - w0], a.c_lex[k]);
+              } else {
+                a.c_live[k] = (mvb[p - w0] == vb && mlx[p - w0] == a.c_lex[k]) ? 1 : 0;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+    }
+    __syncthreads();
+    // band (solvers.hpp:499-511)
+    unsigned long long mx = 0;
+    bool any = false;
+    for (int k = cb + threadIdx.x; k < cb + cc; k += kThreads)
+      if (a.c_live[k]) {
+        const unsigned long long vb = vbits(a.c_value[k]);
+        mx = vb > mx ? vb : mx;
+        any = true;
+      }
+    if (threadIdx.x == 0) {
+      s_max = 0;
+      s_cnt = 0;
+    }
+    __syncthreads();
+    if (any) atomicMax(&s_max, mx);
+    __syncthreads();
+    const double thresh = dsub(__longlong_as_double(static_cast<long long>(s_max)), a.band);
+    int cnt = 0;
+    for (int k = cb + threadIdx.x; k < cb + cc; k += kThreads) {
+      const bool keep = a.c_live[k] && a.c_value[k] >= thresh;
+      a.c_live[k] = keep ? 1 : 0;
+      cnt += keep;
+    }
+    atomicAdd(&s_cnt, cnt);
+    __syncthreads();
+    const int total = s_cnt;
+    if (total > 0) {
+      if (threadIdx.x == 0) {
+        int q0, gi;
+        if (alloc_out(a, s, nxt, total, &q0, &gi, phi)) {
+          s_q0 = q0;
+          s_g = gi;
+          N.g_start[gi] = q0;
+          N.g_size[gi] = total;
+          N.g_status[gi] = a.ns_key[id];
+          N.g_alive[gi] = total;
+          atomicAdd(&a.ctl->n_alive[nxt], total);
+        } else {
+          s_q0 = -1;
+        }
+      }
+      __syncthreads();
+      if (s_q0 >= 0) {
+        // ordered compaction of survivors (block scan over chunks)
+        int run = 0;
+        for (int c0 = cb; c0 < cb + cc; c0 += kThreads) {
+          const int k = c0 + threadIdx.x;
+          const bool keep = k < cb + cc && a.c_live[k];
+          const unsigned bal = __ballot_sync(0xffffffffu, keep);
+          if ((threadIdx.x & 31) == 0) s_wsum[threadIdx.x >> 5] = __popc(bal);
+          __syncthreads();
+          int off = run;
+          for (int w2 = 0; w2 < (threadIdx.x >> 5); ++w2) off += s_wsum[w2];
+          off += __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
+          if (keep) write_state(a, s, nxt, s_q0 + off, s_g, a.ns_key[id], k);
+          int tot = 0;
+          for (int w2 = 0; w2 < kWarps; ++w2) tot += s_wsum[w2];
+          run += tot;
+          __syncthreads();
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // warp path
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    int w = 0;
+    if (lane == 0) w = atomicAdd(&sc.cur_ns_small, 1);
+    w = __shfl_sync(0xffffffffu, w, 0);
+    if (w >= sc.n_ns_small) break;
+    const int id = a.ns_small[w];
+    const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id], ub = a.ns_ubase[id], uc = a.ns_ucnt[id];
+    unsigned long long mx = 0;
+    bool any = false;
+    for (int k = cb + lane; k < cb + cc; k += 32) {
+      const bool live = merged_live(a, ub, uc, k);
+      a.c_live[k] = live ? 1 : 0;
+      if (live) {
+        const unsigned long long vb = vbits(a.c_value[k]);
+        mx = vb > mx ? vb : mx;
+        any = true;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
+      mx = y > mx ? y : mx;
+    }
+    any = __any_sync(0xffffffffu, any);
+    if (!any) continue;
+    const double thresh = dsub(__longlong_as_double(static_cast<long long>(mx)), a.band);
+    int total = 0;
+    for (int k0 = cb; k0 < cb + cc; k0 += 32) {
+      const int k = k0 + lane;
+      const bool keep = k < cb + cc && a.c_live[k] && a.c_value[k] >= thresh;
+      total += __popc(__ballot_sync(0xffffffffu, keep));
+    }
+    if (total == 0) continue;
+    int q0 = 0, gi = 0, ok = 1;
+    if (lane == 0) {
+      ok = alloc_out(a, s, nxt, total, &q0, &gi, phi) ? 1 : 0;
+      if (ok) {
+        N.g_start[gi] = q0;
+        N.g_size[gi] = total;
+        N.g_status[gi] = a.ns_key[id];
+        N.g_alive[gi] = total;
+        atomicAdd(&a.ctl->n_alive[nxt], total);
+      }
+    }
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    q0 = __shfl_sync(0xffffffffu, q0, 0);
+    gi = __shfl_sync(0xffffffffu, gi, 0);
+    if (!ok) continue;
+    int run = 0;
+    const uint32_t key = a.ns_key[id];
+    for (int k0 = cb; k0 < cb + cc; k0 += 32) {
+      const int k = k0 + lane;
+      const bool keep = k < cb + cc && a.c_live[k] && a.c_value[k] >= thresh;
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
+      run += __popc(bal);
+    }
+  }
+}
+
+// S7: status dominance within placement buckets (solvers.hpp:514-537)
+__device__ void phase_dominance(const V2& a, int s) {
+  const int nxt = (s + 1) & 1;
+  const FrontierV2& N = a.f[nxt];
+  const Codec codec{a.t.S};
+  const int lane = threadIdx.x & 31;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int p = wid; p < a.sp.P1; p += nw) {
+    const int n = a.pcnt[p];
+    if (n >= 2 && n <= 64) {
+      const int* bk = a.pbucket + p * 64;
+      int q[2];
+      uint32_t st[2];
+      double v[2];
+      uint64_t lx[2];
+      for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        q[h] = j < n ? bk[j] : -1;
+        st[h] = q[h] >= 0 ? N.status[q[h]] : 0;
+        v[h] = q[h] >= 0 ? N.value[q[h]] : 0.0;
+        lx[h] = q[h] >= 0 ? N.lex[q[h]] : 0;
+      }
+      bool dead[2] = {false, false};
+      for (int j = 0; j < n; ++j) {
+        const int h = j >> 5, src = j & 31;
+        const uint32_t sa = __shfl_sync(0xffffffffu, st[h], src);
+        const double va = __shfl_sync(0xffffffffu, v[h], src);
+        const uint64_t la = __shfl_sync(0xffffffffu, lx[h], src);
+        for (int hb = 0; hb < 2; ++hb) {
+          if (q[hb] < 0 || lane + 32 * hb == j) continue;
+          bool dom = true;
+          for (int m = 0; m < a.t.M && dom; ++m)
+            dom = status_dominates(codec, (sa >> (16 * m)) & 0xffff, (st[hb] >> (16 * m)) & 0xffff);
+          if (dom && better(va, la, v[hb], lx[hb])) dead[hb] = true;
+        }
+      }
+      for (int h = 0; h < 2; ++h)
+        if (q[h] >= 0 && dead[h]) {
+          N.alive[q[h]] = 0;
+          atomicSub(&N.g_alive[N.group[q[h]]], 1);
+          atomicSub(&a.ctl->n_alive[nxt], 1);
+        }
+    }
+    if (lane == 0) a.pcnt[p] = 0;
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(kThreads, 2) k_solve_v2(V2 a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ unsigned long long smem_u64[];
+  const int P1 = a.sp.P1;
+  TransSmem T;
+  T.ex = smem_u64;
+  T.vb = smem_u64 + P1;
+  T.rk = reinterpret_cast<uint32_t*>(T.vb + a.n_partial);
+  T.ix = reinterpret_cast<int32_t*>(T.rk + a.n_partial);
+  T.tg = reinterpret_cast<uint32_t*>(T.ix + a.n_partial);
+  for (int i = threadIdx.x; i < P1; i += kThreads) T.ex[i] = 0ull;  // tags start at 1
+  for (int i = threadIdx.x; i < a.n_partial; i += kThreads) T.tg[i] = 0u;
+  uint32_t tag = 0;
+  __syncthreads();
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  int phi = 0;
+  int ranks_prev = 1;  // live states of F_{s-1} (parent rank space); root: 1
+  for (int s = 0; s < a.S; ++s) {
+    const int cur = s & 1, nxt = (s + 1) & 1;
+    Ctl* ctl = a.ctl;
+    StepCounters& sc = ctl->sc[s & 1];
+    // frontier checks for F_s (solvers.hpp:348 and :539-542 of the previous step)
+    const int alive_cur = ctl->n_alive[cur];
+    if (alive_cur == 0) {
+      if (gtid == 0) raise_err(a, phi, MGS_ERR_INFEASIBLE_JOINT, s);
+    } else if (s > 0 && static_cast<uint64_t>(alive_cur) > a.budget) {
+      if (gtid == 0) raise_err(a, phi, MGS_ERR_STATE_BUDGET, s, alive_cur);
+    }
+    if (s > 0 && gtid == 0) {
+      ctl->ftot += alive_cur;
+      if (static_cast<unsigned long long>(alive_cur) > ctl->fpeak) ctl->fpeak = alive_cur;
+    }
+    // S1
+    phase_units<M>(a, s, phi);
+    if (barrier(grid, a, phi)) return;
+    // S2: scans
+    {
+      ScanJob jobs[5] = {{a.ns_ccnt, a.ns_cbase, sc.n_ns},
+                         {a.ns_ucnt, a.ns_ubase, sc.n_ns},
+                         {a.u_chs, a.u_sbase, sc.n_units},
+                         {a.u_chb, a.u_bbase, sc.n_units},
+                         {a.kid_cnt[cur], a.kid_base, ranks_prev}};
+      multi_scan(a, jobs, 5, s + 1, &sc.ticket, ctl->scan_total);
+    }
+    if (barrier(grid, a, phi)) return;
+    {
+      const int T_ = ctl->scan_total[0];
+      if (gtid == 0) {
+        sc.T = T_;
+        sc.items_s = ctl->scan_total[2];
+        sc.items_b = ctl->scan_total[3];
+        ctl->tr += static_cast<unsigned long long>(T_);
+        ctl->tbytes += static_cast<unsigned long long>(ctl->n_store[cur]) * 20ull +
+                       static_cast<unsigned long long>(T_) * 37ull;
+        if (T_ > a.ccap) raise_err(a, phi, kOverflow, s, 0, 7, T_);
+        if (ctl->scan_total[2] > a.itcap || ctl->scan_total[3] > a.itcap)
+          raise_err(a, phi, kOverflow, s, 0, 8, max(ctl->scan_total[2], ctl->scan_total[3]));
+      }
+    }
+    // S3 (reads scan totals written before the barrier)
+    if (ctl->scan_total[0] <= a.ccap && ctl->scan_total[2] <= a.itcap && ctl->scan_total[3] <= a.itcap)
+      phase_place(a, s, phi);
+    if (barrier(grid, a, phi)) return;
+    // S4
+    phase_ranks(a, s, smem_u64);
+    if (barrier(grid, a, phi)) return;
+    // S5
+    // the shared-memory tables are clobbered by S4/S6: start each S5 clean
+    for (int i = threadIdx.x; i < P1; i += kThreads) T.ex[i] = 0ull;
+    for (int i = threadIdx.x; i < a.n_partial; i += kThreads) T.tg[i] = 0u;
+    tag = 0;
+    __syncthreads();
+    phase_trans<M>(a, s, T, tag);
+    // reset the counters of the step after next and the hash table
+    if (gtid == 0) {
+      StepCounters& o = ctl->sc[(s + 1) & 1];
+      o = StepCounters{};
+      ctl->n_store[nxt] = 0;
+      ctl->n_groups[nxt] = 0;
+      ctl->n_alive[nxt] = 0;
+    }
+    for (int i = gtid; i <= a.hmask; i += gstride) a.hash[i] = 0ull;
+    if (barrier(grid, a, phi)) return;
+    // S6
+    phase_merge_out(a, s, phi, smem_u64, smem_u64 + kMergeWin);
+    if (barrier(grid, a, phi)) return;
+    // S7
+    if (a.dominance_ok) phase_dominance(a, s);
+    {
+      const int NS = sc.n_ns;
+      for (int i = gtid; i < NS; i += gstride) {
+        a.ns_ucnt[i] = 0;
+        a.ns_ccnt[i] = 0;
+        a.ns_ucur[i] = 0;
+        a.ns_ccur[i] = 0;
+      }
+      for (int i = gtid; i < ranks_prev; i += gstride) {
+        a.kid_cnt[cur][i] = 0;
+        a.kid_cur[cur][i] = 0;
+      }
+      if (gtid == 0) a.hist_base[s + 2 <= a.S ? s + 2 : a.S] = a.hist_base[s + 1] + ctl->n_store[nxt];
+    }
+    ranks_prev = alive_cur;
+    if (barrier(grid, a, phi)) return;
+  }
+  // terminal (solvers.hpp:552-565)
+  const int fin = a.S & 1;
+  const int alive_fin = a.ctl->n_alive[fin];
+  if (static_cast<uint64_t>(alive_fin) > a.budget) {
+    if (gtid == 0) raise_err(a, phi, MGS_ERR_STATE_BUDGET, a.S, alive_fin);
+  }
+  if (gtid == 0) {
+    a.ctl->ftot += alive_fin;
+    if (static_cast<unsigned long long>(alive_fin) > a.ctl->fpeak) a.ctl->fpeak = alive_fin;
+  }
+  uint32_t all_done = 0;
+  for (int m = 0; m < a.t.M; ++m) all_done |= static_cast<uint32_t>(Codec::done()) << (16 * m);
+  const FrontierV2& F = a.f[fin];
+  const int n = a.ctl->n_store[fin];
+  unsigned long long mv = 0;
+  bool any = false;
+  for (int i = gtid; i < n; i += gstride)
+    if (F.alive[i] && F.status[i] == all_done) {
+      const unsigned long long vb = vbits(F.value[i]);
+      mv = any && mv > vb ? mv : vb;
+      any = true;
+    }
+  if (any) atomicMax(&a.ctl->best_vb, mv + 1);  // +1: 0 = none
+  if (barrier(grid, a, phi)) return;
+  const unsigned long long bvb = a.ctl->best_vb;
+  if (bvb == 0) {
+    if (gtid == 0) raise_err(a, phi, MGS_ERR_INFEASIBLE_JOINT, a.S);
+  } else {
+    for (int i = gtid; i < n; i += gstride)
+      if (F.alive[i] && F.status[i] == all_done && vbits(F.value[i]) + 1 == bvb) atomicMin(&a.ctl->best_lex, F.lex[i]);
+  }
+  if (barrier(grid, a, phi)) return;
+  for (int i = gtid; i < n; i += gstride)
+    if (F.alive[i] && F.status[i] == all_done && vbits(F.value[i]) + 1 == bvb && F.lex[i] == a.ctl->best_lex)
+      a.ctl->best_idx = i;
+  if (barrier(grid, a, phi)) return;
+  if (gtid == 0) {  // parent walk (solvers.hpp:567-574)
+    int idx = a.ctl->best_idx;
+    for (int s = a.S - 1; s >= 0; --s) {
+      const long long h = a.hist_base[s + 1] + idx;
+      a.chosen[s] = a.h_oi[h];
+      idx = a.h_parent[h];
+    }
+  }
+}
+
+__global__ void k_init_root(V2 a, uint32_t root_pid) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  FrontierV2 F = a.f[0];
+  F.status[0] = 0;
+  F.pid[0] = root_pid;
+  F.value[0] = 0.0;
+  F.lex[0] = 0;
+  F.alive[0] = 1;
+  F.group[0] = 0;
+  F.rank[0] = 0;
+  F.g_start[0] = 0;
+  F.g_size[0] = 1;
+  F.g_status[0] = 0;
+  F.g_alive[0] = 1;
+  Ctl* c = a.ctl;
+  c->n_store[0] = 1;
+  c->n_groups[0] = 1;
+  c->n_alive[0] = 1;
+  c->best_vb = 0;
+  c->best_lex = ~0ull;
+  c->best_idx = -1;
+  a.hist_base[0] = 0;
+  a.hist_base[1] = 0;
+}
+
+__global__ void k_sig_len(const int32_t* sig_off, int n_sig, int32_t* sig_len) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_sig; i += gridDim.x * blockDim.x)
+    sig_len[i] = sig_off[i + 1] - sig_off[i];
+}
+
+struct Caps {
+  int fcap, gcap, ucap, nscap, itcap, ccap, hbits;
+  long long hcap;
+};
+
+}  // namespace
+
+bool solve_dp_v2_supported(const Prepared& pr, const DevSpace& sp) {
+  if (pr.t.M > 2) return false;
+  const char* e = std::getenv("MGS_DP_ENGINE");
+  if (e && std::string(e) == "v1") return false;
+  (void)sp;
+  return true;
+}
+
+void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& sp, const double* d_recv,
+                 const double* d_ub, const double* d_incumbent, SolveOut& out) {
+  const HostTables& t = pr.t;
+  const int M = t.M, S = t.S;
+  double acc_max[KM] = {0, 0, 0, 0};
+  bool dominance_ok = true;
+  for (int m = 0; m < M; ++m) {
+    acc_max[m] = std::max(t.pre[m], t.post[m]);
+    dominance_ok = dominance_ok && t.post[m] >= t.pre[m];
+  }
+  std::vector<double> pc(static_cast<size_t>(sp.P) * KM);
+  MGS_CUDA_OK(cudaMemcpyAsync(pc.data(), sp.pl_cap, pc.size() * 8, cudaMemcpyDeviceToHost, c.stream));
+  MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+  double cap_max[KM] = {0, 0, 0, 0};
+  for (int q = 0; q < sp.P; ++q)
+    for (int m = 0; m < M; ++m) cap_max[m] = std::max(cap_max[m], pc[q * KM + m]);
+  double band = 1e-9;  // solvers.hpp:266-267
+  for (int m = 0; m < M; ++m) band += t.loss[m] * cap_max[m] * acc_max[m];
+
+  const int n_sub = 1 << M;
+  const int n_partial = sp.proj_base[n_sub - 1];  // all subsets but the full one
+  const size_t smem_trans = static_cast<size_t>(sp.P1) * 8 + static_cast<size_t>(n_partial) * 20;
+  const size_t smem = std::max({smem_trans, static_cast<size_t>(2 * kMergeWin * 8), static_cast<size_t>(kSortCap * 8)});
+  auto kern = M == 1 ? k_solve_v2<1> : k_solve_v2<2>;
+  MGS_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int occ = 0;
+  MGS_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
+  if (occ < 1) throw PlanFail{MGS_ERR_CUDA, "persistent DP kernel does not fit on an SM"};
+  const int grid = c.sm_count * std::min(occ, 2);
+
+  static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 17, 1 << 18, 1 << 22, 18, 64ll << 20};
+  const uint64_t budget = p.state_budget;
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    V2 a{};
+    a.sp = sp;
+    a.t = t;
+    a.S = S;
+    a.has_initial = pr.has_initial;
+    a.dominance_ok = dominance_ok ? 1 : 0;
+    a.band = band;
+    a.budget = budget;
+    a.recv = d_recv;
+    a.ub = d_ub;
+    a.incumbent = d_incumbent;
+    a.fcap = caps.fcap;
+    a.gcap = caps.gcap;
+    for (int b = 0; b < 2; ++b) {
+      std::string tg = b ? "v2b_" : "v2a_";
+      FrontierV2& f = a.f[b];
+      f.status = c.buf<uint32_t>((tg + "status").c_str(), caps.fcap);
+      f.pid = c.buf<int32_t>((tg + "pid").c_str(), caps.fcap);
+      f.value = c.buf<double>((tg + "value").c_str(), caps.fcap);
+      f.lex = c.buf<uint64_t>((tg + "lex").c_str(), caps.fcap);
+      f.rank = c.buf<uint32_t>((tg + "rank").c_str(), caps.fcap);
+      f.alive = c.buf<uint8_t>((tg + "alive").c_str(), caps.fcap);
+      f.group = c.buf<int32_t>((tg + "group").c_str(), caps.fcap);
+      f.g_start = c.buf<int32_t>((tg + "gstart").c_str(), caps.gcap);
+      f.g_size = c.buf<int32_t>((tg + "gsize").c_str(), caps.gcap);
+      f.g_status = c.buf<uint32_t>((tg + "gstatus").c_str(), caps.gcap);
+      f.g_alive = c.buf<int32_t>((tg + "galive").c_str(), caps.gcap);
+      a.kid_cnt[b] = c.buf<int32_t>((tg + "kidcnt").c_str(), caps.fcap);
+      a.kid_cur[b] = c.buf<int32_t>((tg + "kidcur").c_str(), caps.fcap);
+      MGS_CUDA_OK(cudaMemsetAsync(a.kid_cnt[b], 0, static_cast<size_t>(caps.fcap) * 4, c.stream));
+      MGS_CUDA_OK(cudaMemsetAsync(a.kid_cur[b], 0, static_cast<size_t>(caps.fcap) * 4, c.stream));
+    }
+    a.kid_base = c.buf<int32_t>("v2_kidbase", caps.fcap + 1);
+    a.kid_items = c.buf<uint64_t>("v2_kiditems", caps.fcap);
+    a.big_bucket = c.buf<int32_t>("v2_bigbucket", caps.fcap);
+    a.hcap = caps.hcap;
+    a.h_parent = c.buf<int32_t>("v2_hparent", caps.hcap);
+    a.h_oi = c.buf<int32_t>("v2_hoi", caps.hcap);
+    a.hist_base = c.buf<long long>("v2_histbase", S + 2);
+    a.ucap = caps.ucap;
+    a.u_group = c.buf<int32_t>("v2_ugroup", caps.ucap);
+    a.u_sig = c.buf<int32_t>("v2_usig", caps.ucap);
+    a.u_ns = c.buf<int32_t>("v2_uns", caps.ucap);
+    a.u_chs = c.buf<int32_t>("v2_uchs", caps.ucap);
+    a.u_chb = c.buf<int32_t>("v2_uchb", caps.ucap);
+    a.u_cbase = c.buf<int32_t>("v2_ucbase", caps.ucap);
+    a.u_sbase = c.buf<int32_t>("v2_usbase", caps.ucap);
+    a.u_bbase = c.buf<int32_t>("v2_ubbase", caps.ucap);
+    a.hmask = (1 << caps.hbits) - 1;
+    a.hash = c.buf<unsigned long long>("v2_hash", a.hmask + 1);
+    MGS_CUDA_OK(cudaMemsetAsync(a.hash, 0, static_cast<size_t>(a.hmask + 1) * 8, c.stream));
+    a.nscap = caps.nscap;
+    a.ns_key = c.buf<uint32_t>("v2_nskey", caps.nscap);
+    a.ns_ucnt = c.buf<int32_t>("v2_nsucnt", caps.nscap);
+    a.ns_ccnt = c.buf<int32_t>("v2_nsccnt", caps.nscap);
+    a.ns_ubase = c.buf<int32_t>("v2_nsubase", caps.nscap);
+    a.ns_cbase = c.buf<int32_t>("v2_nscbase", caps.nscap);
+    a.ns_ucur = c.buf<int32_t>("v2_nsucur", caps.nscap);
+    a.ns_ccur = c.buf<int32_t>("v2_nsccur", caps.nscap);
+    a.ns_units = c.buf<int32_t>("v2_nsunits", caps.ucap);
+    a.ns_big = c.buf<int32_t>("v2_nsbig", caps.nscap);
+    a.ns_small = c.buf<int32_t>("v2_nssmall", caps.nscap);
+    for (int32_t* z : {a.ns_ucnt, a.ns_ccnt, a.ns_ucur, a.ns_ccur})
+      MGS_CUDA_OK(cudaMemsetAsync(z, 0, static_cast<size_t>(caps.nscap) * 4, c.stream));
+    a.itcap = caps.itcap;
+    a.it_s_unit = c.buf<int32_t>("v2_itsu", caps.itcap);
+    a.it_s_chunk = c.buf<int32_t>("v2_itsc", caps.itcap);
+    a.it_b_unit = c.buf<int32_t>("v2_itbu", caps.itcap);
+    a.it_b_chunk = c.buf<int32_t>("v2_itbc", caps.itcap);
+    a.ccap = caps.ccap;
+    a.c_value = c.buf<double>("v2_cvalue", caps.ccap);
+    a.c_lex = c.buf<uint64_t>("v2_clex", caps.ccap);
+    a.c_parent = c.buf<int32_t>("v2_cparent", caps.ccap);
+    a.c_pid = c.buf<int32_t>("v2_cpid", caps.ccap);
+    a.c_ok = c.buf<uint8_t>("v2_cok", caps.ccap);
+    a.c_live = c.buf<uint8_t>("v2_clive", caps.ccap);
+    a.pcnt = c.buf<int32_t>("v2_pcnt", sp.P1);
+    a.pbucket = c.buf<int32_t>("v2_pbucket", static_cast<size_t>(sp.P1) * 64);
+    MGS_CUDA_OK(cudaMemsetAsync(a.pcnt, 0, static_cast<size_t>(sp.P1) * 4, c.stream));
+    a.scan_cap = 5 * (caps.fcap / kTile + 8) + 4 * (caps.ucap / kTile + 8);
+    a.scan_state = c.buf<unsigned long long>("v2_scan", a.scan_cap);
+    MGS_CUDA_OK(cudaMemsetAsync(a.scan_state, 0, static_cast<size_t>(a.scan_cap) * 8, c.stream));
+    a.sig_len = c.buf<int32_t>("v2_siglen", sp.n_sig);
+    k_sig_len<<<ceil_div(sp.n_sig, 256), 256, 0, c.stream>>>(sp.sig_off, sp.n_sig, a.sig_len);
+    ++c.kernel_launches;
+    a.ctl = c.buf<Ctl>("v2_ctl", 1);
+    MGS_CUDA_OK(cudaMemsetAsync(a.ctl, 0, sizeof(Ctl), c.stream));
+    a.chosen = c.buf<int32_t>("v2_chosen", S);
+    a.n_partial = n_partial;
+    k_init_root<<<1, 32, 0, c.stream>>>(a, static_cast<uint32_t>(sp.root_pid));
+    ++c.kernel_launches;
+    void* args[] = {&a};
+    MGS_CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, kThreads, args, smem, c.stream));
+    ++c.kernel_launches;
+    Ctl h{};
+    MGS_CUDA_OK(cudaMemcpyAsync(&h, a.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
+    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+    if (h.err_code == kOverflow) {
+      const long long need = h.need;
+      switch (h.need_what) {
+        case 1: caps.nscap = static_cast<int>(std::max<long long>(need * 2, caps.nscap * 2ll)); break;
+        case 2: caps.hbits += 2; break;
+        case 3: caps.ucap = static_cast<int>(std::max<long long>(need * 2, caps.ucap * 2ll)); break;
+        case 4: caps.fcap = static_cast<int>(std::max<long long>(need * 2, caps.fcap * 2ll)); break;
+        case 5: caps.gcap = static_cast<int>(std::max<long long>(need * 2, caps.gcap * 2ll)); break;
+        case 6: caps.hcap = std::max<long long>(need * 2, caps.hcap * 2); break;
+        case 7: caps.ccap = static_cast<int>(std::max<long long>(need * 2, caps.ccap * 2ll)); break;
+        case 8: caps.itcap = static_cast<int>(std::max<long long>(need * 2, caps.itcap * 2ll)); break;
+        default: throw PlanFail{MGS_ERR_CUDA, "persistent DP: unknown capacity overflow"};
+      }
+      if (caps.nscap > caps.ucap) caps.ucap = caps.nscap;
+      while ((1 << caps.hbits) < 4 * caps.nscap) ++caps.hbits;
+      continue;
+    }
+    if (h.err_code == MGS_ERR_STATE_BUDGET)
+      throw PlanFail{MGS_ERR_STATE_BUDGET,
+                     "dynamic-program frontier reached " + std::to_string(h.err_count) + " states at step " +
+                         std::to_string(h.err_step) + " (budget " + std::to_string(budget) + ")",
+                     h.err_step, h.err_count};
+    if (h.err_code == MGS_ERR_INFEASIBLE_JOINT)
+      throw PlanFail{MGS_ERR_INFEASIBLE_JOINT, "no feasible allocation sequence exists for this window"};
+    if (h.err_code != 0) throw PlanFail{MGS_ERR_CUDA, "persistent DP: error " + std::to_string(h.err_code)};
+    out.options.resize(S);
+    MGS_CUDA_OK(cudaMemcpyAsync(out.options.data(), a.chosen, S * 4, cudaMemcpyDeviceToHost, c.stream));
+    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+    out.stats.options = sp.n_opt;
+    out.stats.candidates = sp.n_cand;
+    out.stats.transitions_ref = h.tr_ref;
+    out.stats.transitions = h.tr;
+    out.stats.frontier_total = h.ftot;
+    out.stats.frontier_peak = h.fpeak;
+    out.stats.transition_bytes = h.tbytes;
+    return;
+  }
+  throw PlanFail{MGS_ERR_CUDA, "persistent DP: capacity growth did not converge"};
+}
+
+}  // namespace mgs

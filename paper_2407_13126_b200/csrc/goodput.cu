@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(1024) k_greedy(DevSpace sp, HostTables t, Recv
   __shared__ int s_state[KM];
   __shared__ uint64_t s_ids;
   __shared__ double s_value;
-  __shared__ int s_alive, s_best_ci;
+  __shared__ int s_alive;
   const Codec codec{t.S};
   if (threadIdx.x == 0) {
     for (int m = 0; m < KM; ++m) s_state[m] = 0;
@@ -136,7 +136,6 @@ __global__ void __launch_bounds__(1024) k_greedy(DevSpace sp, HostTables t, Recv
           ci = s_ci[w];
         }
       }
-      s_best_ci = ci;
       if (ci < 0) {
         s_alive = 0;
         greedy[s] = -1;
