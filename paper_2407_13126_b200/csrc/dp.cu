@@ -22,6 +22,8 @@
 // Lex ranks: inside one frontier the dense rank orders states exactly like
 // their lex keys, so rank replaces lex in every within-frontier comparison.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cub/cub.cuh>
 
 #include "ctx.cuh"
@@ -908,6 +910,9 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
       ++c.kernel_launches;
     }
     MGS_CUDA_OK(cudaGetLastError());
+    if (std::getenv("MGS_DEBUG_STEPS"))
+      std::fprintf(stderr, "v1 step %d units %d ns %d T %d store %d groups %d alive_in %d\n", s, NU, n_ns, T, n_next,
+                   g_next, cur.n);
     ftot += n_next;
     fpeak = std::max<uint64_t>(fpeak, n_next);
     cur = nx;

@@ -32,6 +32,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "ctx.cuh"
@@ -49,7 +50,6 @@ constexpr int kChunkB = 512;        // targets per CTA item
 constexpr int kTile = kThreads * 8;  // scan tile
 constexpr int kBigNs = 1024;        // successor statuses with more candidates use the CTA path
 constexpr int kMergeWin = 2048;     // pid window of the CTA merge table
-constexpr int kSortCap = 4096;      // children buckets sorted in shared memory
 
 enum Err : int { kOk = 0, kOverflow = 100 };
 
@@ -126,7 +126,6 @@ struct V2 {
   int32_t* kid_cur[2];
   int32_t* kid_base;
   uint64_t* kid_items;
-  int32_t* big_bucket;
   int32_t* pcnt;
   int32_t* pbucket;
   unsigned long long* scan_state;
@@ -134,7 +133,9 @@ struct V2 {
   int32_t* sig_len;  // [n_sig]
   Ctl* ctl;
   int32_t* chosen;
-  int n_partial;  // entries of the partial-subset tables (all subsets but the full one)
+  int n_partial;
+  long long* dbg;  // [S][6] per-step counters (debug dump)
+  unsigned long long* dbg_time;  // [phases] barrier timestamps (debug)  // entries of the partial-subset tables (all subsets but the full one)
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
@@ -157,8 +158,15 @@ __device__ void raise_err(const V2& a, int phi, int code, int step = 0, unsigned
 
 // grid barrier + uniform error check (errors raised in phase phi become
 // visible to every CTA after the barrier that ends phi)
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ bool barrier(cg::grid_group& grid, const V2& a, int& phi) {
   grid.sync();
+  if (a.dbg_time && blockIdx.x == 0 && threadIdx.x == 0) a.dbg_time[phi] = globaltimer();
   const int e = ld_volatile(&a.ctl->err[phi & 1]);
   ++phi;
   return e != 0;
@@ -384,70 +392,25 @@ __device__ void phase_place(const V2& a, int s, int phi) {
     const int pr = static_cast<int>(F.lex[i] >> 32);
     const int q = atomicAdd(&a.kid_cur[cur][pr], 1);
     a.kid_items[a.kid_base[pr] + q] = ((F.lex[i] & 0xffffffffull) << 32) | static_cast<uint32_t>(i);
-    if (q == 0 && a.kid_cnt[cur][pr] > 32) a.big_bucket[atomicAdd(&sc.n_big_bucket, 1)] = pr;
   }
 }
 
-// S4: dense ranks of F_s = parent's child offset + position by option index
-__device__ void phase_ranks(const V2& a, int s, unsigned long long* sm64) {
+// S4: dense ranks of F_s = parent's first child slot + position of the option
+// index among the parent's children. Thread per bucket slot: slots of one
+// parent are adjacent, so a warp's bucket reads are broadcasts.
+__device__ void phase_ranks(const V2& a, int s) {
   const int cur = s & 1;
-  StepCounters& sc = a.ctl->sc[s & 1];
   const FrontierV2& F = a.f[cur];
-  __shared__ int s_b;
-  // big buckets: CTA bitonic sort in shared memory
-  while (true) {
-    if (threadIdx.x == 0) s_b = atomicAdd(&sc.cur_bucket, 1);
-    __syncthreads();
-    const int b = s_b;
-    __syncthreads();
-    if (b >= sc.n_big_bucket) break;
-    const int pr = a.big_bucket[b];
-    const int base = a.kid_base[pr], c = a.kid_cnt[cur][pr];
-    if (c <= kSortCap) {
-      int n2 = 1;
-      while (n2 < c) n2 <<= 1;
-      for (int i = threadIdx.x; i < n2; i += kThreads) sm64[i] = i < c ? a.kid_items[base + i] : ~0ull;
-      __syncthreads();
-      for (int k = 2; k <= n2; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          for (int i = threadIdx.x; i < n2; i += kThreads) {
-            const int l = i ^ j;
-            if (l > i) {
-              const unsigned long long x = sm64[i], y = sm64[l];
-              const bool up = (i & k) == 0;
-              if ((x > y) == up) {
-                sm64[i] = y;
-                sm64[l] = x;
-              }
-            }
-          }
-          __syncthreads();
-        }
-      for (int i = threadIdx.x; i < c; i += kThreads) F.rank[static_cast<uint32_t>(sm64[i])] = base + i;
-      __syncthreads();
-    } else {  // beyond shared memory: quadratic counting (rare, correct)
-      for (int i = threadIdx.x; i < c; i += kThreads) {
-        const unsigned long long me = a.kid_items[base + i];
-        int pos = 0;
-        for (int k = 0; k < c; ++k) pos += a.kid_items[base + k] < me;
-        F.rank[static_cast<uint32_t>(me)] = base + pos;
-      }
-      __syncthreads();
-    }
-  }
-  // small buckets: thread per state
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
-  const int n = a.ctl->n_store[cur];
+  const int n = a.ctl->scan_total[4];  // live states of F_s = filled slots
   for (int i = gtid; i < n; i += gstride) {
-    if (!F.alive[i]) continue;
-    const int pr = static_cast<int>(F.lex[i] >> 32);
-    const int c = a.kid_cnt[cur][pr];
-    if (c > 32) continue;
-    const int base = a.kid_base[pr];
-    const unsigned long long me = ((F.lex[i] & 0xffffffffull) << 32) | static_cast<uint32_t>(i);
+    const unsigned long long me = a.kid_items[i];
+    const int idx = static_cast<int>(me & 0xffffffffu);
+    const int pr = static_cast<int>(F.lex[idx] >> 32);
+    const int base = a.kid_base[pr], c = a.kid_cnt[cur][pr];
     int pos = 0;
     for (int k = 0; k < c; ++k) pos += a.kid_items[base + k] < me;
-    F.rank[i] = base + pos;
+    F.rank[idx] = base + pos;
   }
 }
 
@@ -837,23 +800,23 @@ __device__ void phase_merge_out(const V2& a, int s, int phi, unsigned long long*
       }
       __syncthreads();
       if (s_q0 >= 0) {
-        // ordered compaction of survivors (block scan over chunks)
-        int run = 0;
-        for (int c0 = cb; c0 < cb + cc; c0 += kThreads) {
-          const int k = c0 + threadIdx.x;
-          const bool keep = k < cb + cc && a.c_live[k];
-          const unsigned bal = __ballot_sync(0xffffffffu, keep);
-          if ((threadIdx.x & 31) == 0) s_wsum[threadIdx.x >> 5] = __popc(bal);
-          __syncthreads();
-          int off = run;
-          for (int w2 = 0; w2 < (threadIdx.x >> 5); ++w2) off += s_wsum[w2];
-          off += __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
-          if (keep) write_state(a, s, nxt, s_q0 + off, s_g, a.ns_key[id], k);
-          int tot = 0;
-          for (int w2 = 0; w2 < kWarps; ++w2) tot += s_wsum[w2];
-          run += tot;
-          __syncthreads();
+        // ordered compaction: each thread owns a contiguous candidate range
+        const int per = (cc + kThreads - 1) / kThreads;
+        const int lo = cb + threadIdx.x * per, hi = min(cb + cc, lo + per);
+        int mine = 0;
+        for (int k = lo; k < hi; ++k) mine += a.c_live[k];
+        int x = mine;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if ((threadIdx.x & 31) >= o) x += y;
         }
+        if ((threadIdx.x & 31) == 31) s_wsum[threadIdx.x >> 5] = x;
+        __syncthreads();
+        int off = x - mine;
+        for (int w2 = 0; w2 < (threadIdx.x >> 5); ++w2) off += s_wsum[w2];
+        const uint32_t key = a.ns_key[id];
+        for (int k = lo; k < hi; ++k)
+          if (a.c_live[k]) write_state(a, s, nxt, s_q0 + off++, s_g, key, k);
       }
     }
     __syncthreads();
@@ -1031,7 +994,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve_v2(V2 a) {
       phase_place(a, s, phi);
     if (barrier(grid, a, phi)) return;
     // S4
-    phase_ranks(a, s, smem_u64);
+    phase_ranks(a, s);
     if (barrier(grid, a, phi)) return;
     // S5
     // the shared-memory tables are clobbered by S4/S6: start each S5 clean
@@ -1067,7 +1030,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve_v2(V2 a) {
         a.kid_cnt[cur][i] = 0;
         a.kid_cur[cur][i] = 0;
       }
-      if (gtid == 0) a.hist_base[s + 2 <= a.S ? s + 2 : a.S] = a.hist_base[s + 1] + ctl->n_store[nxt];
+      if (gtid == 0) a.hist_base[s + 2] = a.hist_base[s + 1] + ctl->n_store[nxt];  // array has S+2 entries
+    }
+    if (gtid == 0) {
+      long long* d = a.dbg + 6ll * s;
+      d[0] = sc.n_units;
+      d[1] = sc.n_ns;
+      d[2] = sc.T;
+      d[3] = ctl->n_store[nxt];
+      d[4] = ctl->n_groups[nxt];
+      d[5] = alive_cur;
     }
     ranks_prev = alive_cur;
     if (barrier(grid, a, phi)) return;
@@ -1185,7 +1157,7 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
   const int n_sub = 1 << M;
   const int n_partial = sp.proj_base[n_sub - 1];  // all subsets but the full one
   const size_t smem_trans = static_cast<size_t>(sp.P1) * 8 + static_cast<size_t>(n_partial) * 20;
-  const size_t smem = std::max({smem_trans, static_cast<size_t>(2 * kMergeWin * 8), static_cast<size_t>(kSortCap * 8)});
+  const size_t smem = std::max(smem_trans, static_cast<size_t>(2 * kMergeWin * 8));
   auto kern = M == 1 ? k_solve_v2<1> : k_solve_v2<2>;
   MGS_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int occ = 0;
@@ -1230,7 +1202,6 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     }
     a.kid_base = c.buf<int32_t>("v2_kidbase", caps.fcap + 1);
     a.kid_items = c.buf<uint64_t>("v2_kiditems", caps.fcap);
-    a.big_bucket = c.buf<int32_t>("v2_bigbucket", caps.fcap);
     a.hcap = caps.hcap;
     a.h_parent = c.buf<int32_t>("v2_hparent", caps.hcap);
     a.h_oi = c.buf<int32_t>("v2_hoi", caps.hcap);
@@ -1284,6 +1255,8 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     a.ctl = c.buf<Ctl>("v2_ctl", 1);
     MGS_CUDA_OK(cudaMemsetAsync(a.ctl, 0, sizeof(Ctl), c.stream));
     a.chosen = c.buf<int32_t>("v2_chosen", S);
+    a.dbg = c.buf<long long>("v2_dbg", 6 * S);
+    a.dbg_time = std::getenv("MGS_DEBUG_STEPS") ? c.buf<unsigned long long>("v2_dbgt", 8 * S + 16) : nullptr;
     a.n_partial = n_partial;
     k_init_root<<<1, 32, 0, c.stream>>>(a, static_cast<uint32_t>(sp.root_pid));
     ++c.kernel_launches;
@@ -1321,6 +1294,28 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     out.options.resize(S);
     MGS_CUDA_OK(cudaMemcpyAsync(out.options.data(), a.chosen, S * 4, cudaMemcpyDeviceToHost, c.stream));
     MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+    if (std::getenv("MGS_DEBUG_STEPS")) {
+      std::vector<long long> d(6 * S);
+      MGS_CUDA_OK(cudaMemcpy(d.data(), a.dbg, d.size() * 8, cudaMemcpyDeviceToHost));
+      for (int s = 0; s < S; ++s)
+        std::fprintf(stderr, "v2 step %d units %lld ns %lld T %lld store %lld groups %lld alive_in %lld\n", s, d[6 * s],
+                     d[6 * s + 1], d[6 * s + 2], d[6 * s + 3], d[6 * s + 4], d[6 * s + 5]);
+      if (a.dbg_time) {
+        std::vector<unsigned long long> tm(8 * S + 16);
+        MGS_CUDA_OK(cudaMemcpy(tm.data(), a.dbg_time, tm.size() * 8, cudaMemcpyDeviceToHost));
+        double ph[7] = {0, 0, 0, 0, 0, 0, 0};
+        for (int s = 0; s < S; ++s)
+          for (int k = 0; k < 7; ++k) {
+            const int i = 7 * s + k;
+            if (i > 0) ph[k] += (tm[i] - tm[i - 1]) * 1e-3;
+          }
+        std::fprintf(stderr, "v2 phase us (sum over steps): units %.1f scans %.1f place %.1f ranks %.1f trans %.1f merge %.1f dom %.1f\n",
+                     ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[6]);
+      }
+      std::fprintf(stderr, "v2 chosen:");
+      for (int s = 0; s < S; ++s) std::fprintf(stderr, " %d", out.options[s]);
+      std::fprintf(stderr, "\n");
+    }
     out.stats.options = sp.n_opt;
     out.stats.candidates = sp.n_cand;
     out.stats.transitions_ref = h.tr_ref;
