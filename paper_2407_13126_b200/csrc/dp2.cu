@@ -50,6 +50,9 @@ constexpr int kChunkB = 512;        // targets per CTA item
 constexpr int kTile = kThreads * 8;  // scan tile
 constexpr int kBigNs = 1024;        // successor statuses with more candidates use the CTA path
 constexpr int kMergeWin = 2048;     // pid window of the CTA merge table
+constexpr int kBucketSmall = 64;    // child buckets up to this size: thread per slot
+constexpr int kBucketChunks = 16;   // CTA items per big bucket (256 slots each)
+constexpr int kBucketStage = 4096;  // big buckets staged in shared memory
 
 enum Err : int { kOk = 0, kOverflow = 100 };
 
@@ -126,6 +129,7 @@ struct V2 {
   int32_t* kid_cur[2];
   int32_t* kid_base;
   uint64_t* kid_items;
+  int32_t* big_bucket;
   int32_t* pcnt;
   int32_t* pbucket;
   unsigned long long* scan_state;
@@ -319,7 +323,8 @@ __device__ int ns_get_id(const V2& a, StepCounters& sc, uint32_t key, int phi, i
 }
 
 // ---------------------------------------------------------------------------
-// S1: units of every live group + children per parent
+// S1: units of every live group + children per parent. Warp per group; lanes
+// split the (<= 8^M) per-tenant retraining-size combinations (solvers.hpp:379-411).
 template <int M>
 __device__ void phase_units(const V2& a, int s, int phi) {
   const int cur = s & 1;
@@ -327,18 +332,64 @@ __device__ void phase_units(const V2& a, int s, int phi) {
   const FrontierV2& F = a.f[cur];
   const int G = a.ctl->n_groups[cur];
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31, wid = gtid >> 5, nw = gstride >> 5;
+  const Codec codec{a.t.S};
   unsigned long long ref = 0;
-  for (int g = gtid; g < G; g += gstride) {
+  for (int g = wid; g < G; g += nw) {
     if (F.g_alive[g] <= 0) continue;
     const int gsize = F.g_size[g];
-    for_each_unit(M, a.t.S, a.t.rt, a.t.min_rt, a.sp.sig_nopt, F.g_status[g], s, [&](int sig, uint64_t ns) {
-      const int u = atomicAdd(&sc.n_units, 1);
+    const uint32_t status = F.g_status[g];
+    int st[M], sizes[M][9], cnt[M], total = 1;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {  // allowed_sizes (solvers.hpp:79-97)
+      st[m] = static_cast<int>((status >> (16 * m)) & 0xffff);
+      cnt[m] = 0;
+      if (Codec::is_running(st[m])) {
+        sizes[m][cnt[m]++] = codec.run_size(st[m]);
+      } else if (st[m] == Codec::done()) {
+        sizes[m][cnt[m]++] = 0;
+      } else {
+        if (a.t.min_rt[m] >= 0 && s + 1 + a.t.min_rt[m] <= a.t.S) sizes[m][cnt[m]++] = 0;
+        for (int k = 1; k <= 7; ++k)
+          if (a.t.rt[m][k] >= 1 && s + a.t.rt[m][k] <= a.t.S) sizes[m][cnt[m]++] = k;
+      }
+      total *= cnt[m];
+    }
+    for (int c0 = 0; c0 < total; c0 += 32) {
+      const int c = c0 + lane;
+      bool ok = c < total;
+      int sig = 0;
+      uint32_t ns = 0;
+      if (ok) {
+        int rem = c, pick[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          pick[m] = rem % cnt[m];
+          rem /= cnt[m];
+        }
+#pragma unroll
+        for (int m = M - 1; m >= 0; --m) sig = sig * 8 + sizes[m][pick[m]];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int adv = codec.advance(a.t.rt[m], st[m], sizes[m][pick[m]], s);
+          ok = ok && adv >= 0 && !(adv == 0 && (a.t.min_rt[m] < 0 || s + 1 + a.t.min_rt[m] > a.t.S));
+          ns |= static_cast<uint32_t>(adv < 0 ? 0 : adv) << (16 * m);
+        }
+        ok = ok && a.sp.sig_nopt[sig] > 0;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, ok);
+      if (!bal) continue;
+      int ubase = 0;
+      if (lane == 0) ubase = atomicAdd(&sc.n_units, __popc(bal));
+      ubase = __shfl_sync(0xffffffffu, ubase, 0);
+      if (!ok) continue;
+      const int u = ubase + __popc(bal & ((1u << lane) - 1u));
       if (u >= a.ucap) {
         raise_err(a, phi, kOverflow, s, 0, 3, u + 1);
-        return;
+        continue;
       }
-      const int id = ns_get_id(a, sc, static_cast<uint32_t>(ns), phi, s);
-      if (id < 0) return;
+      const int id = ns_get_id(a, sc, ns, phi, s);
+      if (id < 0) continue;
       const int L = a.sig_len[sig];
       a.u_group[u] = g;
       a.u_sig[u] = sig;
@@ -349,10 +400,10 @@ __device__ void phase_units(const V2& a, int s, int phi) {
       atomicAdd(&a.ns_ucnt[id], 1);
       atomicAdd(&a.ns_ccnt[id], L);
       ref += static_cast<unsigned long long>(a.sp.sig_nopt[sig]);
-    });
+    }
   }
   for (int o = 16; o > 0; o >>= 1) ref += __shfl_down_sync(0xffffffffu, ref, o);
-  if ((threadIdx.x & 31) == 0 && ref) atomicAdd(&a.ctl->tr_ref, ref);
+  if (lane == 0 && ref) atomicAdd(&a.ctl->tr_ref, ref);
   // children per parent (rank buckets of F_s)
   const int n = a.ctl->n_store[cur];
   for (int i = gtid; i < n; i += gstride)
@@ -381,7 +432,7 @@ __device__ void phase_place(const V2& a, int s, int phi) {
   }
   for (int id = gtid; id < NS; id += gstride) {
     if (a.ns_ucnt[id] == 0) continue;  // reserved id lost to a concurrent insert
-    const bool big = a.ns_ccnt[id] > kBigNs;
+    const bool big = a.ns_ucnt[id] > 1 || a.ns_ccnt[id] > kBigNs;
     if (big) a.ns_big[atomicAdd(&sc.n_ns_big, 1)] = id;
     else a.ns_small[atomicAdd(&sc.n_ns_small, 1)] = id;
   }
@@ -392,22 +443,52 @@ __device__ void phase_place(const V2& a, int s, int phi) {
     const int pr = static_cast<int>(F.lex[i] >> 32);
     const int q = atomicAdd(&a.kid_cur[cur][pr], 1);
     a.kid_items[a.kid_base[pr] + q] = ((F.lex[i] & 0xffffffffull) << 32) | static_cast<uint32_t>(i);
+    if (q == 0 && a.kid_cnt[cur][pr] > kBucketSmall) a.big_bucket[atomicAdd(&sc.n_big_bucket, 1)] = pr;
   }
 }
 
 // S4: dense ranks of F_s = parent's first child slot + position of the option
-// index among the parent's children. Thread per bucket slot: slots of one
-// parent are adjacent, so a warp's bucket reads are broadcasts.
-__device__ void phase_ranks(const V2& a, int s) {
+// index among the parent's children. Small buckets: thread per slot (slots of
+// one parent are adjacent, so bucket reads are warp broadcasts). Big buckets:
+// CTA items of 256 slots counting against the bucket staged in shared memory.
+__device__ void phase_ranks(const V2& a, int s, unsigned long long* sm64) {
   const int cur = s & 1;
+  StepCounters& sc = a.ctl->sc[s & 1];
   const FrontierV2& F = a.f[cur];
+  __shared__ int s_v;
+  const int nb = sc.n_big_bucket;
+  while (true) {
+    if (threadIdx.x == 0) s_v = atomicAdd(&sc.cur_bucket, 1);
+    __syncthreads();
+    const int v = s_v;
+    __syncthreads();
+    if (v >= nb * kBucketChunks) break;
+    const int pr = a.big_bucket[v / kBucketChunks], chunk = v % kBucketChunks;
+    const int base = a.kid_base[pr], c = a.kid_cnt[cur][pr];
+    if (chunk * kThreads >= c) continue;
+    const bool staged = c <= kBucketStage;
+    if (staged) {
+      for (int k = threadIdx.x; k < c; k += kThreads) sm64[k] = a.kid_items[base + k];
+      __syncthreads();
+    }
+    const unsigned long long* keys = staged ? sm64 : reinterpret_cast<const unsigned long long*>(a.kid_items + base);
+    for (int i = chunk * kThreads + threadIdx.x; i < c; i += kThreads * kBucketChunks) {
+      const unsigned long long me = keys[i];
+      int pos = 0;
+      for (int k = 0; k < c; ++k) pos += keys[k] < me;
+      F.rank[static_cast<uint32_t>(me)] = base + pos;
+    }
+    __syncthreads();
+  }
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const int n = a.ctl->scan_total[4];  // live states of F_s = filled slots
   for (int i = gtid; i < n; i += gstride) {
     const unsigned long long me = a.kid_items[i];
     const int idx = static_cast<int>(me & 0xffffffffu);
     const int pr = static_cast<int>(F.lex[idx] >> 32);
-    const int base = a.kid_base[pr], c = a.kid_cnt[cur][pr];
+    const int c = a.kid_cnt[cur][pr];
+    if (c > kBucketSmall) continue;
+    const int base = a.kid_base[pr];
     int pos = 0;
     for (int k = 0; k < c; ++k) pos += a.kid_items[base + k] < me;
     F.rank[idx] = base + pos;
@@ -882,6 +963,14 @@ __device__ void phase_merge_out(const V2& a, int s, int phi, unsigned long long*
   }
 }
 
+// decoded-status form of status_dominates: equal, or x done, or both running on
+// the same size with x's remaining steps <= y's
+__device__ __forceinline__ bool dom_decoded(uint32_t x, uint32_t y) {
+  if (x == y) return true;
+  if ((x >> 24) == 1) return true;
+  return (x >> 24) == 2 && (y >> 24) == 2 && ((x ^ y) & 0x00ff0000u) == 0 && (x & 0xffffu) <= (y & 0xffffu);
+}
+
 // S7: status dominance within placement buckets (solvers.hpp:514-537)
 __device__ void phase_dominance(const V2& a, int s) {
   const int nxt = (s + 1) & 1;
@@ -904,17 +993,28 @@ __device__ void phase_dominance(const V2& a, int s) {
         v[h] = q[h] >= 0 ? N.value[q[h]] : 0.0;
         lx[h] = q[h] >= 0 ? N.lex[q[h]] : 0;
       }
+      // decode every tenant status once: kind (0 idle, 1 done, 2 running) | size | rem
+      uint32_t dk[2][2];
+      for (int h = 0; h < 2; ++h)
+        for (int m = 0; m < 2; ++m) {
+          const int code = m < a.t.M ? static_cast<int>((st[h] >> (16 * m)) & 0xffff) : 0;
+          dk[h][m] = code == Codec::done() ? (1u << 24)
+                     : Codec::is_running(code)
+                         ? (2u << 24) | (static_cast<uint32_t>(codec.run_size(code)) << 16) |
+                               static_cast<uint32_t>(codec.run_rem(code))
+                         : 0u;
+        }
       bool dead[2] = {false, false};
       for (int j = 0; j < n; ++j) {
         const int h = j >> 5, src = j & 31;
-        const uint32_t sa = __shfl_sync(0xffffffffu, st[h], src);
+        const uint32_t d0 = __shfl_sync(0xffffffffu, dk[h][0], src);
+        const uint32_t d1 = __shfl_sync(0xffffffffu, dk[h][1], src);
         const double va = __shfl_sync(0xffffffffu, v[h], src);
         const uint64_t la = __shfl_sync(0xffffffffu, lx[h], src);
         for (int hb = 0; hb < 2; ++hb) {
           if (q[hb] < 0 || lane + 32 * hb == j) continue;
-          bool dom = true;
-          for (int m = 0; m < a.t.M && dom; ++m)
-            dom = status_dominates(codec, (sa >> (16 * m)) & 0xffff, (st[hb] >> (16 * m)) & 0xffff);
+          // status_dominates (solvers.hpp:128-134) on decoded fields, every tenant
+          const bool dom = dom_decoded(d0, dk[hb][0]) && dom_decoded(d1, dk[hb][1]);
           if (dom && better(va, la, v[hb], lx[hb])) dead[hb] = true;
         }
       }
@@ -945,6 +1045,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve_v2(V2 a) {
   uint32_t tag = 0;
   __syncthreads();
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  if (a.dbg_time) {  // barrier cost probe (debug only)
+    grid.sync();
+    const unsigned long long t0 = globaltimer();
+    for (int k = 0; k < 64; ++k) grid.sync();
+    if (gtid == 0) a.dbg_time[8 * a.S + 8] = (globaltimer() - t0) / 64;
+  }
   int phi = 0;
   int ranks_prev = 1;  // live states of F_{s-1} (parent rank space); root: 1
   for (int s = 0; s < a.S; ++s) {
@@ -994,7 +1100,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve_v2(V2 a) {
       phase_place(a, s, phi);
     if (barrier(grid, a, phi)) return;
     // S4
-    phase_ranks(a, s);
+    phase_ranks(a, s, smem_u64);
     if (barrier(grid, a, phi)) return;
     // S5
     // the shared-memory tables are clobbered by S4/S6: start each S5 clean
@@ -1157,7 +1263,7 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
   const int n_sub = 1 << M;
   const int n_partial = sp.proj_base[n_sub - 1];  // all subsets but the full one
   const size_t smem_trans = static_cast<size_t>(sp.P1) * 8 + static_cast<size_t>(n_partial) * 20;
-  const size_t smem = std::max(smem_trans, static_cast<size_t>(2 * kMergeWin * 8));
+  const size_t smem = std::max({smem_trans, static_cast<size_t>(2 * kMergeWin * 8), static_cast<size_t>(kBucketStage * 8)});
   auto kern = M == 1 ? k_solve_v2<1> : k_solve_v2<2>;
   MGS_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int occ = 0;
@@ -1243,6 +1349,7 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     a.c_pid = c.buf<int32_t>("v2_cpid", caps.ccap);
     a.c_ok = c.buf<uint8_t>("v2_cok", caps.ccap);
     a.c_live = c.buf<uint8_t>("v2_clive", caps.ccap);
+    a.big_bucket = c.buf<int32_t>("v2_bigbucket", caps.fcap);
     a.pcnt = c.buf<int32_t>("v2_pcnt", sp.P1);
     a.pbucket = c.buf<int32_t>("v2_pbucket", static_cast<size_t>(sp.P1) * 64);
     MGS_CUDA_OK(cudaMemsetAsync(a.pcnt, 0, static_cast<size_t>(sp.P1) * 4, c.stream));
@@ -1309,8 +1416,8 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
             const int i = 7 * s + k;
             if (i > 0) ph[k] += (tm[i] - tm[i - 1]) * 1e-3;
           }
-        std::fprintf(stderr, "v2 phase us (sum over steps): units %.1f scans %.1f place %.1f ranks %.1f trans %.1f merge %.1f dom %.1f\n",
-                     ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[6]);
+        std::fprintf(stderr, "v2 phase us (sum over steps): units %.1f scans %.1f place %.1f ranks %.1f trans %.1f merge %.1f dom %.1f | grid.sync %.2f us\n",
+                     ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[6], tm[8 * S + 8] * 1e-3);
       }
       std::fprintf(stderr, "v2 chosen:");
       for (int s = 0; s < S; ++s) std::fprintf(stderr, " %d", out.options[s]);
