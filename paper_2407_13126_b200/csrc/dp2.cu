@@ -1,30 +1,34 @@
 // Persistent single-launch DP engine (M <= 2): the whole per-window search of
 // solve_dp (solvers.hpp:242-579) as ONE cooperative kernel, 7 grid barriers per
-// slot, no host round trips, no sorts.
+// slot, no host round trips, no sorts, no hot (same-address) global atomics.
 //
 // Same procedure as the reference (and as the multi-launch engine in dp.cu):
 // subset representatives per status group, subset-candidate predecessor choice
 // + exact fold, strict bound test, equal-key merge, band, status dominance in
 // placement buckets of <= 64, state budget, dense lex ranks, terminal + parent
-// walk. What differs is only how the work is laid out on B200:
+// walk. What differs is how the work is laid out on B200:
 //
 //   per slot s (F_s = current frontier, status groups contiguous in HBM)
-//   S1  units: thread per group enumerates (signature, successor status);
-//       successor statuses get ids from an open-addressing hash (no sort);
-//       per-id unit / candidate counters. Also: children per parent (ranks).
-//   S2  five decoupled-look-back scans in one pass (candidate and unit offsets
-//       per successor status, warp / CTA work items per unit, child offsets per
-//       parent).
+//   S1  units: CTAs own contiguous group ranges; a warp per group enumerates
+//       the (signature, successor status) combinations lane-parallel; unit
+//       slots are reserved with ONE atomic per CTA batch; successor statuses
+//       are keyed by their slot in an open-addressing hash (the slot *is* the
+//       id). Also: children per parent (for the ranks) and live-state count.
+//   S2  seven decoupled-look-back scans in one pass (candidate / unit offsets
+//       per successor status, big / small status lists, warp / CTA work items
+//       per unit, child offsets per parent).
 //   S3  placement: units get contiguous candidate ranges inside their status,
-//       work items are materialised, children are bucketed by parent.
-//   S4  dense lex ranks of F_s: rank = first child slot of the parent + rank of
-//       the option index inside the parent's bucket (lex = parent rank, option).
+//       work items and status lists are materialised, children are bucketed
+//       by parent.
+//   S4  dense lex ranks of F_s: rank = first child slot of the parent + rank
+//       of the option index inside the parent's bucket (lex = (rank, option)).
 //   S5  transitions: CTAs take big-group items (shared-memory subset tables
 //       built with a two-phase max-value / min-rank reduction), warps take
 //       small-group items (broadcast scan of the group's states).
-//   S6  per successor status: equal-key merge across its units, band, output
-//       of the surviving states straight into F_{s+1} (atomic segment
-//       allocation), history, dominance buckets.
+//   S6  per successor status: equal-key merge across its units (multi-unit
+//       statuses, CTA, dense shared-memory table), band, output of the
+//       survivors straight into F_{s+1} (one allocation atomic per CTA batch),
+//       history, dominance buckets.
 //   S7  status dominance per placement bucket (2..64 states); resets.
 //
 // Dead (dominated) states stay in F_{s+1} as holes flagged alive = 0 and are
@@ -44,20 +48,23 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kSmall = 128;         // groups up to this size: warp path
-constexpr int kChunkS = 32;         // targets per warp item
-constexpr int kChunkB = 512;        // targets per CTA item
+constexpr int kSmall = 128;          // groups up to this size: warp path
+constexpr int kChunkS = 32;          // targets per warp item
+constexpr int kChunkB = 512;         // targets per CTA item
 constexpr int kTile = kThreads * 8;  // scan tile
-constexpr int kBigNs = 1024;        // successor statuses with more candidates use the CTA path
-constexpr int kMergeWin = 2048;     // pid window of the CTA merge table
-constexpr int kBucketSmall = 64;    // child buckets up to this size: thread per slot
-constexpr int kBucketChunks = 16;   // CTA items per big bucket (256 slots each)
-constexpr int kBucketStage = 4096;  // big buckets staged in shared memory
+constexpr int kBigNs = 1024;         // single-unit statuses with more candidates use the CTA path
+constexpr int kMergeWin = 2048;      // pid window of the CTA merge table
+constexpr int kBucketSmall = 64;     // child buckets up to this size: thread per slot
+constexpr int kBucketChunks = 16;    // CTA items per big bucket (256 slots each)
+constexpr int kBucketStage = 4096;   // big buckets staged in shared memory
+constexpr int kBatch = 512;          // groups / statuses per CTA allocation batch
+constexpr int kNumScans = 7;
 
 enum Err : int { kOk = 0, kOverflow = 100 };
 
 struct FrontierV2 {
   uint32_t* status;
+  uint32_t* ids;  // placement's per-tenant mask ids (16 bits each)
   int32_t* pid;
   double* value;
   uint64_t* lex;
@@ -70,9 +77,8 @@ struct FrontierV2 {
   int32_t* g_alive;
 };
 
-struct StepCounters {  // reset for the step after next (double buffered)
-  int n_units, n_ns, T, items_s, items_b, ticket, cur_big, cur_small, n_big_bucket, n_ns_big, n_ns_small,
-      cur_ns_big, cur_ns_small, cur_bucket, pad;
+struct StepCounters {  // double buffered; zeroed one step ahead
+  int n_units, T, items_s, items_b, n_big, n_small, n_big_bucket, ticket, kids;
 };
 
 struct Ctl {
@@ -81,15 +87,14 @@ struct Ctl {
   unsigned long long err_count;
   long long need;
   int need_what;
-  int n_store[2];   // storage size of F (incl. dead)
+  int n_store[2];  // storage size of F (incl. dead)
   int n_groups[2];
-  int n_alive[2];
-  long long hist_top;  // history entries used
+  int alive_now[2];  // live states, counted at the start of the step that consumes F
   StepCounters sc[2];
   unsigned long long tr_ref, tr, ftot, fpeak, tbytes;
   unsigned long long best_vb, best_lex;
   int best_idx;
-  int scan_total[5];
+  int scan_total[kNumScans];
 };
 
 struct V2 {
@@ -108,14 +113,13 @@ struct V2 {
   int32_t* h_parent;
   int32_t* h_oi;
   long long hcap;
-  long long* hist_base;  // [S+1]
+  long long* hist_base;  // [S+2]
   int32_t *u_group, *u_sig, *u_ns, *u_chs, *u_chb, *u_cbase, *u_sbase, *u_bbase;
   int ucap;
-  unsigned long long* hash;
+  uint32_t* hash;  // key+1 per slot; the slot index is the successor-status id
   int hmask;
-  uint32_t* ns_key;
-  int32_t *ns_ucnt, *ns_ccnt, *ns_ubase, *ns_cbase, *ns_ucur, *ns_ccur, *ns_units, *ns_big, *ns_small;
-  int nscap;
+  int32_t *ns_ucnt, *ns_ccnt, *ns_ubase, *ns_cbase, *ns_ucur, *ns_ccur, *ns_units, *ns_bigpos, *ns_smallpos;
+  int32_t *ns_big, *ns_small;
   int32_t *it_s_unit, *it_s_chunk, *it_b_unit, *it_b_chunk;
   int itcap;
   double* c_value;
@@ -129,6 +133,7 @@ struct V2 {
   int32_t* kid_cur[2];
   int32_t* kid_base;
   uint64_t* kid_items;
+  int32_t* kid_pr;
   int32_t* big_bucket;
   int32_t* pcnt;
   int32_t* pbucket;
@@ -137,9 +142,9 @@ struct V2 {
   int32_t* sig_len;  // [n_sig]
   Ctl* ctl;
   int32_t* chosen;
-  int n_partial;
-  long long* dbg;  // [S][6] per-step counters (debug dump)
-  unsigned long long* dbg_time;  // [phases] barrier timestamps (debug)  // entries of the partial-subset tables (all subsets but the full one)
+  int n_partial;                 // entries of the partial-subset tables (all subsets but the full one)
+  long long* dbg;                // [S][6] per-step counters (debug dump)
+  unsigned long long* dbg_time;  // barrier timestamps (debug)
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
@@ -148,6 +153,11 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
   return v;
 }
 __device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ void raise_err(const V2& a, int phi, int code, int step = 0, unsigned long long count = 0, int what = 0,
                           long long need = 0) {
@@ -162,12 +172,6 @@ __device__ void raise_err(const V2& a, int phi, int code, int step = 0, unsigned
 
 // grid barrier + uniform error check (errors raised in phase phi become
 // visible to every CTA after the barrier that ends phi)
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
 __device__ __forceinline__ bool barrier(cg::grid_group& grid, const V2& a, int& phi) {
   grid.sync();
   if (a.dbg_time && blockIdx.x == 0 && threadIdx.x == 0) a.dbg_time[phi] = globaltimer();
@@ -177,18 +181,26 @@ __device__ __forceinline__ bool barrier(cg::grid_group& grid, const V2& a, int& 
 }
 
 // ---------------------------------------------------------------------------
-// block-level exclusive scan of a tile (kThreads x 8 items)
-__device__ int block_scan_tile(const int32_t* in, int32_t* out, int n, int base, int* sm) {
-  const int tid = threadIdx.x;
-  int v[8];
-  int sum = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int i = base + tid * 8 + k;
-    v[k] = i < n ? in[i] : 0;
-    sum += v[k];
+// block reductions / scans (kThreads threads)
+__device__ __forceinline__ long long block_sum(long long x, long long* sm) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = x;
+  __syncthreads();
+  long long t = 0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < kWarps ? sm[threadIdx.x] : 0;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
   }
-  int x = sum;  // warp inclusive scan
+  __syncthreads();
+  return t;  // valid in thread 0
+}
+
+// exclusive scan of n <= 2*kThreads ints in place (smem); returns total
+__device__ int block_scan_small(int* v, int n, int* sm) {
+  const int tid = threadIdx.x;
+  const int a0 = 2 * tid < n ? v[2 * tid] : 0, a1 = 2 * tid + 1 < n ? v[2 * tid + 1] : 0;
+  const int sum = a0 + a1;
+  int x = sum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, x, o);
@@ -197,54 +209,104 @@ __device__ int block_scan_tile(const int32_t* in, int32_t* out, int n, int base,
   if ((tid & 31) == 31) sm[tid >> 5] = x;
   __syncthreads();
   if (tid < 32) {
-    int w = tid < kWarps ? sm[tid] : 0;
+    const int w = tid < kWarps ? sm[tid] : 0;
     int z = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, z, o);
       if (tid >= o) z += y;
     }
-    if (tid < kWarps) sm[32 + tid] = z - w;  // exclusive warp offsets
-    if (tid == kWarps - 1) sm[64] = z;       // tile aggregate
+    if (tid < kWarps) sm[32 + tid] = z - w;
+    if (tid == kWarps - 1) sm[64] = z;
+  }
+  __syncthreads();
+  const int ex = sm[32 + (tid >> 5)] + x - sum;
+  if (2 * tid < n) v[2 * tid] = ex;
+  if (2 * tid + 1 < n) v[2 * tid + 1] = ex + a0;
+  const int total = sm[64];
+  __syncthreads();
+  return total;
+}
+
+struct ScanJob {
+  const int32_t* in;
+  const int32_t* in2;  // mode 1/2: statuses' candidate counts
+  int32_t* out;
+  int n;
+  int mode;  // 0 plain, 1 big-status flag, 2 small-status flag
+};
+
+__device__ __forceinline__ int scan_load(const ScanJob& J, int i) {
+  if (i >= J.n) return 0;
+  if (J.mode == 0) return J.in[i];
+  const int uc = J.in[i];
+  if (uc == 0) return 0;
+  const bool big = uc > 1 || J.in2[i] > kBigNs;
+  return (J.mode == 1) == big ? 1 : 0;
+}
+
+__device__ int block_scan_tile(const ScanJob& J, int base, int* sm) {
+  const int tid = threadIdx.x;
+  int v[8];
+  int sum = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    v[k] = scan_load(J, base + tid * 8 + k);
+    sum += v[k];
+  }
+  int x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((tid & 31) >= o) x += y;
+  }
+  if ((tid & 31) == 31) sm[tid >> 5] = x;
+  __syncthreads();
+  if (tid < 32) {
+    const int w = tid < kWarps ? sm[tid] : 0;
+    int z = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, z, o);
+      if (tid >= o) z += y;
+    }
+    if (tid < kWarps) sm[32 + tid] = z - w;
+    if (tid == kWarps - 1) sm[64] = z;
   }
   __syncthreads();
   int run = sm[32 + (tid >> 5)] + x - sum;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {  // exclusive within the tile
+  for (int k = 0; k < 8; ++k) {
     const int tmp = v[k];
     v[k] = run;
     run += tmp;
   }
-  // store tile-relative exclusive values (offset added by the caller)
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int i = base + tid * 8 + k;
-    if (i < n) out[i] = v[k];
+    if (i < J.n) J.out[i] = v[k];
   }
   const int agg = sm[64];
   __syncthreads();
   return agg;
 }
 
-struct ScanJob {
-  const int32_t* in;
-  int32_t* out;
-  int n;
-};
-
 // Several exclusive scans in one pass: tiles are handed out by a ticket, so
 // every tile's predecessors are already owned by running CTAs (decoupled
 // look-back cannot deadlock in a cooperative launch).
-__device__ void multi_scan(const V2& a, const ScanJob* jobs, int njobs, int epoch, int* ticket, int* totals) {
+__device__ void multi_scan(const V2& a, const ScanJob* jobs, int epoch, int* ticket, int* totals) {
   __shared__ int sm[80];
   __shared__ int s_tile, s_excl;
-  int tiles[5], tbase[6];
+  int tiles[kNumScans], tbase[kNumScans + 1];
   tbase[0] = 0;
-  for (int k = 0; k < njobs; ++k) {
+  for (int k = 0; k < kNumScans; ++k) {
     tiles[k] = (jobs[k].n + kTile - 1) / kTile;
     tbase[k + 1] = tbase[k] + tiles[k];
   }
-  const int total_tiles = tbase[njobs];
+  const int total_tiles = tbase[kNumScans];
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int k = 0; k < kNumScans; ++k)
+      if (tiles[k] == 0) totals[k] = 0;
   while (true) {
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
     __syncthreads();
@@ -255,16 +317,15 @@ __device__ void multi_scan(const V2& a, const ScanJob* jobs, int njobs, int epoc
     while (t >= tbase[k + 1]) ++k;
     const int j = t - tbase[k];
     const ScanJob& J = jobs[k];
-    const int agg = block_scan_tile(J.in, J.out, J.n, j * kTile, sm);
+    const int agg = block_scan_tile(J, j * kTile, sm);
     if (threadIdx.x == 0) {
       unsigned long long* st = a.scan_state + t;
       const unsigned long long ep = static_cast<unsigned long long>(epoch) << 34;
       int excl = 0;
+      __threadfence();
       if (j == 0) {
-        __threadfence();
         atomicExch(st, ep | (2ull << 32) | static_cast<uint32_t>(agg));
       } else {
-        __threadfence();
         atomicExch(st, ep | (1ull << 32) | static_cast<uint32_t>(agg));
         int q = t - 1;
         while (true) {
@@ -282,66 +343,36 @@ __device__ void multi_scan(const V2& a, const ScanJob* jobs, int njobs, int epoc
     }
     __syncthreads();
     const int excl = s_excl;
-    if (excl) {
+    if (excl)
       for (int i = j * kTile + threadIdx.x; i < min(J.n, (j + 1) * kTile); i += kThreads) J.out[i] += excl;
-    }
     __syncthreads();
   }
-  for (int k = 0; k < njobs; ++k)
-    if (tiles[k] == 0 && blockIdx.x == 0 && threadIdx.x == 0) totals[k] = 0;
 }
 
 // ---------------------------------------------------------------------------
-__device__ int ns_get_id(const V2& a, StepCounters& sc, uint32_t key, int phi, int step) {
-  const unsigned long long want_hi = static_cast<unsigned long long>(key) + 1;
-  unsigned h = key * 2654435761u;
-  int reserved = -1;
-  for (int probe = 0; probe <= a.hmask; ++probe) {
-    const int slot = (h + probe) & a.hmask;
-    unsigned long long w = a.hash[slot];
-    while (true) {
-      if ((w >> 32) == want_hi) return static_cast<int>(w & 0xffffffffu);
-      if (w != 0) break;  // other key: next slot
-      if (reserved < 0) {
-        reserved = atomicAdd(&sc.n_ns, 1);
-        if (reserved >= a.nscap) {
-          raise_err(a, phi, kOverflow, step, 0, 1, reserved + 1);
-          return -1;
-        }
-      }
-      const unsigned long long mine = (want_hi << 32) | static_cast<unsigned>(reserved);
-      const unsigned long long prev = atomicCAS(&a.hash[slot], 0ull, mine);
-      if (prev == 0) {
-        a.ns_key[reserved] = key;
-        return reserved;
-      }
-      w = prev;  // lost the race: re-examine this slot
-    }
+// successor-status hash: the slot holding key+1 is the status id
+__device__ int ns_slot(const V2& a, uint32_t key, int phi, int step) {
+  const uint32_t want = key + 1u;
+  const unsigned h = key * 2654435761u;
+  for (int probe = 0; probe <= (a.hmask >> 1); ++probe) {
+    const int slot = static_cast<int>((h + static_cast<unsigned>(probe)) & static_cast<unsigned>(a.hmask));
+    uint32_t w = a.hash[slot];
+    if (w == 0) w = atomicCAS(&a.hash[slot], 0u, want);
+    if (w == 0 || w == want) return slot;
   }
-  raise_err(a, phi, kOverflow, step, 0, 2, 0);
+  raise_err(a, phi, kOverflow, step, 0, 2, 0);  // table too full
   return -1;
 }
 
-// ---------------------------------------------------------------------------
-// S1: units of every live group + children per parent. Warp per group; lanes
-// split the (<= 8^M) per-tenant retraining-size combinations (solvers.hpp:379-411).
+// per-tenant allowed retraining sizes of a status (allowed_sizes, solvers.hpp:79-97)
 template <int M>
-__device__ void phase_units(const V2& a, int s, int phi) {
-  const int cur = s & 1;
-  StepCounters& sc = a.ctl->sc[s & 1];
-  const FrontierV2& F = a.f[cur];
-  const int G = a.ctl->n_groups[cur];
-  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
-  const int lane = threadIdx.x & 31, wid = gtid >> 5, nw = gstride >> 5;
-  const Codec codec{a.t.S};
-  unsigned long long ref = 0;
-  for (int g = wid; g < G; g += nw) {
-    if (F.g_alive[g] <= 0) continue;
-    const int gsize = F.g_size[g];
-    const uint32_t status = F.g_status[g];
-    int st[M], sizes[M][9], cnt[M], total = 1;
+struct UnitSpace {
+  int st[M], sizes[M][9], cnt[M], total;
+  __device__ void init(const V2& a, uint32_t status, int s) {
+    const Codec codec{a.t.S};
+    total = 1;
 #pragma unroll
-    for (int m = 0; m < M; ++m) {  // allowed_sizes (solvers.hpp:79-97)
+    for (int m = 0; m < M; ++m) {
       st[m] = static_cast<int>((status >> (16 * m)) & 0xffff);
       cnt[m] = 0;
       if (Codec::is_running(st[m])) {
@@ -355,123 +386,193 @@ __device__ void phase_units(const V2& a, int s, int phi) {
       }
       total *= cnt[m];
     }
-    for (int c0 = 0; c0 < total; c0 += 32) {
-      const int c = c0 + lane;
-      bool ok = c < total;
-      int sig = 0;
-      uint32_t ns = 0;
-      if (ok) {
-        int rem = c, pick[M];
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          pick[m] = rem % cnt[m];
-          rem /= cnt[m];
-        }
-#pragma unroll
-        for (int m = M - 1; m >= 0; --m) sig = sig * 8 + sizes[m][pick[m]];
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          const int adv = codec.advance(a.t.rt[m], st[m], sizes[m][pick[m]], s);
-          ok = ok && adv >= 0 && !(adv == 0 && (a.t.min_rt[m] < 0 || s + 1 + a.t.min_rt[m] > a.t.S));
-          ns |= static_cast<uint32_t>(adv < 0 ? 0 : adv) << (16 * m);
-        }
-        ok = ok && a.sp.sig_nopt[sig] > 0;
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, ok);
-      if (!bal) continue;
-      int ubase = 0;
-      if (lane == 0) ubase = atomicAdd(&sc.n_units, __popc(bal));
-      ubase = __shfl_sync(0xffffffffu, ubase, 0);
-      if (!ok) continue;
-      const int u = ubase + __popc(bal & ((1u << lane) - 1u));
-      if (u >= a.ucap) {
-        raise_err(a, phi, kOverflow, s, 0, 3, u + 1);
-        continue;
-      }
-      const int id = ns_get_id(a, sc, ns, phi, s);
-      if (id < 0) continue;
-      const int L = a.sig_len[sig];
-      a.u_group[u] = g;
-      a.u_sig[u] = sig;
-      a.u_ns[u] = id;
-      const bool small = gsize <= kSmall;
-      a.u_chs[u] = small ? (L + kChunkS - 1) / kChunkS : 0;
-      a.u_chb[u] = small ? 0 : (L + kChunkB - 1) / kChunkB;
-      atomicAdd(&a.ns_ucnt[id], 1);
-      atomicAdd(&a.ns_ccnt[id], L);
-      ref += static_cast<unsigned long long>(a.sp.sig_nopt[sig]);
-    }
   }
-  for (int o = 16; o > 0; o >>= 1) ref += __shfl_down_sync(0xffffffffu, ref, o);
-  if (lane == 0 && ref) atomicAdd(&a.ctl->tr_ref, ref);
-  // children per parent (rank buckets of F_s)
+  // combination c -> (valid, signature, successor status) (solvers.hpp:388-402)
+  __device__ bool combo(const V2& a, int c, int s, int* sig_out, uint32_t* ns_out) const {
+    const Codec codec{a.t.S};
+    int rem = c, pick[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      pick[m] = rem % cnt[m];
+      rem /= cnt[m];
+    }
+    int sig = 0;
+#pragma unroll
+    for (int m = M - 1; m >= 0; --m) sig = sig * 8 + sizes[m][pick[m]];
+    bool ok = true;
+    uint32_t ns = 0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int adv = codec.advance(a.t.rt[m], st[m], sizes[m][pick[m]], s);
+      ok = ok && adv >= 0 && !(adv == 0 && (a.t.min_rt[m] < 0 || s + 1 + a.t.min_rt[m] > a.t.S));
+      ns |= static_cast<uint32_t>(adv < 0 ? 0 : adv) << (16 * m);
+    }
+    *sig_out = sig;
+    *ns_out = ns;
+    return ok && a.sp.sig_nopt[sig] > 0;
+  }
+};
+
+// S1
+template <int M>
+__device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* s_red) {
+  const int cur = s & 1;
+  StepCounters& sc = a.ctl->sc[s & 1];
+  const FrontierV2& F = a.f[cur];
+  const int G = a.ctl->n_groups[cur];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int s_base, s_scan[80];
+  const int g0 = static_cast<int>(static_cast<long long>(G) * blockIdx.x / gridDim.x);
+  const int g1 = static_cast<int>(static_cast<long long>(G) * (blockIdx.x + 1) / gridDim.x);
+  long long ref = 0;
+  for (int bs = g0; bs < g1; bs += kBatch) {
+    const int be = min(g1, bs + kBatch);
+    // pass 1: unit count per group
+    for (int g = bs + warp; g < be; g += kWarps) {
+      int n = 0;
+      if (F.g_alive[g] > 0) {
+        UnitSpace<M> us;
+        us.init(a, F.g_status[g], s);
+        for (int c0 = 0; c0 < us.total; c0 += 32) {
+          int sig;
+          uint32_t ns;
+          const bool ok = c0 + lane < us.total && us.combo(a, c0 + lane, s, &sig, &ns);
+          n += __popc(__ballot_sync(0xffffffffu, ok));
+        }
+      }
+      if (lane == 0) s_cnt[g - bs] = n;
+    }
+    __syncthreads();
+    const int total = block_scan_small(s_cnt, be - bs, s_scan);
+    if (threadIdx.x == 0) {
+      s_base = atomicAdd(&sc.n_units, total);
+      if (s_base + total > a.ucap) raise_err(a, phi, kOverflow, s, 0, 3, static_cast<long long>(s_base) + total);
+    }
+    __syncthreads();
+    const int base = s_base;
+    if (base + total <= a.ucap) {
+      // pass 2: write the units (same enumeration order)
+      for (int g = bs + warp; g < be; g += kWarps) {
+        if (F.g_alive[g] <= 0) continue;
+        const bool small = F.g_size[g] <= kSmall;
+        UnitSpace<M> us;
+        us.init(a, F.g_status[g], s);
+        int run = base + s_cnt[g - bs];
+        for (int c0 = 0; c0 < us.total; c0 += 32) {
+          int sig = 0;
+          uint32_t ns = 0;
+          const bool ok = c0 + lane < us.total && us.combo(a, c0 + lane, s, &sig, &ns);
+          const unsigned bal = __ballot_sync(0xffffffffu, ok);
+          if (ok) {
+            const int u = run + __popc(bal & ((1u << lane) - 1u));
+            const int id = ns_slot(a, ns, phi, s);
+            if (id >= 0) {
+              const int L = a.sig_len[sig];
+              a.u_group[u] = g;
+              a.u_sig[u] = sig;
+              a.u_ns[u] = id;
+              a.u_chs[u] = small ? (L + kChunkS - 1) / kChunkS : 0;
+              a.u_chb[u] = small ? 0 : (L + kChunkB - 1) / kChunkB;
+              atomicAdd(&a.ns_ucnt[id], 1);
+              atomicAdd(&a.ns_ccnt[id], L);
+              ref += a.sp.sig_nopt[sig];
+            }
+          }
+          run += __popc(bal);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // children per parent (rank buckets of F_s) + live-state count
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const int n = a.ctl->n_store[cur];
+  long long live = 0;
   for (int i = gtid; i < n; i += gstride)
-    if (F.alive[i]) atomicAdd(&a.kid_cnt[cur][F.lex[i] >> 32], 1);
+    if (F.alive[i]) {
+      atomicAdd(&a.kid_cnt[cur][F.lex[i] >> 32], 1);
+      ++live;
+    }
+  const long long rs = block_sum(ref, s_red);
+  const long long ls = block_sum(live, s_red);
+  if (threadIdx.x == 0) {
+    if (rs) atomicAdd(&a.ctl->tr_ref, static_cast<unsigned long long>(rs));
+    if (ls) atomicAdd(&a.ctl->alive_now[cur], static_cast<int>(ls));
+  }
 }
 
 // S3: placement
-__device__ void phase_place(const V2& a, int s, int phi) {
+__device__ void phase_place(const V2& a, int s) {
   const int cur = s & 1;
   StepCounters& sc = a.ctl->sc[s & 1];
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
-  const int NU = sc.n_units, NS = sc.n_ns;
+  const int NU = sc.n_units;
   for (int u = gtid; u < NU; u += gstride) {
     const int id = a.u_ns[u];
     const int L = a.sig_len[a.u_sig[u]];
     a.u_cbase[u] = a.ns_cbase[id] + atomicAdd(&a.ns_ccur[id], L);
     a.ns_units[a.ns_ubase[id] + atomicAdd(&a.ns_ucur[id], 1)] = u;
-    for (int c = 0; c < a.u_chs[u]; ++c) {
-      a.it_s_unit[a.u_sbase[u] + c] = u;
-      a.it_s_chunk[a.u_sbase[u] + c] = c;
+    const int nsm = a.u_chs[u], nbg = a.u_chb[u];
+    const int sb = a.u_sbase[u], bb = a.u_bbase[u];
+    for (int c = 0; c < nsm; ++c) {
+      a.it_s_unit[sb + c] = u;
+      a.it_s_chunk[sb + c] = c;
     }
-    for (int c = 0; c < a.u_chb[u]; ++c) {
-      a.it_b_unit[a.u_bbase[u] + c] = u;
-      a.it_b_chunk[a.u_bbase[u] + c] = c;
+    for (int c = 0; c < nbg; ++c) {
+      a.it_b_unit[bb + c] = u;
+      a.it_b_chunk[bb + c] = c;
     }
   }
-  for (int id = gtid; id < NS; id += gstride) {
-    if (a.ns_ucnt[id] == 0) continue;  // reserved id lost to a concurrent insert
-    const bool big = a.ns_ucnt[id] > 1 || a.ns_ccnt[id] > kBigNs;
-    if (big) a.ns_big[atomicAdd(&sc.n_ns_big, 1)] = id;
-    else a.ns_small[atomicAdd(&sc.n_ns_small, 1)] = id;
+  for (int id = gtid; id <= a.hmask; id += gstride) {
+    const int uc = a.ns_ucnt[id];
+    if (uc == 0) continue;
+    if (uc > 1 || a.ns_ccnt[id] > kBigNs) a.ns_big[a.ns_bigpos[id]] = id;
+    else a.ns_small[a.ns_smallpos[id]] = id;
   }
   const FrontierV2& F = a.f[cur];
   const int n = a.ctl->n_store[cur];
-  for (int i = gtid; i < n; i += gstride) {
-    if (!F.alive[i]) continue;
-    const int pr = static_cast<int>(F.lex[i] >> 32);
-    const int q = atomicAdd(&a.kid_cur[cur][pr], 1);
-    a.kid_items[a.kid_base[pr] + q] = ((F.lex[i] & 0xffffffffull) << 32) | static_cast<uint32_t>(i);
-    if (q == 0 && a.kid_cnt[cur][pr] > kBucketSmall) a.big_bucket[atomicAdd(&sc.n_big_bucket, 1)] = pr;
+  const int lane = threadIdx.x & 31;
+  for (int i0 = gtid - lane; i0 < n; i0 += gstride) {  // warp-uniform trip count
+    const int i = i0 + lane;
+    bool big_first = false;
+    int pr = 0;
+    if (i < n && F.alive[i]) {
+      pr = static_cast<int>(F.lex[i] >> 32);
+      const int q = atomicAdd(&a.kid_cur[cur][pr], 1);
+      const int slot = a.kid_base[pr] + q;
+      a.kid_items[slot] = ((F.lex[i] & 0xffffffffull) << 32) | static_cast<uint32_t>(i);
+      a.kid_pr[slot] = pr;
+      big_first = q == 0 && a.kid_cnt[cur][pr] > kBucketSmall;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, big_first);
+    if (bal) {
+      int b0 = 0;
+      if (lane == 0) b0 = atomicAdd(&sc.n_big_bucket, __popc(bal));
+      b0 = __shfl_sync(0xffffffffu, b0, 0);
+      if (big_first) a.big_bucket[b0 + __popc(bal & ((1u << lane) - 1u))] = pr;
+    }
   }
 }
 
-// S4: dense ranks of F_s = parent's first child slot + position of the option
-// index among the parent's children. Small buckets: thread per slot (slots of
-// one parent are adjacent, so bucket reads are warp broadcasts). Big buckets:
-// CTA items of 256 slots counting against the bucket staged in shared memory.
+// S4: dense ranks of F_s (solvers.hpp:544-548 restated: lex = (parent rank,
+// option index), so the rank is the parent's first child slot plus the
+// position of the option index among the parent's children)
 __device__ void phase_ranks(const V2& a, int s, unsigned long long* sm64) {
   const int cur = s & 1;
   StepCounters& sc = a.ctl->sc[s & 1];
   const FrontierV2& F = a.f[cur];
-  __shared__ int s_v;
   const int nb = sc.n_big_bucket;
-  while (true) {
-    if (threadIdx.x == 0) s_v = atomicAdd(&sc.cur_bucket, 1);
-    __syncthreads();
-    const int v = s_v;
-    __syncthreads();
-    if (v >= nb * kBucketChunks) break;
+  for (int v = blockIdx.x; v < nb * kBucketChunks; v += gridDim.x) {
     const int pr = a.big_bucket[v / kBucketChunks], chunk = v % kBucketChunks;
     const int base = a.kid_base[pr], c = a.kid_cnt[cur][pr];
-    if (chunk * kThreads >= c) continue;
+    if (chunk * kThreads >= c) continue;  // uniform over the CTA
     const bool staged = c <= kBucketStage;
     if (staged) {
       for (int k = threadIdx.x; k < c; k += kThreads) sm64[k] = a.kid_items[base + k];
       __syncthreads();
     }
-    const unsigned long long* keys = staged ? sm64 : reinterpret_cast<const unsigned long long*>(a.kid_items + base);
+    const unsigned long long* keys =
+        staged ? sm64 : reinterpret_cast<const unsigned long long*>(a.kid_items + base);
     for (int i = chunk * kThreads + threadIdx.x; i < c; i += kThreads * kBucketChunks) {
       const unsigned long long me = keys[i];
       int pos = 0;
@@ -481,17 +582,16 @@ __device__ void phase_ranks(const V2& a, int s, unsigned long long* sm64) {
     __syncthreads();
   }
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
-  const int n = a.ctl->scan_total[4];  // live states of F_s = filled slots
+  const int n = sc.kids;  // live states of F_s = filled slots
   for (int i = gtid; i < n; i += gstride) {
-    const unsigned long long me = a.kid_items[i];
-    const int idx = static_cast<int>(me & 0xffffffffu);
-    const int pr = static_cast<int>(F.lex[idx] >> 32);
+    const int pr = a.kid_pr[i];
     const int c = a.kid_cnt[cur][pr];
     if (c > kBucketSmall) continue;
     const int base = a.kid_base[pr];
+    const unsigned long long me = a.kid_items[i];
     int pos = 0;
     for (int k = 0; k < c; ++k) pos += a.kid_items[base + k] < me;
-    F.rank[idx] = base + pos;
+    F.rank[static_cast<uint32_t>(me)] = base + pos;
   }
 }
 
@@ -535,12 +635,12 @@ __device__ __forceinline__ void emit_target(const V2& a, int s, int charge, int 
     }
   }
   const int slot = a.u_cbase[unit] + t_idx;
-  if (chosen < 0) {  // group without live states cannot happen (units skip them); keep safe
+  if (chosen < 0) {  // cannot happen: units come from groups with live states
     a.c_ok[slot] = 0;
     return;
   }
   const int pred = gs + chosen;
-  const uint32_t pids = static_cast<uint32_t>(a.sp.pl_ids[F.pid[pred]]);
+  const uint32_t pids = F.ids[pred];
   double v = F.value[pred];  // exact fold (solvers.hpp:451-458)
 #pragma unroll
   for (int m = 0; m < M; ++m) {
@@ -548,7 +648,7 @@ __device__ __forceinline__ void emit_target(const V2& a, int s, int charge, int 
     const double eff = eff_cap(cap[m], changed ? t.loss[m] : 0.0);
     v = dadd(v, dmul(thr_of(a.recv[m * t.S + s], eff), acc[m]));
   }
-  const bool ok = !(dadd(v, a.ub[s + 1]) < *a.incumbent);  // solvers.hpp:459
+  const bool ok = !(dadd(v, a.ub[s + 1]) < *a.incumbent);  // solvers.hpp:459 (strict)
   a.c_value[slot] = v;
   a.c_lex[slot] = (static_cast<uint64_t>(F.rank[pred]) << 32) | static_cast<uint32_t>(oi);
   a.c_parent[slot] = pred;
@@ -578,22 +678,16 @@ __device__ void phase_trans(const V2& a, int s, TransSmem& T, uint32_t& tag) {
   const FrontierV2& F = a.f[cur];
   const int charge = (s > 0 || a.has_initial) ? 1 : 0;
   const int P1 = a.sp.P1;
-  __shared__ int s_item;
-  // CTA items: big groups, shared-memory subset tables
-  while (true) {
-    if (threadIdx.x == 0) s_item = atomicAdd(&sc.cur_big, 1);
-    __syncthreads();
-    const int item = s_item;
-    __syncthreads();
-    if (item >= sc.items_b) break;
+  // CTA items (big groups): shared-memory subset tables
+  const int nib = sc.items_b;
+  for (int item = blockIdx.x; item < nib; item += gridDim.x) {
     ++tag;
     const int unit = a.it_b_unit[item], chunk = a.it_b_chunk[item];
     const int g = a.u_group[unit], sig = a.u_sig[unit];
     const int gs = F.g_start[g], gn = F.g_size[g];
     double acc[M];
     group_acc<M>(a, F.g_status[g], acc);
-    // phase 0: claim entries
-    for (int j = threadIdx.x; j < gn; j += kThreads) {
+    for (int j = threadIdx.x; j < gn; j += kThreads) {  // claim entries
       if (!F.alive[gs + j]) continue;
       const int pj = F.pid[gs + j];
       T.ex[pj] = (static_cast<unsigned long long>(tag) << 32) | static_cast<uint32_t>(j);
@@ -607,15 +701,16 @@ __device__ void phase_trans(const V2& a, int s, TransSmem& T, uint32_t& tag) {
       }
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < gn; j += kThreads) {
+    for (int j = threadIdx.x; j < gn; j += kThreads) {  // max value
       if (!F.alive[gs + j]) continue;
       const int pj = F.pid[gs + j];
       const unsigned long long vb = vbits(F.value[gs + j]);
 #pragma unroll
-      for (int sub = 0; sub < (1 << M) - 1; ++sub) atomicMax(&T.vb[a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj]], vb);
+      for (int sub = 0; sub < (1 << M) - 1; ++sub)
+        atomicMax(&T.vb[a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj]], vb);
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < gn; j += kThreads) {
+    for (int j = threadIdx.x; j < gn; j += kThreads) {  // min rank among the max
       if (!F.alive[gs + j]) continue;
       const int pj = F.pid[gs + j];
       const unsigned long long vb = vbits(F.value[gs + j]);
@@ -627,7 +722,7 @@ __device__ void phase_trans(const V2& a, int s, TransSmem& T, uint32_t& tag) {
       }
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < gn; j += kThreads) {
+    for (int j = threadIdx.x; j < gn; j += kThreads) {  // representative index
       if (!F.alive[gs + j]) continue;
       const int pj = F.pid[gs + j];
       const unsigned long long vb = vbits(F.value[gs + j]);
@@ -671,21 +766,19 @@ __device__ void phase_trans(const V2& a, int s, TransSmem& T, uint32_t& tag) {
     }
     __syncthreads();
   }
-  // warp items: small groups, broadcast scan
+  // warp items (small groups): broadcast scan of the group's states
   const int lane = threadIdx.x & 31;
-  while (true) {
-    int item = 0;
-    if (lane == 0) item = atomicAdd(&sc.cur_small, 1);
-    item = __shfl_sync(0xffffffffu, item, 0);
-    if (item >= sc.items_s) break;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const int nis = sc.items_s;
+  for (int item = wid; item < nis; item += nw) {
     const int unit = a.it_s_unit[item], chunk = a.it_s_chunk[item];
     const int g = a.u_group[unit], sig = a.u_sig[unit];
     const int gs = F.g_start[g], gn = F.g_size[g];
-    double acc[M];
-    group_acc<M>(a, F.g_status[g], acc);
     const int sb = a.sp.sig_off[sig], L = a.sp.sig_off[sig + 1] - sb;
     const int ti = chunk * kChunkS + lane;
     if (ti >= L) continue;
+    double acc[M];
+    group_acc<M>(a, F.g_status[g], acc);
     const int p = a.sp.cand_pid[sb + ti];
     const int oi = a.sp.cand_oi[sb + ti];
     const uint32_t ids_p = static_cast<uint32_t>(a.sp.pl_ids[p]);
@@ -696,11 +789,13 @@ __device__ void phase_trans(const V2& a, int s, TransSmem& T, uint32_t& tag) {
       b.v[k] = 0.0;
       b.r[k] = 0xffffffffu;
     }
+#pragma unroll 4
     for (int j = 0; j < gn; ++j) {
-      if (!F.alive[gs + j]) continue;
+      const bool al = F.alive[gs + j];
       const double vj = F.value[gs + j];
       const uint32_t rj = F.rank[gs + j];
-      const uint32_t idj = static_cast<uint32_t>(a.sp.pl_ids[F.pid[gs + j]]);
+      const uint32_t idj = F.ids[gs + j];
+      if (!al) continue;
       int mt = 0;
 #pragma unroll
       for (int m = 0; m < M; ++m) mt |= (((idj ^ ids_p) >> (16 * m)) & 0xffff) == 0 ? (1 << m) : 0;
@@ -719,39 +814,13 @@ __device__ void phase_trans(const V2& a, int s, TransSmem& T, uint32_t& tag) {
 }
 
 // ---------------------------------------------------------------------------
-// S6: merge + band + output, per successor status
-// live after the equal-key merge (binary search in the other units' lists)
-__device__ bool merged_live(const V2& a, int ub, int uc, int k) {
-  if (!a.c_ok[k]) return false;
-  if (uc == 1) return true;
-  const int p = a.c_pid[k];
-  const double v = a.c_value[k];
-  const uint64_t lx = a.c_lex[k];
-  for (int q = 0; q < uc; ++q) {
-    const int u = a.ns_units[ub + q];
-    const int cb = a.u_cbase[u];
-    const int sig = a.u_sig[u];
-    const int b = a.sp.sig_off[sig], n = a.sp.sig_off[sig + 1] - b;
-    if (k >= cb && k < cb + n) continue;  // own unit
-    int lo = 0, hi = n;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (a.sp.cand_pid[b + mid] < p) lo = mid + 1;
-      else hi = mid;
-    }
-    if (lo < n && a.sp.cand_pid[b + lo] == p) {
-      const int k2 = cb + lo;
-      if (a.c_ok[k2] && better(a.c_value[k2], a.c_lex[k2], v, lx)) return false;
-    }
-  }
-  return true;
-}
-
+// S6: merge + band + output
 __device__ __forceinline__ void write_state(const V2& a, int s, int nxt, int q, int gidx, uint32_t key, int k) {
   const FrontierV2& N = a.f[nxt];
   const int p = a.c_pid[k];
   const uint64_t lx = a.c_lex[k];
   N.status[q] = key;
+  N.ids[q] = static_cast<uint32_t>(a.sp.pl_ids[p]);
   N.pid[q] = p;
   N.value[q] = a.c_value[k];
   N.lex[q] = lx;
@@ -766,43 +835,40 @@ __device__ __forceinline__ void write_state(const V2& a, int s, int nxt, int q, 
   }
 }
 
-__device__ bool alloc_out(const V2& a, int s, int nxt, int count, int* q0, int* gidx, int phi) {
-  *q0 = atomicAdd(&a.ctl->n_store[nxt], count);
-  *gidx = atomicAdd(&a.ctl->n_groups[nxt], 1);
-  if (*q0 + count > a.fcap) {
-    raise_err(a, phi, kOverflow, s, 0, 4, static_cast<long long>(*q0) + count);
+__device__ bool check_out(const V2& a, int s, long long q_end, long long g_end, int phi) {
+  if (q_end > a.fcap) {
+    raise_err(a, phi, kOverflow, s, 0, 4, q_end);
     return false;
   }
-  if (*gidx >= a.gcap) {
-    raise_err(a, phi, kOverflow, s, 0, 5, *gidx + 1);
+  if (g_end > a.gcap) {
+    raise_err(a, phi, kOverflow, s, 0, 5, g_end);
     return false;
   }
-  if (a.hist_base[s + 1] + *q0 + count > a.hcap) {
-    raise_err(a, phi, kOverflow, s, 0, 6, a.hist_base[s + 1] + *q0 + count);
+  if (a.hist_base[s + 1] + q_end > a.hcap) {
+    raise_err(a, phi, kOverflow, s, 0, 6, a.hist_base[s + 1] + q_end);
     return false;
   }
   return true;
 }
 
-__device__ void phase_merge_out(const V2& a, int s, int phi, unsigned long long* mvb, unsigned long long* mlx) {
+__device__ void phase_merge_out(const V2& a, int s, int phi, unsigned long long* mvb, unsigned long long* mlx,
+                                int* s_cnt, int* s_gof) {
   const int nxt = (s + 1) & 1;
   StepCounters& sc = a.ctl->sc[s & 1];
   const FrontierV2& N = a.f[nxt];
-  __shared__ int s_id, s_q0, s_g, s_cnt;
+  __shared__ int s_q0, s_g;
   __shared__ unsigned long long s_max;
+  __shared__ int s_scan[80];
   __shared__ int s_wsum[kWarps];
-  // CTA path: big successor statuses
-  while (true) {
-    if (threadIdx.x == 0) s_id = atomicAdd(&sc.cur_ns_big, 1);
-    __syncthreads();
-    const int w = s_id;
-    __syncthreads();
-    if (w >= sc.n_ns_big) break;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // big statuses (multi-unit or large): one CTA each
+  const int nbig = sc.n_big;
+  for (int w = blockIdx.x; w < nbig; w += gridDim.x) {
     const int id = a.ns_big[w];
     const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id], ub = a.ns_ubase[id], uc = a.ns_ucnt[id];
     if (uc == 1) {
       for (int k = cb + threadIdx.x; k < cb + cc; k += kThreads) a.c_live[k] = a.c_ok[k];
-    } else {
+    } else {  // equal-key merge (solvers.hpp:467-468): max value, then min lex, per placement
       const int P1 = a.sp.P1;
       for (int w0 = 0; w0 < P1; w0 += kMergeWin) {
         for (int i = threadIdx.x; i < kMergeWin; i += kThreads) {
@@ -816,17 +882,24 @@ __device__ void phase_merge_out(const V2& a, int s, int phi, unsigned long long*
             const int sig = a.u_sig[u];
             const int b = a.sp.sig_off[sig], n = a.sp.sig_off[sig + 1] - b;
             const int cbu = a.u_cbase[u];
-            for (int t = threadIdx.x; t < n; t += kThreads) {
+            int lo = 0, hi = n;  // the unit's candidates are sorted by placement: clip to the window
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (a.sp.cand_pid[b + mid] < w0) lo = mid + 1;
+              else hi = mid;
+            }
+            for (int t = lo + threadIdx.x; t < n; t += kThreads) {
               const int p = a.sp.cand_pid[b + t];
-              if (p < w0 || p >= w0 + kMergeWin) continue;
+              if (p >= w0 + kMergeWin) break;
               const int k = cbu + t;
               if (!a.c_ok[k]) {
                 if (pass == 2) a.c_live[k] = 0;
                 continue;
               }
               const unsigned long long vb = vbits(a.c_value[k]);
-              if (pass == 0) atomicMax(&mvb[p - w0], vb);
-              else if (pass == 1) {
+              if (pass == 0) {
+                atomicMax(&mvb[p - w0], vb);
+              } else if (pass == 1) {
                 if (mvb[p - w0] == vb) atomicMin(&mlx[p - w0], a.c_lex[k]);
               } else {
                 a.c_live[k] = (mvb[p - w0] == vb && mlx[p - w0] == a.c_lex[k]) ? 1 : 0;
@@ -847,124 +920,128 @@ __device__ void phase_merge_out(const V2& a, int s, int phi, unsigned long long*
         mx = vb > mx ? vb : mx;
         any = true;
       }
-    if (threadIdx.x == 0) {
-      s_max = 0;
-      s_cnt = 0;
-    }
+    if (threadIdx.x == 0) s_max = 0;
     __syncthreads();
     if (any) atomicMax(&s_max, mx);
     __syncthreads();
     const double thresh = dsub(__longlong_as_double(static_cast<long long>(s_max)), a.band);
-    int cnt = 0;
-    for (int k = cb + threadIdx.x; k < cb + cc; k += kThreads) {
+    const int per = (cc + kThreads - 1) / kThreads;
+    const int lo = cb + threadIdx.x * per, hi = min(cb + cc, lo + per);
+    int mine = 0;
+    for (int k = lo; k < hi; ++k) {
       const bool keep = a.c_live[k] && a.c_value[k] >= thresh;
       a.c_live[k] = keep ? 1 : 0;
-      cnt += keep;
+      mine += keep;
     }
-    atomicAdd(&s_cnt, cnt);
+    int x = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
     __syncthreads();
-    const int total = s_cnt;
+    int off = x - mine, total = 0;
+    for (int w2 = 0; w2 < kWarps; ++w2) {
+      if (w2 < warp) off += s_wsum[w2];
+      total += s_wsum[w2];
+    }
     if (total > 0) {
       if (threadIdx.x == 0) {
-        int q0, gi;
-        if (alloc_out(a, s, nxt, total, &q0, &gi, phi)) {
-          s_q0 = q0;
-          s_g = gi;
+        const int q0 = atomicAdd(&a.ctl->n_store[nxt], total);
+        const int gi = atomicAdd(&a.ctl->n_groups[nxt], 1);
+        s_q0 = check_out(a, s, static_cast<long long>(q0) + total, gi + 1ll, phi) ? q0 : -1;
+        s_g = gi;
+        if (s_q0 >= 0) {
           N.g_start[gi] = q0;
           N.g_size[gi] = total;
-          N.g_status[gi] = a.ns_key[id];
+          N.g_status[gi] = a.hash[id] - 1u;
           N.g_alive[gi] = total;
-          atomicAdd(&a.ctl->n_alive[nxt], total);
-        } else {
-          s_q0 = -1;
         }
       }
       __syncthreads();
       if (s_q0 >= 0) {
-        // ordered compaction: each thread owns a contiguous candidate range
-        const int per = (cc + kThreads - 1) / kThreads;
-        const int lo = cb + threadIdx.x * per, hi = min(cb + cc, lo + per);
-        int mine = 0;
-        for (int k = lo; k < hi; ++k) mine += a.c_live[k];
-        int x = mine;
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, x, o);
-          if ((threadIdx.x & 31) >= o) x += y;
-        }
-        if ((threadIdx.x & 31) == 31) s_wsum[threadIdx.x >> 5] = x;
-        __syncthreads();
-        int off = x - mine;
-        for (int w2 = 0; w2 < (threadIdx.x >> 5); ++w2) off += s_wsum[w2];
-        const uint32_t key = a.ns_key[id];
+        const uint32_t key = a.hash[id] - 1u;
         for (int k = lo; k < hi; ++k)
           if (a.c_live[k]) write_state(a, s, nxt, s_q0 + off++, s_g, key, k);
       }
     }
     __syncthreads();
   }
-  // warp path
-  const int lane = threadIdx.x & 31;
-  while (true) {
-    int w = 0;
-    if (lane == 0) w = atomicAdd(&sc.cur_ns_small, 1);
-    w = __shfl_sync(0xffffffffu, w, 0);
-    if (w >= sc.n_ns_small) break;
-    const int id = a.ns_small[w];
-    const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id], ub = a.ns_ubase[id], uc = a.ns_ucnt[id];
-    unsigned long long mx = 0;
-    bool any = false;
-    for (int k = cb + lane; k < cb + cc; k += 32) {
-      const bool live = merged_live(a, ub, uc, k);
-      a.c_live[k] = live ? 1 : 0;
-      if (live) {
-        const unsigned long long vb = vbits(a.c_value[k]);
-        mx = vb > mx ? vb : mx;
-        any = true;
+  // small statuses (single unit, <= kBigNs candidates): warps, one allocation per CTA batch
+  const int nsm = sc.n_small;
+  const int r0 = static_cast<int>(static_cast<long long>(nsm) * blockIdx.x / gridDim.x);
+  const int r1 = static_cast<int>(static_cast<long long>(nsm) * (blockIdx.x + 1) / gridDim.x);
+  for (int bs = r0; bs < r1; bs += kBatch) {
+    const int be = min(r1, bs + kBatch);
+    for (int i = bs + warp; i < be; i += kWarps) {  // band + survivor count
+      const int id = a.ns_small[i];
+      const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
+      unsigned long long mx = 0;
+      bool any = false;
+      for (int k = cb + lane; k < cb + cc; k += 32)
+        if (a.c_ok[k]) {
+          const unsigned long long vb = vbits(a.c_value[k]);
+          mx = vb > mx ? vb : mx;
+          any = true;
+        }
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = y > mx ? y : mx;
+      }
+      any = __any_sync(0xffffffffu, any);
+      const double thresh = dsub(__longlong_as_double(static_cast<long long>(mx)), a.band);
+      int total = 0;
+      for (int k0 = cb; k0 < cb + cc; k0 += 32) {
+        const int k = k0 + lane;
+        const bool keep = any && k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh;
+        if (k < cb + cc) a.c_live[k] = keep ? 1 : 0;
+        total += __popc(__ballot_sync(0xffffffffu, keep));
+      }
+      if (lane == 0) {
+        s_cnt[i - bs] = total;
+        s_gof[i - bs] = total > 0 ? 1 : 0;
       }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
-      mx = y > mx ? y : mx;
+    __syncthreads();
+    const int tot = block_scan_small(s_cnt, be - bs, s_scan);
+    const int ngr = block_scan_small(s_gof, be - bs, s_scan);
+    if (threadIdx.x == 0) {
+      const int q0 = atomicAdd(&a.ctl->n_store[nxt], tot);
+      const int g0 = atomicAdd(&a.ctl->n_groups[nxt], ngr);
+      s_q0 = check_out(a, s, static_cast<long long>(q0) + tot, static_cast<long long>(g0) + ngr, phi) ? q0 : -1;
+      s_g = g0;
     }
-    any = __any_sync(0xffffffffu, any);
-    if (!any) continue;
-    const double thresh = dsub(__longlong_as_double(static_cast<long long>(mx)), a.band);
-    int total = 0;
-    for (int k0 = cb; k0 < cb + cc; k0 += 32) {
-      const int k = k0 + lane;
-      const bool keep = k < cb + cc && a.c_live[k] && a.c_value[k] >= thresh;
-      total += __popc(__ballot_sync(0xffffffffu, keep));
-    }
-    if (total == 0) continue;
-    int q0 = 0, gi = 0, ok = 1;
-    if (lane == 0) {
-      ok = alloc_out(a, s, nxt, total, &q0, &gi, phi) ? 1 : 0;
-      if (ok) {
-        N.g_start[gi] = q0;
-        N.g_size[gi] = total;
-        N.g_status[gi] = a.ns_key[id];
-        N.g_alive[gi] = total;
-        atomicAdd(&a.ctl->n_alive[nxt], total);
+    __syncthreads();
+    if (s_q0 >= 0) {
+      for (int i = bs + warp; i < be; i += kWarps) {
+        const int cnt = (i + 1 < be ? s_cnt[i + 1 - bs] : tot) - s_cnt[i - bs];
+        if (cnt == 0) continue;
+        const int id = a.ns_small[i];
+        const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
+        const int q0 = s_q0 + s_cnt[i - bs], gi = s_g + s_gof[i - bs];
+        const uint32_t key = a.hash[id] - 1u;
+        if (lane == 0) {
+          N.g_start[gi] = q0;
+          N.g_size[gi] = cnt;
+          N.g_status[gi] = key;
+          N.g_alive[gi] = cnt;
+        }
+        int run = 0;
+        for (int k0 = cb; k0 < cb + cc; k0 += 32) {
+          const int k = k0 + lane;
+          const bool keep = k < cb + cc && a.c_live[k];
+          const unsigned bal = __ballot_sync(0xffffffffu, keep);
+          if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
+          run += __popc(bal);
+        }
       }
     }
-    ok = __shfl_sync(0xffffffffu, ok, 0);
-    q0 = __shfl_sync(0xffffffffu, q0, 0);
-    gi = __shfl_sync(0xffffffffu, gi, 0);
-    if (!ok) continue;
-    int run = 0;
-    const uint32_t key = a.ns_key[id];
-    for (int k0 = cb; k0 < cb + cc; k0 += 32) {
-      const int k = k0 + lane;
-      const bool keep = k < cb + cc && a.c_live[k] && a.c_value[k] >= thresh;
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
-      run += __popc(bal);
-    }
+    __syncthreads();
   }
 }
 
-// decoded-status form of status_dominates: equal, or x done, or both running on
-// the same size with x's remaining steps <= y's
+// decoded-status form of status_dominates (solvers.hpp:128-134): equal, or x
+// done, or both running on the same size with x's remaining steps <= y's
 __device__ __forceinline__ bool dom_decoded(uint32_t x, uint32_t y) {
   if (x == y) return true;
   if ((x >> 24) == 1) return true;
@@ -983,27 +1060,23 @@ __device__ void phase_dominance(const V2& a, int s) {
     if (n >= 2 && n <= 64) {
       const int* bk = a.pbucket + p * 64;
       int q[2];
-      uint32_t st[2];
+      uint32_t dk[2][2];
       double v[2];
       uint64_t lx[2];
       for (int h = 0; h < 2; ++h) {
         const int j = lane + 32 * h;
         q[h] = j < n ? bk[j] : -1;
-        st[h] = q[h] >= 0 ? N.status[q[h]] : 0;
+        const uint32_t st = q[h] >= 0 ? N.status[q[h]] : 0;
         v[h] = q[h] >= 0 ? N.value[q[h]] : 0.0;
         lx[h] = q[h] >= 0 ? N.lex[q[h]] : 0;
-      }
-      // decode every tenant status once: kind (0 idle, 1 done, 2 running) | size | rem
-      uint32_t dk[2][2];
-      for (int h = 0; h < 2; ++h)
-        for (int m = 0; m < 2; ++m) {
-          const int code = m < a.t.M ? static_cast<int>((st[h] >> (16 * m)) & 0xffff) : 0;
+        for (int m = 0; m < 2; ++m) {  // decode once: kind (0 idle, 1 done, 2 running) | size | rem
+          const int code = m < a.t.M ? static_cast<int>((st >> (16 * m)) & 0xffff) : 0;
           dk[h][m] = code == Codec::done() ? (1u << 24)
-                     : Codec::is_running(code)
-                         ? (2u << 24) | (static_cast<uint32_t>(codec.run_size(code)) << 16) |
-                               static_cast<uint32_t>(codec.run_rem(code))
-                         : 0u;
+                     : Codec::is_running(code) ? (2u << 24) | (static_cast<uint32_t>(codec.run_size(code)) << 16) |
+                                                     static_cast<uint32_t>(codec.run_rem(code))
+                                               : 0u;
         }
+      }
       bool dead[2] = {false, false};
       for (int j = 0; j < n; ++j) {
         const int h = j >> 5, src = j & 31;
@@ -1013,16 +1086,14 @@ __device__ void phase_dominance(const V2& a, int s) {
         const uint64_t la = __shfl_sync(0xffffffffu, lx[h], src);
         for (int hb = 0; hb < 2; ++hb) {
           if (q[hb] < 0 || lane + 32 * hb == j) continue;
-          // status_dominates (solvers.hpp:128-134) on decoded fields, every tenant
-          const bool dom = dom_decoded(d0, dk[hb][0]) && dom_decoded(d1, dk[hb][1]);
-          if (dom && better(va, la, v[hb], lx[hb])) dead[hb] = true;
+          if (dom_decoded(d0, dk[hb][0]) && dom_decoded(d1, dk[hb][1]) && better(va, la, v[hb], lx[hb]))
+            dead[hb] = true;
         }
       }
       for (int h = 0; h < 2; ++h)
         if (q[h] >= 0 && dead[h]) {
           N.alive[q[h]] = 0;
           atomicSub(&N.g_alive[N.group[q[h]]], 1);
-          atomicSub(&a.ctl->n_alive[nxt], 1);
         }
     }
     if (lane == 0) a.pcnt[p] = 0;
@@ -1033,6 +1104,8 @@ template <int M>
 __global__ void __launch_bounds__(kThreads, 2) k_solve_v2(V2 a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ unsigned long long smem_u64[];
+  __shared__ int s_cnt[kBatch], s_gof[kBatch];
+  __shared__ long long s_red[32];
   const int P1 = a.sp.P1;
   TransSmem T;
   T.ex = smem_u64;
@@ -1040,10 +1113,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve_v2(V2 a) {
   T.rk = reinterpret_cast<uint32_t*>(T.vb + a.n_partial);
   T.ix = reinterpret_cast<int32_t*>(T.rk + a.n_partial);
   T.tg = reinterpret_cast<uint32_t*>(T.ix + a.n_partial);
-  for (int i = threadIdx.x; i < P1; i += kThreads) T.ex[i] = 0ull;  // tags start at 1
-  for (int i = threadIdx.x; i < a.n_partial; i += kThreads) T.tg[i] = 0u;
   uint32_t tag = 0;
-  __syncthreads();
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   if (a.dbg_time) {  // barrier cost probe (debug only)
     grid.sync();
@@ -1057,123 +1127,126 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve_v2(V2 a) {
     const int cur = s & 1, nxt = (s + 1) & 1;
     Ctl* ctl = a.ctl;
     StepCounters& sc = ctl->sc[s & 1];
-    // frontier checks for F_s (solvers.hpp:348 and :539-542 of the previous step)
-    const int alive_cur = ctl->n_alive[cur];
-    if (alive_cur == 0) {
-      if (gtid == 0) raise_err(a, phi, MGS_ERR_INFEASIBLE_JOINT, s);
-    } else if (s > 0 && static_cast<uint64_t>(alive_cur) > a.budget) {
-      if (gtid == 0) raise_err(a, phi, MGS_ERR_STATE_BUDGET, s, alive_cur);
-    }
-    if (s > 0 && gtid == 0) {
-      ctl->ftot += alive_cur;
-      if (static_cast<unsigned long long>(alive_cur) > ctl->fpeak) ctl->fpeak = alive_cur;
-    }
     // S1
-    phase_units<M>(a, s, phi);
+    phase_units<M>(a, s, phi, s_cnt, s_red);
     if (barrier(grid, a, phi)) return;
-    // S2: scans
-    {
-      ScanJob jobs[5] = {{a.ns_ccnt, a.ns_cbase, sc.n_ns},
-                         {a.ns_ucnt, a.ns_ubase, sc.n_ns},
-                         {a.u_chs, a.u_sbase, sc.n_units},
-                         {a.u_chb, a.u_bbase, sc.n_units},
-                         {a.kid_cnt[cur], a.kid_base, ranks_prev}};
-      multi_scan(a, jobs, 5, s + 1, &sc.ticket, ctl->scan_total);
-    }
-    if (barrier(grid, a, phi)) return;
-    {
-      const int T_ = ctl->scan_total[0];
-      if (gtid == 0) {
-        sc.T = T_;
-        sc.items_s = ctl->scan_total[2];
-        sc.items_b = ctl->scan_total[3];
-        ctl->tr += static_cast<unsigned long long>(T_);
-        ctl->tbytes += static_cast<unsigned long long>(ctl->n_store[cur]) * 20ull +
-                       static_cast<unsigned long long>(T_) * 37ull;
-        if (T_ > a.ccap) raise_err(a, phi, kOverflow, s, 0, 7, T_);
-        if (ctl->scan_total[2] > a.itcap || ctl->scan_total[3] > a.itcap)
-          raise_err(a, phi, kOverflow, s, 0, 8, max(ctl->scan_total[2], ctl->scan_total[3]));
+    // frontier checks for F_s (solvers.hpp:348, and :539-542 of the previous step)
+    const int alive_cur = ctl->alive_now[cur];
+    if (gtid == 0) {
+      if (alive_cur == 0) raise_err(a, phi, MGS_ERR_INFEASIBLE_JOINT, s);
+      else if (s > 0 && static_cast<uint64_t>(alive_cur) > a.budget)
+        raise_err(a, phi, MGS_ERR_STATE_BUDGET, s, alive_cur);
+      if (s > 0) {
+        ctl->ftot += alive_cur;
+        if (static_cast<unsigned long long>(alive_cur) > ctl->fpeak) ctl->fpeak = alive_cur;
       }
     }
-    // S3 (reads scan totals written before the barrier)
-    if (ctl->scan_total[0] <= a.ccap && ctl->scan_total[2] <= a.itcap && ctl->scan_total[3] <= a.itcap)
-      phase_place(a, s, phi);
+    // S2: scans
+    {
+      const int H = a.hmask + 1;
+      ScanJob jobs[kNumScans] = {{a.ns_ccnt, nullptr, a.ns_cbase, H, 0},
+                                 {a.ns_ucnt, nullptr, a.ns_ubase, H, 0},
+                                 {a.ns_ucnt, a.ns_ccnt, a.ns_bigpos, H, 1},
+                                 {a.ns_ucnt, a.ns_ccnt, a.ns_smallpos, H, 2},
+                                 {a.u_chs, nullptr, a.u_sbase, sc.n_units, 0},
+                                 {a.u_chb, nullptr, a.u_bbase, sc.n_units, 0},
+                                 {a.kid_cnt[cur], nullptr, a.kid_base, ranks_prev, 0}};
+      multi_scan(a, jobs, s + 1, &sc.ticket, ctl->scan_total);
+    }
+    if (barrier(grid, a, phi)) return;
+    const int T_ = ctl->scan_total[0];
+    if (gtid == 0) {
+      sc.T = T_;
+      sc.n_big = ctl->scan_total[2];
+      sc.n_small = ctl->scan_total[3];
+      sc.items_s = ctl->scan_total[4];
+      sc.items_b = ctl->scan_total[5];
+      sc.kids = ctl->scan_total[6];
+      ctl->tr += static_cast<unsigned long long>(T_);
+      ctl->tbytes +=
+          static_cast<unsigned long long>(ctl->n_store[cur]) * 20ull + static_cast<unsigned long long>(T_) * 37ull;
+      if (T_ > a.ccap) raise_err(a, phi, kOverflow, s, 0, 7, T_);
+      if (ctl->scan_total[4] > a.itcap || ctl->scan_total[5] > a.itcap)
+        raise_err(a, phi, kOverflow, s, 0, 8, max(ctl->scan_total[4], ctl->scan_total[5]));
+    }
+    // S3
+    if (T_ <= a.ccap && ctl->scan_total[4] <= a.itcap && ctl->scan_total[5] <= a.itcap) phase_place(a, s);
     if (barrier(grid, a, phi)) return;
     // S4
     phase_ranks(a, s, smem_u64);
     if (barrier(grid, a, phi)) return;
-    // S5
-    // the shared-memory tables are clobbered by S4/S6: start each S5 clean
+    // S5 (the shared-memory tables are clobbered by S4 / S6: start clean)
     for (int i = threadIdx.x; i < P1; i += kThreads) T.ex[i] = 0ull;
     for (int i = threadIdx.x; i < a.n_partial; i += kThreads) T.tg[i] = 0u;
     tag = 0;
     __syncthreads();
     phase_trans<M>(a, s, T, tag);
-    // reset the counters of the step after next and the hash table
-    if (gtid == 0) {
-      StepCounters& o = ctl->sc[(s + 1) & 1];
-      o = StepCounters{};
+    if (gtid == 0) {  // counters of the next step
+      ctl->sc[nxt] = StepCounters{};
       ctl->n_store[nxt] = 0;
       ctl->n_groups[nxt] = 0;
-      ctl->n_alive[nxt] = 0;
+      ctl->alive_now[nxt] = 0;
     }
-    for (int i = gtid; i <= a.hmask; i += gstride) a.hash[i] = 0ull;
     if (barrier(grid, a, phi)) return;
     // S6
-    phase_merge_out(a, s, phi, smem_u64, smem_u64 + kMergeWin);
+    phase_merge_out(a, s, phi, smem_u64, smem_u64 + kMergeWin, s_cnt, s_gof);
     if (barrier(grid, a, phi)) return;
     // S7
     if (a.dominance_ok) phase_dominance(a, s);
-    {
-      const int NS = sc.n_ns;
-      for (int i = gtid; i < NS; i += gstride) {
-        a.ns_ucnt[i] = 0;
-        a.ns_ccnt[i] = 0;
-        a.ns_ucur[i] = 0;
-        a.ns_ccur[i] = 0;
-      }
-      for (int i = gtid; i < ranks_prev; i += gstride) {
-        a.kid_cnt[cur][i] = 0;
-        a.kid_cur[cur][i] = 0;
-      }
-      if (gtid == 0) a.hist_base[s + 2] = a.hist_base[s + 1] + ctl->n_store[nxt];  // array has S+2 entries
+    for (int i = gtid; i <= a.hmask; i += gstride) {  // S6 read the keys from the hash: clear now
+      a.hash[i] = 0u;
+      a.ns_ucnt[i] = 0;
+      a.ns_ccnt[i] = 0;
+      a.ns_ucur[i] = 0;
+      a.ns_ccur[i] = 0;
+    }
+    for (int i = gtid; i < ranks_prev; i += gstride) {
+      a.kid_cnt[cur][i] = 0;
+      a.kid_cur[cur][i] = 0;
     }
     if (gtid == 0) {
-      long long* d = a.dbg + 6ll * s;
-      d[0] = sc.n_units;
-      d[1] = sc.n_ns;
-      d[2] = sc.T;
-      d[3] = ctl->n_store[nxt];
-      d[4] = ctl->n_groups[nxt];
-      d[5] = alive_cur;
+      a.hist_base[s + 2] = a.hist_base[s + 1] + ctl->n_store[nxt];  // array has S+2 entries
+      if (a.dbg) {
+        long long* d = a.dbg + 6ll * s;
+        d[0] = sc.n_units;
+        d[1] = sc.n_big + sc.n_small;
+        d[2] = sc.T;
+        d[3] = ctl->n_store[nxt];
+        d[4] = ctl->n_groups[nxt];
+        d[5] = alive_cur;
+      }
     }
     ranks_prev = alive_cur;
     if (barrier(grid, a, phi)) return;
   }
-  // terminal (solvers.hpp:552-565)
+  // terminal (solvers.hpp:552-565): live count of F_S, budget, best all-done state
   const int fin = a.S & 1;
-  const int alive_fin = a.ctl->n_alive[fin];
-  if (static_cast<uint64_t>(alive_fin) > a.budget) {
-    if (gtid == 0) raise_err(a, phi, MGS_ERR_STATE_BUDGET, a.S, alive_fin);
-  }
-  if (gtid == 0) {
-    a.ctl->ftot += alive_fin;
-    if (static_cast<unsigned long long>(alive_fin) > a.ctl->fpeak) a.ctl->fpeak = alive_fin;
-  }
-  uint32_t all_done = 0;
-  for (int m = 0; m < a.t.M; ++m) all_done |= static_cast<uint32_t>(Codec::done()) << (16 * m);
   const FrontierV2& F = a.f[fin];
   const int n = a.ctl->n_store[fin];
+  uint32_t all_done = 0;
+  for (int m = 0; m < a.t.M; ++m) all_done |= static_cast<uint32_t>(Codec::done()) << (16 * m);
+  long long live = 0;
   unsigned long long mv = 0;
   bool any = false;
   for (int i = gtid; i < n; i += gstride)
-    if (F.alive[i] && F.status[i] == all_done) {
-      const unsigned long long vb = vbits(F.value[i]);
-      mv = any && mv > vb ? mv : vb;
-      any = true;
+    if (F.alive[i]) {
+      ++live;
+      if (F.status[i] == all_done) {
+        const unsigned long long vb = vbits(F.value[i]);
+        mv = any && mv > vb ? mv : vb;
+        any = true;
+      }
     }
+  const long long ls = block_sum(live, s_red);
+  if (threadIdx.x == 0 && ls) atomicAdd(&a.ctl->alive_now[fin], static_cast<int>(ls));
   if (any) atomicMax(&a.ctl->best_vb, mv + 1);  // +1: 0 = none
   if (barrier(grid, a, phi)) return;
+  const int alive_fin = a.ctl->alive_now[fin];
+  if (gtid == 0) {
+    a.ctl->ftot += alive_fin;
+    if (static_cast<unsigned long long>(alive_fin) > a.ctl->fpeak) a.ctl->fpeak = alive_fin;
+    if (static_cast<uint64_t>(alive_fin) > a.budget) raise_err(a, phi, MGS_ERR_STATE_BUDGET, a.S, alive_fin);
+  }
   const unsigned long long bvb = a.ctl->best_vb;
   if (bvb == 0) {
     if (gtid == 0) raise_err(a, phi, MGS_ERR_INFEASIBLE_JOINT, a.S);
@@ -1200,6 +1273,7 @@ __global__ void k_init_root(V2 a, uint32_t root_pid) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   FrontierV2 F = a.f[0];
   F.status[0] = 0;
+  F.ids[0] = static_cast<uint32_t>(a.sp.pl_ids[root_pid]);
   F.pid[0] = root_pid;
   F.value[0] = 0.0;
   F.lex[0] = 0;
@@ -1213,7 +1287,6 @@ __global__ void k_init_root(V2 a, uint32_t root_pid) {
   Ctl* c = a.ctl;
   c->n_store[0] = 1;
   c->n_groups[0] = 1;
-  c->n_alive[0] = 1;
   c->best_vb = 0;
   c->best_lex = ~0ull;
   c->best_idx = -1;
@@ -1227,7 +1300,7 @@ __global__ void k_sig_len(const int32_t* sig_off, int n_sig, int32_t* sig_len) {
 }
 
 struct Caps {
-  int fcap, gcap, ucap, nscap, itcap, ccap, hbits;
+  int fcap, gcap, ucap, itcap, ccap, hbits;
   long long hcap;
 };
 
@@ -1263,7 +1336,8 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
   const int n_sub = 1 << M;
   const int n_partial = sp.proj_base[n_sub - 1];  // all subsets but the full one
   const size_t smem_trans = static_cast<size_t>(sp.P1) * 8 + static_cast<size_t>(n_partial) * 20;
-  const size_t smem = std::max({smem_trans, static_cast<size_t>(2 * kMergeWin * 8), static_cast<size_t>(kBucketStage * 8)});
+  const size_t smem =
+      std::max({smem_trans, static_cast<size_t>(2 * kMergeWin * 8), static_cast<size_t>(kBucketStage * 8)});
   auto kern = M == 1 ? k_solve_v2<1> : k_solve_v2<2>;
   MGS_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int occ = 0;
@@ -1271,9 +1345,10 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
   if (occ < 1) throw PlanFail{MGS_ERR_CUDA, "persistent DP kernel does not fit on an SM"};
   const int grid = c.sm_count * std::min(occ, 2);
 
-  static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 17, 1 << 18, 1 << 22, 18, 64ll << 20};
+  static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 64ll << 20};
   const uint64_t budget = p.state_budget;
-  for (int attempt = 0; attempt < 8; ++attempt) {
+  const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr;
+  for (int attempt = 0; attempt < 10; ++attempt) {
     V2 a{};
     a.sp = sp;
     a.t = t;
@@ -1291,6 +1366,7 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
       std::string tg = b ? "v2b_" : "v2a_";
       FrontierV2& f = a.f[b];
       f.status = c.buf<uint32_t>((tg + "status").c_str(), caps.fcap);
+      f.ids = c.buf<uint32_t>((tg + "ids").c_str(), caps.fcap);
       f.pid = c.buf<int32_t>((tg + "pid").c_str(), caps.fcap);
       f.value = c.buf<double>((tg + "value").c_str(), caps.fcap);
       f.lex = c.buf<uint64_t>((tg + "lex").c_str(), caps.fcap);
@@ -1308,6 +1384,8 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     }
     a.kid_base = c.buf<int32_t>("v2_kidbase", caps.fcap + 1);
     a.kid_items = c.buf<uint64_t>("v2_kiditems", caps.fcap);
+    a.kid_pr = c.buf<int32_t>("v2_kidpr", caps.fcap);
+    a.big_bucket = c.buf<int32_t>("v2_bigbucket", caps.fcap);
     a.hcap = caps.hcap;
     a.h_parent = c.buf<int32_t>("v2_hparent", caps.hcap);
     a.h_oi = c.buf<int32_t>("v2_hoi", caps.hcap);
@@ -1321,22 +1399,23 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     a.u_cbase = c.buf<int32_t>("v2_ucbase", caps.ucap);
     a.u_sbase = c.buf<int32_t>("v2_usbase", caps.ucap);
     a.u_bbase = c.buf<int32_t>("v2_ubbase", caps.ucap);
-    a.hmask = (1 << caps.hbits) - 1;
-    a.hash = c.buf<unsigned long long>("v2_hash", a.hmask + 1);
-    MGS_CUDA_OK(cudaMemsetAsync(a.hash, 0, static_cast<size_t>(a.hmask + 1) * 8, c.stream));
-    a.nscap = caps.nscap;
-    a.ns_key = c.buf<uint32_t>("v2_nskey", caps.nscap);
-    a.ns_ucnt = c.buf<int32_t>("v2_nsucnt", caps.nscap);
-    a.ns_ccnt = c.buf<int32_t>("v2_nsccnt", caps.nscap);
-    a.ns_ubase = c.buf<int32_t>("v2_nsubase", caps.nscap);
-    a.ns_cbase = c.buf<int32_t>("v2_nscbase", caps.nscap);
-    a.ns_ucur = c.buf<int32_t>("v2_nsucur", caps.nscap);
-    a.ns_ccur = c.buf<int32_t>("v2_nsccur", caps.nscap);
     a.ns_units = c.buf<int32_t>("v2_nsunits", caps.ucap);
-    a.ns_big = c.buf<int32_t>("v2_nsbig", caps.nscap);
-    a.ns_small = c.buf<int32_t>("v2_nssmall", caps.nscap);
-    for (int32_t* z : {a.ns_ucnt, a.ns_ccnt, a.ns_ucur, a.ns_ccur})
-      MGS_CUDA_OK(cudaMemsetAsync(z, 0, static_cast<size_t>(caps.nscap) * 4, c.stream));
+    a.hmask = (1 << caps.hbits) - 1;
+    const size_t H = static_cast<size_t>(a.hmask) + 1;
+    a.hash = c.buf<uint32_t>("v2_hash", H);
+    a.ns_ucnt = c.buf<int32_t>("v2_nsucnt", H);
+    a.ns_ccnt = c.buf<int32_t>("v2_nsccnt", H);
+    a.ns_ubase = c.buf<int32_t>("v2_nsubase", H);
+    a.ns_cbase = c.buf<int32_t>("v2_nscbase", H);
+    a.ns_ucur = c.buf<int32_t>("v2_nsucur", H);
+    a.ns_ccur = c.buf<int32_t>("v2_nsccur", H);
+    a.ns_bigpos = c.buf<int32_t>("v2_nsbigpos", H);
+    a.ns_smallpos = c.buf<int32_t>("v2_nssmallpos", H);
+    a.ns_big = c.buf<int32_t>("v2_nsbig", H);
+    a.ns_small = c.buf<int32_t>("v2_nssmall", H);
+    for (void* z : {static_cast<void*>(a.hash), static_cast<void*>(a.ns_ucnt), static_cast<void*>(a.ns_ccnt),
+                    static_cast<void*>(a.ns_ucur), static_cast<void*>(a.ns_ccur)})
+      MGS_CUDA_OK(cudaMemsetAsync(z, 0, H * 4, c.stream));
     a.itcap = caps.itcap;
     a.it_s_unit = c.buf<int32_t>("v2_itsu", caps.itcap);
     a.it_s_chunk = c.buf<int32_t>("v2_itsc", caps.itcap);
@@ -1349,11 +1428,10 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     a.c_pid = c.buf<int32_t>("v2_cpid", caps.ccap);
     a.c_ok = c.buf<uint8_t>("v2_cok", caps.ccap);
     a.c_live = c.buf<uint8_t>("v2_clive", caps.ccap);
-    a.big_bucket = c.buf<int32_t>("v2_bigbucket", caps.fcap);
     a.pcnt = c.buf<int32_t>("v2_pcnt", sp.P1);
     a.pbucket = c.buf<int32_t>("v2_pbucket", static_cast<size_t>(sp.P1) * 64);
     MGS_CUDA_OK(cudaMemsetAsync(a.pcnt, 0, static_cast<size_t>(sp.P1) * 4, c.stream));
-    a.scan_cap = 5 * (caps.fcap / kTile + 8) + 4 * (caps.ucap / kTile + 8);
+    a.scan_cap = 4 * static_cast<int>(H / kTile + 8) + 2 * (caps.ucap / kTile + 8) + (caps.fcap / kTile + 8);
     a.scan_state = c.buf<unsigned long long>("v2_scan", a.scan_cap);
     MGS_CUDA_OK(cudaMemsetAsync(a.scan_state, 0, static_cast<size_t>(a.scan_cap) * 8, c.stream));
     a.sig_len = c.buf<int32_t>("v2_siglen", sp.n_sig);
@@ -1362,9 +1440,9 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     a.ctl = c.buf<Ctl>("v2_ctl", 1);
     MGS_CUDA_OK(cudaMemsetAsync(a.ctl, 0, sizeof(Ctl), c.stream));
     a.chosen = c.buf<int32_t>("v2_chosen", S);
-    a.dbg = c.buf<long long>("v2_dbg", 6 * S);
-    a.dbg_time = std::getenv("MGS_DEBUG_STEPS") ? c.buf<unsigned long long>("v2_dbgt", 8 * S + 16) : nullptr;
     a.n_partial = n_partial;
+    a.dbg = debug ? c.buf<long long>("v2_dbg", 6 * S) : nullptr;
+    a.dbg_time = debug ? c.buf<unsigned long long>("v2_dbgt", 8 * S + 16) : nullptr;
     k_init_root<<<1, 32, 0, c.stream>>>(a, static_cast<uint32_t>(sp.root_pid));
     ++c.kernel_launches;
     void* args[] = {&a};
@@ -1376,8 +1454,7 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     if (h.err_code == kOverflow) {
       const long long need = h.need;
       switch (h.need_what) {
-        case 1: caps.nscap = static_cast<int>(std::max<long long>(need * 2, caps.nscap * 2ll)); break;
-        case 2: caps.hbits += 2; break;
+        case 2: caps.hbits += 1; break;
         case 3: caps.ucap = static_cast<int>(std::max<long long>(need * 2, caps.ucap * 2ll)); break;
         case 4: caps.fcap = static_cast<int>(std::max<long long>(need * 2, caps.fcap * 2ll)); break;
         case 5: caps.gcap = static_cast<int>(std::max<long long>(need * 2, caps.gcap * 2ll)); break;
@@ -1386,9 +1463,26 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
         case 8: caps.itcap = static_cast<int>(std::max<long long>(need * 2, caps.itcap * 2ll)); break;
         default: throw PlanFail{MGS_ERR_CUDA, "persistent DP: unknown capacity overflow"};
       }
-      if (caps.nscap > caps.ucap) caps.ucap = caps.nscap;
-      while ((1 << caps.hbits) < 4 * caps.nscap) ++caps.hbits;
       continue;
+    }
+    if (debug) {
+      std::vector<long long> d(6 * S);
+      MGS_CUDA_OK(cudaMemcpy(d.data(), a.dbg, d.size() * 8, cudaMemcpyDeviceToHost));
+      for (int s = 0; s < S; ++s)
+        std::fprintf(stderr, "v2 step %d units %lld ns %lld T %lld store %lld groups %lld alive_in %lld\n", s, d[6 * s],
+                     d[6 * s + 1], d[6 * s + 2], d[6 * s + 3], d[6 * s + 4], d[6 * s + 5]);
+      std::vector<unsigned long long> tm(8 * S + 16);
+      MGS_CUDA_OK(cudaMemcpy(tm.data(), a.dbg_time, tm.size() * 8, cudaMemcpyDeviceToHost));
+      double ph[7] = {0, 0, 0, 0, 0, 0, 0};
+      for (int s = 0; s < S; ++s)
+        for (int k = 0; k < 7; ++k) {
+          const int i = 7 * s + k;
+          if (i > 0) ph[k] += (tm[i] - tm[i - 1]) * 1e-3;
+        }
+      std::fprintf(stderr,
+                   "v2 phase us (sum over steps): units %.1f scans %.1f place %.1f ranks %.1f trans %.1f merge %.1f dom "
+                   "%.1f | grid.sync %.2f us | grid %d CTAs\n",
+                   ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[6], tm[8 * S + 8] * 1e-3, grid);
     }
     if (h.err_code == MGS_ERR_STATE_BUDGET)
       throw PlanFail{MGS_ERR_STATE_BUDGET,
@@ -1401,28 +1495,6 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     out.options.resize(S);
     MGS_CUDA_OK(cudaMemcpyAsync(out.options.data(), a.chosen, S * 4, cudaMemcpyDeviceToHost, c.stream));
     MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
-    if (std::getenv("MGS_DEBUG_STEPS")) {
-      std::vector<long long> d(6 * S);
-      MGS_CUDA_OK(cudaMemcpy(d.data(), a.dbg, d.size() * 8, cudaMemcpyDeviceToHost));
-      for (int s = 0; s < S; ++s)
-        std::fprintf(stderr, "v2 step %d units %lld ns %lld T %lld store %lld groups %lld alive_in %lld\n", s, d[6 * s],
-                     d[6 * s + 1], d[6 * s + 2], d[6 * s + 3], d[6 * s + 4], d[6 * s + 5]);
-      if (a.dbg_time) {
-        std::vector<unsigned long long> tm(8 * S + 16);
-        MGS_CUDA_OK(cudaMemcpy(tm.data(), a.dbg_time, tm.size() * 8, cudaMemcpyDeviceToHost));
-        double ph[7] = {0, 0, 0, 0, 0, 0, 0};
-        for (int s = 0; s < S; ++s)
-          for (int k = 0; k < 7; ++k) {
-            const int i = 7 * s + k;
-            if (i > 0) ph[k] += (tm[i] - tm[i - 1]) * 1e-3;
-          }
-        std::fprintf(stderr, "v2 phase us (sum over steps): units %.1f scans %.1f place %.1f ranks %.1f trans %.1f merge %.1f dom %.1f | grid.sync %.2f us\n",
-                     ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[6], tm[8 * S + 8] * 1e-3);
-      }
-      std::fprintf(stderr, "v2 chosen:");
-      for (int s = 0; s < S; ++s) std::fprintf(stderr, " %d", out.options[s]);
-      std::fprintf(stderr, "\n");
-    }
     out.stats.options = sp.n_opt;
     out.stats.candidates = sp.n_cand;
     out.stats.transitions_ref = h.tr_ref;
