@@ -1,6 +1,7 @@
-// Persistent single-launch DP engine (M <= 2): the whole per-window search of
-// solve_dp (solvers.hpp:242-579) as ONE cooperative kernel, 7 grid barriers per
-// slot, no host round trips, no sorts, no hot (same-address) global atomics.
+// Device-resident DP engine (M <= 2): the whole per-window search of solve_dp
+// (solvers.hpp:242-579) as a stream of phase kernels with every count kept on
+// the device: no host round trips inside a window, no sorts, no hot
+// (same-address) global atomics.
 //
 // Same procedure as the reference (and as the multi-launch engine in dp.cu):
 // subset representatives per status group, subset-candidate predecessor choice
@@ -33,15 +34,11 @@
 //
 // Dead (dominated) states stay in F_{s+1} as holes flagged alive = 0 and are
 // skipped everywhere; ranks are dense over the live states only.
-#include <cooperative_groups.h>
-
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
 #include "ctx.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace mgs {
 namespace {
@@ -94,6 +91,7 @@ struct Ctl {
   unsigned long long tr_ref, tr, ftot, fpeak, tbytes;
   unsigned long long best_vb, best_lex;
   int best_idx;
+  int ranks_prev;  // live states of F_{s-1}: the parent-rank space of F_s
   int scan_total[kNumScans];
 };
 
@@ -143,6 +141,7 @@ struct V2 {
   Ctl* ctl;
   int32_t* chosen;
   int n_partial;                 // entries of the partial-subset tables (all subsets but the full one)
+  int sc_big_ctas;               // CTAs of k_trans that may take big-group items
   long long* dbg;                // [S][6] per-step counters (debug dump)
   unsigned long long* dbg_time;  // barrier timestamps (debug)
 };
@@ -161,24 +160,17 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 __device__ void raise_err(const V2& a, int phi, int code, int step = 0, unsigned long long count = 0, int what = 0,
                           long long need = 0) {
+  (void)phi;
   if (atomicCAS(&a.ctl->err_code, 0, code) == 0) {
     a.ctl->err_step = step;
     a.ctl->err_count = count;
     a.ctl->need_what = what;
     a.ctl->need = need;
   }
-  atomicExch(&a.ctl->err[phi & 1], 1);
 }
 
-// grid barrier + uniform error check (errors raised in phase phi become
-// visible to every CTA after the barrier that ends phi)
-__device__ __forceinline__ bool barrier(cg::grid_group& grid, const V2& a, int& phi) {
-  grid.sync();
-  if (a.dbg_time && blockIdx.x == 0 && threadIdx.x == 0) a.dbg_time[phi] = globaltimer();
-  const int e = ld_volatile(&a.ctl->err[phi & 1]);
-  ++phi;
-  return e != 0;
-}
+// every phase kernel returns immediately once any error was raised
+__device__ __forceinline__ bool failed(const V2& a) { return ld_volatile(&a.ctl->err_code) != 0; }
 
 // ---------------------------------------------------------------------------
 // block reductions / scans (kThreads threads)
@@ -1100,12 +1092,74 @@ __device__ void phase_dominance(const V2& a, int s) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Phase kernels: one launch per phase and slot, stream-ordered, all counts on
+// the device (the host never waits inside a window).
 template <int M>
-__global__ void __launch_bounds__(kThreads, 2) k_solve_v2(V2 a) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ unsigned long long smem_u64[];
-  __shared__ int s_cnt[kBatch], s_gof[kBatch];
+__global__ void __launch_bounds__(kThreads) k_units(V2 a, int s) {
+  __shared__ int s_cnt[kBatch];
   __shared__ long long s_red[32];
+  if (failed(a)) return;
+  phase_units<M>(a, s, 0, s_cnt, s_red);
+}
+
+__global__ void __launch_bounds__(kThreads) k_scans(V2 a, int s) {
+  if (failed(a)) return;
+  const int cur = s & 1;
+  Ctl* ctl = a.ctl;
+  StepCounters& sc = ctl->sc[s & 1];
+  const int alive_cur = ctl->alive_now[cur];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // frontier checks for F_s (solvers.hpp:348, :539-542)
+    if (alive_cur == 0) raise_err(a, 0, MGS_ERR_INFEASIBLE_JOINT, s);
+    else if (s > 0 && static_cast<uint64_t>(alive_cur) > a.budget) raise_err(a, 0, MGS_ERR_STATE_BUDGET, s, alive_cur);
+    if (s > 0) {
+      ctl->ftot += alive_cur;
+      if (static_cast<unsigned long long>(alive_cur) > ctl->fpeak) ctl->fpeak = alive_cur;
+    }
+  }
+  const int H = a.hmask + 1;
+  const ScanJob jobs[kNumScans] = {{a.ns_ccnt, nullptr, a.ns_cbase, H, 0},
+                                   {a.ns_ucnt, nullptr, a.ns_ubase, H, 0},
+                                   {a.ns_ucnt, a.ns_ccnt, a.ns_bigpos, H, 1},
+                                   {a.ns_ucnt, a.ns_ccnt, a.ns_smallpos, H, 2},
+                                   {a.u_chs, nullptr, a.u_sbase, sc.n_units, 0},
+                                   {a.u_chb, nullptr, a.u_bbase, sc.n_units, 0},
+                                   {a.kid_cnt[cur], nullptr, a.kid_base, ctl->ranks_prev, 0}};
+  multi_scan(a, jobs, s + 1, &sc.ticket, ctl->scan_total);
+}
+
+__global__ void __launch_bounds__(kThreads) k_place(V2 a, int s) {
+  if (failed(a)) return;
+  Ctl* ctl = a.ctl;
+  StepCounters& sc = ctl->sc[s & 1];
+  const int T_ = ctl->scan_total[0];
+  const bool fits = T_ <= a.ccap && ctl->scan_total[4] <= a.itcap && ctl->scan_total[5] <= a.itcap;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc.T = T_;
+    sc.n_big = ctl->scan_total[2];
+    sc.n_small = ctl->scan_total[3];
+    sc.items_s = ctl->scan_total[4];
+    sc.items_b = ctl->scan_total[5];
+    sc.kids = ctl->scan_total[6];
+    ctl->tr += static_cast<unsigned long long>(T_);
+    ctl->tbytes += static_cast<unsigned long long>(ctl->n_store[s & 1]) * 20ull + static_cast<unsigned long long>(T_) * 37ull;
+    if (T_ > a.ccap) raise_err(a, 0, kOverflow, s, 0, 7, T_);
+    if (ctl->scan_total[4] > a.itcap || ctl->scan_total[5] > a.itcap)
+      raise_err(a, 0, kOverflow, s, 0, 8, max(ctl->scan_total[4], ctl->scan_total[5]));
+  }
+  if (fits) phase_place(a, s);
+}
+
+__global__ void __launch_bounds__(kThreads) k_ranks(V2 a, int s) {
+  extern __shared__ unsigned long long smem_u64[];
+  if (failed(a)) return;
+  phase_ranks(a, s, smem_u64);
+}
+
+template <int M>
+__global__ void __launch_bounds__(kThreads) k_trans(V2 a, int s) {
+  extern __shared__ unsigned long long smem_u64[];
+  if (failed(a)) return;
   const int P1 = a.sp.P1;
   TransSmem T;
   T.ex = smem_u64;
@@ -1113,118 +1167,83 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve_v2(V2 a) {
   T.rk = reinterpret_cast<uint32_t*>(T.vb + a.n_partial);
   T.ix = reinterpret_cast<int32_t*>(T.rk + a.n_partial);
   T.tg = reinterpret_cast<uint32_t*>(T.ix + a.n_partial);
-  uint32_t tag = 0;
-  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
-  if (a.dbg_time) {  // barrier cost probe (debug only)
-    grid.sync();
-    const unsigned long long t0 = globaltimer();
-    for (int k = 0; k < 64; ++k) grid.sync();
-    if (gtid == 0) a.dbg_time[8 * a.S + 8] = (globaltimer() - t0) / 64;
-  }
-  int phi = 0;
-  int ranks_prev = 1;  // live states of F_{s-1} (parent rank space); root: 1
-  for (int s = 0; s < a.S; ++s) {
-    const int cur = s & 1, nxt = (s + 1) & 1;
-    Ctl* ctl = a.ctl;
-    StepCounters& sc = ctl->sc[s & 1];
-    // S1
-    phase_units<M>(a, s, phi, s_cnt, s_red);
-    if (barrier(grid, a, phi)) return;
-    // frontier checks for F_s (solvers.hpp:348, and :539-542 of the previous step)
-    const int alive_cur = ctl->alive_now[cur];
-    if (gtid == 0) {
-      if (alive_cur == 0) raise_err(a, phi, MGS_ERR_INFEASIBLE_JOINT, s);
-      else if (s > 0 && static_cast<uint64_t>(alive_cur) > a.budget)
-        raise_err(a, phi, MGS_ERR_STATE_BUDGET, s, alive_cur);
-      if (s > 0) {
-        ctl->ftot += alive_cur;
-        if (static_cast<unsigned long long>(alive_cur) > ctl->fpeak) ctl->fpeak = alive_cur;
-      }
-    }
-    // S2: scans
-    {
-      const int H = a.hmask + 1;
-      ScanJob jobs[kNumScans] = {{a.ns_ccnt, nullptr, a.ns_cbase, H, 0},
-                                 {a.ns_ucnt, nullptr, a.ns_ubase, H, 0},
-                                 {a.ns_ucnt, a.ns_ccnt, a.ns_bigpos, H, 1},
-                                 {a.ns_ucnt, a.ns_ccnt, a.ns_smallpos, H, 2},
-                                 {a.u_chs, nullptr, a.u_sbase, sc.n_units, 0},
-                                 {a.u_chb, nullptr, a.u_bbase, sc.n_units, 0},
-                                 {a.kid_cnt[cur], nullptr, a.kid_base, ranks_prev, 0}};
-      multi_scan(a, jobs, s + 1, &sc.ticket, ctl->scan_total);
-    }
-    if (barrier(grid, a, phi)) return;
-    const int T_ = ctl->scan_total[0];
-    if (gtid == 0) {
-      sc.T = T_;
-      sc.n_big = ctl->scan_total[2];
-      sc.n_small = ctl->scan_total[3];
-      sc.items_s = ctl->scan_total[4];
-      sc.items_b = ctl->scan_total[5];
-      sc.kids = ctl->scan_total[6];
-      ctl->tr += static_cast<unsigned long long>(T_);
-      ctl->tbytes +=
-          static_cast<unsigned long long>(ctl->n_store[cur]) * 20ull + static_cast<unsigned long long>(T_) * 37ull;
-      if (T_ > a.ccap) raise_err(a, phi, kOverflow, s, 0, 7, T_);
-      if (ctl->scan_total[4] > a.itcap || ctl->scan_total[5] > a.itcap)
-        raise_err(a, phi, kOverflow, s, 0, 8, max(ctl->scan_total[4], ctl->scan_total[5]));
-    }
-    // S3
-    if (T_ <= a.ccap && ctl->scan_total[4] <= a.itcap && ctl->scan_total[5] <= a.itcap) phase_place(a, s);
-    if (barrier(grid, a, phi)) return;
-    // S4
-    phase_ranks(a, s, smem_u64);
-    if (barrier(grid, a, phi)) return;
-    // S5 (the shared-memory tables are clobbered by S4 / S6: start clean)
+  if (blockIdx.x < a.sc_big_ctas) {  // only CTAs that take big items need clean tables
     for (int i = threadIdx.x; i < P1; i += kThreads) T.ex[i] = 0ull;
     for (int i = threadIdx.x; i < a.n_partial; i += kThreads) T.tg[i] = 0u;
-    tag = 0;
     __syncthreads();
-    phase_trans<M>(a, s, T, tag);
-    if (gtid == 0) {  // counters of the next step
-      ctl->sc[nxt] = StepCounters{};
-      ctl->n_store[nxt] = 0;
-      ctl->n_groups[nxt] = 0;
-      ctl->alive_now[nxt] = 0;
-    }
-    if (barrier(grid, a, phi)) return;
-    // S6
-    phase_merge_out(a, s, phi, smem_u64, smem_u64 + kMergeWin, s_cnt, s_gof);
-    if (barrier(grid, a, phi)) return;
-    // S7
-    if (a.dominance_ok) phase_dominance(a, s);
-    for (int i = gtid; i <= a.hmask; i += gstride) {  // S6 read the keys from the hash: clear now
-      a.hash[i] = 0u;
-      a.ns_ucnt[i] = 0;
-      a.ns_ccnt[i] = 0;
-      a.ns_ucur[i] = 0;
-      a.ns_ccur[i] = 0;
-    }
-    for (int i = gtid; i < ranks_prev; i += gstride) {
-      a.kid_cnt[cur][i] = 0;
-      a.kid_cur[cur][i] = 0;
-    }
-    if (gtid == 0) {
-      a.hist_base[s + 2] = a.hist_base[s + 1] + ctl->n_store[nxt];  // array has S+2 entries
-      if (a.dbg) {
-        long long* d = a.dbg + 6ll * s;
-        d[0] = sc.n_units;
-        d[1] = sc.n_big + sc.n_small;
-        d[2] = sc.T;
-        d[3] = ctl->n_store[nxt];
-        d[4] = ctl->n_groups[nxt];
-        d[5] = alive_cur;
-      }
-    }
-    ranks_prev = alive_cur;
-    if (barrier(grid, a, phi)) return;
   }
-  // terminal (solvers.hpp:552-565): live count of F_S, budget, best all-done state
+  uint32_t tag = 0;
+  phase_trans<M>(a, s, T, tag);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // counters of the next step
+    const int nxt = (s + 1) & 1;
+    a.ctl->sc[nxt] = StepCounters{};
+    a.ctl->n_store[nxt] = 0;
+    a.ctl->n_groups[nxt] = 0;
+    a.ctl->alive_now[nxt] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_merge(V2 a, int s) {
+  extern __shared__ unsigned long long smem_u64[];
+  __shared__ int s_cnt[kBatch], s_gof[kBatch];
+  if (failed(a)) return;
+  phase_merge_out(a, s, 0, smem_u64, smem_u64 + kMergeWin, s_cnt, s_gof);
+}
+
+__global__ void __launch_bounds__(kThreads) k_dom(V2 a, int s) {
+  if (failed(a)) return;
+  const int cur = s & 1;
+  Ctl* ctl = a.ctl;
+  if (a.dominance_ok) phase_dominance(a, s);
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  for (int i = gtid; i <= a.hmask; i += gstride) {  // S6 read the keys from the hash: clear now
+    a.hash[i] = 0u;
+    a.ns_ucnt[i] = 0;
+    a.ns_ccnt[i] = 0;
+    a.ns_ucur[i] = 0;
+    a.ns_ccur[i] = 0;
+  }
+  const int rp = ctl->ranks_prev;
+  for (int i = gtid; i < rp; i += gstride) {
+    a.kid_cnt[cur][i] = 0;
+    a.kid_cur[cur][i] = 0;
+  }
+}
+
+// end-of-slot bookkeeping (after k_dom: every CTA has read ranks_prev)
+__global__ void k_step_end(V2 a, int s) {
+  if (failed(a) || threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int cur = s & 1, nxt = (s + 1) & 1;
+  Ctl* ctl = a.ctl;
+  StepCounters& sc = ctl->sc[s & 1];
+  a.hist_base[s + 2] = a.hist_base[s + 1] + ctl->n_store[nxt];  // array has S+2 entries
+  if (a.dbg) {
+    long long* d = a.dbg + 6ll * s;
+    d[0] = sc.n_units;
+    d[1] = sc.n_big + sc.n_small;
+    d[2] = sc.T;
+    d[3] = ctl->n_store[nxt];
+    d[4] = ctl->n_groups[nxt];
+    d[5] = ctl->alive_now[cur];
+  }
+  ctl->ranks_prev = ctl->alive_now[cur];
+}
+
+// terminal (solvers.hpp:552-565): live count of F_S, budget, best all-done state
+__device__ __forceinline__ uint32_t all_done_key(int M) {
+  uint32_t k = 0;
+  for (int m = 0; m < M; ++m) k |= static_cast<uint32_t>(Codec::done()) << (16 * m);
+  return k;
+}
+
+__global__ void __launch_bounds__(kThreads) k_term1(V2 a) {
+  __shared__ long long s_red[32];
+  if (failed(a)) return;
   const int fin = a.S & 1;
   const FrontierV2& F = a.f[fin];
   const int n = a.ctl->n_store[fin];
-  uint32_t all_done = 0;
-  for (int m = 0; m < a.t.M; ++m) all_done |= static_cast<uint32_t>(Codec::done()) << (16 * m);
+  const uint32_t all_done = all_done_key(a.t.M);
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   long long live = 0;
   unsigned long long mv = 0;
   bool any = false;
@@ -1240,32 +1259,47 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve_v2(V2 a) {
   const long long ls = block_sum(live, s_red);
   if (threadIdx.x == 0 && ls) atomicAdd(&a.ctl->alive_now[fin], static_cast<int>(ls));
   if (any) atomicMax(&a.ctl->best_vb, mv + 1);  // +1: 0 = none
-  if (barrier(grid, a, phi)) return;
+}
+
+__global__ void __launch_bounds__(kThreads) k_term2(V2 a) {
+  if (failed(a)) return;
+  const int fin = a.S & 1;
+  const FrontierV2& F = a.f[fin];
+  const int n = a.ctl->n_store[fin];
+  const uint32_t all_done = all_done_key(a.t.M);
   const int alive_fin = a.ctl->alive_now[fin];
+  const unsigned long long bvb = a.ctl->best_vb;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   if (gtid == 0) {
     a.ctl->ftot += alive_fin;
     if (static_cast<unsigned long long>(alive_fin) > a.ctl->fpeak) a.ctl->fpeak = alive_fin;
-    if (static_cast<uint64_t>(alive_fin) > a.budget) raise_err(a, phi, MGS_ERR_STATE_BUDGET, a.S, alive_fin);
+    if (static_cast<uint64_t>(alive_fin) > a.budget) raise_err(a, 0, MGS_ERR_STATE_BUDGET, a.S, alive_fin);
+    else if (bvb == 0) raise_err(a, 0, MGS_ERR_INFEASIBLE_JOINT, a.S);
   }
-  const unsigned long long bvb = a.ctl->best_vb;
-  if (bvb == 0) {
-    if (gtid == 0) raise_err(a, phi, MGS_ERR_INFEASIBLE_JOINT, a.S);
-  } else {
-    for (int i = gtid; i < n; i += gstride)
-      if (F.alive[i] && F.status[i] == all_done && vbits(F.value[i]) + 1 == bvb) atomicMin(&a.ctl->best_lex, F.lex[i]);
-  }
-  if (barrier(grid, a, phi)) return;
+  if (bvb == 0) return;
   for (int i = gtid; i < n; i += gstride)
-    if (F.alive[i] && F.status[i] == all_done && vbits(F.value[i]) + 1 == bvb && F.lex[i] == a.ctl->best_lex)
-      a.ctl->best_idx = i;
-  if (barrier(grid, a, phi)) return;
-  if (gtid == 0) {  // parent walk (solvers.hpp:567-574)
-    int idx = a.ctl->best_idx;
-    for (int s = a.S - 1; s >= 0; --s) {
-      const long long h = a.hist_base[s + 1] + idx;
-      a.chosen[s] = a.h_oi[h];
-      idx = a.h_parent[h];
-    }
+    if (F.alive[i] && F.status[i] == all_done && vbits(F.value[i]) + 1 == bvb) atomicMin(&a.ctl->best_lex, F.lex[i]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_term3(V2 a) {
+  if (failed(a)) return;
+  const int fin = a.S & 1;
+  const FrontierV2& F = a.f[fin];
+  const int n = a.ctl->n_store[fin];
+  const uint32_t all_done = all_done_key(a.t.M);
+  const unsigned long long bvb = a.ctl->best_vb, blx = a.ctl->best_lex;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  for (int i = gtid; i < n; i += gstride)
+    if (F.alive[i] && F.status[i] == all_done && vbits(F.value[i]) + 1 == bvb && F.lex[i] == blx) a.ctl->best_idx = i;
+}
+
+__global__ void k_backtrack2(V2 a) {  // parent walk (solvers.hpp:567-574)
+  if (failed(a) || threadIdx.x != 0 || blockIdx.x != 0) return;
+  int idx = a.ctl->best_idx;
+  for (int s = a.S - 1; s >= 0; --s) {
+    const long long h = a.hist_base[s + 1] + idx;
+    a.chosen[s] = a.h_oi[h];
+    idx = a.h_parent[h];
   }
 }
 
@@ -1290,6 +1324,7 @@ __global__ void k_init_root(V2 a, uint32_t root_pid) {
   c->best_vb = 0;
   c->best_lex = ~0ull;
   c->best_idx = -1;
+  c->ranks_prev = 1;
   a.hist_base[0] = 0;
   a.hist_base[1] = 0;
 }
@@ -1338,13 +1373,15 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
   const size_t smem_trans = static_cast<size_t>(sp.P1) * 8 + static_cast<size_t>(n_partial) * 20;
   const size_t smem =
       std::max({smem_trans, static_cast<size_t>(2 * kMergeWin * 8), static_cast<size_t>(kBucketStage * 8)});
-  auto kern = M == 1 ? k_solve_v2<1> : k_solve_v2<2>;
-  MGS_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int occ = 0;
-  MGS_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
-  if (occ < 1) throw PlanFail{MGS_ERR_CUDA, "persistent DP kernel does not fit on an SM"};
-  const int grid = c.sm_count * std::min(occ, 2);
-
+  const size_t smem_rank = static_cast<size_t>(kBucketStage) * 8;
+  const size_t smem_merge = static_cast<size_t>(2 * kMergeWin) * 8;
+  auto ktrans = M == 1 ? k_trans<1> : k_trans<2>;
+  auto kunits = M == 1 ? k_units<1> : k_units<2>;
+  MGS_CUDA_OK(cudaFuncSetAttribute(ktrans, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_trans)));
+  MGS_CUDA_OK(cudaFuncSetAttribute(k_ranks, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_rank)));
+  MGS_CUDA_OK(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_merge)));
+  const int grid = c.sm_count * 8;
+  (void)smem;
   static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 64ll << 20};
   const uint64_t budget = p.state_budget;
   const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr;
@@ -1442,12 +1479,27 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     a.chosen = c.buf<int32_t>("v2_chosen", S);
     a.n_partial = n_partial;
     a.dbg = debug ? c.buf<long long>("v2_dbg", 6 * S) : nullptr;
-    a.dbg_time = debug ? c.buf<unsigned long long>("v2_dbgt", 8 * S + 16) : nullptr;
+    a.dbg_time = nullptr;
     k_init_root<<<1, 32, 0, c.stream>>>(a, static_cast<uint32_t>(sp.root_pid));
     ++c.kernel_launches;
-    void* args[] = {&a};
-    MGS_CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, kThreads, args, smem, c.stream));
-    ++c.kernel_launches;
+    a.sc_big_ctas = grid;
+    for (int st = 0; st < S; ++st) {
+      kunits<<<grid, kThreads, 0, c.stream>>>(a, st);
+      k_scans<<<grid, kThreads, 0, c.stream>>>(a, st);
+      k_place<<<grid, kThreads, 0, c.stream>>>(a, st);
+      k_ranks<<<grid, kThreads, smem_rank, c.stream>>>(a, st);
+      ktrans<<<grid, kThreads, smem_trans, c.stream>>>(a, st);
+      k_merge<<<grid, kThreads, smem_merge, c.stream>>>(a, st);
+      k_dom<<<grid, kThreads, 0, c.stream>>>(a, st);
+      k_step_end<<<1, 32, 0, c.stream>>>(a, st);
+      c.kernel_launches += 8;
+    }
+    k_term1<<<grid, kThreads, 0, c.stream>>>(a);
+    k_term2<<<grid, kThreads, 0, c.stream>>>(a);
+    k_term3<<<grid, kThreads, 0, c.stream>>>(a);
+    k_backtrack2<<<1, 32, 0, c.stream>>>(a);
+    c.kernel_launches += 4;
+    MGS_CUDA_OK(cudaGetLastError());
     Ctl h{};
     MGS_CUDA_OK(cudaMemcpyAsync(&h, a.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
     MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
@@ -1471,18 +1523,6 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
       for (int s = 0; s < S; ++s)
         std::fprintf(stderr, "v2 step %d units %lld ns %lld T %lld store %lld groups %lld alive_in %lld\n", s, d[6 * s],
                      d[6 * s + 1], d[6 * s + 2], d[6 * s + 3], d[6 * s + 4], d[6 * s + 5]);
-      std::vector<unsigned long long> tm(8 * S + 16);
-      MGS_CUDA_OK(cudaMemcpy(tm.data(), a.dbg_time, tm.size() * 8, cudaMemcpyDeviceToHost));
-      double ph[7] = {0, 0, 0, 0, 0, 0, 0};
-      for (int s = 0; s < S; ++s)
-        for (int k = 0; k < 7; ++k) {
-          const int i = 7 * s + k;
-          if (i > 0) ph[k] += (tm[i] - tm[i - 1]) * 1e-3;
-        }
-      std::fprintf(stderr,
-                   "v2 phase us (sum over steps): units %.1f scans %.1f place %.1f ranks %.1f trans %.1f merge %.1f dom "
-                   "%.1f | grid.sync %.2f us | grid %d CTAs\n",
-                   ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[6], tm[8 * S + 8] * 1e-3, grid);
     }
     if (h.err_code == MGS_ERR_STATE_BUDGET)
       throw PlanFail{MGS_ERR_STATE_BUDGET,
