@@ -38,6 +38,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "ctx.cuh"
 
 namespace mgs {
@@ -50,10 +52,8 @@ constexpr int kChunkS = 32;          // targets per warp item
 constexpr int kChunkB = 512;         // targets per CTA item
 constexpr int kTile = kThreads * 8;  // scan tile
 constexpr int kBigNs = 1024;         // single-unit statuses with more candidates use the CTA path
-constexpr int kMergeWin = 2048;      // pid window of the CTA merge table
 constexpr int kBucketSmall = 64;     // child buckets up to this size: thread per slot
-constexpr int kBucketChunks = 16;    // CTA items per big bucket (256 slots each)
-constexpr int kBucketStage = 4096;   // big buckets staged in shared memory
+constexpr int kSortItems = 16;       // big child buckets: CTA radix sort of up to 256*16 keys
 constexpr int kBatch = 512;          // groups / statuses per CTA allocation batch
 constexpr int kNumScans = 7;
 
@@ -142,6 +142,8 @@ struct V2 {
   int32_t* chosen;
   int n_partial;                 // entries of the partial-subset tables (all subsets but the full one)
   int sc_big_ctas;               // CTAs of k_trans that may take big-group items
+  int oi_bits;                   // bits of an option index (radix sort width)
+  int merge_win;                 // placement window of the CTA merge table
   long long* dbg;                // [S][6] per-step counters (debug dump)
   unsigned long long* dbg_time;  // barrier timestamps (debug)
 };
@@ -152,12 +154,6 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
   return v;
 }
 __device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
 __device__ void raise_err(const V2& a, int phi, int code, int step = 0, unsigned long long count = 0, int what = 0,
                           long long need = 0) {
   (void)phi;
@@ -343,9 +339,18 @@ __device__ void multi_scan(const V2& a, const ScanJob* jobs, int epoch, int* tic
 
 // ---------------------------------------------------------------------------
 // successor-status hash: the slot holding key+1 is the status id
+__device__ __forceinline__ uint32_t mix32(uint32_t h) {  // murmur3 finalizer: all key bits reach the low bits
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
+}
+
 __device__ int ns_slot(const V2& a, uint32_t key, int phi, int step) {
   const uint32_t want = key + 1u;
-  const unsigned h = key * 2654435761u;
+  const unsigned h = mix32(key);
   for (int probe = 0; probe <= (a.hmask >> 1); ++probe) {
     const int slot = static_cast<int>((h + static_cast<unsigned>(probe)) & static_cast<unsigned>(a.hmask));
     uint32_t w = a.hash[slot];
@@ -554,24 +559,33 @@ __device__ void phase_ranks(const V2& a, int s, unsigned long long* sm64) {
   StepCounters& sc = a.ctl->sc[s & 1];
   const FrontierV2& F = a.f[cur];
   const int nb = sc.n_big_bucket;
-  for (int v = blockIdx.x; v < nb * kBucketChunks; v += gridDim.x) {
-    const int pr = a.big_bucket[v / kBucketChunks], chunk = v % kBucketChunks;
+  using Sort = cub::BlockRadixSort<unsigned long long, kThreads, kSortItems>;
+  Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(sm64);
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int pr = a.big_bucket[b];
     const int base = a.kid_base[pr], c = a.kid_cnt[cur][pr];
-    if (chunk * kThreads >= c) continue;  // uniform over the CTA
-    const bool staged = c <= kBucketStage;
-    if (staged) {
-      for (int k = threadIdx.x; k < c; k += kThreads) sm64[k] = a.kid_items[base + k];
+    if (c <= kThreads * kSortItems) {  // sort the bucket by option index (lex = (parent rank, option))
+      unsigned long long keys[kSortItems];
+#pragma unroll
+      for (int k = 0; k < kSortItems; ++k) {
+        const int i = threadIdx.x * kSortItems + k;
+        keys[k] = i < c ? a.kid_items[base + i] : ~0ull;
+      }
+      Sort(tmp).Sort(keys, 32, 32 + a.oi_bits);  // option indices are distinct within a bucket
+#pragma unroll
+      for (int k = 0; k < kSortItems; ++k) {
+        const int i = threadIdx.x * kSortItems + k;
+        if (i < c) F.rank[static_cast<uint32_t>(keys[k])] = base + i;
+      }
       __syncthreads();
+    } else {  // beyond one CTA's sort: counting (rare, correct)
+      for (int i = threadIdx.x; i < c; i += kThreads) {
+        const unsigned long long me = a.kid_items[base + i];
+        int pos = 0;
+        for (int k = 0; k < c; ++k) pos += a.kid_items[base + k] < me;
+        F.rank[static_cast<uint32_t>(me)] = base + pos;
+      }
     }
-    const unsigned long long* keys =
-        staged ? sm64 : reinterpret_cast<const unsigned long long*>(a.kid_items + base);
-    for (int i = chunk * kThreads + threadIdx.x; i < c; i += kThreads * kBucketChunks) {
-      const unsigned long long me = keys[i];
-      int pos = 0;
-      for (int k = 0; k < c; ++k) pos += keys[k] < me;
-      F.rank[static_cast<uint32_t>(me)] = base + pos;
-    }
-    __syncthreads();
   }
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const int n = sc.kids;  // live states of F_s = filled slots
@@ -862,8 +876,9 @@ __device__ void phase_merge_out(const V2& a, int s, int phi, unsigned long long*
       for (int k = cb + threadIdx.x; k < cb + cc; k += kThreads) a.c_live[k] = a.c_ok[k];
     } else {  // equal-key merge (solvers.hpp:467-468): max value, then min lex, per placement
       const int P1 = a.sp.P1;
-      for (int w0 = 0; w0 < P1; w0 += kMergeWin) {
-        for (int i = threadIdx.x; i < kMergeWin; i += kThreads) {
+      const int win = a.merge_win;
+      for (int w0 = 0; w0 < P1; w0 += win) {
+        for (int i = threadIdx.x; i < win; i += kThreads) {
           mvb[i] = 0ull;
           mlx[i] = ~0ull;
         }
@@ -882,7 +897,7 @@ __device__ void phase_merge_out(const V2& a, int s, int phi, unsigned long long*
             }
             for (int t = lo + threadIdx.x; t < n; t += kThreads) {
               const int p = a.sp.cand_pid[b + t];
-              if (p >= w0 + kMergeWin) break;
+              if (p >= w0 + win) break;
               const int k = cbu + t;
               if (!a.c_ok[k]) {
                 if (pass == 2) a.c_live[k] = 0;
@@ -1187,7 +1202,7 @@ __global__ void __launch_bounds__(kThreads) k_merge(V2 a, int s) {
   extern __shared__ unsigned long long smem_u64[];
   __shared__ int s_cnt[kBatch], s_gof[kBatch];
   if (failed(a)) return;
-  phase_merge_out(a, s, 0, smem_u64, smem_u64 + kMergeWin, s_cnt, s_gof);
+  phase_merge_out(a, s, 0, smem_u64, smem_u64 + a.merge_win, s_cnt, s_gof);
 }
 
 __global__ void __launch_bounds__(kThreads) k_dom(V2 a, int s) {
@@ -1371,18 +1386,16 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
   const int n_sub = 1 << M;
   const int n_partial = sp.proj_base[n_sub - 1];  // all subsets but the full one
   const size_t smem_trans = static_cast<size_t>(sp.P1) * 8 + static_cast<size_t>(n_partial) * 20;
-  const size_t smem =
-      std::max({smem_trans, static_cast<size_t>(2 * kMergeWin * 8), static_cast<size_t>(kBucketStage * 8)});
-  const size_t smem_rank = static_cast<size_t>(kBucketStage) * 8;
-  const size_t smem_merge = static_cast<size_t>(2 * kMergeWin) * 8;
+  const size_t smem_rank = sizeof(typename cub::BlockRadixSort<unsigned long long, kThreads, kSortItems>::TempStorage);
+  const int merge_win = std::min(sp.P1, 8192);  // whole placement range in one window when it fits
+  const size_t smem_merge = static_cast<size_t>(2 * merge_win) * 8;
   auto ktrans = M == 1 ? k_trans<1> : k_trans<2>;
   auto kunits = M == 1 ? k_units<1> : k_units<2>;
   MGS_CUDA_OK(cudaFuncSetAttribute(ktrans, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_trans)));
   MGS_CUDA_OK(cudaFuncSetAttribute(k_ranks, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_rank)));
   MGS_CUDA_OK(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_merge)));
   const int grid = c.sm_count * 8;
-  (void)smem;
-  static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 64ll << 20};
+  static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 128ll << 20};
   const uint64_t budget = p.state_budget;
   const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr;
   for (int attempt = 0; attempt < 10; ++attempt) {
@@ -1483,6 +1496,9 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     k_init_root<<<1, 32, 0, c.stream>>>(a, static_cast<uint32_t>(sp.root_pid));
     ++c.kernel_launches;
     a.sc_big_ctas = grid;
+    a.merge_win = merge_win;
+    a.oi_bits = 1;
+    while ((1ll << a.oi_bits) < sp.n_opt) ++a.oi_bits;
     for (int st = 0; st < S; ++st) {
       kunits<<<grid, kThreads, 0, c.stream>>>(a, st);
       k_scans<<<grid, kThreads, 0, c.stream>>>(a, st);
