@@ -75,7 +75,7 @@ struct FrontierV2 {
 };
 
 struct StepCounters {  // double buffered; zeroed one step ahead
-  int n_units, T, items_s, items_b, n_big, n_small, n_big_bucket, ticket, kids;
+  int n_units, T, items_s, items_b, n_big, n_small, n_big_bucket, ticket, kids, ticket2;
 };
 
 struct Ctl {
@@ -93,6 +93,7 @@ struct Ctl {
   int best_idx;
   int ranks_prev;  // live states of F_{s-1}: the parent-rank space of F_s
   int scan_total[kNumScans];
+  int out_total[2];  // survivors, groups of F_{s+1}
 };
 
 struct V2 {
@@ -118,6 +119,7 @@ struct V2 {
   int hmask;
   int32_t *ns_ucnt, *ns_ccnt, *ns_ubase, *ns_cbase, *ns_ucur, *ns_ccur, *ns_units, *ns_bigpos, *ns_smallpos;
   int32_t *ns_big, *ns_small;
+  int32_t *ns_out, *ns_obase, *ns_gbase;  // survivors per status, their offsets and group index
   int32_t *it_s_unit, *it_s_chunk, *it_b_unit, *it_b_chunk;
   int itcap;
   double* c_value;
@@ -221,12 +223,13 @@ struct ScanJob {
   const int32_t* in2;  // mode 1/2: statuses' candidate counts
   int32_t* out;
   int n;
-  int mode;  // 0 plain, 1 big-status flag, 2 small-status flag
+  int mode;  // 0 plain, 1 big-status flag, 2 small-status flag, 3 nonzero flag
 };
 
 __device__ __forceinline__ int scan_load(const ScanJob& J, int i) {
   if (i >= J.n) return 0;
   if (J.mode == 0) return J.in[i];
+  if (J.mode == 3) return J.in[i] > 0 ? 1 : 0;
   const int uc = J.in[i];
   if (uc == 0) return 0;
   const bool big = uc > 1 || J.in2[i] > kBigNs;
@@ -282,18 +285,18 @@ __device__ int block_scan_tile(const ScanJob& J, int base, int* sm) {
 // Several exclusive scans in one pass: tiles are handed out by a ticket, so
 // every tile's predecessors are already owned by running CTAs (decoupled
 // look-back cannot deadlock in a cooperative launch).
-__device__ void multi_scan(const V2& a, const ScanJob* jobs, int epoch, int* ticket, int* totals) {
+__device__ void multi_scan(const V2& a, const ScanJob* jobs, int njobs, int epoch, int* ticket, int* totals) {
   __shared__ int sm[80];
   __shared__ int s_tile, s_excl;
   int tiles[kNumScans], tbase[kNumScans + 1];
   tbase[0] = 0;
-  for (int k = 0; k < kNumScans; ++k) {
+  for (int k = 0; k < njobs; ++k) {
     tiles[k] = (jobs[k].n + kTile - 1) / kTile;
     tbase[k + 1] = tbase[k] + tiles[k];
   }
-  const int total_tiles = tbase[kNumScans];
+  const int total_tiles = tbase[njobs];
   if (blockIdx.x == 0 && threadIdx.x == 0)
-    for (int k = 0; k < kNumScans; ++k)
+    for (int k = 0; k < njobs; ++k)
       if (tiles[k] == 0) totals[k] = 0;
   while (true) {
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
@@ -553,8 +556,9 @@ __device__ void phase_place(const V2& a, int s) {
 
 // S4: dense ranks of F_s (solvers.hpp:544-548 restated: lex = (parent rank,
 // option index), so the rank is the parent's first child slot plus the
-// position of the option index among the parent's children)
-__device__ void phase_ranks(const V2& a, int s, unsigned long long* sm64) {
+// position of the option index among the parent's children).
+// Big buckets: one CTA each, block radix sort of the option indices.
+__device__ void phase_ranks_big(const V2& a, int s, unsigned long long* sm64) {
   const int cur = s & 1;
   StepCounters& sc = a.ctl->sc[s & 1];
   const FrontierV2& F = a.f[cur];
@@ -564,7 +568,7 @@ __device__ void phase_ranks(const V2& a, int s, unsigned long long* sm64) {
   for (int b = blockIdx.x; b < nb; b += gridDim.x) {
     const int pr = a.big_bucket[b];
     const int base = a.kid_base[pr], c = a.kid_cnt[cur][pr];
-    if (c <= kThreads * kSortItems) {  // sort the bucket by option index (lex = (parent rank, option))
+    if (c <= kThreads * kSortItems) {
       unsigned long long keys[kSortItems];
 #pragma unroll
       for (int k = 0; k < kSortItems; ++k) {
@@ -587,17 +591,26 @@ __device__ void phase_ranks(const V2& a, int s, unsigned long long* sm64) {
       }
     }
   }
+}
+
+// Small buckets: thread per slot (a parent's slots are adjacent: warp broadcasts)
+__device__ void phase_ranks_small(const V2& a, int s) {
+  const int cur = s & 1;
+  StepCounters& sc = a.ctl->sc[s & 1];
+  const FrontierV2& F = a.f[cur];
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const int n = sc.kids;  // live states of F_s = filled slots
   for (int i = gtid; i < n; i += gstride) {
     const int pr = a.kid_pr[i];
     const int c = a.kid_cnt[cur][pr];
     if (c > kBucketSmall) continue;
-    const int base = a.kid_base[pr];
     const unsigned long long me = a.kid_items[i];
-    int pos = 0;
-    for (int k = 0; k < c; ++k) pos += a.kid_items[base + k] < me;
-    F.rank[static_cast<uint32_t>(me)] = base + pos;
+    int rank = a.kid_base[pr];
+    if (c > 1) {
+      const int base = rank;
+      for (int k = 0; k < c; ++k) rank += a.kid_items[base + k] < me;
+    }
+    F.rank[static_cast<uint32_t>(me)] = rank;
   }
 }
 
@@ -671,21 +684,27 @@ __device__ __forceinline__ void group_acc(const V2& a, uint32_t gstat, double* a
 
 struct TransSmem {
   unsigned long long* ex;  // [P1] (tag << 32) | idx of the group's state at that placement
-  unsigned long long* vb;  // [n_partial]
-  uint32_t* rk;
-  int32_t* ix;
-  uint32_t* tg;
+  unsigned long long* vb;  // [n_partial] max value bits per (subset, projection)
+  unsigned long long* rx;  // [n_partial] (rank << 32) | idx: min rank among the max
+  uint32_t* tg;            // [n_partial] entry owner tag
 };
 
+// Big groups: one CTA per (unit, chunk) item. The group's best representative
+// per (subset, projected placement) is built in shared memory: the empty subset
+// by a block reduction, the others by a max-value then min-(rank,idx) atomic
+// pass; the full subset is the state at that placement itself.
 template <int M>
-__device__ void phase_trans(const V2& a, int s, TransSmem& T, uint32_t& tag) {
+__device__ void phase_trans_big(const V2& a, int s, TransSmem& T) {
   const int cur = s & 1;
   StepCounters& sc = a.ctl->sc[s & 1];
   const FrontierV2& F = a.f[cur];
   const int charge = (s > 0 || a.has_initial) ? 1 : 0;
   const int P1 = a.sp.P1;
-  // CTA items (big groups): shared-memory subset tables
+  __shared__ unsigned long long s_bv[kWarps], s_brx[kWarps];
+  __shared__ unsigned long long s_v0, s_rx0;
+  uint32_t tag = 0;
   const int nib = sc.items_b;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int item = blockIdx.x; item < nib; item += gridDim.x) {
     ++tag;
     const int unit = a.it_b_unit[item], chunk = a.it_b_chunk[item];
@@ -693,50 +712,68 @@ __device__ void phase_trans(const V2& a, int s, TransSmem& T, uint32_t& tag) {
     const int gs = F.g_start[g], gn = F.g_size[g];
     double acc[M];
     group_acc<M>(a, F.g_status[g], acc);
-    for (int j = threadIdx.x; j < gn; j += kThreads) {  // claim entries
+    // claim entries + empty-subset best (value desc, rank asc)
+    unsigned long long bv = 0, brx = ~0ull;
+    for (int j = threadIdx.x; j < gn; j += kThreads) {
       if (!F.alive[gs + j]) continue;
       const int pj = F.pid[gs + j];
+      const unsigned long long vb = vbits(F.value[gs + j]);
+      const unsigned long long rx = (static_cast<unsigned long long>(F.rank[gs + j]) << 32) | static_cast<uint32_t>(j);
+      if (brx == ~0ull || vb > bv || (vb == bv && rx < brx)) {
+        bv = vb;
+        brx = rx;
+      }
       T.ex[pj] = (static_cast<unsigned long long>(tag) << 32) | static_cast<uint32_t>(j);
 #pragma unroll
-      for (int sub = 0; sub < (1 << M) - 1; ++sub) {
+      for (int sub = 1; sub < (1 << M) - 1; ++sub) {
         const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj];
         T.tg[e] = tag;
         T.vb[e] = 0ull;
-        T.rk[e] = 0xffffffffu;
-        T.ix[e] = -1;
+        T.rx[e] = ~0ull;
       }
     }
-    __syncthreads();
-    for (int j = threadIdx.x; j < gn; j += kThreads) {  // max value
-      if (!F.alive[gs + j]) continue;
-      const int pj = F.pid[gs + j];
-      const unsigned long long vb = vbits(F.value[gs + j]);
-#pragma unroll
-      for (int sub = 0; sub < (1 << M) - 1; ++sub)
-        atomicMax(&T.vb[a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj]], vb);
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < gn; j += kThreads) {  // min rank among the max
-      if (!F.alive[gs + j]) continue;
-      const int pj = F.pid[gs + j];
-      const unsigned long long vb = vbits(F.value[gs + j]);
-      const uint32_t rj = F.rank[gs + j];
-#pragma unroll
-      for (int sub = 0; sub < (1 << M) - 1; ++sub) {
-        const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj];
-        if (T.vb[e] == vb) atomicMin(&T.rk[e], rj);
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long ov = __shfl_down_sync(0xffffffffu, bv, o);
+      const unsigned long long orx = __shfl_down_sync(0xffffffffu, brx, o);
+      if (orx != ~0ull && (brx == ~0ull || ov > bv || (ov == bv && orx < brx))) {
+        bv = ov;
+        brx = orx;
       }
     }
+    if (lane == 0) {
+      s_bv[warp] = bv;
+      s_brx[warp] = brx;
+    }
     __syncthreads();
-    for (int j = threadIdx.x; j < gn; j += kThreads) {  // representative index
-      if (!F.alive[gs + j]) continue;
-      const int pj = F.pid[gs + j];
-      const unsigned long long vb = vbits(F.value[gs + j]);
-      const uint32_t rj = F.rank[gs + j];
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < kWarps; ++w)
+        if (s_brx[w] != ~0ull && (brx == ~0ull || s_bv[w] > bv || (s_bv[w] == bv && s_brx[w] < brx))) {
+          bv = s_bv[w];
+          brx = s_brx[w];
+        }
+      s_v0 = bv;
+      s_rx0 = brx;
+    }
+    if (M > 1) {
+      for (int j = threadIdx.x; j < gn; j += kThreads) {  // max value per entry
+        if (!F.alive[gs + j]) continue;
+        const int pj = F.pid[gs + j];
+        const unsigned long long vb = vbits(F.value[gs + j]);
 #pragma unroll
-      for (int sub = 0; sub < (1 << M) - 1; ++sub) {
-        const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj];
-        if (T.vb[e] == vb && T.rk[e] == rj) T.ix[e] = j;
+        for (int sub = 1; sub < (1 << M) - 1; ++sub)
+          atomicMax(&T.vb[a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj]], vb);
+      }
+      __syncthreads();
+      for (int j = threadIdx.x; j < gn; j += kThreads) {  // min (rank, idx) among the max
+        if (!F.alive[gs + j]) continue;
+        const int pj = F.pid[gs + j];
+        const unsigned long long vb = vbits(F.value[gs + j]);
+        const unsigned long long rx = (static_cast<unsigned long long>(F.rank[gs + j]) << 32) | static_cast<uint32_t>(j);
+#pragma unroll
+        for (int sub = 1; sub < (1 << M) - 1; ++sub) {
+          const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj];
+          if (T.vb[e] == vb) atomicMin(&T.rx[e], rx);
+        }
       }
     }
     __syncthreads();
@@ -746,13 +783,16 @@ __device__ void phase_trans(const V2& a, int s, TransSmem& T, uint32_t& tag) {
       const int p = a.sp.cand_pid[sb + ti];
       const int oi = a.sp.cand_oi[sb + ti];
       BestT<M> b;
+      b.i[0] = s_rx0 == ~0ull ? -1 : static_cast<int>(s_rx0 & 0xffffffffu);
+      b.v[0] = __longlong_as_double(static_cast<long long>(s_v0));
+      b.r[0] = static_cast<uint32_t>(s_rx0 >> 32);
 #pragma unroll
-      for (int sub = 0; sub < (1 << M) - 1; ++sub) {
+      for (int sub = 1; sub < (1 << M) - 1; ++sub) {
         const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + p];
-        const bool hit = T.tg[e] == tag && T.ix[e] >= 0;
-        b.i[sub] = hit ? T.ix[e] : -1;
+        const bool hit = T.tg[e] == tag && T.rx[e] != ~0ull;
+        b.i[sub] = hit ? static_cast<int>(T.rx[e] & 0xffffffffu) : -1;
         b.v[sub] = hit ? __longlong_as_double(static_cast<long long>(T.vb[e])) : 0.0;
-        b.r[sub] = hit ? T.rk[e] : 0u;
+        b.r[sub] = hit ? static_cast<uint32_t>(T.rx[e] >> 32) : 0u;
       }
       {
         const unsigned long long w = T.ex[p];
@@ -772,7 +812,16 @@ __device__ void phase_trans(const V2& a, int s, TransSmem& T, uint32_t& tag) {
     }
     __syncthreads();
   }
-  // warp items (small groups): broadcast scan of the group's states
+}
+
+// Small groups: one warp per (unit, 32 targets) item; every lane owns a target
+// and scans the group's states (broadcast loads) keeping the best per subset.
+template <int M>
+__device__ void phase_trans_small(const V2& a, int s) {
+  const int cur = s & 1;
+  StepCounters& sc = a.ctl->sc[s & 1];
+  const FrontierV2& F = a.f[cur];
+  const int charge = (s > 0 || a.has_initial) ? 1 : 0;
   const int lane = threadIdx.x & 31;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const int nis = sc.items_s;
@@ -841,32 +890,12 @@ __device__ __forceinline__ void write_state(const V2& a, int s, int nxt, int q, 
   }
 }
 
-__device__ bool check_out(const V2& a, int s, long long q_end, long long g_end, int phi) {
-  if (q_end > a.fcap) {
-    raise_err(a, phi, kOverflow, s, 0, 4, q_end);
-    return false;
-  }
-  if (g_end > a.gcap) {
-    raise_err(a, phi, kOverflow, s, 0, 5, g_end);
-    return false;
-  }
-  if (a.hist_base[s + 1] + q_end > a.hcap) {
-    raise_err(a, phi, kOverflow, s, 0, 6, a.hist_base[s + 1] + q_end);
-    return false;
-  }
-  return true;
-}
-
-__device__ void phase_merge_out(const V2& a, int s, int phi, unsigned long long* mvb, unsigned long long* mlx,
-                                int* s_cnt, int* s_gof) {
-  const int nxt = (s + 1) & 1;
+// S6a: equal-key merge (multi-unit statuses) + band + survivor count per status
+__device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned long long* mlx) {
   StepCounters& sc = a.ctl->sc[s & 1];
-  const FrontierV2& N = a.f[nxt];
-  __shared__ int s_q0, s_g;
   __shared__ unsigned long long s_max;
-  __shared__ int s_scan[80];
-  __shared__ int s_wsum[kWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int s_cnt;
+  const int lane = threadIdx.x & 31;
   // big statuses (multi-unit or large): one CTA each
   const int nbig = sc.n_big;
   for (int w = blockIdx.x; w < nbig; w += gridDim.x) {
@@ -889,11 +918,14 @@ __device__ void phase_merge_out(const V2& a, int s, int phi, unsigned long long*
             const int sig = a.u_sig[u];
             const int b = a.sp.sig_off[sig], n = a.sp.sig_off[sig + 1] - b;
             const int cbu = a.u_cbase[u];
-            int lo = 0, hi = n;  // the unit's candidates are sorted by placement: clip to the window
-            while (lo < hi) {
-              const int mid = (lo + hi) >> 1;
-              if (a.sp.cand_pid[b + mid] < w0) lo = mid + 1;
-              else hi = mid;
+            int lo = 0;
+            if (w0 > 0) {  // the unit's candidates are sorted by placement: clip to the window
+              int hi = n;
+              while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (a.sp.cand_pid[b + mid] < w0) lo = mid + 1;
+                else hi = mid;
+              }
             }
             for (int t = lo + threadIdx.x; t < n; t += kThreads) {
               const int p = a.sp.cand_pid[b + t];
@@ -927,19 +959,82 @@ __device__ void phase_merge_out(const V2& a, int s, int phi, unsigned long long*
         mx = vb > mx ? vb : mx;
         any = true;
       }
-    if (threadIdx.x == 0) s_max = 0;
+    if (threadIdx.x == 0) {
+      s_max = 0;
+      s_cnt = 0;
+    }
     __syncthreads();
     if (any) atomicMax(&s_max, mx);
     __syncthreads();
     const double thresh = dsub(__longlong_as_double(static_cast<long long>(s_max)), a.band);
-    const int per = (cc + kThreads - 1) / kThreads;
-    const int lo = cb + threadIdx.x * per, hi = min(cb + cc, lo + per);
     int mine = 0;
-    for (int k = lo; k < hi; ++k) {
+    for (int k = cb + threadIdx.x; k < cb + cc; k += kThreads) {
       const bool keep = a.c_live[k] && a.c_value[k] >= thresh;
       a.c_live[k] = keep ? 1 : 0;
       mine += keep;
     }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, o);
+    if (lane == 0 && mine) atomicAdd(&s_cnt, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) a.ns_out[id] = s_cnt;
+    __syncthreads();
+  }
+  // small statuses (single unit, <= kBigNs candidates): a warp each, no merge needed
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const int nsm = sc.n_small;
+  for (int i = wid; i < nsm; i += nw) {
+    const int id = a.ns_small[i];
+    const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
+    unsigned long long mx = 0;
+    bool any = false;
+    for (int k = cb + lane; k < cb + cc; k += 32)
+      if (a.c_ok[k]) {
+        const unsigned long long vb = vbits(a.c_value[k]);
+        mx = vb > mx ? vb : mx;
+        any = true;
+      }
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
+      mx = y > mx ? y : mx;
+    }
+    any = __any_sync(0xffffffffu, any);
+    const double thresh = dsub(__longlong_as_double(static_cast<long long>(mx)), a.band);
+    int total = 0;
+    for (int k0 = cb; k0 < cb + cc; k0 += 32) {
+      const int k = k0 + lane;
+      const bool keep = any && k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh;
+      if (k < cb + cc) a.c_live[k] = keep ? 1 : 0;
+      total += __popc(__ballot_sync(0xffffffffu, keep));
+    }
+    if (lane == 0) a.ns_out[id] = total;
+  }
+}
+
+// S6c: survivors of every status written at their scanned offsets
+__device__ void phase_write(const V2& a, int s) {
+  const int nxt = (s + 1) & 1;
+  StepCounters& sc = a.ctl->sc[s & 1];
+  const FrontierV2& N = a.f[nxt];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int s_wsum[kWarps];
+  const int nbig = sc.n_big;
+  for (int w = blockIdx.x; w < nbig; w += gridDim.x) {
+    const int id = a.ns_big[w];
+    const int total = a.ns_out[id];
+    if (total == 0) continue;  // uniform
+    const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
+    const int q0 = a.ns_obase[id], gi = a.ns_gbase[id];
+    const uint32_t key = a.hash[id] - 1u;
+    if (threadIdx.x == 0) {
+      N.g_start[gi] = q0;
+      N.g_size[gi] = total;
+      N.g_status[gi] = key;
+      N.g_alive[gi] = total;
+    }
+    const int per = (cc + kThreads - 1) / kThreads;  // ordered compaction: contiguous ranges + block scan
+    const int lo = cb + threadIdx.x * per, hi = min(cb + cc, lo + per);
+    int mine = 0;
+    for (int k = lo; k < hi; ++k) mine += a.c_live[k];
     int x = mine;
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, x, o);
@@ -947,103 +1042,35 @@ __device__ void phase_merge_out(const V2& a, int s, int phi, unsigned long long*
     }
     if (lane == 31) s_wsum[warp] = x;
     __syncthreads();
-    int off = x - mine, total = 0;
-    for (int w2 = 0; w2 < kWarps; ++w2) {
-      if (w2 < warp) off += s_wsum[w2];
-      total += s_wsum[w2];
-    }
-    if (total > 0) {
-      if (threadIdx.x == 0) {
-        const int q0 = atomicAdd(&a.ctl->n_store[nxt], total);
-        const int gi = atomicAdd(&a.ctl->n_groups[nxt], 1);
-        s_q0 = check_out(a, s, static_cast<long long>(q0) + total, gi + 1ll, phi) ? q0 : -1;
-        s_g = gi;
-        if (s_q0 >= 0) {
-          N.g_start[gi] = q0;
-          N.g_size[gi] = total;
-          N.g_status[gi] = a.hash[id] - 1u;
-          N.g_alive[gi] = total;
-        }
-      }
-      __syncthreads();
-      if (s_q0 >= 0) {
-        const uint32_t key = a.hash[id] - 1u;
-        for (int k = lo; k < hi; ++k)
-          if (a.c_live[k]) write_state(a, s, nxt, s_q0 + off++, s_g, key, k);
-      }
-    }
+    int off = x - mine;
+    for (int w2 = 0; w2 < warp; ++w2) off += s_wsum[w2];
+    for (int k = lo; k < hi; ++k)
+      if (a.c_live[k]) write_state(a, s, nxt, q0 + off++, gi, key, k);
     __syncthreads();
   }
-  // small statuses (single unit, <= kBigNs candidates): warps, one allocation per CTA batch
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const int nsm = sc.n_small;
-  const int r0 = static_cast<int>(static_cast<long long>(nsm) * blockIdx.x / gridDim.x);
-  const int r1 = static_cast<int>(static_cast<long long>(nsm) * (blockIdx.x + 1) / gridDim.x);
-  for (int bs = r0; bs < r1; bs += kBatch) {
-    const int be = min(r1, bs + kBatch);
-    for (int i = bs + warp; i < be; i += kWarps) {  // band + survivor count
-      const int id = a.ns_small[i];
-      const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
-      unsigned long long mx = 0;
-      bool any = false;
-      for (int k = cb + lane; k < cb + cc; k += 32)
-        if (a.c_ok[k]) {
-          const unsigned long long vb = vbits(a.c_value[k]);
-          mx = vb > mx ? vb : mx;
-          any = true;
-        }
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
-        mx = y > mx ? y : mx;
-      }
-      any = __any_sync(0xffffffffu, any);
-      const double thresh = dsub(__longlong_as_double(static_cast<long long>(mx)), a.band);
-      int total = 0;
-      for (int k0 = cb; k0 < cb + cc; k0 += 32) {
-        const int k = k0 + lane;
-        const bool keep = any && k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh;
-        if (k < cb + cc) a.c_live[k] = keep ? 1 : 0;
-        total += __popc(__ballot_sync(0xffffffffu, keep));
-      }
-      if (lane == 0) {
-        s_cnt[i - bs] = total;
-        s_gof[i - bs] = total > 0 ? 1 : 0;
-      }
+  for (int i = wid; i < nsm; i += nw) {
+    const int id = a.ns_small[i];
+    const int total = a.ns_out[id];
+    if (total == 0) continue;
+    const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
+    const int q0 = a.ns_obase[id], gi = a.ns_gbase[id];
+    const uint32_t key = a.hash[id] - 1u;
+    if (lane == 0) {
+      N.g_start[gi] = q0;
+      N.g_size[gi] = total;
+      N.g_status[gi] = key;
+      N.g_alive[gi] = total;
     }
-    __syncthreads();
-    const int tot = block_scan_small(s_cnt, be - bs, s_scan);
-    const int ngr = block_scan_small(s_gof, be - bs, s_scan);
-    if (threadIdx.x == 0) {
-      const int q0 = atomicAdd(&a.ctl->n_store[nxt], tot);
-      const int g0 = atomicAdd(&a.ctl->n_groups[nxt], ngr);
-      s_q0 = check_out(a, s, static_cast<long long>(q0) + tot, static_cast<long long>(g0) + ngr, phi) ? q0 : -1;
-      s_g = g0;
+    int run = 0;
+    for (int k0 = cb; k0 < cb + cc; k0 += 32) {
+      const int k = k0 + lane;
+      const bool keep = k < cb + cc && a.c_live[k];
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
+      run += __popc(bal);
     }
-    __syncthreads();
-    if (s_q0 >= 0) {
-      for (int i = bs + warp; i < be; i += kWarps) {
-        const int cnt = (i + 1 < be ? s_cnt[i + 1 - bs] : tot) - s_cnt[i - bs];
-        if (cnt == 0) continue;
-        const int id = a.ns_small[i];
-        const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
-        const int q0 = s_q0 + s_cnt[i - bs], gi = s_g + s_gof[i - bs];
-        const uint32_t key = a.hash[id] - 1u;
-        if (lane == 0) {
-          N.g_start[gi] = q0;
-          N.g_size[gi] = cnt;
-          N.g_status[gi] = key;
-          N.g_alive[gi] = cnt;
-        }
-        int run = 0;
-        for (int k0 = cb; k0 < cb + cc; k0 += 32) {
-          const int k = k0 + lane;
-          const bool keep = k < cb + cc && a.c_live[k];
-          const unsigned bal = __ballot_sync(0xffffffffu, keep);
-          if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
-          run += __popc(bal);
-        }
-      }
-    }
-    __syncthreads();
   }
 }
 
@@ -1140,7 +1167,7 @@ __global__ void __launch_bounds__(kThreads) k_scans(V2 a, int s) {
                                    {a.u_chs, nullptr, a.u_sbase, sc.n_units, 0},
                                    {a.u_chb, nullptr, a.u_bbase, sc.n_units, 0},
                                    {a.kid_cnt[cur], nullptr, a.kid_base, ctl->ranks_prev, 0}};
-  multi_scan(a, jobs, s + 1, &sc.ticket, ctl->scan_total);
+  multi_scan(a, jobs, kNumScans, 2 * (s + 1), &sc.ticket, ctl->scan_total);
 }
 
 __global__ void __launch_bounds__(kThreads) k_place(V2 a, int s) {
@@ -1165,44 +1192,72 @@ __global__ void __launch_bounds__(kThreads) k_place(V2 a, int s) {
   if (fits) phase_place(a, s);
 }
 
-__global__ void __launch_bounds__(kThreads) k_ranks(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads) k_ranks_big(V2 a, int s) {
   extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
-  phase_ranks(a, s, smem_u64);
+  phase_ranks_big(a, s, smem_u64);
+}
+
+__global__ void __launch_bounds__(kThreads) k_ranks_small(V2 a, int s) {
+  if (failed(a)) return;
+  phase_ranks_small(a, s);
 }
 
 template <int M>
-__global__ void __launch_bounds__(kThreads) k_trans(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads) k_trans_big(V2 a, int s) {
   extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
+  if (static_cast<int>(blockIdx.x) >= a.ctl->sc[s & 1].items_b) return;  // no item for this CTA
   const int P1 = a.sp.P1;
   TransSmem T;
   T.ex = smem_u64;
   T.vb = smem_u64 + P1;
-  T.rk = reinterpret_cast<uint32_t*>(T.vb + a.n_partial);
-  T.ix = reinterpret_cast<int32_t*>(T.rk + a.n_partial);
-  T.tg = reinterpret_cast<uint32_t*>(T.ix + a.n_partial);
-  if (blockIdx.x < a.sc_big_ctas) {  // only CTAs that take big items need clean tables
-    for (int i = threadIdx.x; i < P1; i += kThreads) T.ex[i] = 0ull;
-    for (int i = threadIdx.x; i < a.n_partial; i += kThreads) T.tg[i] = 0u;
-    __syncthreads();
-  }
-  uint32_t tag = 0;
-  phase_trans<M>(a, s, T, tag);
+  T.rx = T.vb + a.n_partial;
+  T.tg = reinterpret_cast<uint32_t*>(T.rx + a.n_partial);
+  for (int i = threadIdx.x; i < P1; i += kThreads) T.ex[i] = 0ull;  // tags start at 1
+  for (int i = threadIdx.x; i < a.n_partial; i += kThreads) T.tg[i] = 0u;
+  __syncthreads();
+  phase_trans_big<M>(a, s, T);
+}
+
+template <int M>
+__global__ void __launch_bounds__(kThreads, 4) k_trans_small(V2 a, int s) {
+  if (failed(a)) return;
+  phase_trans_small<M>(a, s);
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // counters of the next step
     const int nxt = (s + 1) & 1;
     a.ctl->sc[nxt] = StepCounters{};
-    a.ctl->n_store[nxt] = 0;
-    a.ctl->n_groups[nxt] = 0;
     a.ctl->alive_now[nxt] = 0;
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_merge(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads) k_band(V2 a, int s) {
   extern __shared__ unsigned long long smem_u64[];
-  __shared__ int s_cnt[kBatch], s_gof[kBatch];
   if (failed(a)) return;
-  phase_merge_out(a, s, 0, smem_u64, smem_u64 + a.merge_win, s_cnt, s_gof);
+  phase_band(a, s, smem_u64, smem_u64 + a.merge_win);
+}
+
+__global__ void __launch_bounds__(kThreads) k_outscan(V2 a, int s) {
+  if (failed(a)) return;
+  const int H = a.hmask + 1;
+  const ScanJob jobs[2] = {{a.ns_out, nullptr, a.ns_obase, H, 0}, {a.ns_out, nullptr, a.ns_gbase, H, 3}};
+  multi_scan(a, jobs, 2, 2 * (s + 1) + 1, &a.ctl->sc[s & 1].ticket2, a.ctl->out_total);
+}
+
+__global__ void __launch_bounds__(kThreads) k_write(V2 a, int s) {
+  if (failed(a)) return;
+  const int nxt = (s + 1) & 1;
+  Ctl* ctl = a.ctl;
+  const int total = ctl->out_total[0], groups = ctl->out_total[1];
+  const bool fits = total <= a.fcap && groups <= a.gcap && a.hist_base[s + 1] + total <= a.hcap;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->n_store[nxt] = total;
+    ctl->n_groups[nxt] = groups;
+    if (total > a.fcap) raise_err(a, 0, kOverflow, s, 0, 4, total);
+    else if (groups > a.gcap) raise_err(a, 0, kOverflow, s, 0, 5, groups);
+    else if (a.hist_base[s + 1] + total > a.hcap) raise_err(a, 0, kOverflow, s, 0, 6, a.hist_base[s + 1] + total);
+  }
+  if (fits) phase_write(a, s);
 }
 
 __global__ void __launch_bounds__(kThreads) k_dom(V2 a, int s) {
@@ -1213,6 +1268,7 @@ __global__ void __launch_bounds__(kThreads) k_dom(V2 a, int s) {
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   for (int i = gtid; i <= a.hmask; i += gstride) {  // S6 read the keys from the hash: clear now
     a.hash[i] = 0u;
+    a.ns_out[i] = 0;
     a.ns_ucnt[i] = 0;
     a.ns_ccnt[i] = 0;
     a.ns_ucur[i] = 0;
@@ -1389,11 +1445,12 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
   const size_t smem_rank = sizeof(typename cub::BlockRadixSort<unsigned long long, kThreads, kSortItems>::TempStorage);
   const int merge_win = std::min(sp.P1, 8192);  // whole placement range in one window when it fits
   const size_t smem_merge = static_cast<size_t>(2 * merge_win) * 8;
-  auto ktrans = M == 1 ? k_trans<1> : k_trans<2>;
+  auto ktbig = M == 1 ? k_trans_big<1> : k_trans_big<2>;
+  auto ktsmall = M == 1 ? k_trans_small<1> : k_trans_small<2>;
   auto kunits = M == 1 ? k_units<1> : k_units<2>;
-  MGS_CUDA_OK(cudaFuncSetAttribute(ktrans, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_trans)));
-  MGS_CUDA_OK(cudaFuncSetAttribute(k_ranks, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_rank)));
-  MGS_CUDA_OK(cudaFuncSetAttribute(k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_merge)));
+  MGS_CUDA_OK(cudaFuncSetAttribute(ktbig, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_trans)));
+  MGS_CUDA_OK(cudaFuncSetAttribute(k_ranks_big, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_rank)));
+  MGS_CUDA_OK(cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_merge)));
   const int grid = c.sm_count * 8;
   static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 128ll << 20};
   const uint64_t budget = p.state_budget;
@@ -1461,10 +1518,13 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     a.ns_ccur = c.buf<int32_t>("v2_nsccur", H);
     a.ns_bigpos = c.buf<int32_t>("v2_nsbigpos", H);
     a.ns_smallpos = c.buf<int32_t>("v2_nssmallpos", H);
+    a.ns_out = c.buf<int32_t>("v2_nsout", H);
+    a.ns_obase = c.buf<int32_t>("v2_nsobase", H);
+    a.ns_gbase = c.buf<int32_t>("v2_nsgbase", H);
     a.ns_big = c.buf<int32_t>("v2_nsbig", H);
     a.ns_small = c.buf<int32_t>("v2_nssmall", H);
     for (void* z : {static_cast<void*>(a.hash), static_cast<void*>(a.ns_ucnt), static_cast<void*>(a.ns_ccnt),
-                    static_cast<void*>(a.ns_ucur), static_cast<void*>(a.ns_ccur)})
+                    static_cast<void*>(a.ns_ucur), static_cast<void*>(a.ns_ccur), static_cast<void*>(a.ns_out)})
       MGS_CUDA_OK(cudaMemsetAsync(z, 0, H * 4, c.stream));
     a.itcap = caps.itcap;
     a.it_s_unit = c.buf<int32_t>("v2_itsu", caps.itcap);
@@ -1481,7 +1541,7 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     a.pcnt = c.buf<int32_t>("v2_pcnt", sp.P1);
     a.pbucket = c.buf<int32_t>("v2_pbucket", static_cast<size_t>(sp.P1) * 64);
     MGS_CUDA_OK(cudaMemsetAsync(a.pcnt, 0, static_cast<size_t>(sp.P1) * 4, c.stream));
-    a.scan_cap = 4 * static_cast<int>(H / kTile + 8) + 2 * (caps.ucap / kTile + 8) + (caps.fcap / kTile + 8);
+    a.scan_cap = 4 * static_cast<int>(H / kTile + 8) + 2 * (caps.ucap / kTile + 8) + (caps.fcap / kTile + 8);  // >= outscan's 2 H-jobs
     a.scan_state = c.buf<unsigned long long>("v2_scan", a.scan_cap);
     MGS_CUDA_OK(cudaMemsetAsync(a.scan_state, 0, static_cast<size_t>(a.scan_cap) * 8, c.stream));
     a.sig_len = c.buf<int32_t>("v2_siglen", sp.n_sig);
@@ -1503,12 +1563,16 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
       kunits<<<grid, kThreads, 0, c.stream>>>(a, st);
       k_scans<<<grid, kThreads, 0, c.stream>>>(a, st);
       k_place<<<grid, kThreads, 0, c.stream>>>(a, st);
-      k_ranks<<<grid, kThreads, smem_rank, c.stream>>>(a, st);
-      ktrans<<<grid, kThreads, smem_trans, c.stream>>>(a, st);
-      k_merge<<<grid, kThreads, smem_merge, c.stream>>>(a, st);
+      k_ranks_big<<<grid, kThreads, smem_rank, c.stream>>>(a, st);
+      k_ranks_small<<<grid, kThreads, 0, c.stream>>>(a, st);
+      ktbig<<<grid, kThreads, smem_trans, c.stream>>>(a, st);
+      ktsmall<<<grid, kThreads, 0, c.stream>>>(a, st);
+      k_band<<<grid, kThreads, smem_merge, c.stream>>>(a, st);
+      k_outscan<<<grid, kThreads, 0, c.stream>>>(a, st);
+      k_write<<<grid, kThreads, 0, c.stream>>>(a, st);
       k_dom<<<grid, kThreads, 0, c.stream>>>(a, st);
       k_step_end<<<1, 32, 0, c.stream>>>(a, st);
-      c.kernel_launches += 8;
+      c.kernel_launches += 12;
     }
     k_term1<<<grid, kThreads, 0, c.stream>>>(a);
     k_term2<<<grid, kThreads, 0, c.stream>>>(a);
