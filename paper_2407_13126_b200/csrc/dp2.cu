@@ -52,7 +52,7 @@ constexpr int kChunkS = 32;          // targets per warp item
 constexpr int kChunkB = 512;         // targets per CTA item
 constexpr int kTile = kThreads * 8;  // scan tile
 constexpr int kBigNs = 1024;         // single-unit statuses with more candidates use the CTA path
-constexpr int kBucketSmall = 64;     // child buckets up to this size: thread per slot
+constexpr int kBucketSmall = 256;    // child buckets up to this size: thread per slot
 constexpr int kSortItems = 16;       // big child buckets: CTA radix sort of up to 256*16 keys
 constexpr int kBatch = 512;          // groups / statuses per CTA allocation batch
 constexpr int kNumScans = 7;
@@ -309,28 +309,44 @@ __device__ void multi_scan(const V2& a, const ScanJob* jobs, int njobs, int epoc
     const int j = t - tbase[k];
     const ScanJob& J = jobs[k];
     const int agg = block_scan_tile(J, j * kTile, sm);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // warp-parallel decoupled look-back over windows of 32 predecessors
+      const int lane = threadIdx.x;
       unsigned long long* st = a.scan_state + t;
-      const unsigned long long ep = static_cast<unsigned long long>(epoch) << 34;
-      int excl = 0;
-      __threadfence();
-      if (j == 0) {
-        atomicExch(st, ep | (2ull << 32) | static_cast<uint32_t>(agg));
-      } else {
-        atomicExch(st, ep | (1ull << 32) | static_cast<uint32_t>(agg));
-        int q = t - 1;
-        while (true) {
-          const unsigned long long w = ld_acquire(a.scan_state + q);
-          if ((w >> 34) != static_cast<unsigned long long>(epoch) || ((w >> 32) & 3) == 0) continue;
-          excl += static_cast<int>(w & 0xffffffffu);
-          if (((w >> 32) & 3) == 2) break;
-          --q;
-        }
+      const unsigned long long ep = static_cast<unsigned long long>(epoch);
+      if (lane == 0) {
         __threadfence();
-        atomicExch(st, ep | (2ull << 32) | static_cast<uint32_t>(excl + agg));
+        atomicExch(st, (ep << 34) | ((j == 0 ? 2ull : 1ull) << 32) | static_cast<uint32_t>(agg));
       }
-      s_excl = excl;
-      if (j == tiles[k] - 1) totals[k] = excl + agg;
+      int excl = 0;
+      if (j > 0) {
+        int hi = t - 1;  // window [hi-31, hi], never below this job's first tile
+        const int first = t - j;
+        while (true) {
+          const int q = hi - lane;
+          unsigned long long w = 0;
+          if (q >= first) {
+            do {
+              w = ld_acquire(a.scan_state + q);
+            } while ((w >> 34) != ep || ((w >> 32) & 3) == 0);
+          }
+          const bool is_prefix = q >= first && ((w >> 32) & 3) == 2;
+          const unsigned pm = __ballot_sync(0xffffffffu, is_prefix);
+          const int stop = pm ? __ffs(pm) - 1 : 32;  // nearest inclusive prefix in the window
+          int v = (q >= first && lane <= stop) ? static_cast<int>(w & 0xffffffffu) : 0;
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          excl += v;
+          if (pm) break;
+          hi -= 32;
+        }
+        if (lane == 0) {
+          __threadfence();
+          atomicExch(st, (ep << 34) | (2ull << 32) | static_cast<uint32_t>(excl + agg));
+        }
+      }
+      if (lane == 0) {
+        s_excl = excl;
+        if (j == tiles[k] - 1) totals[k] = excl + agg;
+      }
     }
     __syncthreads();
     const int excl = s_excl;
