@@ -91,7 +91,7 @@ struct Ctl {
   unsigned long long tr_ref, tr, ftot, fpeak, tbytes;
   unsigned long long best_vb, best_lex;
   int best_idx;
-  int ranks_prev;  // live states of F_{s-1}: the parent-rank space of F_s
+  int ranks_prev[2];  // [s&1]: live states of F_{s-1}, the parent-rank space of F_s
   int scan_total[kNumScans];
   int out_total[2];  // survivors, groups of F_{s+1}
 };
@@ -298,6 +298,7 @@ __device__ void multi_scan(const V2& a, const ScanJob* jobs, int njobs, int epoc
   if (blockIdx.x == 0 && threadIdx.x == 0)
     for (int k = 0; k < njobs; ++k)
       if (tiles[k] == 0) totals[k] = 0;
+  if (static_cast<int>(blockIdx.x) >= total_tiles) return;  // no tile for this CTA: stay off the ticket
   while (true) {
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
     __syncthreads();
@@ -1182,7 +1183,7 @@ __global__ void __launch_bounds__(kThreads) k_scans(V2 a, int s) {
                                    {a.ns_ucnt, a.ns_ccnt, a.ns_smallpos, H, 2},
                                    {a.u_chs, nullptr, a.u_sbase, sc.n_units, 0},
                                    {a.u_chb, nullptr, a.u_bbase, sc.n_units, 0},
-                                   {a.kid_cnt[cur], nullptr, a.kid_base, ctl->ranks_prev, 0}};
+                                   {a.kid_cnt[cur], nullptr, a.kid_base, ctl->ranks_prev[s & 1], 0}};
   multi_scan(a, jobs, kNumScans, 2 * (s + 1), &sc.ticket, ctl->scan_total);
 }
 
@@ -1290,30 +1291,26 @@ __global__ void __launch_bounds__(kThreads) k_dom(V2 a, int s) {
     a.ns_ucur[i] = 0;
     a.ns_ccur[i] = 0;
   }
-  const int rp = ctl->ranks_prev;
+  const int rp = ctl->ranks_prev[s & 1];
   for (int i = gtid; i < rp; i += gstride) {
     a.kid_cnt[cur][i] = 0;
     a.kid_cur[cur][i] = 0;
   }
-}
-
-// end-of-slot bookkeeping (after k_dom: every CTA has read ranks_prev)
-__global__ void k_step_end(V2 a, int s) {
-  if (failed(a) || threadIdx.x != 0 || blockIdx.x != 0) return;
-  const int cur = s & 1, nxt = (s + 1) & 1;
-  Ctl* ctl = a.ctl;
-  StepCounters& sc = ctl->sc[s & 1];
-  a.hist_base[s + 2] = a.hist_base[s + 1] + ctl->n_store[nxt];  // array has S+2 entries
-  if (a.dbg) {
-    long long* d = a.dbg + 6ll * s;
-    d[0] = sc.n_units;
-    d[1] = sc.n_big + sc.n_small;
-    d[2] = sc.T;
-    d[3] = ctl->n_store[nxt];
-    d[4] = ctl->n_groups[nxt];
-    d[5] = ctl->alive_now[cur];
+  if (gtid == 0) {  // end-of-slot bookkeeping (every value read here is final)
+    const int nxt = (s + 1) & 1;
+    StepCounters& sc = ctl->sc[s & 1];
+    a.hist_base[s + 2] = a.hist_base[s + 1] + ctl->n_store[nxt];  // array has S+2 entries
+    if (a.dbg) {
+      long long* d = a.dbg + 6ll * s;
+      d[0] = sc.n_units;
+      d[1] = sc.n_big + sc.n_small;
+      d[2] = sc.T;
+      d[3] = ctl->n_store[nxt];
+      d[4] = ctl->n_groups[nxt];
+      d[5] = ctl->alive_now[cur];
+    }
+    ctl->ranks_prev[nxt] = ctl->alive_now[cur];
   }
-  ctl->ranks_prev = ctl->alive_now[cur];
 }
 
 // terminal (solvers.hpp:552-565): live count of F_S, budget, best all-done state
@@ -1411,7 +1408,7 @@ __global__ void k_init_root(V2 a, uint32_t root_pid) {
   c->best_vb = 0;
   c->best_lex = ~0ull;
   c->best_idx = -1;
-  c->ranks_prev = 1;
+  c->ranks_prev[0] = 1;
   a.hist_base[0] = 0;
   a.hist_base[1] = 0;
 }
@@ -1467,7 +1464,24 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
   MGS_CUDA_OK(cudaFuncSetAttribute(ktbig, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_trans)));
   MGS_CUDA_OK(cudaFuncSetAttribute(k_ranks_big, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_rank)));
   MGS_CUDA_OK(cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_merge)));
+  // one resident wave per kernel: grid = SMs x max co-resident CTAs
+  auto wave = [&](const void* k, size_t dyn) {
+    int occ = 0;
+    MGS_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, dyn));
+    return c.sm_count * std::max(1, occ);
+  };
   const int grid = c.sm_count * 8;
+  const int g_units = wave(reinterpret_cast<const void*>(kunits), 0);
+  const int g_scans = wave(reinterpret_cast<const void*>(k_scans), 0);
+  const int g_place = wave(reinterpret_cast<const void*>(k_place), 0);
+  const int g_rbig = wave(reinterpret_cast<const void*>(k_ranks_big), smem_rank);
+  const int g_rsmall = wave(reinterpret_cast<const void*>(k_ranks_small), 0);
+  const int g_tbig = wave(reinterpret_cast<const void*>(ktbig), smem_trans);
+  const int g_tsmall = wave(reinterpret_cast<const void*>(ktsmall), 0);
+  const int g_band = wave(reinterpret_cast<const void*>(k_band), smem_merge);
+  const int g_oscan = wave(reinterpret_cast<const void*>(k_outscan), 0);
+  const int g_write = wave(reinterpret_cast<const void*>(k_write), 0);
+  const int g_dom = wave(reinterpret_cast<const void*>(k_dom), 0);
   static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 128ll << 20};
   const uint64_t budget = p.state_budget;
   const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr;
@@ -1575,20 +1589,56 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     a.merge_win = merge_win;
     a.oi_bits = 1;
     while ((1ll << a.oi_bits) < sp.n_opt) ++a.oi_bits;
+    // debug: per-kernel CUDA-event timing inside the stream (MGS_DEBUG_STEPS)
+    constexpr int kK = 11;
+    static const char* kNames[kK] = {"units", "scans", "place", "ranks_big", "ranks_small", "trans_big",
+                                     "trans_small", "band", "outscan", "write", "dom"};
+    std::vector<cudaEvent_t> evs;
+    auto mark = [&]() {
+      if (!debug) return;
+      cudaEvent_t e;
+      MGS_CUDA_OK(cudaEventCreate(&e));
+      MGS_CUDA_OK(cudaEventRecord(e, c.stream));
+      evs.push_back(e);
+    };
+    mark();
     for (int st = 0; st < S; ++st) {
-      kunits<<<grid, kThreads, 0, c.stream>>>(a, st);
-      k_scans<<<grid, kThreads, 0, c.stream>>>(a, st);
-      k_place<<<grid, kThreads, 0, c.stream>>>(a, st);
-      k_ranks_big<<<grid, kThreads, smem_rank, c.stream>>>(a, st);
-      k_ranks_small<<<grid, kThreads, 0, c.stream>>>(a, st);
-      ktbig<<<grid, kThreads, smem_trans, c.stream>>>(a, st);
-      ktsmall<<<grid, kThreads, 0, c.stream>>>(a, st);
-      k_band<<<grid, kThreads, smem_merge, c.stream>>>(a, st);
-      k_outscan<<<grid, kThreads, 0, c.stream>>>(a, st);
-      k_write<<<grid, kThreads, 0, c.stream>>>(a, st);
-      k_dom<<<grid, kThreads, 0, c.stream>>>(a, st);
-      k_step_end<<<1, 32, 0, c.stream>>>(a, st);
-      c.kernel_launches += 12;
+      kunits<<<g_units, kThreads, 0, c.stream>>>(a, st);
+      mark();
+      k_scans<<<g_scans, kThreads, 0, c.stream>>>(a, st);
+      mark();
+      k_place<<<g_place, kThreads, 0, c.stream>>>(a, st);
+      mark();
+      k_ranks_big<<<g_rbig, kThreads, smem_rank, c.stream>>>(a, st);
+      mark();
+      k_ranks_small<<<g_rsmall, kThreads, 0, c.stream>>>(a, st);
+      mark();
+      ktbig<<<g_tbig, kThreads, smem_trans, c.stream>>>(a, st);
+      mark();
+      ktsmall<<<g_tsmall, kThreads, 0, c.stream>>>(a, st);
+      mark();
+      k_band<<<g_band, kThreads, smem_merge, c.stream>>>(a, st);
+      mark();
+      k_outscan<<<g_oscan, kThreads, 0, c.stream>>>(a, st);
+      mark();
+      k_write<<<g_write, kThreads, 0, c.stream>>>(a, st);
+      mark();
+      k_dom<<<g_dom, kThreads, 0, c.stream>>>(a, st);
+      mark();
+      c.kernel_launches += 11;
+    }
+    if (debug) {
+      MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+      double acc[kK] = {0};
+      for (size_t i = 1; i < evs.size(); ++i) {
+        float ms = 0.f;
+        MGS_CUDA_OK(cudaEventElapsedTime(&ms, evs[i - 1], evs[i]));
+        acc[(i - 1) % kK] += ms;
+      }
+      for (auto e : evs) cudaEventDestroy(e);
+      std::fprintf(stderr, "v2 in-stream ms per window:");
+      for (int k = 0; k < kK; ++k) std::fprintf(stderr, " %s %.2f", kNames[k], acc[k]);
+      std::fprintf(stderr, "\n");
     }
     k_term1<<<grid, kThreads, 0, c.stream>>>(a);
     k_term2<<<grid, kThreads, 0, c.stream>>>(a);
