@@ -162,6 +162,7 @@ struct Ctx {
   HostPinned pinned;
   uint64_t kernel_launches = 0;
   History history;
+  std::map<std::string, cudaGraphExec_t> graphs;  // cached per-window kernel sequences
 
   template <class T>
   T* buf(const char* name, size_t n) {
@@ -170,6 +171,7 @@ struct Ctx {
   ~Ctx() {
     for (auto& kv : bufs) kv.second.release();
     history.release();
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (pinned.p) cudaFreeHost(pinned.p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);

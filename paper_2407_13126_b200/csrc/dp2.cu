@@ -35,6 +35,7 @@
 // Dead (dominated) states stay in F_{s+1} as holes flagged alive = 0 and are
 // skipped everywhere; ranks are dense over the live states only.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1155,14 +1156,16 @@ __device__ void phase_dominance(const V2& a, int s) {
 // Phase kernels: one launch per phase and slot, stream-ordered, all counts on
 // the device (the host never waits inside a window).
 template <int M>
-__global__ void __launch_bounds__(kThreads) k_units(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads) k_units(const V2* __restrict__ ap, int s) {
+  const V2& a = *ap;
   __shared__ int s_cnt[kBatch];
   __shared__ long long s_red[32];
   if (failed(a)) return;
   phase_units<M>(a, s, 0, s_cnt, s_red);
 }
 
-__global__ void __launch_bounds__(kThreads) k_scans(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, int s) {
+  const V2& a = *ap;
   if (failed(a)) return;
   const int cur = s & 1;
   Ctl* ctl = a.ctl;
@@ -1187,7 +1190,8 @@ __global__ void __launch_bounds__(kThreads) k_scans(V2 a, int s) {
   multi_scan(a, jobs, kNumScans, 2 * (s + 1), &sc.ticket, ctl->scan_total);
 }
 
-__global__ void __launch_bounds__(kThreads) k_place(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads) k_place(const V2* __restrict__ ap, int s) {
+  const V2& a = *ap;
   if (failed(a)) return;
   Ctl* ctl = a.ctl;
   StepCounters& sc = ctl->sc[s & 1];
@@ -1209,19 +1213,22 @@ __global__ void __launch_bounds__(kThreads) k_place(V2 a, int s) {
   if (fits) phase_place(a, s);
 }
 
-__global__ void __launch_bounds__(kThreads) k_ranks_big(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads) k_ranks_big(const V2* __restrict__ ap, int s) {
+  const V2& a = *ap;
   extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
   phase_ranks_big(a, s, smem_u64);
 }
 
-__global__ void __launch_bounds__(kThreads) k_ranks_small(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads) k_ranks_small(const V2* __restrict__ ap, int s) {
+  const V2& a = *ap;
   if (failed(a)) return;
   phase_ranks_small(a, s);
 }
 
 template <int M>
-__global__ void __launch_bounds__(kThreads) k_trans_big(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads) k_trans_big(const V2* __restrict__ ap, int s) {
+  const V2& a = *ap;
   extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
   if (static_cast<int>(blockIdx.x) >= a.ctl->sc[s & 1].items_b) return;  // no item for this CTA
@@ -1238,7 +1245,8 @@ __global__ void __launch_bounds__(kThreads) k_trans_big(V2 a, int s) {
 }
 
 template <int M>
-__global__ void __launch_bounds__(kThreads, 4) k_trans_small(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads, 4) k_trans_small(const V2* __restrict__ ap, int s) {
+  const V2& a = *ap;
   if (failed(a)) return;
   phase_trans_small<M>(a, s);
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // counters of the next step
@@ -1248,20 +1256,23 @@ __global__ void __launch_bounds__(kThreads, 4) k_trans_small(V2 a, int s) {
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_band(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads) k_band(const V2* __restrict__ ap, int s) {
+  const V2& a = *ap;
   extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
   phase_band(a, s, smem_u64, smem_u64 + a.merge_win);
 }
 
-__global__ void __launch_bounds__(kThreads) k_outscan(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads) k_outscan(const V2* __restrict__ ap, int s) {
+  const V2& a = *ap;
   if (failed(a)) return;
   const int H = a.hmask + 1;
   const ScanJob jobs[2] = {{a.ns_out, nullptr, a.ns_obase, H, 0}, {a.ns_out, nullptr, a.ns_gbase, H, 3}};
   multi_scan(a, jobs, 2, 2 * (s + 1) + 1, &a.ctl->sc[s & 1].ticket2, a.ctl->out_total);
 }
 
-__global__ void __launch_bounds__(kThreads) k_write(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads) k_write(const V2* __restrict__ ap, int s) {
+  const V2& a = *ap;
   if (failed(a)) return;
   const int nxt = (s + 1) & 1;
   Ctl* ctl = a.ctl;
@@ -1277,7 +1288,8 @@ __global__ void __launch_bounds__(kThreads) k_write(V2 a, int s) {
   if (fits) phase_write(a, s);
 }
 
-__global__ void __launch_bounds__(kThreads) k_dom(V2 a, int s) {
+__global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int s) {
+  const V2& a = *ap;
   if (failed(a)) return;
   const int cur = s & 1;
   Ctl* ctl = a.ctl;
@@ -1320,7 +1332,8 @@ __device__ __forceinline__ uint32_t all_done_key(int M) {
   return k;
 }
 
-__global__ void __launch_bounds__(kThreads) k_term1(V2 a) {
+__global__ void __launch_bounds__(kThreads) k_term1(const V2* __restrict__ ap) {
+  const V2& a = *ap;
   __shared__ long long s_red[32];
   if (failed(a)) return;
   const int fin = a.S & 1;
@@ -1345,7 +1358,8 @@ __global__ void __launch_bounds__(kThreads) k_term1(V2 a) {
   if (any) atomicMax(&a.ctl->best_vb, mv + 1);  // +1: 0 = none
 }
 
-__global__ void __launch_bounds__(kThreads) k_term2(V2 a) {
+__global__ void __launch_bounds__(kThreads) k_term2(const V2* __restrict__ ap) {
+  const V2& a = *ap;
   if (failed(a)) return;
   const int fin = a.S & 1;
   const FrontierV2& F = a.f[fin];
@@ -1365,7 +1379,8 @@ __global__ void __launch_bounds__(kThreads) k_term2(V2 a) {
     if (F.alive[i] && F.status[i] == all_done && vbits(F.value[i]) + 1 == bvb) atomicMin(&a.ctl->best_lex, F.lex[i]);
 }
 
-__global__ void __launch_bounds__(kThreads) k_term3(V2 a) {
+__global__ void __launch_bounds__(kThreads) k_term3(const V2* __restrict__ ap) {
+  const V2& a = *ap;
   if (failed(a)) return;
   const int fin = a.S & 1;
   const FrontierV2& F = a.f[fin];
@@ -1377,7 +1392,8 @@ __global__ void __launch_bounds__(kThreads) k_term3(V2 a) {
     if (F.alive[i] && F.status[i] == all_done && vbits(F.value[i]) + 1 == bvb && F.lex[i] == blx) a.ctl->best_idx = i;
 }
 
-__global__ void k_backtrack2(V2 a) {  // parent walk (solvers.hpp:567-574)
+__global__ void k_backtrack2(const V2* __restrict__ ap) {
+  const V2& a = *ap;  // parent walk (solvers.hpp:567-574)
   if (failed(a) || threadIdx.x != 0 || blockIdx.x != 0) return;
   int idx = a.ctl->best_idx;
   for (int s = a.S - 1; s >= 0; --s) {
@@ -1387,7 +1403,8 @@ __global__ void k_backtrack2(V2 a) {  // parent walk (solvers.hpp:567-574)
   }
 }
 
-__global__ void k_init_root(V2 a, uint32_t root_pid) {
+__global__ void k_init_root(const V2* __restrict__ ap, uint32_t root_pid) {
+  const V2& a = *ap;
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   FrontierV2 F = a.f[0];
   F.status[0] = 0;
@@ -1583,52 +1600,66 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     a.n_partial = n_partial;
     a.dbg = debug ? c.buf<long long>("v2_dbg", 6 * S) : nullptr;
     a.dbg_time = nullptr;
-    k_init_root<<<1, 32, 0, c.stream>>>(a, static_cast<uint32_t>(sp.root_pid));
+    V2* d_args = c.buf<V2>("v2_args", 1);
+    MGS_CUDA_OK(cudaMemcpyAsync(d_args, &a, sizeof(V2), cudaMemcpyHostToDevice, c.stream));
+    k_init_root<<<1, 32, 0, c.stream>>>(d_args, static_cast<uint32_t>(sp.root_pid));
     ++c.kernel_launches;
     a.sc_big_ctas = grid;
     a.merge_win = merge_win;
     a.oi_bits = 1;
     while ((1ll << a.oi_bits) < sp.n_opt) ++a.oi_bits;
-    // debug: per-kernel CUDA-event timing inside the stream (MGS_DEBUG_STEPS)
+    // The window's kernel sequence depends only on S, M and launch shapes (all
+    // problem data lives behind d_args), so it is captured once into a CUDA
+    // graph and replayed; MGS_DEBUG_STEPS launches eagerly with per-kernel events.
     constexpr int kK = 11;
     static const char* kNames[kK] = {"units", "scans", "place", "ranks_big", "ranks_small", "trans_big",
                                      "trans_small", "band", "outscan", "write", "dom"};
     std::vector<cudaEvent_t> evs;
-    auto mark = [&]() {
-      if (!debug) return;
-      cudaEvent_t e;
-      MGS_CUDA_OK(cudaEventCreate(&e));
-      MGS_CUDA_OK(cudaEventRecord(e, c.stream));
-      evs.push_back(e);
+    auto enqueue = [&](cudaStream_t st_, bool timed) {
+      auto mark = [&]() {
+        if (!timed) return;
+        cudaEvent_t e;
+        MGS_CUDA_OK(cudaEventCreate(&e));
+        MGS_CUDA_OK(cudaEventRecord(e, st_));
+        evs.push_back(e);
+      };
+      mark();
+      for (int st = 0; st < S; ++st) {
+        kunits<<<g_units, kThreads, 0, st_>>>(d_args, st);
+        mark();
+        k_scans<<<g_scans, kThreads, 0, st_>>>(d_args, st);
+        mark();
+        k_place<<<g_place, kThreads, 0, st_>>>(d_args, st);
+        mark();
+        k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(d_args, st);
+        mark();
+        k_ranks_small<<<g_rsmall, kThreads, 0, st_>>>(d_args, st);
+        mark();
+        ktbig<<<g_tbig, kThreads, smem_trans, st_>>>(d_args, st);
+        mark();
+        ktsmall<<<g_tsmall, kThreads, 0, st_>>>(d_args, st);
+        mark();
+        k_band<<<g_band, kThreads, smem_merge, st_>>>(d_args, st);
+        mark();
+        k_outscan<<<g_oscan, kThreads, 0, st_>>>(d_args, st);
+        mark();
+        k_write<<<g_write, kThreads, 0, st_>>>(d_args, st);
+        mark();
+        k_dom<<<g_dom, kThreads, 0, st_>>>(d_args, st);
+        mark();
+      }
+      k_term1<<<grid, kThreads, 0, st_>>>(d_args);
+      k_term2<<<grid, kThreads, 0, st_>>>(d_args);
+      k_term3<<<grid, kThreads, 0, st_>>>(d_args);
+      k_backtrack2<<<1, 32, 0, st_>>>(d_args);
     };
-    mark();
-    for (int st = 0; st < S; ++st) {
-      kunits<<<g_units, kThreads, 0, c.stream>>>(a, st);
-      mark();
-      k_scans<<<g_scans, kThreads, 0, c.stream>>>(a, st);
-      mark();
-      k_place<<<g_place, kThreads, 0, c.stream>>>(a, st);
-      mark();
-      k_ranks_big<<<g_rbig, kThreads, smem_rank, c.stream>>>(a, st);
-      mark();
-      k_ranks_small<<<g_rsmall, kThreads, 0, c.stream>>>(a, st);
-      mark();
-      ktbig<<<g_tbig, kThreads, smem_trans, c.stream>>>(a, st);
-      mark();
-      ktsmall<<<g_tsmall, kThreads, 0, c.stream>>>(a, st);
-      mark();
-      k_band<<<g_band, kThreads, smem_merge, c.stream>>>(a, st);
-      mark();
-      k_outscan<<<g_oscan, kThreads, 0, c.stream>>>(a, st);
-      mark();
-      k_write<<<g_write, kThreads, 0, c.stream>>>(a, st);
-      mark();
-      k_dom<<<g_dom, kThreads, 0, c.stream>>>(a, st);
-      mark();
-      c.kernel_launches += 11;
-    }
+    c.kernel_launches += 11ull * S + 4;
     if (debug) {
+      const auto host_t0 = std::chrono::steady_clock::now();
+      enqueue(c.stream, true);
+      const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
       MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+      std::fprintf(stderr, "v2 host enqueue ms %.2f (eager, with events)\n", host_ms);
       double acc[kK] = {0};
       for (size_t i = 1; i < evs.size(); ++i) {
         float ms = 0.f;
@@ -1639,12 +1670,30 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
       std::fprintf(stderr, "v2 in-stream ms per window:");
       for (int k = 0; k < kK; ++k) std::fprintf(stderr, " %s %.2f", kNames[k], acc[k]);
       std::fprintf(stderr, "\n");
+    } else {
+      char key[256];
+      std::snprintf(key, sizeof key, "v2:%d:%d:%zu:%zu:%zu:%p", S, M, smem_trans, smem_merge, smem_rank,
+                    static_cast<void*>(d_args));
+      auto it = c.graphs.find(key);
+      if (it == c.graphs.end()) {
+        cudaStream_t cap;
+        MGS_CUDA_OK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        cudaGraph_t graph;
+        MGS_CUDA_OK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        enqueue(cap, false);
+        MGS_CUDA_OK(cudaStreamEndCapture(cap, &graph));
+        cudaGraphExec_t exec;
+        MGS_CUDA_OK(cudaGraphInstantiate(&exec, graph, 0));
+        MGS_CUDA_OK(cudaGraphDestroy(graph));
+        MGS_CUDA_OK(cudaStreamDestroy(cap));
+        if (c.graphs.size() >= 16) {
+          cudaGraphExecDestroy(c.graphs.begin()->second);
+          c.graphs.erase(c.graphs.begin());
+        }
+        it = c.graphs.emplace(key, exec).first;
+      }
+      MGS_CUDA_OK(cudaGraphLaunch(it->second, c.stream));
     }
-    k_term1<<<grid, kThreads, 0, c.stream>>>(a);
-    k_term2<<<grid, kThreads, 0, c.stream>>>(a);
-    k_term3<<<grid, kThreads, 0, c.stream>>>(a);
-    k_backtrack2<<<1, 32, 0, c.stream>>>(a);
-    c.kernel_launches += 4;
     MGS_CUDA_OK(cudaGetLastError());
     Ctl h{};
     MGS_CUDA_OK(cudaMemcpyAsync(&h, a.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
