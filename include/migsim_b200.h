@@ -13,6 +13,8 @@
  *   mgs_precheck       precheck_scenario               solvers.hpp:27-69
  *   mgs_goodput_table  solve_dp ub_suffix + incumbent  solvers.hpp:258-322
  *   mgs_solve_window   solve_dp                        solvers.hpp:242-579
+ *   mgs_bruteforce     solve_bruteforce                solvers.hpp:143-228
+ *   mgs_precheck       precheck_scenario (all violations, reference order)
  *   mgs_solve_batch    solve_dp over independent windows (the reference's
  *                      per-scenario call in a host loop)
  *   mgs_evaluate_batch evaluate_plan(verify=false)     evaluate.hpp:153-210
@@ -52,7 +54,8 @@ typedef enum {
   MGS_ERR_STATE_BUDGET = 9,            /* "planner.state-budget" solvers.hpp:539-542 */
   MGS_ERR_PLAN_INFEASIBLE = 10,        /* "plan.infeasible" evaluate.hpp:165 */
   MGS_ERR_CUDA = 11,                   /* device failure (no reference analogue) */
-  MGS_ERR_ARGUMENT = 12                /* null pointer / size out of range */
+  MGS_ERR_ARGUMENT = 12,               /* null pointer / size out of range */
+  MGS_ERR_BRUTEFORCE_CAP = 13          /* "planner.bruteforce-cap" solvers.hpp:153-158 */
 } mgs_status;
 
 typedef struct {
@@ -118,6 +121,15 @@ typedef struct {
   uint64_t transition_bytes;
 } mgs_stats;
 
+/* One precheck_scenario violation (solvers.hpp:27-69): code is
+ * MGS_ERR_DEPLOYMENT_FLOOR / MGS_ERR_RETRAINING_WINDOW / MGS_ERR_NO_COEXISTENCE,
+ * model the offending tenant or -1 (the "no configuration deploys every
+ * inference task" case). The host wrapper formats the reference's message. */
+typedef struct {
+  int32_t code;
+  int32_t model;
+} mgs_violation;
+
 typedef struct mgs_ctx mgs_ctx;
 
 MGS_API int mgs_open(int device, mgs_ctx** out);
@@ -151,6 +163,19 @@ MGS_API int mgs_goodput_table(mgs_ctx* ctx, const mgs_problem* p, double* ub_suf
  * may be NULL. */
 MGS_API int mgs_solve_window(mgs_ctx* ctx, const mgs_problem* p, int32_t* out_option, int32_t* out_config,
                      int8_t* out_labels, double* out_objective, mgs_stats* stats, mgs_error* err);
+
+/* precheck_scenario: writes up to cap violations (reference order) and the
+ * total count to *n_out. Returns MGS_OK even when violations exist; input
+ * errors (input.scenario / input.catalog) are returned as status codes. */
+MGS_API int mgs_precheck(mgs_ctx* ctx, const mgs_lattice* lattice, const mgs_tables* tables, mgs_violation* out,
+                         int32_t cap, int32_t* n_out, mgs_error* err);
+
+/* solve_bruteforce on one window: every allocation sequence scored on the
+ * device, best by (objective desc, option-index sequence asc). Gated like the
+ * reference by |O|^S <= bruteforce_cap (MGS_ERR_BRUTEFORCE_CAP otherwise).
+ * Outputs as for mgs_solve_window. */
+MGS_API int mgs_bruteforce(mgs_ctx* ctx, const mgs_problem* p, double bruteforce_cap, int32_t* out_option,
+                           int32_t* out_config, int8_t* out_labels, double* out_objective, mgs_error* err);
 
 /* n independent windows (different scenarios / traces) solved back to back on
  * the device; per-problem outputs at out_option[i*S_max...], status[i],

@@ -33,6 +33,7 @@ STATUS_CODES = {
     10: "plan.infeasible",
     11: "device.cuda",
     12: "input.argument",
+    13: "planner.bruteforce-cap",
 }
 
 
@@ -58,6 +59,10 @@ class mgs_problem(C.Structure):
     _fields_ = [("lattice", mgs_lattice), ("tables", mgs_tables), ("forecast", C.POINTER(C.c_int64)),
                 ("forecast_len", C.c_int32), ("has_initial", C.c_int32), ("init_mask", C.c_uint32 * MAX_MODELS),
                 ("state_budget", C.c_uint64), ("workers", C.c_int32)]
+
+
+class mgs_violation(C.Structure):
+    _fields_ = [("code", C.c_int32), ("model", C.c_int32)]
 
 
 class mgs_stats(C.Structure):
@@ -120,12 +125,17 @@ def load():
                                     P(C.c_double), P(C.c_int32), P(mgs_stats), P(mgs_error)]
     lib.mgs_evaluate_batch.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_int32), C.c_int32, P(C.c_int64),
                                        C.c_int32, P(C.c_double), P(C.c_double), P(mgs_error)]
+    lib.mgs_precheck.argtypes = [C.c_void_p, P(mgs_lattice), P(mgs_tables), P(mgs_violation), C.c_int32,
+                                 P(C.c_int32), P(mgs_error)]
+    lib.mgs_bruteforce.argtypes = [C.c_void_p, P(mgs_problem), C.c_double, P(C.c_int32), P(C.c_int32), P(C.c_int8),
+                                   P(C.c_double), P(mgs_error)]
     _LIB = lib
     return lib
 
 
 EXPORTED_SYMBOLS = ["mgs_open", "mgs_close", "mgs_status_code", "mgs_version", "mgs_set_stream", "mgs_enumerate",
-                    "mgs_goodput_table", "mgs_solve_window", "mgs_solve_batch", "mgs_evaluate_batch"]
+                    "mgs_goodput_table", "mgs_solve_window", "mgs_solve_batch", "mgs_evaluate_batch",
+                    "mgs_precheck", "mgs_bruteforce"]
 
 
 def empty_error():

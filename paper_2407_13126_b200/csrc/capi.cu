@@ -80,6 +80,36 @@ double* upload_forecast(Ctx& c, const mgs_problem& p, int M, int S) {
   return d_f;
 }
 
+// evaluate_plan(...).total of one plan on the device (forecast_i64 resident)
+double plan_total(Ctx& c, const mgs::Prepared& pr, const mgs::DevSpace& sp, const std::vector<int32_t>& plan) {
+  const int M = pr.t.M, S = pr.t.S;
+  int32_t* d_plan = c.buf<int32_t>("plan_eval", S);
+  double* d_total = c.buf<double>("plan_total", 1);
+  MGS_CUDA_OK(cudaMemcpyAsync(d_plan, plan.data(), S * 4, cudaMemcpyHostToDevice, c.stream));
+  int64_t* d_arr = c.buf<int64_t>("forecast_i64", static_cast<size_t>(M) * S);
+  mgs::evaluate_batch(c, pr, sp, d_plan, 1, d_arr, 1, d_total, nullptr);
+  double* h = c.pinned.get<double>(1);
+  MGS_CUDA_OK(cudaMemcpyAsync(h, d_total, 8, cudaMemcpyDeviceToHost, c.stream));
+  MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+  return *h;
+}
+
+void copy_plan_labels(Ctx& c, const mgs::DevSpace& sp, const std::vector<int32_t>& plan, int32_t* out_config,
+                      int8_t* out_labels) {
+  if (!out_config && !out_labels) return;
+  std::vector<int32_t> cfg(sp.n_opt);
+  std::vector<int8_t> lab(static_cast<size_t>(sp.n_opt) * MGS_MAX_SLOTS);
+  MGS_CUDA_OK(cudaMemcpyAsync(cfg.data(), sp.opt_config, sp.n_opt * 4, cudaMemcpyDeviceToHost, c.stream));
+  MGS_CUDA_OK(cudaMemcpyAsync(lab.data(), sp.opt_labels, lab.size(), cudaMemcpyDeviceToHost, c.stream));
+  MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+  for (size_t s = 0; s < plan.size(); ++s) {
+    const int o = plan[s];
+    if (out_config) out_config[s] = cfg[o];
+    if (out_labels)
+      for (int k = 0; k < MGS_MAX_SLOTS; ++k) out_labels[s * MGS_MAX_SLOTS + k] = lab[static_cast<size_t>(o) * MGS_MAX_SLOTS + k];
+  }
+}
+
 void solve_one(Ctx& c, const mgs_problem& p, int32_t* out_option, int32_t* out_config, int8_t* out_labels,
                double* out_objective, mgs_stats* stats) {
   MGS_CUDA_OK(cudaEventRecord(c.ev0, c.stream));
@@ -163,6 +193,7 @@ const char* mgs_status_code(int status) {
     case MGS_ERR_PLAN_INFEASIBLE: return "plan.infeasible";
     case MGS_ERR_CUDA: return "device.cuda";
     case MGS_ERR_ARGUMENT: return "input.argument";
+    case MGS_ERR_BRUTEFORCE_CAP: return "planner.bruteforce-cap";
     default: return "unknown";
   }
 }
@@ -242,6 +273,55 @@ int mgs_goodput_table(mgs_ctx* ctx, const mgs_problem* p, double* ub_suffix, dou
     if (incumbent) MGS_CUDA_OK(cudaMemcpyAsync(incumbent, d_inc, 8, cudaMemcpyDeviceToHost, c.stream));
     if (greedy_option) MGS_CUDA_OK(cudaMemcpyAsync(greedy_option, d_greedy, S * 4, cudaMemcpyDeviceToHost, c.stream));
     MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int mgs_precheck(mgs_ctx* ctx, const mgs_lattice* lattice, const mgs_tables* tables, mgs_violation* out, int32_t cap,
+                 int32_t* n_out, mgs_error* err) {
+  if (!ctx || !lattice || !tables || !n_out || cap < 0 || (cap > 0 && !out)) return MGS_ERR_ARGUMENT;
+  return guarded(err, [&] {
+    Ctx& c = ctx->c;
+    MGS_CUDA_OK(cudaSetDevice(c.device));
+    mgs::Prepared pr = mgs::prepare_tables(*lattice, *tables);
+    mgs::DevSpace sp;
+    mgs::build_space(c, *lattice, pr, sp);
+    const auto v = mgs::collect_violations(c, *lattice, pr, sp);
+    *n_out = static_cast<int32_t>(v.size());
+    for (int i = 0; i < static_cast<int>(v.size()) && i < cap; ++i) out[i] = mgs_violation{v[i].first, v[i].second};
+  });
+}
+
+int mgs_bruteforce(mgs_ctx* ctx, const mgs_problem* p, double bruteforce_cap, int32_t* out_option, int32_t* out_config,
+                   int8_t* out_labels, double* out_objective, mgs_error* err) {
+  if (!ctx || !p) return MGS_ERR_ARGUMENT;
+  return guarded(err, [&] {
+    Ctx& c = ctx->c;
+    MGS_CUDA_OK(cudaSetDevice(c.device));
+    c.kernel_launches = 0;
+    mgs::Prepared pr = prepare_problem(*p);
+    mgs::DevSpace sp;
+    mgs::build_space(c, p->lattice, pr, sp);
+    mgs::precheck_space(c, p->lattice, pr, sp);  // throw_if_infeasible(precheck_scenario) (solvers.hpp:146)
+    const int M = pr.t.M, S = pr.t.S;
+    if (p->forecast_len != S) throw PlanFail{MGS_ERR_INPUT_FORECAST, "forecast horizon != window size"};
+    const double estimate = std::pow(static_cast<double>(sp.n_opt), S);  // solvers.hpp:153-158
+    if (estimate > bruteforce_cap) {
+      char a[64], b[64];
+      std::snprintf(a, sizeof a, "%.9g", estimate);
+      std::snprintf(b, sizeof b, "%.9g", bruteforce_cap);
+      throw PlanFail{MGS_ERR_BRUTEFORCE_CAP, std::string("brute-force space estimate ") + a + " (=" +
+                                                 std::to_string(sp.n_opt) + "^" + std::to_string(S) +
+                                                 ") exceeds the cap " + b};
+    }
+    double* d_recv = upload_forecast(c, *p, M, S);
+    std::vector<int32_t> plan;
+    if (!mgs::bruteforce(c, pr, sp, d_recv, plan))
+      throw PlanFail{MGS_ERR_INFEASIBLE_JOINT, "no feasible allocation sequence exists for this window"};
+    const double total = plan_total(c, pr, sp, plan);
+    copy_plan_labels(c, sp, plan, out_config, out_labels);
+    if (out_option)
+      for (int s = 0; s < S; ++s) out_option[s] = plan[s];
+    if (out_objective) *out_objective = total;
   });
 }
 

@@ -193,6 +193,10 @@ struct Prepared {
 Prepared prepare_tables(const mgs_lattice& lat, const mgs_tables& tab);
 void build_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, DevSpace& sp);
 void precheck_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, const DevSpace& sp);
+std::vector<std::pair<int, int>> collect_violations(Ctx& c, const mgs_lattice& lat, const Prepared& pr,
+                                                    const DevSpace& sp);
+// bruteforce.cu: solve_bruteforce; false when no feasible all-done sequence
+bool bruteforce(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* d_recv, std::vector<int32_t>& plan);
 // goodput.cu
 void goodput_reductions(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* d_recv, double* d_ub,
                         double* d_incumbent, int32_t* d_greedy);

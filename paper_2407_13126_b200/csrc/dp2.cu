@@ -1501,7 +1501,11 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
   const int g_dom = wave(reinterpret_cast<const void*>(k_dom), 0);
   static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 128ll << 20};
   const uint64_t budget = p.state_budget;
-  const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr;
+  const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr || std::getenv("MGS_TRACE") != nullptr;
+  if (std::getenv("MGS_TRACE"))
+    std::fprintf(stderr, "trace v2 setup: S %d M %d P1 %d n_partial %d smem trans %zu rank %zu merge %zu grids %d %d %d %d %d %d %d %d %d %d %d\n", S, M,
+                 sp.P1, n_partial, smem_trans, smem_rank, smem_merge, g_units, g_scans, g_place, g_rbig, g_rsmall, g_tbig,
+                 g_tsmall, g_band, g_oscan, g_write, g_dom);
   for (int attempt = 0; attempt < 10; ++attempt) {
     V2 a{};
     a.sp = sp;
@@ -1600,14 +1604,14 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     a.n_partial = n_partial;
     a.dbg = debug ? c.buf<long long>("v2_dbg", 6 * S) : nullptr;
     a.dbg_time = nullptr;
-    V2* d_args = c.buf<V2>("v2_args", 1);
-    MGS_CUDA_OK(cudaMemcpyAsync(d_args, &a, sizeof(V2), cudaMemcpyHostToDevice, c.stream));
-    k_init_root<<<1, 32, 0, c.stream>>>(d_args, static_cast<uint32_t>(sp.root_pid));
-    ++c.kernel_launches;
     a.sc_big_ctas = grid;
     a.merge_win = merge_win;
     a.oi_bits = 1;
     while ((1ll << a.oi_bits) < sp.n_opt) ++a.oi_bits;
+    V2* d_args = c.buf<V2>("v2_args", 1);
+    MGS_CUDA_OK(cudaMemcpyAsync(d_args, &a, sizeof(V2), cudaMemcpyHostToDevice, c.stream));
+    k_init_root<<<1, 32, 0, c.stream>>>(d_args, static_cast<uint32_t>(sp.root_pid));
+    ++c.kernel_launches;
     // The window's kernel sequence depends only on S, M and launch shapes (all
     // problem data lives behind d_args), so it is captured once into a CUDA
     // graph and replayed; MGS_DEBUG_STEPS launches eagerly with per-kernel events.
@@ -1624,29 +1628,47 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
         evs.push_back(e);
       };
       mark();
+      const bool trace = timed && std::getenv("MGS_TRACE") != nullptr;
+      auto after = [&](const char* name, int st) {  // MGS_TRACE: serialise + name the kernel that hangs/faults
+        if (trace) {
+          cudaError_t e = cudaStreamSynchronize(st_);
+          Ctl hc{};
+          cudaMemcpy(&hc, a.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost);
+          const StepCounters& q = hc.sc[st & 1];
+          std::fprintf(stderr,
+                       "trace step %d %s -> %s | err %d units %d T %d its %d itb %d big %d small %d kids %d tk %d tk2 %d"
+                       " store %d/%d groups %d/%d alive %d/%d out %d/%d scan %d %d %d %d %d %d %d\n",
+                       st, name, cudaGetErrorString(e), hc.err_code, q.n_units, q.T, q.items_s, q.items_b, q.n_big,
+                       q.n_small, q.kids, q.ticket, q.ticket2, hc.n_store[0], hc.n_store[1], hc.n_groups[0],
+                       hc.n_groups[1], hc.alive_now[0], hc.alive_now[1], hc.out_total[0], hc.out_total[1],
+                       hc.scan_total[0], hc.scan_total[1], hc.scan_total[2], hc.scan_total[3], hc.scan_total[4],
+                       hc.scan_total[5], hc.scan_total[6]);
+        }
+        mark();
+      };
       for (int st = 0; st < S; ++st) {
         kunits<<<g_units, kThreads, 0, st_>>>(d_args, st);
-        mark();
+        after("units", st);
         k_scans<<<g_scans, kThreads, 0, st_>>>(d_args, st);
-        mark();
+        after("scans", st);
         k_place<<<g_place, kThreads, 0, st_>>>(d_args, st);
-        mark();
+        after("place", st);
         k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(d_args, st);
-        mark();
+        after("ranks_big", st);
         k_ranks_small<<<g_rsmall, kThreads, 0, st_>>>(d_args, st);
-        mark();
+        after("ranks_small", st);
         ktbig<<<g_tbig, kThreads, smem_trans, st_>>>(d_args, st);
-        mark();
+        after("trans_big", st);
         ktsmall<<<g_tsmall, kThreads, 0, st_>>>(d_args, st);
-        mark();
+        after("trans_small", st);
         k_band<<<g_band, kThreads, smem_merge, st_>>>(d_args, st);
-        mark();
+        after("band", st);
         k_outscan<<<g_oscan, kThreads, 0, st_>>>(d_args, st);
-        mark();
+        after("outscan", st);
         k_write<<<g_write, kThreads, 0, st_>>>(d_args, st);
-        mark();
+        after("write", st);
         k_dom<<<g_dom, kThreads, 0, st_>>>(d_args, st);
-        mark();
+        after("dom", st);
       }
       k_term1<<<grid, kThreads, 0, st_>>>(d_args);
       k_term2<<<grid, kThreads, 0, st_>>>(d_args);

@@ -420,41 +420,57 @@ void build_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, DevSpace& s
 // precheck_scenario (solvers.hpp:27-69) over the device-built signature
 // histogram. Messages follow the reference text with "<m>" standing in for
 // the model name (the C++ drop-in re-renders them with names).
-void precheck_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, const DevSpace& sp) {
+// precheck_scenario (solvers.hpp:27-69): every violation in the reference's
+// order as (status code, model or -1).
+std::vector<std::pair<int, int>> collect_violations(Ctx& c, const mgs_lattice& lat, const Prepared& pr,
+                                                    const DevSpace& sp) {
   const HostTables& t = pr.t;
+  std::vector<std::pair<int, int>> out;
   for (int m = 0; m < t.M; ++m) {
     bool anchor = false;
     for (int i = 0; i < lat.slot_offset[lat.n_configs]; ++i)
       if (lat.slot_size[i] >= t.floor_[m]) anchor = true;
-    if (!anchor)
-      throw PlanFail{MGS_ERR_DEPLOYMENT_FLOOR,
-                     "deployment-floor unsatisfiable: no catalog instance reaches " + std::to_string(t.floor_[m]) +
-                         " GPCs for model <" + std::to_string(m) + ">",
-                     0, 0, m};
-    if (t.min_rt[m] < 0)
-      throw PlanFail{MGS_ERR_RETRAINING_WINDOW,
-                     "model <" + std::to_string(m) + ">: every retraining time exceeds the window (" +
-                         std::to_string(t.S) + " steps)",
-                     0, 0, m};
+    if (!anchor) {
+      out.push_back({MGS_ERR_DEPLOYMENT_FLOOR, m});
+      continue;
+    }
+    if (t.min_rt[m] < 0) out.push_back({MGS_ERR_RETRAINING_WINDOW, m});
   }
+  if (!out.empty()) return out;
   std::vector<int32_t> nopt(sp.n_sig, 0);
   if (sp.n_opt > 0) {
     MGS_CUDA_OK(cudaMemcpyAsync(nopt.data(), sp.sig_nopt, sp.n_sig * 4, cudaMemcpyDeviceToHost, c.stream));
     MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
   }
-  if (nopt[0] == 0)
-    throw PlanFail{MGS_ERR_DEPLOYMENT_FLOOR,
-                   "deployment-floor unsatisfiable: no configuration deploys every inference task simultaneously"};
+  if (nopt[0] == 0) {
+    out.push_back({MGS_ERR_DEPLOYMENT_FLOOR, -1});
+    return out;
+  }
   for (int m = 0; m < t.M; ++m) {
     bool co = false;
     for (int s = 0; s < sp.n_sig; ++s)
       if (nopt[s] > 0 && ((s >> (3 * m)) & 7)) co = true;
-    if (!co)
-      throw PlanFail{MGS_ERR_NO_COEXISTENCE,
-                     "no-coexistence-configuration: no configuration runs <" + std::to_string(m) +
-                         ">:r alongside every inference task",
-                     0, 0, m};
+    if (!co) out.push_back({MGS_ERR_NO_COEXISTENCE, m});
   }
+  return out;
+}
+
+void precheck_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, const DevSpace& sp) {
+  const auto v = collect_violations(c, lat, pr, sp);
+  if (v.empty()) return;
+  const int code = v.front().first, m = v.front().second;
+  const std::string who = "<" + std::to_string(m) + ">";
+  std::string msg;
+  if (code == MGS_ERR_DEPLOYMENT_FLOOR && m >= 0)
+    msg = "deployment-floor unsatisfiable: no catalog instance reaches " + std::to_string(pr.t.floor_[m]) +
+          " GPCs for model " + who;
+  else if (code == MGS_ERR_DEPLOYMENT_FLOOR)
+    msg = "deployment-floor unsatisfiable: no configuration deploys every inference task simultaneously";
+  else if (code == MGS_ERR_RETRAINING_WINDOW)
+    msg = "model " + who + ": every retraining time exceeds the window (" + std::to_string(pr.t.S) + " steps)";
+  else
+    msg = "no-coexistence-configuration: no configuration runs " + who + ":r alongside every inference task";
+  throw PlanFail{code, msg, 0, 0, m};
 }
 
 }  // namespace mgs

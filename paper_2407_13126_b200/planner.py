@@ -90,6 +90,33 @@ class Planner:
             raise capi.PlannerError(st, err)
         return opt, cfg, lab, obj.value, stats.as_dict()
 
+    # -- precheck_scenario -------------------------------------------------------
+    def precheck(self, problem: Problem):
+        """All violations as [(code string, model or -1)], reference order."""
+        out = (capi.mgs_violation * 16)()
+        n = C.c_int32()
+        err = capi.empty_error()
+        st = self.lib.mgs_precheck(self.h, C.byref(problem.c.lattice), C.byref(problem.c.tables), out, 16,
+                                   C.byref(n), C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        return [(capi.STATUS_CODES[out[i].code], out[i].model) for i in range(min(n.value, 16))]
+
+    # -- solve_bruteforce -------------------------------------------------------
+    def solve_bruteforce(self, problem: Problem, bruteforce_cap: float = 5e7):
+        """Returns (options[S], config[S], labels[S][8], objective)."""
+        S = problem.S
+        opt = np.zeros(S, np.int32)
+        cfg = np.zeros(S, np.int32)
+        lab = np.zeros((S, capi.MAX_SLOTS), np.int8)
+        obj = C.c_double()
+        err = capi.empty_error()
+        st = self.lib.mgs_bruteforce(self.h, problem.byref(), float(bruteforce_cap), capi.ptr(opt, C.c_int32),
+                                     capi.ptr(cfg, C.c_int32), capi.ptr(lab, C.c_int8), C.byref(obj), C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        return opt, cfg, lab, obj.value
+
     def solve_batch(self, problems):
         n = len(problems)
         s_max = max(p.S for p in problems)

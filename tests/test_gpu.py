@@ -178,3 +178,41 @@ def test_deterministic_repeat(gpu, golden_dir):
     a = gpu_solve(gpu, path)
     b = gpu_solve(gpu, path)
     assert a[2] == b[2] and bits(a[3]) == bits(b[3])
+
+
+def test_bruteforce_matches_reference(gpu, golden_dir):
+    """solve_bruteforce on the GPU == the reference's DFS (plan and objective bits),
+    cold and chained, on the whole random corpus."""
+    for stem, path, g in golden_dir["random"]:
+        sc = SC.load_scenario(path)
+        for initial, want in ((None, g["bf"]), ([tuple(x) for x in g["chain"]["initial"]], g["chain"]["bf"])):
+            p = SC.Problem(sc, 0, initial=initial)
+            if "error" in want:
+                with pytest.raises(capi.PlannerError) as e:
+                    gpu.solve_bruteforce(p)
+                assert e.value.code == want["error"], stem
+                continue
+            opt, cfg, lab, obj = gpu.solve_bruteforce(p)
+            assert planner.encode(cfg, lab, nslots(sc)) == want["encode"], stem
+            assert bits(obj) == want["obj"], stem
+
+
+def test_bruteforce_cap_and_errors(gpu, golden_dir):
+    kat = {stem: (path, g) for stem, path, g in golden_dir["kat"]}
+    p = SC.Problem(SC.load_scenario(kat["small_two_model"][0]), 0)
+    with pytest.raises(capi.PlannerError) as e:
+        gpu.solve_bruteforce(p, bruteforce_cap=10.0)
+    assert e.value.code == "planner.bruteforce-cap"
+    assert e.value.message.startswith("brute-force space estimate ")
+    p = SC.Problem(SC.load_scenario(kat["worked_example"][0]), 0)
+    opt, cfg, lab, obj = gpu.solve_bruteforce(p)
+    assert obj == 12.5
+    for name in ("no_coexistence", "deployment_floor"):
+        p = SC.Problem(SC.load_scenario(kat[name][0]), 0)
+        with pytest.raises(capi.PlannerError) as e:
+            gpu.solve_bruteforce(p)
+        assert e.value.code == kat[name][1]["expect_error"]
+        v = gpu.precheck(p)
+        assert v and "infeasible." + v[0][0].split(".", 1)[1] == kat[name][1]["expect_error"]
+    p = SC.Problem(SC.load_scenario(kat["worked_example"][0]), 0)
+    assert gpu.precheck(p) == []
