@@ -38,6 +38,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include <cub/block/block_radix_sort.cuh>
 
@@ -150,6 +151,11 @@ struct V2 {
   long long* dbg;                // [S][6] per-step counters (debug dump)
   unsigned long long* dbg_time;  // barrier timestamps (debug)
 };
+
+// Per-solve argument block (uploaded before each window; see solve_dp_v2).
+// (raw bytes: V2 has default member initialisers, which __constant__ forbids)
+__constant__ alignas(16) unsigned char c_v2_raw[sizeof(V2)];
+#define c_v2 (*reinterpret_cast<const V2*>(c_v2_raw))
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
@@ -1156,16 +1162,16 @@ __device__ void phase_dominance(const V2& a, int s) {
 // Phase kernels: one launch per phase and slot, stream-ordered, all counts on
 // the device (the host never waits inside a window).
 template <int M>
-__global__ void __launch_bounds__(kThreads) k_units(const V2* __restrict__ ap, int s) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads) k_units(int s) {
+  const V2& a = c_v2;
   __shared__ int s_cnt[kBatch];
   __shared__ long long s_red[32];
   if (failed(a)) return;
   phase_units<M>(a, s, 0, s_cnt, s_red);
 }
 
-__global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, int s) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads) k_scans(int s) {
+  const V2& a = c_v2;
   if (failed(a)) return;
   const int cur = s & 1;
   Ctl* ctl = a.ctl;
@@ -1190,8 +1196,8 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
   multi_scan(a, jobs, kNumScans, 2 * (s + 1), &sc.ticket, ctl->scan_total);
 }
 
-__global__ void __launch_bounds__(kThreads) k_place(const V2* __restrict__ ap, int s) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads) k_place(int s) {
+  const V2& a = c_v2;
   if (failed(a)) return;
   Ctl* ctl = a.ctl;
   StepCounters& sc = ctl->sc[s & 1];
@@ -1213,22 +1219,22 @@ __global__ void __launch_bounds__(kThreads) k_place(const V2* __restrict__ ap, i
   if (fits) phase_place(a, s);
 }
 
-__global__ void __launch_bounds__(kThreads) k_ranks_big(const V2* __restrict__ ap, int s) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads) k_ranks_big(int s) {
+  const V2& a = c_v2;
   extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
   phase_ranks_big(a, s, smem_u64);
 }
 
-__global__ void __launch_bounds__(kThreads) k_ranks_small(const V2* __restrict__ ap, int s) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads) k_ranks_small(int s) {
+  const V2& a = c_v2;
   if (failed(a)) return;
   phase_ranks_small(a, s);
 }
 
 template <int M>
-__global__ void __launch_bounds__(kThreads) k_trans_big(const V2* __restrict__ ap, int s) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads) k_trans_big(int s) {
+  const V2& a = c_v2;
   extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
   if (static_cast<int>(blockIdx.x) >= a.ctl->sc[s & 1].items_b) return;  // no item for this CTA
@@ -1245,8 +1251,8 @@ __global__ void __launch_bounds__(kThreads) k_trans_big(const V2* __restrict__ a
 }
 
 template <int M>
-__global__ void __launch_bounds__(kThreads, 4) k_trans_small(const V2* __restrict__ ap, int s) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads, 4) k_trans_small(int s) {
+  const V2& a = c_v2;
   if (failed(a)) return;
   phase_trans_small<M>(a, s);
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // counters of the next step
@@ -1256,23 +1262,23 @@ __global__ void __launch_bounds__(kThreads, 4) k_trans_small(const V2* __restric
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_band(const V2* __restrict__ ap, int s) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads) k_band(int s) {
+  const V2& a = c_v2;
   extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
   phase_band(a, s, smem_u64, smem_u64 + a.merge_win);
 }
 
-__global__ void __launch_bounds__(kThreads) k_outscan(const V2* __restrict__ ap, int s) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads) k_outscan(int s) {
+  const V2& a = c_v2;
   if (failed(a)) return;
   const int H = a.hmask + 1;
   const ScanJob jobs[2] = {{a.ns_out, nullptr, a.ns_obase, H, 0}, {a.ns_out, nullptr, a.ns_gbase, H, 3}};
   multi_scan(a, jobs, 2, 2 * (s + 1) + 1, &a.ctl->sc[s & 1].ticket2, a.ctl->out_total);
 }
 
-__global__ void __launch_bounds__(kThreads) k_write(const V2* __restrict__ ap, int s) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads) k_write(int s) {
+  const V2& a = c_v2;
   if (failed(a)) return;
   const int nxt = (s + 1) & 1;
   Ctl* ctl = a.ctl;
@@ -1288,8 +1294,8 @@ __global__ void __launch_bounds__(kThreads) k_write(const V2* __restrict__ ap, i
   if (fits) phase_write(a, s);
 }
 
-__global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int s) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads) k_dom(int s) {
+  const V2& a = c_v2;
   if (failed(a)) return;
   const int cur = s & 1;
   Ctl* ctl = a.ctl;
@@ -1332,8 +1338,8 @@ __device__ __forceinline__ uint32_t all_done_key(int M) {
   return k;
 }
 
-__global__ void __launch_bounds__(kThreads) k_term1(const V2* __restrict__ ap) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads) k_term1() {
+  const V2& a = c_v2;
   __shared__ long long s_red[32];
   if (failed(a)) return;
   const int fin = a.S & 1;
@@ -1358,8 +1364,8 @@ __global__ void __launch_bounds__(kThreads) k_term1(const V2* __restrict__ ap) {
   if (any) atomicMax(&a.ctl->best_vb, mv + 1);  // +1: 0 = none
 }
 
-__global__ void __launch_bounds__(kThreads) k_term2(const V2* __restrict__ ap) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads) k_term2() {
+  const V2& a = c_v2;
   if (failed(a)) return;
   const int fin = a.S & 1;
   const FrontierV2& F = a.f[fin];
@@ -1379,8 +1385,8 @@ __global__ void __launch_bounds__(kThreads) k_term2(const V2* __restrict__ ap) {
     if (F.alive[i] && F.status[i] == all_done && vbits(F.value[i]) + 1 == bvb) atomicMin(&a.ctl->best_lex, F.lex[i]);
 }
 
-__global__ void __launch_bounds__(kThreads) k_term3(const V2* __restrict__ ap) {
-  const V2& a = *ap;
+__global__ void __launch_bounds__(kThreads) k_term3() {
+  const V2& a = c_v2;
   if (failed(a)) return;
   const int fin = a.S & 1;
   const FrontierV2& F = a.f[fin];
@@ -1392,8 +1398,8 @@ __global__ void __launch_bounds__(kThreads) k_term3(const V2* __restrict__ ap) {
     if (F.alive[i] && F.status[i] == all_done && vbits(F.value[i]) + 1 == bvb && F.lex[i] == blx) a.ctl->best_idx = i;
 }
 
-__global__ void k_backtrack2(const V2* __restrict__ ap) {
-  const V2& a = *ap;  // parent walk (solvers.hpp:567-574)
+__global__ void k_backtrack2() {
+  const V2& a = c_v2;  // parent walk (solvers.hpp:567-574)
   if (failed(a) || threadIdx.x != 0 || blockIdx.x != 0) return;
   int idx = a.ctl->best_idx;
   for (int s = a.S - 1; s >= 0; --s) {
@@ -1403,8 +1409,8 @@ __global__ void k_backtrack2(const V2* __restrict__ ap) {
   }
 }
 
-__global__ void k_init_root(const V2* __restrict__ ap, uint32_t root_pid) {
-  const V2& a = *ap;
+__global__ void k_init_root(uint32_t root_pid) {
+  const V2& a = c_v2;
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   FrontierV2 F = a.f[0];
   F.status[0] = 0;
@@ -1452,6 +1458,10 @@ bool solve_dp_v2_supported(const Prepared& pr, const DevSpace& sp) {
 
 void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& sp, const double* d_recv,
                  const double* d_ub, const double* d_incumbent, SolveOut& out) {
+  // c_v2 is one constant-memory block per process: windows solved from
+  // several host threads are serialised here (each solve is synchronous).
+  static std::mutex v2_mutex;
+  std::lock_guard<std::mutex> lock(v2_mutex);
   const HostTables& t = pr.t;
   const int M = t.M, S = t.S;
   double acc_max[KM] = {0, 0, 0, 0};
@@ -1485,6 +1495,8 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
   auto wave = [&](const void* k, size_t dyn) {
     int occ = 0;
     MGS_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, dyn));
+    static const int cap = std::getenv("MGS_GRID_CAP") ? std::atoi(std::getenv("MGS_GRID_CAP")) : 0;  // tuning probe
+    if (cap > 0) occ = std::min(occ, cap);
     return c.sm_count * std::max(1, occ);
   };
   const int grid = c.sm_count * 8;
@@ -1608,9 +1620,10 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
     a.merge_win = merge_win;
     a.oi_bits = 1;
     while ((1ll << a.oi_bits) < sp.n_opt) ++a.oi_bits;
-    V2* d_args = c.buf<V2>("v2_args", 1);
-    MGS_CUDA_OK(cudaMemcpyAsync(d_args, &a, sizeof(V2), cudaMemcpyHostToDevice, c.stream));
-    k_init_root<<<1, 32, 0, c.stream>>>(d_args, static_cast<uint32_t>(sp.root_pid));
+    // the argument block lives in constant memory: every kernel reads its
+    // fields through the constant cache instead of chasing a global pointer
+    MGS_CUDA_OK(cudaMemcpyToSymbolAsync(c_v2_raw, &a, sizeof(V2), 0, cudaMemcpyHostToDevice, c.stream));
+    k_init_root<<<1, 32, 0, c.stream>>>(static_cast<uint32_t>(sp.root_pid));
     ++c.kernel_launches;
     // The window's kernel sequence depends only on S, M and launch shapes (all
     // problem data lives behind d_args), so it is captured once into a CUDA
@@ -1647,33 +1660,33 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
         mark();
       };
       for (int st = 0; st < S; ++st) {
-        kunits<<<g_units, kThreads, 0, st_>>>(d_args, st);
+        kunits<<<g_units, kThreads, 0, st_>>>(st);
         after("units", st);
-        k_scans<<<g_scans, kThreads, 0, st_>>>(d_args, st);
+        k_scans<<<g_scans, kThreads, 0, st_>>>(st);
         after("scans", st);
-        k_place<<<g_place, kThreads, 0, st_>>>(d_args, st);
+        k_place<<<g_place, kThreads, 0, st_>>>(st);
         after("place", st);
-        k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(d_args, st);
+        k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(st);
         after("ranks_big", st);
-        k_ranks_small<<<g_rsmall, kThreads, 0, st_>>>(d_args, st);
+        k_ranks_small<<<g_rsmall, kThreads, 0, st_>>>(st);
         after("ranks_small", st);
-        ktbig<<<g_tbig, kThreads, smem_trans, st_>>>(d_args, st);
+        ktbig<<<g_tbig, kThreads, smem_trans, st_>>>(st);
         after("trans_big", st);
-        ktsmall<<<g_tsmall, kThreads, 0, st_>>>(d_args, st);
+        ktsmall<<<g_tsmall, kThreads, 0, st_>>>(st);
         after("trans_small", st);
-        k_band<<<g_band, kThreads, smem_merge, st_>>>(d_args, st);
+        k_band<<<g_band, kThreads, smem_merge, st_>>>(st);
         after("band", st);
-        k_outscan<<<g_oscan, kThreads, 0, st_>>>(d_args, st);
+        k_outscan<<<g_oscan, kThreads, 0, st_>>>(st);
         after("outscan", st);
-        k_write<<<g_write, kThreads, 0, st_>>>(d_args, st);
+        k_write<<<g_write, kThreads, 0, st_>>>(st);
         after("write", st);
-        k_dom<<<g_dom, kThreads, 0, st_>>>(d_args, st);
+        k_dom<<<g_dom, kThreads, 0, st_>>>(st);
         after("dom", st);
       }
-      k_term1<<<grid, kThreads, 0, st_>>>(d_args);
-      k_term2<<<grid, kThreads, 0, st_>>>(d_args);
-      k_term3<<<grid, kThreads, 0, st_>>>(d_args);
-      k_backtrack2<<<1, 32, 0, st_>>>(d_args);
+      k_term1<<<grid, kThreads, 0, st_>>>();
+      k_term2<<<grid, kThreads, 0, st_>>>();
+      k_term3<<<grid, kThreads, 0, st_>>>();
+      k_backtrack2<<<1, 32, 0, st_>>>();
     };
     c.kernel_launches += 11ull * S + 4;
     if (debug) {
@@ -1689,13 +1702,14 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
         acc[(i - 1) % kK] += ms;
       }
       for (auto e : evs) cudaEventDestroy(e);
+      std::fprintf(stderr, "v2 caps: fcap %d gcap %d ucap %d itcap %d ccap %d hbits %d hcap %lld\n", caps.fcap, caps.gcap,
+                   caps.ucap, caps.itcap, caps.ccap, caps.hbits, caps.hcap);
       std::fprintf(stderr, "v2 in-stream ms per window:");
       for (int k = 0; k < kK; ++k) std::fprintf(stderr, " %s %.2f", kNames[k], acc[k]);
       std::fprintf(stderr, "\n");
     } else {
       char key[256];
-      std::snprintf(key, sizeof key, "v2:%d:%d:%zu:%zu:%zu:%p", S, M, smem_trans, smem_merge, smem_rank,
-                    static_cast<void*>(d_args));
+      std::snprintf(key, sizeof key, "v2:%d:%d:%zu:%zu:%zu", S, M, smem_trans, smem_merge, smem_rank);
       auto it = c.graphs.find(key);
       if (it == c.graphs.end()) {
         cudaStream_t cap;
