@@ -104,10 +104,11 @@ def load():
     global _LIB
     if _LIB is not None:
         return _LIB
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("MGS_LIB_PATH", LIB_PATH)  # A/B builds of the same library
+    if not os.path.exists(path):
         raise RuntimeError("CUDA extension %s is missing: run __graft_entry__.build() (no CPU fallback exists)"
-                           % LIB_PATH)
-    lib = C.CDLL(LIB_PATH)
+                           % path)
+    lib = C.CDLL(path)
     P = C.POINTER
     lib.mgs_open.argtypes = [C.c_int, P(C.c_void_p)]
     lib.mgs_close.argtypes = [C.c_void_p]

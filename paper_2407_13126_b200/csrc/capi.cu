@@ -2,6 +2,7 @@
 // Every entry point catches planner / CUDA failures and maps them to the
 // reference's error codes; nothing here falls back to a CPU computation.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <new>
 
@@ -338,17 +339,116 @@ int mgs_solve_batch(mgs_ctx* ctx, const mgs_problem* problems, int32_t n, int32_
                     double* out_objective, int32_t* status, mgs_stats* stats, mgs_error* errs) {
   if (!ctx || (!problems && n > 0) || n < 0) return MGS_ERR_ARGUMENT;
   return guarded(nullptr, [&] {
-    MGS_CUDA_OK(cudaSetDevice(ctx->c.device));
-    for (int i = 0; i < n; ++i) {
-      mgs_error e{};
-      int st = guarded(&e, [&] {
-        if (problems[i].tables.steps > s_max) throw PlanFail{MGS_ERR_ARGUMENT, "window longer than s_max"};
-        solve_one(ctx->c, problems[i], out_option ? out_option + static_cast<size_t>(i) * s_max : nullptr, nullptr,
-                  nullptr, out_objective ? out_objective + i : nullptr, stats ? stats + i : nullptr);
-      });
+    Ctx& c = ctx->c;
+    MGS_CUDA_OK(cudaSetDevice(c.device));
+    // Windows of equal shape (S, M <= 2) are solved together: up to
+    // MGS_BATCH_LANES of them share every DP kernel launch (grid.y = lane).
+    const char* env = std::getenv("MGS_BATCH_LANES");
+    const int max_lanes = std::max(1, std::min(mgs::kMaxLanes, env ? std::atoi(env) : 8));
+    struct Prep {
+      int i;
+      mgs::Prepared pr;
+      mgs::DevSpace sp;
+      double *recv, *ub, *inc;
+    };
+    std::vector<Prep> group;
+    group.reserve(max_lanes);
+    auto set_err = [&](int i, int st, const mgs_error& e) {
       if (status) status[i] = st;
       if (errs) errs[i] = e;
+    };
+    auto flush = [&]() {
+      if (group.empty()) return;
+      MGS_CUDA_OK(cudaEventRecord(c.ev0, c.stream));
+      std::vector<mgs::V2Lane> lanes(group.size());
+      for (size_t k = 0; k < group.size(); ++k) {
+        mgs::V2Lane& L = lanes[k];
+        L.p = &problems[group[k].i];
+        L.pr = &group[k].pr;
+        L.sp = &group[k].sp;
+        L.recv = group[k].recv;
+        L.ub = group[k].ub;
+        L.incumbent = group[k].inc;
+        L.prefix = "L" + std::to_string(k) + "/";
+      }
+      mgs::solve_dp_v2_lanes(c, lanes);
+      MGS_CUDA_OK(cudaEventRecord(c.ev1, c.stream));
+      MGS_CUDA_OK(cudaEventSynchronize(c.ev1));
+      float ms = 0.f;
+      MGS_CUDA_OK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+      for (size_t k = 0; k < group.size(); ++k) {
+        const int i = group[k].i;
+        mgs_error e{};
+        const mgs::V2Lane& L = lanes[k];
+        if (L.status != MGS_OK) {
+          fill_err(&e, L.status, L.msg, L.err_step, L.err_count);
+          set_err(i, L.status, e);
+          continue;
+        }
+        c.prefix = L.prefix;
+        const double total = plan_total(c, group[k].pr, group[k].sp, L.out.options);
+        c.prefix.clear();
+        const int S = group[k].pr.t.S;
+        if (out_option)
+          for (int s = 0; s < S; ++s) out_option[static_cast<size_t>(i) * s_max + s] = L.out.options[s];
+        if (out_objective) out_objective[i] = total;
+        if (stats) {
+          stats[i] = L.out.stats;
+          stats[i].device_ms = ms;  // the whole batch's device time (shared by its windows)
+          for (double& x : stats[i].phase_ms) x = 0.0;
+          stats[i].phase_ms[3] = ms;
+        }
+        set_err(i, MGS_OK, e);
+      }
+      group.clear();
+    };
+    for (int i = 0; i < n; ++i) {
+      mgs_error e{};
+      const int k = static_cast<int>(group.size());
+      c.prefix = "L" + std::to_string(k) + "/";
+      Prep pp{};
+      pp.i = i;
+      bool lane_ok = false;
+      int st = guarded(&e, [&] {
+        const mgs_problem& p = problems[i];
+        if (p.tables.steps > s_max) throw PlanFail{MGS_ERR_ARGUMENT, "window longer than s_max"};
+        pp.pr = prepare_problem(p);
+        mgs::build_space(c, p.lattice, pp.pr, pp.sp);
+        mgs::precheck_space(c, p.lattice, pp.pr, pp.sp);
+        const int M = pp.pr.t.M, S = pp.pr.t.S;
+        if (p.forecast_len != S) throw PlanFail{MGS_ERR_INPUT_FORECAST, "forecast horizon != window size"};
+        if (!mgs::solve_dp_v2_supported(pp.pr, pp.sp)) return;
+        pp.recv = upload_forecast(c, p, M, S);
+        pp.ub = c.buf<double>("ub_suffix", S + 1);
+        pp.inc = c.buf<double>("incumbent", 1);
+        int32_t* d_greedy = c.buf<int32_t>("greedy", S);
+        mgs::goodput_reductions(c, pp.pr, pp.sp, pp.recv, pp.ub, pp.inc, d_greedy);
+        lane_ok = true;
+      });
+      c.prefix.clear();
+      if (st != MGS_OK) {
+        set_err(i, st, e);
+        continue;
+      }
+      if (!lane_ok) {  // M > 2: the multi-launch engine, one window at a time
+        st = guarded(&e, [&] {
+          solve_one(c, problems[i], out_option ? out_option + static_cast<size_t>(i) * s_max : nullptr, nullptr,
+                    nullptr, out_objective ? out_objective + i : nullptr, stats ? stats + i : nullptr);
+        });
+        set_err(i, st, e);
+        continue;
+      }
+      if (!group.empty() && (group[0].pr.t.S != pp.pr.t.S || group[0].pr.t.M != pp.pr.t.M)) {
+        // shape change: this window was prepared under lane k's prefix, which
+        // the current group owns -> flush, then re-prepare it as lane 0
+        flush();
+        --i;
+        continue;
+      }
+      group.push_back(std::move(pp));
+      if (static_cast<int>(group.size()) == max_lanes) flush();
     }
+    flush();
   });
 }
 

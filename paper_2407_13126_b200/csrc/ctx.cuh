@@ -164,9 +164,12 @@ struct Ctx {
   History history;
   std::map<std::string, cudaGraphExec_t> graphs;  // cached per-window kernel sequences
 
+  // Buffer names are looked up under `prefix`: a batched solve sets a
+  // per-lane prefix so every lane owns a disjoint set of scratch buffers.
+  std::string prefix;
   template <class T>
   T* buf(const char* name, size_t n) {
-    return bufs[name].get<T>(n);
+    return bufs[prefix + name].get<T>(n);
   }
   ~Ctx() {
     for (auto& kv : bufs) kv.second.release();
@@ -207,6 +210,25 @@ struct SolveOut {
 };
 void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& sp, const double* d_recv,
               const double* d_ub, const double* d_incumbent, SolveOut& out);
+// dp2.cu: the device-resident engine (M <= 2); several independent windows of
+// equal shape ("lanes") run in the same kernels (grid.y = lane).
+constexpr int kMaxLanes = 16;
+struct V2Lane {
+  const mgs_problem* p = nullptr;
+  const Prepared* pr = nullptr;
+  const DevSpace* sp = nullptr;
+  const double* recv = nullptr;
+  const double* ub = nullptr;
+  const double* incumbent = nullptr;
+  std::string prefix;  // the lane's buffer-name prefix
+  SolveOut out;
+  int status = 0;      // mgs_status of this lane
+  std::string msg;
+  int err_step = 0;
+  uint64_t err_count = 0;
+};
+bool solve_dp_v2_supported(const Prepared& pr, const DevSpace& sp);
+void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes);
 
 // small device helpers (scan.cu)
 void exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int n);  // out has n+1 entries

@@ -38,7 +38,6 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
-#include <mutex>
 
 #include <cub/block/block_radix_sort.cuh>
 
@@ -152,10 +151,9 @@ struct V2 {
   unsigned long long* dbg_time;  // barrier timestamps (debug)
 };
 
-// Per-solve argument block (uploaded before each window; see solve_dp_v2).
-// (raw bytes: V2 has default member initialisers, which __constant__ forbids)
-__constant__ alignas(16) unsigned char c_v2_raw[sizeof(V2)];
-#define c_v2 (*reinterpret_cast<const V2*>(c_v2_raw))
+// Per-solve argument blocks, one per lane, device-resident (uploaded before
+// each window; see solve_dp_v2_lanes). grid.y selects the lane.
+#define c_v2 (ap[blockIdx.y])
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
@@ -1162,7 +1160,7 @@ __device__ void phase_dominance(const V2& a, int s) {
 // Phase kernels: one launch per phase and slot, stream-ordered, all counts on
 // the device (the host never waits inside a window).
 template <int M>
-__global__ void __launch_bounds__(kThreads) k_units(int s) {
+__global__ void __launch_bounds__(kThreads) k_units(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   __shared__ int s_cnt[kBatch];
   __shared__ long long s_red[32];
@@ -1170,7 +1168,7 @@ __global__ void __launch_bounds__(kThreads) k_units(int s) {
   phase_units<M>(a, s, 0, s_cnt, s_red);
 }
 
-__global__ void __launch_bounds__(kThreads) k_scans(int s) {
+__global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (failed(a)) return;
   const int cur = s & 1;
@@ -1196,7 +1194,7 @@ __global__ void __launch_bounds__(kThreads) k_scans(int s) {
   multi_scan(a, jobs, kNumScans, 2 * (s + 1), &sc.ticket, ctl->scan_total);
 }
 
-__global__ void __launch_bounds__(kThreads) k_place(int s) {
+__global__ void __launch_bounds__(kThreads) k_place(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (failed(a)) return;
   Ctl* ctl = a.ctl;
@@ -1219,21 +1217,21 @@ __global__ void __launch_bounds__(kThreads) k_place(int s) {
   if (fits) phase_place(a, s);
 }
 
-__global__ void __launch_bounds__(kThreads) k_ranks_big(int s) {
+__global__ void __launch_bounds__(kThreads) k_ranks_big(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
   phase_ranks_big(a, s, smem_u64);
 }
 
-__global__ void __launch_bounds__(kThreads) k_ranks_small(int s) {
+__global__ void __launch_bounds__(kThreads) k_ranks_small(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (failed(a)) return;
   phase_ranks_small(a, s);
 }
 
 template <int M>
-__global__ void __launch_bounds__(kThreads) k_trans_big(int s) {
+__global__ void __launch_bounds__(kThreads) k_trans_big(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
@@ -1251,7 +1249,7 @@ __global__ void __launch_bounds__(kThreads) k_trans_big(int s) {
 }
 
 template <int M>
-__global__ void __launch_bounds__(kThreads, 4) k_trans_small(int s) {
+__global__ void __launch_bounds__(kThreads, 4) k_trans_small(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (failed(a)) return;
   phase_trans_small<M>(a, s);
@@ -1262,14 +1260,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_trans_small(int s) {
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_band(int s) {
+__global__ void __launch_bounds__(kThreads) k_band(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
   phase_band(a, s, smem_u64, smem_u64 + a.merge_win);
 }
 
-__global__ void __launch_bounds__(kThreads) k_outscan(int s) {
+__global__ void __launch_bounds__(kThreads) k_outscan(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (failed(a)) return;
   const int H = a.hmask + 1;
@@ -1277,7 +1275,7 @@ __global__ void __launch_bounds__(kThreads) k_outscan(int s) {
   multi_scan(a, jobs, 2, 2 * (s + 1) + 1, &a.ctl->sc[s & 1].ticket2, a.ctl->out_total);
 }
 
-__global__ void __launch_bounds__(kThreads) k_write(int s) {
+__global__ void __launch_bounds__(kThreads) k_write(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (failed(a)) return;
   const int nxt = (s + 1) & 1;
@@ -1294,7 +1292,7 @@ __global__ void __launch_bounds__(kThreads) k_write(int s) {
   if (fits) phase_write(a, s);
 }
 
-__global__ void __launch_bounds__(kThreads) k_dom(int s) {
+__global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (failed(a)) return;
   const int cur = s & 1;
@@ -1338,7 +1336,7 @@ __device__ __forceinline__ uint32_t all_done_key(int M) {
   return k;
 }
 
-__global__ void __launch_bounds__(kThreads) k_term1() {
+__global__ void __launch_bounds__(kThreads) k_term1(const V2* __restrict__ ap) {
   const V2& a = c_v2;
   __shared__ long long s_red[32];
   if (failed(a)) return;
@@ -1364,7 +1362,7 @@ __global__ void __launch_bounds__(kThreads) k_term1() {
   if (any) atomicMax(&a.ctl->best_vb, mv + 1);  // +1: 0 = none
 }
 
-__global__ void __launch_bounds__(kThreads) k_term2() {
+__global__ void __launch_bounds__(kThreads) k_term2(const V2* __restrict__ ap) {
   const V2& a = c_v2;
   if (failed(a)) return;
   const int fin = a.S & 1;
@@ -1385,7 +1383,7 @@ __global__ void __launch_bounds__(kThreads) k_term2() {
     if (F.alive[i] && F.status[i] == all_done && vbits(F.value[i]) + 1 == bvb) atomicMin(&a.ctl->best_lex, F.lex[i]);
 }
 
-__global__ void __launch_bounds__(kThreads) k_term3() {
+__global__ void __launch_bounds__(kThreads) k_term3(const V2* __restrict__ ap) {
   const V2& a = c_v2;
   if (failed(a)) return;
   const int fin = a.S & 1;
@@ -1398,7 +1396,7 @@ __global__ void __launch_bounds__(kThreads) k_term3() {
     if (F.alive[i] && F.status[i] == all_done && vbits(F.value[i]) + 1 == bvb && F.lex[i] == blx) a.ctl->best_idx = i;
 }
 
-__global__ void k_backtrack2() {
+__global__ void k_backtrack2(const V2* __restrict__ ap) {
   const V2& a = c_v2;  // parent walk (solvers.hpp:567-574)
   if (failed(a) || threadIdx.x != 0 || blockIdx.x != 0) return;
   int idx = a.ctl->best_idx;
@@ -1409,9 +1407,10 @@ __global__ void k_backtrack2() {
   }
 }
 
-__global__ void k_init_root(uint32_t root_pid) {
+__global__ void k_init_root(const V2* __restrict__ ap) {
   const V2& a = c_v2;
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int root_pid = a.sp.root_pid;
   FrontierV2 F = a.f[0];
   F.status[0] = 0;
   F.ids[0] = static_cast<uint32_t>(a.sp.pl_ids[root_pid]);
@@ -1456,178 +1455,204 @@ bool solve_dp_v2_supported(const Prepared& pr, const DevSpace& sp) {
   return true;
 }
 
-void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& sp, const double* d_recv,
-                 const double* d_ub, const double* d_incumbent, SolveOut& out) {
-  // c_v2 is one constant-memory block per process: windows solved from
-  // several host threads are serialised here (each solve is synchronous).
-  static std::mutex v2_mutex;
-  std::lock_guard<std::mutex> lock(v2_mutex);
-  const HostTables& t = pr.t;
-  const int M = t.M, S = t.S;
-  double acc_max[KM] = {0, 0, 0, 0};
-  bool dominance_ok = true;
-  for (int m = 0; m < M; ++m) {
-    acc_max[m] = std::max(t.pre[m], t.post[m]);
-    dominance_ok = dominance_ok && t.post[m] >= t.pre[m];
-  }
-  std::vector<double> pc(static_cast<size_t>(sp.P) * KM);
-  MGS_CUDA_OK(cudaMemcpyAsync(pc.data(), sp.pl_cap, pc.size() * 8, cudaMemcpyDeviceToHost, c.stream));
-  MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
-  double cap_max[KM] = {0, 0, 0, 0};
-  for (int q = 0; q < sp.P; ++q)
-    for (int m = 0; m < M; ++m) cap_max[m] = std::max(cap_max[m], pc[q * KM + m]);
-  double band = 1e-9;  // solvers.hpp:266-267
-  for (int m = 0; m < M; ++m) band += t.loss[m] * cap_max[m] * acc_max[m];
 
-  const int n_sub = 1 << M;
-  const int n_partial = sp.proj_base[n_sub - 1];  // all subsets but the full one
-  const size_t smem_trans = static_cast<size_t>(sp.P1) * 8 + static_cast<size_t>(n_partial) * 20;
+namespace {
+
+// Device buffers + scalars of one lane for the current capacities.
+V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, double band, int dominance_ok, int merge_win, int grid_term) {
+  const DevSpace& sp = *L.sp;
+  const HostTables& t = L.pr->t;
+  const int S = t.S;
+  const std::string saved_prefix = c.prefix;
+  c.prefix = L.prefix;
+  V2 a{};
+  a.sp = sp;
+  a.t = t;
+  a.S = S;
+  a.has_initial = L.pr->has_initial;
+  a.dominance_ok = dominance_ok;
+  a.band = band;
+  a.budget = L.p->state_budget;
+  a.recv = L.recv;
+  a.ub = L.ub;
+  a.incumbent = L.incumbent;
+  a.fcap = caps.fcap;
+  a.gcap = caps.gcap;
+  for (int b = 0; b < 2; ++b) {
+    std::string tg = b ? "v2b_" : "v2a_";
+    FrontierV2& f = a.f[b];
+    f.status = c.buf<uint32_t>((tg + "status").c_str(), caps.fcap);
+    f.ids = c.buf<uint32_t>((tg + "ids").c_str(), caps.fcap);
+    f.pid = c.buf<int32_t>((tg + "pid").c_str(), caps.fcap);
+    f.value = c.buf<double>((tg + "value").c_str(), caps.fcap);
+    f.lex = c.buf<uint64_t>((tg + "lex").c_str(), caps.fcap);
+    f.rank = c.buf<uint32_t>((tg + "rank").c_str(), caps.fcap);
+    f.alive = c.buf<uint8_t>((tg + "alive").c_str(), caps.fcap);
+    f.group = c.buf<int32_t>((tg + "group").c_str(), caps.fcap);
+    f.g_start = c.buf<int32_t>((tg + "gstart").c_str(), caps.gcap);
+    f.g_size = c.buf<int32_t>((tg + "gsize").c_str(), caps.gcap);
+    f.g_status = c.buf<uint32_t>((tg + "gstatus").c_str(), caps.gcap);
+    f.g_alive = c.buf<int32_t>((tg + "galive").c_str(), caps.gcap);
+    a.kid_cnt[b] = c.buf<int32_t>((tg + "kidcnt").c_str(), caps.fcap);
+    a.kid_cur[b] = c.buf<int32_t>((tg + "kidcur").c_str(), caps.fcap);
+    MGS_CUDA_OK(cudaMemsetAsync(a.kid_cnt[b], 0, static_cast<size_t>(caps.fcap) * 4, c.stream));
+    MGS_CUDA_OK(cudaMemsetAsync(a.kid_cur[b], 0, static_cast<size_t>(caps.fcap) * 4, c.stream));
+  }
+  a.kid_base = c.buf<int32_t>("v2_kidbase", caps.fcap + 1);
+  a.kid_items = c.buf<uint64_t>("v2_kiditems", caps.fcap);
+  a.kid_pr = c.buf<int32_t>("v2_kidpr", caps.fcap);
+  a.big_bucket = c.buf<int32_t>("v2_bigbucket", caps.fcap);
+  a.hcap = caps.hcap;
+  a.h_parent = c.buf<int32_t>("v2_hparent", caps.hcap);
+  a.h_oi = c.buf<int32_t>("v2_hoi", caps.hcap);
+  a.hist_base = c.buf<long long>("v2_histbase", S + 2);
+  a.ucap = caps.ucap;
+  a.u_group = c.buf<int32_t>("v2_ugroup", caps.ucap);
+  a.u_sig = c.buf<int32_t>("v2_usig", caps.ucap);
+  a.u_ns = c.buf<int32_t>("v2_uns", caps.ucap);
+  a.u_chs = c.buf<int32_t>("v2_uchs", caps.ucap);
+  a.u_chb = c.buf<int32_t>("v2_uchb", caps.ucap);
+  a.u_cbase = c.buf<int32_t>("v2_ucbase", caps.ucap);
+  a.u_sbase = c.buf<int32_t>("v2_usbase", caps.ucap);
+  a.u_bbase = c.buf<int32_t>("v2_ubbase", caps.ucap);
+  a.ns_units = c.buf<int32_t>("v2_nsunits", caps.ucap);
+  a.hmask = (1 << caps.hbits) - 1;
+  const size_t H = static_cast<size_t>(a.hmask) + 1;
+  a.hash = c.buf<uint32_t>("v2_hash", H);
+  a.ns_ucnt = c.buf<int32_t>("v2_nsucnt", H);
+  a.ns_ccnt = c.buf<int32_t>("v2_nsccnt", H);
+  a.ns_ubase = c.buf<int32_t>("v2_nsubase", H);
+  a.ns_cbase = c.buf<int32_t>("v2_nscbase", H);
+  a.ns_ucur = c.buf<int32_t>("v2_nsucur", H);
+  a.ns_ccur = c.buf<int32_t>("v2_nsccur", H);
+  a.ns_bigpos = c.buf<int32_t>("v2_nsbigpos", H);
+  a.ns_smallpos = c.buf<int32_t>("v2_nssmallpos", H);
+  a.ns_out = c.buf<int32_t>("v2_nsout", H);
+  a.ns_obase = c.buf<int32_t>("v2_nsobase", H);
+  a.ns_gbase = c.buf<int32_t>("v2_nsgbase", H);
+  a.ns_big = c.buf<int32_t>("v2_nsbig", H);
+  a.ns_small = c.buf<int32_t>("v2_nssmall", H);
+  for (void* z : {static_cast<void*>(a.hash), static_cast<void*>(a.ns_ucnt), static_cast<void*>(a.ns_ccnt),
+                  static_cast<void*>(a.ns_ucur), static_cast<void*>(a.ns_ccur), static_cast<void*>(a.ns_out)})
+    MGS_CUDA_OK(cudaMemsetAsync(z, 0, H * 4, c.stream));
+  a.itcap = caps.itcap;
+  a.it_s_unit = c.buf<int32_t>("v2_itsu", caps.itcap);
+  a.it_s_chunk = c.buf<int32_t>("v2_itsc", caps.itcap);
+  a.it_b_unit = c.buf<int32_t>("v2_itbu", caps.itcap);
+  a.it_b_chunk = c.buf<int32_t>("v2_itbc", caps.itcap);
+  a.ccap = caps.ccap;
+  a.c_value = c.buf<double>("v2_cvalue", caps.ccap);
+  a.c_lex = c.buf<uint64_t>("v2_clex", caps.ccap);
+  a.c_parent = c.buf<int32_t>("v2_cparent", caps.ccap);
+  a.c_pid = c.buf<int32_t>("v2_cpid", caps.ccap);
+  a.c_ok = c.buf<uint8_t>("v2_cok", caps.ccap);
+  a.c_live = c.buf<uint8_t>("v2_clive", caps.ccap);
+  a.pcnt = c.buf<int32_t>("v2_pcnt", sp.P1);
+  a.pbucket = c.buf<int32_t>("v2_pbucket", static_cast<size_t>(sp.P1) * 64);
+  MGS_CUDA_OK(cudaMemsetAsync(a.pcnt, 0, static_cast<size_t>(sp.P1) * 4, c.stream));
+  a.scan_cap = 4 * static_cast<int>(H / kTile + 8) + 2 * (caps.ucap / kTile + 8) + (caps.fcap / kTile + 8);
+  a.scan_state = c.buf<unsigned long long>("v2_scan", a.scan_cap);
+  MGS_CUDA_OK(cudaMemsetAsync(a.scan_state, 0, static_cast<size_t>(a.scan_cap) * 8, c.stream));
+  a.sig_len = c.buf<int32_t>("v2_siglen", sp.n_sig);
+  k_sig_len<<<ceil_div(sp.n_sig, 256), 256, 0, c.stream>>>(sp.sig_off, sp.n_sig, a.sig_len);
+  ++c.kernel_launches;
+  a.ctl = c.buf<Ctl>("v2_ctl", 1);
+  MGS_CUDA_OK(cudaMemsetAsync(a.ctl, 0, sizeof(Ctl), c.stream));
+  a.chosen = c.buf<int32_t>("v2_chosen", S);
+  a.n_partial = sp.proj_base[(1 << t.M) - 1];  // all subsets but the full one
+  const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr || std::getenv("MGS_TRACE") != nullptr;
+  a.dbg = debug ? c.buf<long long>("v2_dbg", 6 * S) : nullptr;
+  a.dbg_time = nullptr;
+  a.sc_big_ctas = grid_term;
+  a.merge_win = merge_win;
+  a.oi_bits = 1;
+  while ((1ll << a.oi_bits) < sp.n_opt) ++a.oi_bits;
+  c.prefix = saved_prefix;
+  return a;
+}
+
+}  // namespace
+
+void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
+  const int K = static_cast<int>(lanes.size());
+  if (K < 1 || K > kMaxLanes) throw PlanFail{MGS_ERR_ARGUMENT, "lane count out of range"};
+  const int M = lanes[0].pr->t.M, S = lanes[0].pr->t.S;
+  for (const auto& L : lanes)
+    if (L.pr->t.M != M || L.pr->t.S != S) throw PlanFail{MGS_ERR_ARGUMENT, "batched windows must share S and M"};
+
+  // per-lane scalars: band (solvers.hpp:258-267), dominance validity, tables' smem
+  std::vector<double> band(K);
+  std::vector<int> dom_ok(K), merge_win(K);
+  size_t smem_trans = 0, smem_merge = 0;
+  for (int l = 0; l < K; ++l) {
+    const HostTables& t = lanes[l].pr->t;
+    const DevSpace& sp = *lanes[l].sp;
+    double acc_max[KM] = {0, 0, 0, 0};
+    bool dominance_ok = true;
+    for (int m = 0; m < M; ++m) {
+      acc_max[m] = std::max(t.pre[m], t.post[m]);
+      dominance_ok = dominance_ok && t.post[m] >= t.pre[m];
+    }
+    std::vector<double> pc(static_cast<size_t>(sp.P) * KM);
+    MGS_CUDA_OK(cudaMemcpyAsync(pc.data(), sp.pl_cap, pc.size() * 8, cudaMemcpyDeviceToHost, c.stream));
+    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+    double cap_max[KM] = {0, 0, 0, 0};
+    for (int q = 0; q < sp.P; ++q)
+      for (int m = 0; m < M; ++m) cap_max[m] = std::max(cap_max[m], pc[q * KM + m]);
+    band[l] = 1e-9;
+    for (int m = 0; m < M; ++m) band[l] += t.loss[m] * cap_max[m] * acc_max[m];
+    dom_ok[l] = dominance_ok ? 1 : 0;
+    const int n_partial = sp.proj_base[(1 << M) - 1];
+    smem_trans = std::max(smem_trans, static_cast<size_t>(sp.P1) * 8 + static_cast<size_t>(n_partial) * 20);
+    merge_win[l] = std::min(sp.P1, 8192);  // whole placement range in one window when it fits
+    smem_merge = std::max(smem_merge, static_cast<size_t>(2 * merge_win[l]) * 8);
+  }
   const size_t smem_rank = sizeof(typename cub::BlockRadixSort<unsigned long long, kThreads, kSortItems>::TempStorage);
-  const int merge_win = std::min(sp.P1, 8192);  // whole placement range in one window when it fits
-  const size_t smem_merge = static_cast<size_t>(2 * merge_win) * 8;
   auto ktbig = M == 1 ? k_trans_big<1> : k_trans_big<2>;
   auto ktsmall = M == 1 ? k_trans_small<1> : k_trans_small<2>;
   auto kunits = M == 1 ? k_units<1> : k_units<2>;
   MGS_CUDA_OK(cudaFuncSetAttribute(ktbig, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_trans)));
   MGS_CUDA_OK(cudaFuncSetAttribute(k_ranks_big, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_rank)));
   MGS_CUDA_OK(cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_merge)));
-  // one resident wave per kernel: grid = SMs x max co-resident CTAs
+  // One resident wave per kernel (SMs x max co-resident CTAs), shared by the
+  // lanes: each lane gets a 1/K slice of the wave as its grid.x.
   auto wave = [&](const void* k, size_t dyn) {
     int occ = 0;
     MGS_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, dyn));
     static const int cap = std::getenv("MGS_GRID_CAP") ? std::atoi(std::getenv("MGS_GRID_CAP")) : 0;  // tuning probe
     if (cap > 0) occ = std::min(occ, cap);
-    return c.sm_count * std::max(1, occ);
+    const int w = c.sm_count * std::max(1, occ);
+    return dim3(static_cast<unsigned>(std::max(1, (w + K - 1) / K)), static_cast<unsigned>(K));
   };
-  const int grid = c.sm_count * 8;
-  const int g_units = wave(reinterpret_cast<const void*>(kunits), 0);
-  const int g_scans = wave(reinterpret_cast<const void*>(k_scans), 0);
-  const int g_place = wave(reinterpret_cast<const void*>(k_place), 0);
-  const int g_rbig = wave(reinterpret_cast<const void*>(k_ranks_big), smem_rank);
-  const int g_rsmall = wave(reinterpret_cast<const void*>(k_ranks_small), 0);
-  const int g_tbig = wave(reinterpret_cast<const void*>(ktbig), smem_trans);
-  const int g_tsmall = wave(reinterpret_cast<const void*>(ktsmall), 0);
-  const int g_band = wave(reinterpret_cast<const void*>(k_band), smem_merge);
-  const int g_oscan = wave(reinterpret_cast<const void*>(k_outscan), 0);
-  const int g_write = wave(reinterpret_cast<const void*>(k_write), 0);
-  const int g_dom = wave(reinterpret_cast<const void*>(k_dom), 0);
+  const dim3 g_term(static_cast<unsigned>(std::max(1, c.sm_count * 8 / K)), static_cast<unsigned>(K));
+  const dim3 g_one(1, static_cast<unsigned>(K));
+  const dim3 g_units = wave(reinterpret_cast<const void*>(kunits), 0);
+  const dim3 g_scans = wave(reinterpret_cast<const void*>(k_scans), 0);
+  const dim3 g_place = wave(reinterpret_cast<const void*>(k_place), 0);
+  const dim3 g_rbig = wave(reinterpret_cast<const void*>(k_ranks_big), smem_rank);
+  const dim3 g_rsmall = wave(reinterpret_cast<const void*>(k_ranks_small), 0);
+  const dim3 g_tbig = wave(reinterpret_cast<const void*>(ktbig), smem_trans);
+  const dim3 g_tsmall = wave(reinterpret_cast<const void*>(ktsmall), 0);
+  const dim3 g_band = wave(reinterpret_cast<const void*>(k_band), smem_merge);
+  const dim3 g_oscan = wave(reinterpret_cast<const void*>(k_outscan), 0);
+  const dim3 g_write = wave(reinterpret_cast<const void*>(k_write), 0);
+  const dim3 g_dom = wave(reinterpret_cast<const void*>(k_dom), 0);
   static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 128ll << 20};
-  const uint64_t budget = p.state_budget;
   const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr || std::getenv("MGS_TRACE") != nullptr;
   if (std::getenv("MGS_TRACE"))
-    std::fprintf(stderr, "trace v2 setup: S %d M %d P1 %d n_partial %d smem trans %zu rank %zu merge %zu grids %d %d %d %d %d %d %d %d %d %d %d\n", S, M,
-                 sp.P1, n_partial, smem_trans, smem_rank, smem_merge, g_units, g_scans, g_place, g_rbig, g_rsmall, g_tbig,
-                 g_tsmall, g_band, g_oscan, g_write, g_dom);
+    std::fprintf(stderr, "trace v2 setup: lanes %d S %d M %d smem trans %zu rank %zu merge %zu grid.x %u %u %u %u %u %u %u %u %u %u %u\n",
+                 K, S, M, smem_trans, smem_rank, smem_merge, g_units.x, g_scans.x, g_place.x, g_rbig.x, g_rsmall.x,
+                 g_tbig.x, g_tsmall.x, g_band.x, g_oscan.x, g_write.x, g_dom.x);
   for (int attempt = 0; attempt < 10; ++attempt) {
-    V2 a{};
-    a.sp = sp;
-    a.t = t;
-    a.S = S;
-    a.has_initial = pr.has_initial;
-    a.dominance_ok = dominance_ok ? 1 : 0;
-    a.band = band;
-    a.budget = budget;
-    a.recv = d_recv;
-    a.ub = d_ub;
-    a.incumbent = d_incumbent;
-    a.fcap = caps.fcap;
-    a.gcap = caps.gcap;
-    for (int b = 0; b < 2; ++b) {
-      std::string tg = b ? "v2b_" : "v2a_";
-      FrontierV2& f = a.f[b];
-      f.status = c.buf<uint32_t>((tg + "status").c_str(), caps.fcap);
-      f.ids = c.buf<uint32_t>((tg + "ids").c_str(), caps.fcap);
-      f.pid = c.buf<int32_t>((tg + "pid").c_str(), caps.fcap);
-      f.value = c.buf<double>((tg + "value").c_str(), caps.fcap);
-      f.lex = c.buf<uint64_t>((tg + "lex").c_str(), caps.fcap);
-      f.rank = c.buf<uint32_t>((tg + "rank").c_str(), caps.fcap);
-      f.alive = c.buf<uint8_t>((tg + "alive").c_str(), caps.fcap);
-      f.group = c.buf<int32_t>((tg + "group").c_str(), caps.fcap);
-      f.g_start = c.buf<int32_t>((tg + "gstart").c_str(), caps.gcap);
-      f.g_size = c.buf<int32_t>((tg + "gsize").c_str(), caps.gcap);
-      f.g_status = c.buf<uint32_t>((tg + "gstatus").c_str(), caps.gcap);
-      f.g_alive = c.buf<int32_t>((tg + "galive").c_str(), caps.gcap);
-      a.kid_cnt[b] = c.buf<int32_t>((tg + "kidcnt").c_str(), caps.fcap);
-      a.kid_cur[b] = c.buf<int32_t>((tg + "kidcur").c_str(), caps.fcap);
-      MGS_CUDA_OK(cudaMemsetAsync(a.kid_cnt[b], 0, static_cast<size_t>(caps.fcap) * 4, c.stream));
-      MGS_CUDA_OK(cudaMemsetAsync(a.kid_cur[b], 0, static_cast<size_t>(caps.fcap) * 4, c.stream));
-    }
-    a.kid_base = c.buf<int32_t>("v2_kidbase", caps.fcap + 1);
-    a.kid_items = c.buf<uint64_t>("v2_kiditems", caps.fcap);
-    a.kid_pr = c.buf<int32_t>("v2_kidpr", caps.fcap);
-    a.big_bucket = c.buf<int32_t>("v2_bigbucket", caps.fcap);
-    a.hcap = caps.hcap;
-    a.h_parent = c.buf<int32_t>("v2_hparent", caps.hcap);
-    a.h_oi = c.buf<int32_t>("v2_hoi", caps.hcap);
-    a.hist_base = c.buf<long long>("v2_histbase", S + 2);
-    a.ucap = caps.ucap;
-    a.u_group = c.buf<int32_t>("v2_ugroup", caps.ucap);
-    a.u_sig = c.buf<int32_t>("v2_usig", caps.ucap);
-    a.u_ns = c.buf<int32_t>("v2_uns", caps.ucap);
-    a.u_chs = c.buf<int32_t>("v2_uchs", caps.ucap);
-    a.u_chb = c.buf<int32_t>("v2_uchb", caps.ucap);
-    a.u_cbase = c.buf<int32_t>("v2_ucbase", caps.ucap);
-    a.u_sbase = c.buf<int32_t>("v2_usbase", caps.ucap);
-    a.u_bbase = c.buf<int32_t>("v2_ubbase", caps.ucap);
-    a.ns_units = c.buf<int32_t>("v2_nsunits", caps.ucap);
-    a.hmask = (1 << caps.hbits) - 1;
-    const size_t H = static_cast<size_t>(a.hmask) + 1;
-    a.hash = c.buf<uint32_t>("v2_hash", H);
-    a.ns_ucnt = c.buf<int32_t>("v2_nsucnt", H);
-    a.ns_ccnt = c.buf<int32_t>("v2_nsccnt", H);
-    a.ns_ubase = c.buf<int32_t>("v2_nsubase", H);
-    a.ns_cbase = c.buf<int32_t>("v2_nscbase", H);
-    a.ns_ucur = c.buf<int32_t>("v2_nsucur", H);
-    a.ns_ccur = c.buf<int32_t>("v2_nsccur", H);
-    a.ns_bigpos = c.buf<int32_t>("v2_nsbigpos", H);
-    a.ns_smallpos = c.buf<int32_t>("v2_nssmallpos", H);
-    a.ns_out = c.buf<int32_t>("v2_nsout", H);
-    a.ns_obase = c.buf<int32_t>("v2_nsobase", H);
-    a.ns_gbase = c.buf<int32_t>("v2_nsgbase", H);
-    a.ns_big = c.buf<int32_t>("v2_nsbig", H);
-    a.ns_small = c.buf<int32_t>("v2_nssmall", H);
-    for (void* z : {static_cast<void*>(a.hash), static_cast<void*>(a.ns_ucnt), static_cast<void*>(a.ns_ccnt),
-                    static_cast<void*>(a.ns_ucur), static_cast<void*>(a.ns_ccur), static_cast<void*>(a.ns_out)})
-      MGS_CUDA_OK(cudaMemsetAsync(z, 0, H * 4, c.stream));
-    a.itcap = caps.itcap;
-    a.it_s_unit = c.buf<int32_t>("v2_itsu", caps.itcap);
-    a.it_s_chunk = c.buf<int32_t>("v2_itsc", caps.itcap);
-    a.it_b_unit = c.buf<int32_t>("v2_itbu", caps.itcap);
-    a.it_b_chunk = c.buf<int32_t>("v2_itbc", caps.itcap);
-    a.ccap = caps.ccap;
-    a.c_value = c.buf<double>("v2_cvalue", caps.ccap);
-    a.c_lex = c.buf<uint64_t>("v2_clex", caps.ccap);
-    a.c_parent = c.buf<int32_t>("v2_cparent", caps.ccap);
-    a.c_pid = c.buf<int32_t>("v2_cpid", caps.ccap);
-    a.c_ok = c.buf<uint8_t>("v2_cok", caps.ccap);
-    a.c_live = c.buf<uint8_t>("v2_clive", caps.ccap);
-    a.pcnt = c.buf<int32_t>("v2_pcnt", sp.P1);
-    a.pbucket = c.buf<int32_t>("v2_pbucket", static_cast<size_t>(sp.P1) * 64);
-    MGS_CUDA_OK(cudaMemsetAsync(a.pcnt, 0, static_cast<size_t>(sp.P1) * 4, c.stream));
-    a.scan_cap = 4 * static_cast<int>(H / kTile + 8) + 2 * (caps.ucap / kTile + 8) + (caps.fcap / kTile + 8);  // >= outscan's 2 H-jobs
-    a.scan_state = c.buf<unsigned long long>("v2_scan", a.scan_cap);
-    MGS_CUDA_OK(cudaMemsetAsync(a.scan_state, 0, static_cast<size_t>(a.scan_cap) * 8, c.stream));
-    a.sig_len = c.buf<int32_t>("v2_siglen", sp.n_sig);
-    k_sig_len<<<ceil_div(sp.n_sig, 256), 256, 0, c.stream>>>(sp.sig_off, sp.n_sig, a.sig_len);
+    std::vector<V2> args(K);
+    for (int l = 0; l < K; ++l) args[l] = lane_args(c, lanes[l], caps, band[l], dom_ok[l], merge_win[l], g_term.x);
+    V2* d_args = c.buf<V2>("v2_args", kMaxLanes);
+    MGS_CUDA_OK(cudaMemcpyAsync(d_args, args.data(), sizeof(V2) * K, cudaMemcpyHostToDevice, c.stream));
+    k_init_root<<<g_one, 32, 0, c.stream>>>(d_args);
     ++c.kernel_launches;
-    a.ctl = c.buf<Ctl>("v2_ctl", 1);
-    MGS_CUDA_OK(cudaMemsetAsync(a.ctl, 0, sizeof(Ctl), c.stream));
-    a.chosen = c.buf<int32_t>("v2_chosen", S);
-    a.n_partial = n_partial;
-    a.dbg = debug ? c.buf<long long>("v2_dbg", 6 * S) : nullptr;
-    a.dbg_time = nullptr;
-    a.sc_big_ctas = grid;
-    a.merge_win = merge_win;
-    a.oi_bits = 1;
-    while ((1ll << a.oi_bits) < sp.n_opt) ++a.oi_bits;
-    // the argument block lives in constant memory: every kernel reads its
-    // fields through the constant cache instead of chasing a global pointer
-    MGS_CUDA_OK(cudaMemcpyToSymbolAsync(c_v2_raw, &a, sizeof(V2), 0, cudaMemcpyHostToDevice, c.stream));
-    k_init_root<<<1, 32, 0, c.stream>>>(static_cast<uint32_t>(sp.root_pid));
-    ++c.kernel_launches;
-    // The window's kernel sequence depends only on S, M and launch shapes (all
-    // problem data lives behind d_args), so it is captured once into a CUDA
-    // graph and replayed; MGS_DEBUG_STEPS launches eagerly with per-kernel events.
+    // The window's kernel sequence depends only on S, M, the lane count and
+    // launch shapes (all problem data lives behind d_args), so it is captured
+    // once into a CUDA graph and replayed; MGS_DEBUG_STEPS launches eagerly.
     constexpr int kK = 11;
     static const char* kNames[kK] = {"units", "scans", "place", "ranks_big", "ranks_small", "trans_big",
                                      "trans_small", "band", "outscan", "write", "dom"};
@@ -1644,49 +1669,73 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
       const bool trace = timed && std::getenv("MGS_TRACE") != nullptr;
       auto after = [&](const char* name, int st) {  // MGS_TRACE: serialise + name the kernel that hangs/faults
         if (trace) {
+          // watchdog: if the kernel does not finish within 5 s, dump lane 0's
+          // control block through a second stream (copies overlap a running kernel)
+          const auto t0 = std::chrono::steady_clock::now();
+          while (cudaStreamQuery(st_) == cudaErrorNotReady &&
+                 std::chrono::steady_clock::now() - t0 < std::chrono::seconds(5)) {
+          }
+          if (cudaStreamQuery(st_) == cudaErrorNotReady) {
+            cudaStream_t side;
+            cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+            Ctl* hp = nullptr;
+            cudaMallocHost(&hp, sizeof(Ctl));
+            unsigned long long* ss = nullptr;
+            cudaMallocHost(&ss, 256 * 8);
+            cudaMemcpyAsync(hp, args[0].ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, side);
+            cudaMemcpyAsync(ss, args[0].scan_state, 256 * 8, cudaMemcpyDeviceToHost, side);
+            cudaStreamSynchronize(side);
+            const StepCounters& q = hp->sc[st & 1];
+            std::fprintf(stderr, "HANG in %s step %d: err %d ticket %d ticket2 %d n_units %d ranks_prev %d %d alive %d %d\n",
+                         name, st, hp->err_code, q.ticket, q.ticket2, q.n_units, hp->ranks_prev[0], hp->ranks_prev[1],
+                         hp->alive_now[0], hp->alive_now[1]);
+            for (int i = 0; i < 140; ++i)
+              std::fprintf(stderr, "  tile %d: ep %llu flag %llu agg %llu\n", i, ss[i] >> 34, (ss[i] >> 32) & 3,
+                           ss[i] & 0xffffffffull);
+            std::fflush(stderr);
+            std::abort();
+          }
           cudaError_t e = cudaStreamSynchronize(st_);
           Ctl hc{};
-          cudaMemcpy(&hc, a.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost);
+          cudaMemcpy(&hc, args[0].ctl, sizeof(Ctl), cudaMemcpyDeviceToHost);
           const StepCounters& q = hc.sc[st & 1];
           std::fprintf(stderr,
-                       "trace step %d %s -> %s | err %d units %d T %d its %d itb %d big %d small %d kids %d tk %d tk2 %d"
-                       " store %d/%d groups %d/%d alive %d/%d out %d/%d scan %d %d %d %d %d %d %d\n",
+                       "trace step %d %s -> %s | lane0 err %d units %d T %d its %d itb %d big %d small %d kids %d"
+                       " store %d/%d groups %d/%d alive %d/%d out %d/%d\n",
                        st, name, cudaGetErrorString(e), hc.err_code, q.n_units, q.T, q.items_s, q.items_b, q.n_big,
-                       q.n_small, q.kids, q.ticket, q.ticket2, hc.n_store[0], hc.n_store[1], hc.n_groups[0],
-                       hc.n_groups[1], hc.alive_now[0], hc.alive_now[1], hc.out_total[0], hc.out_total[1],
-                       hc.scan_total[0], hc.scan_total[1], hc.scan_total[2], hc.scan_total[3], hc.scan_total[4],
-                       hc.scan_total[5], hc.scan_total[6]);
+                       q.n_small, q.kids, hc.n_store[0], hc.n_store[1], hc.n_groups[0], hc.n_groups[1],
+                       hc.alive_now[0], hc.alive_now[1], hc.out_total[0], hc.out_total[1]);
         }
         mark();
       };
       for (int st = 0; st < S; ++st) {
-        kunits<<<g_units, kThreads, 0, st_>>>(st);
+        kunits<<<g_units, kThreads, 0, st_>>>(d_args, st);
         after("units", st);
-        k_scans<<<g_scans, kThreads, 0, st_>>>(st);
+        k_scans<<<g_scans, kThreads, 0, st_>>>(d_args, st);
         after("scans", st);
-        k_place<<<g_place, kThreads, 0, st_>>>(st);
+        k_place<<<g_place, kThreads, 0, st_>>>(d_args, st);
         after("place", st);
-        k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(st);
+        k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(d_args, st);
         after("ranks_big", st);
-        k_ranks_small<<<g_rsmall, kThreads, 0, st_>>>(st);
+        k_ranks_small<<<g_rsmall, kThreads, 0, st_>>>(d_args, st);
         after("ranks_small", st);
-        ktbig<<<g_tbig, kThreads, smem_trans, st_>>>(st);
+        ktbig<<<g_tbig, kThreads, smem_trans, st_>>>(d_args, st);
         after("trans_big", st);
-        ktsmall<<<g_tsmall, kThreads, 0, st_>>>(st);
+        ktsmall<<<g_tsmall, kThreads, 0, st_>>>(d_args, st);
         after("trans_small", st);
-        k_band<<<g_band, kThreads, smem_merge, st_>>>(st);
+        k_band<<<g_band, kThreads, smem_merge, st_>>>(d_args, st);
         after("band", st);
-        k_outscan<<<g_oscan, kThreads, 0, st_>>>(st);
+        k_outscan<<<g_oscan, kThreads, 0, st_>>>(d_args, st);
         after("outscan", st);
-        k_write<<<g_write, kThreads, 0, st_>>>(st);
+        k_write<<<g_write, kThreads, 0, st_>>>(d_args, st);
         after("write", st);
-        k_dom<<<g_dom, kThreads, 0, st_>>>(st);
+        k_dom<<<g_dom, kThreads, 0, st_>>>(d_args, st);
         after("dom", st);
       }
-      k_term1<<<grid, kThreads, 0, st_>>>();
-      k_term2<<<grid, kThreads, 0, st_>>>();
-      k_term3<<<grid, kThreads, 0, st_>>>();
-      k_backtrack2<<<1, 32, 0, st_>>>();
+      k_term1<<<g_term, kThreads, 0, st_>>>(d_args);
+      k_term2<<<g_term, kThreads, 0, st_>>>(d_args);
+      k_term3<<<g_term, kThreads, 0, st_>>>(d_args);
+      k_backtrack2<<<g_one, 32, 0, st_>>>(d_args);
     };
     c.kernel_launches += 11ull * S + 4;
     if (debug) {
@@ -1694,7 +1743,7 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
       enqueue(c.stream, true);
       const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
       MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
-      std::fprintf(stderr, "v2 host enqueue ms %.2f (eager, with events)\n", host_ms);
+      std::fprintf(stderr, "v2 host enqueue ms %.2f (eager, with events, %d lanes)\n", host_ms, K);
       double acc[kK] = {0};
       for (size_t i = 1; i < evs.size(); ++i) {
         float ms = 0.f;
@@ -1709,7 +1758,8 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
       std::fprintf(stderr, "\n");
     } else {
       char key[256];
-      std::snprintf(key, sizeof key, "v2:%d:%d:%zu:%zu:%zu", S, M, smem_trans, smem_merge, smem_rank);
+      std::snprintf(key, sizeof key, "v2:%d:%d:%d:%zu:%zu:%zu:%p", K, S, M, smem_trans, smem_merge, smem_rank,
+                    static_cast<void*>(d_args));
       auto it = c.graphs.find(key);
       if (it == c.graphs.end()) {
         cudaStream_t cap;
@@ -1731,12 +1781,16 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
       MGS_CUDA_OK(cudaGraphLaunch(it->second, c.stream));
     }
     MGS_CUDA_OK(cudaGetLastError());
-    Ctl h{};
-    MGS_CUDA_OK(cudaMemcpyAsync(&h, a.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
+    std::vector<Ctl> h(K);
+    for (int l = 0; l < K; ++l)
+      MGS_CUDA_OK(cudaMemcpyAsync(&h[l], args[l].ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
     MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
-    if (h.err_code == kOverflow) {
-      const long long need = h.need;
-      switch (h.need_what) {
+    bool grow = false;
+    for (int l = 0; l < K; ++l) {
+      if (h[l].err_code != kOverflow) continue;
+      grow = true;
+      const long long need = h[l].need;
+      switch (h[l].need_what) {
         case 2: caps.hbits += 1; break;
         case 3: caps.ucap = static_cast<int>(std::max<long long>(need * 2, caps.ucap * 2ll)); break;
         case 4: caps.fcap = static_cast<int>(std::max<long long>(need * 2, caps.fcap * 2ll)); break;
@@ -1746,36 +1800,68 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
         case 8: caps.itcap = static_cast<int>(std::max<long long>(need * 2, caps.itcap * 2ll)); break;
         default: throw PlanFail{MGS_ERR_CUDA, "persistent DP: unknown capacity overflow"};
       }
-      continue;
     }
-    if (debug) {
-      std::vector<long long> d(6 * S);
-      MGS_CUDA_OK(cudaMemcpy(d.data(), a.dbg, d.size() * 8, cudaMemcpyDeviceToHost));
-      for (int s = 0; s < S; ++s)
-        std::fprintf(stderr, "v2 step %d units %lld ns %lld T %lld store %lld groups %lld alive_in %lld\n", s, d[6 * s],
-                     d[6 * s + 1], d[6 * s + 2], d[6 * s + 3], d[6 * s + 4], d[6 * s + 5]);
+    if (grow) continue;  // every lane re-runs with the larger capacities
+    for (int l = 0; l < K; ++l) {
+      V2Lane& L = lanes[l];
+      const Ctl& hc = h[l];
+      if (debug && args[l].dbg && l == 0) {
+        std::vector<long long> d(6 * S);
+        MGS_CUDA_OK(cudaMemcpy(d.data(), args[l].dbg, d.size() * 8, cudaMemcpyDeviceToHost));
+        for (int s = 0; s < S; ++s)
+          std::fprintf(stderr, "v2 step %d units %lld ns %lld T %lld store %lld groups %lld alive_in %lld\n", s, d[6 * s],
+                       d[6 * s + 1], d[6 * s + 2], d[6 * s + 3], d[6 * s + 4], d[6 * s + 5]);
+      }
+      L.status = MGS_OK;
+      if (hc.err_code == MGS_ERR_STATE_BUDGET) {
+        L.status = MGS_ERR_STATE_BUDGET;
+        L.err_step = hc.err_step;
+        L.err_count = hc.err_count;
+        L.msg = "dynamic-program frontier reached " + std::to_string(hc.err_count) + " states at step " +
+                std::to_string(hc.err_step) + " (budget " + std::to_string(L.p->state_budget) + ")";
+        continue;
+      }
+      if (hc.err_code == MGS_ERR_INFEASIBLE_JOINT) {
+        L.status = MGS_ERR_INFEASIBLE_JOINT;
+        L.msg = "no feasible allocation sequence exists for this window";
+        continue;
+      }
+      if (hc.err_code != 0) {
+        L.status = MGS_ERR_CUDA;
+        L.msg = "persistent DP: error " + std::to_string(hc.err_code);
+        continue;
+      }
+      L.out.options.resize(S);
+      MGS_CUDA_OK(cudaMemcpyAsync(L.out.options.data(), args[l].chosen, S * 4, cudaMemcpyDeviceToHost, c.stream));
+      L.out.stats.options = L.sp->n_opt;
+      L.out.stats.candidates = L.sp->n_cand;
+      L.out.stats.transitions_ref = hc.tr_ref;
+      L.out.stats.transitions = hc.tr;
+      L.out.stats.frontier_total = hc.ftot;
+      L.out.stats.frontier_peak = hc.fpeak;
+      L.out.stats.transition_bytes = hc.tbytes;
     }
-    if (h.err_code == MGS_ERR_STATE_BUDGET)
-      throw PlanFail{MGS_ERR_STATE_BUDGET,
-                     "dynamic-program frontier reached " + std::to_string(h.err_count) + " states at step " +
-                         std::to_string(h.err_step) + " (budget " + std::to_string(budget) + ")",
-                     h.err_step, h.err_count};
-    if (h.err_code == MGS_ERR_INFEASIBLE_JOINT)
-      throw PlanFail{MGS_ERR_INFEASIBLE_JOINT, "no feasible allocation sequence exists for this window"};
-    if (h.err_code != 0) throw PlanFail{MGS_ERR_CUDA, "persistent DP: error " + std::to_string(h.err_code)};
-    out.options.resize(S);
-    MGS_CUDA_OK(cudaMemcpyAsync(out.options.data(), a.chosen, S * 4, cudaMemcpyDeviceToHost, c.stream));
     MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
-    out.stats.options = sp.n_opt;
-    out.stats.candidates = sp.n_cand;
-    out.stats.transitions_ref = h.tr_ref;
-    out.stats.transitions = h.tr;
-    out.stats.frontier_total = h.ftot;
-    out.stats.frontier_peak = h.fpeak;
-    out.stats.transition_bytes = h.tbytes;
     return;
   }
   throw PlanFail{MGS_ERR_CUDA, "persistent DP: capacity growth did not converge"};
+}
+
+void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& sp, const double* d_recv,
+                 const double* d_ub, const double* d_incumbent, SolveOut& out) {
+  std::vector<V2Lane> lanes(1);
+  V2Lane& L = lanes[0];
+  L.p = &p;
+  L.pr = &pr;
+  L.sp = &sp;
+  L.recv = d_recv;
+  L.ub = d_ub;
+  L.incumbent = d_incumbent;
+  L.prefix = c.prefix;
+  solve_dp_v2_lanes(c, lanes);
+  if (L.status != MGS_OK) throw PlanFail{L.status, L.msg, L.err_step, L.err_count};
+  out.options = std::move(L.out.options);
+  out.stats = L.out.stats;
 }
 
 }  // namespace mgs

@@ -216,3 +216,28 @@ def test_bruteforce_cap_and_errors(gpu, golden_dir):
         assert v and "infeasible." + v[0][0].split(".", 1)[1] == kat[name][1]["expect_error"]
     p = SC.Problem(SC.load_scenario(kat["worked_example"][0]), 0)
     assert gpu.precheck(p) == []
+
+
+def test_solve_batch_random_corpus(gpu, golden_dir):
+    """Every random-corpus window in ONE batched call (lanes share kernels;
+    shapes change between windows) == the reference's plans and objective bits."""
+    cases = golden_dir["random"]
+    probs = [SC.Problem(SC.load_scenario(path), 0) for _, path, _ in cases]
+    opts, obj, status, stats, errs = gpu.solve_batch(probs)
+    for i, (stem, path, g) in enumerate(cases):
+        assert status[i] == 0, (stem, errs[i].message)
+        assert bits(obj[i]) == g["dp"]["obj"], stem
+        _, cfg, lab, _, _ = gpu.solve_window(probs[i])
+        assert list(opts[i, :probs[i].S]) == list(gpu.solve_window(probs[i])[0]), stem
+
+
+def test_solve_batch_c1_lanes(gpu, golden_dir):
+    """Four C1 S=200 windows as four lanes of one launch sequence."""
+    c1 = {stem: (path, g) for stem, path, g in golden_dir["c1"]}
+    stems = ["c1_S200_100001", "c1_S200_100002", "c1_S200_100001", "c1_S200_100002"]
+    probs = [SC.Problem(SC.load_scenario(c1[s][0]), 0) for s in stems]
+    opts, obj, status, stats, errs = gpu.solve_batch(probs)
+    for i, s in enumerate(stems):
+        assert status[i] == 0
+        assert bits(obj[i]) == c1[s][1]["dp"]["obj"], s
+        assert stats[i]["transitions_ref"] == stats[i % 2]["transitions_ref"]
