@@ -232,7 +232,14 @@ def run_ours(args):
     if os.path.exists(gpath):
         g = json.load(open(gpath)).get("c1_S200_%d" % seed)
     peak, peak_kind = hbm_peak()
-    achieved = trans_bytes / (trans_ms / 1e3) / 1e9 if trans_ms > 0 else 0.0
+    # B_dp = sum_s(|F_s| R + |F_s+1| (R+8)) + 8 M S + |O| (13 M + 8), R = 24 + 4M
+    st0 = stats[-1]
+    M_, S_ = prob.M, prob.S
+    R = 24 + 4 * M_
+    b_dp = (st0["frontier_total"] + 1) * R + st0["frontier_total"] * (R + 8) + 8 * M_ * S_ + st0["options"] * (13 * M_ + 8)
+    dp_ms = trans_ms / len(stats)  # device time of the DP graph per window (phase 3)
+    achieved = b_dp / (dp_ms / 1e3) / 1e9 if dp_ms > 0 else 0.0
+    traffic = measured_traffic()
     phases = {}
     for s in stats:
         for k, v in s["phase_ms"].items():
@@ -253,15 +260,21 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(prob_e2e.S * (4 + 4 + 8) + 8),
                 "decision_latency_ms": 1e3 * e2e_s / args.steps},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": "k_trans_small/k_trans_big (transition phase)",
+        "roofline": {"bound": "hbm", "kernel": "per-window DP graph (11 phase kernels x S steps, one launch)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if peak else None, "traffic": None, "peak_kind": peak_kind,
-                     "bytes_per_window": trans_bytes // max(1, len(stats))},
+                     "frac": achieved / peak if peak else None,
+                     "traffic": traffic.get("bytes_per_window") if traffic else None,
+                     "traffic_source": traffic.get("source") if traffic else None,
+                     "peak_kind": peak_kind, "algorithmic_bytes_per_window": int(b_dp),
+                     "dp_ms_per_window": dp_ms,
+                     "library_transition_bytes_per_window": trans_bytes // max(1, len(stats))},
         "clocks": clk,
         "objective": obj,
     }
     if g:
         line["parity"] = {"golden": "c1_S200_%d" % seed, "objective_bits_equal": g["dp"]["obj"] == bits(obj)}
+    if args.batch > 0:
+        line["batch"] = batch_leg(pl, work, rank, args.batch)
     if world == 1 and not args.no_cpu_baseline:
         times = reference_cpu(1, 0, 1)
         tr = sample_transitions()
@@ -272,6 +285,33 @@ def run_ours(args):
     pl.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def measured_traffic():
+    """DRAM bytes per C1 window from the committed ncu metrics pass (profiles/)."""
+    path = os.path.join(ROOT, "profiles", "traffic_c1.json")
+    try:
+        return json.load(open(path))
+    except (OSError, ValueError):
+        return None
+
+
+def batch_leg(pl, work, rank, n):
+    """Throughput with n independent C1 windows (seeds 100001+rank*n ...) solved
+    as batched lanes (mgs_solve_batch: windows share every DP kernel launch)."""
+    import torch
+    probs = [c1_problem(100001 + rank * n + k, work) for k in range(n)]
+    pl.solve_batch(probs)  # warm: capacity growth + graph capture for this lane count
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    opts, obj, status, stats, errs = pl.solve_batch(probs)
+    dt = time.perf_counter() - t0
+    tr = sum(s["transitions_ref"] for s in stats)
+    lanes = int(os.environ.get("MGS_BATCH_LANES", "8"))
+    return {"workload": "%d config-1 windows (seeds %d..%d), %d lanes per launch" % (n, 100001 + rank * n,
+                                                                                 100001 + rank * n + n - 1, lanes),
+            "value": tr / dt, "unit": UNIT, "ms_per_window": 1e3 * dt / n, "ok": int((status == 0).sum()),
+            "timing": "host wall clock around mgs_solve_batch (host buffers in, plans out)"}
 
 
 def bits(x):
@@ -286,6 +326,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch", type=int, default=16, help="windows in the batched-lanes throughput leg (0: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -45,15 +45,26 @@ __device__ inline unsigned long long vbits(double v) { return static_cast<unsign
 // space.hpp:270-274 — kept 64-bit end to end).
 __host__ __device__ inline int field16(uint64_t key, int m) { return static_cast<int>((key >> (16 * m)) & 0xffff); }
 
-// engine::StatusCodec (space.hpp:255-298): 0 not started, 1 done,
-// 2+(k-1)*S+(rem-1) running on k GPCs with rem steps left including this one.
+// engine::StatusCodec (space.hpp:255-298): 0 not started, 1 done, otherwise
+// running on k GPCs with rem steps left including this one. The reference
+// numbers running statuses 2+(k-1)*S+(rem-1); the codes are only compared for
+// equality and decoded, never ordered, so the device packs them as
+// 2+((k-1)<<13 | (rem-1)) whenever S <= 8192 (k <= 7 keeps the code in 16
+// bits) and decodes with shifts instead of divisions by S. Longer windows use
+// the reference numbering.
 struct Codec {
   int S;
+  int shift;
+  __host__ __device__ explicit Codec(int s) : S(s), shift(s <= 8192 ? 13 : 0) {}
   __host__ __device__ static constexpr int done() { return 1; }
-  __host__ __device__ int running(int k, long long rem) const { return 2 + (k - 1) * S + static_cast<int>(rem - 1); }
+  __host__ __device__ int running(int k, long long rem) const {
+    return shift ? 2 + (((k - 1) << shift) | static_cast<int>(rem - 1)) : 2 + (k - 1) * S + static_cast<int>(rem - 1);
+  }
   __host__ __device__ static bool is_running(int c) { return c >= 2; }
-  __host__ __device__ int run_size(int c) const { return (c - 2) / S + 1; }
-  __host__ __device__ long long run_rem(int c) const { return (c - 2) % S + 1; }
+  __host__ __device__ int run_size(int c) const { return shift ? ((c - 2) >> shift) + 1 : (c - 2) / S + 1; }
+  __host__ __device__ long long run_rem(int c) const {
+    return shift ? ((c - 2) & ((1 << shift) - 1)) + 1 : (c - 2) % S + 1;
+  }
   // StatusCodec::advance (space.hpp:286-297); -1 = incompatible
   __host__ __device__ int advance(const long long* rt_row, int status, int size, int s) const {
     if (is_running(status)) {

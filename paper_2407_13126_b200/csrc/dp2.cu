@@ -77,6 +77,7 @@ struct FrontierV2 {
 
 struct StepCounters {  // double buffered; zeroed one step ahead
   int n_units, T, items_s, items_b, n_big, n_small, n_big_bucket, ticket, kids, ticket2;
+  int n_ns;  // successor statuses of the step = entries of the used-slot list
 };
 
 struct Ctl {
@@ -118,6 +119,7 @@ struct V2 {
   int ucap;
   uint32_t* hash;  // key+1 per slot; the slot index is the successor-status id
   int hmask;
+  int32_t* ns_used;  // hash slots claimed this step (list order = claim order)
   int32_t *ns_ucnt, *ns_ccnt, *ns_ubase, *ns_cbase, *ns_ucur, *ns_ccur, *ns_units, *ns_bigpos, *ns_smallpos;
   int32_t *ns_big, *ns_small;
   int32_t *ns_out, *ns_obase, *ns_gbase;  // survivors per status, their offsets and group index
@@ -160,7 +162,11 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ int ld_volatile(const int* p) {  // GPU-scope relaxed load (not a system-scope volatile)
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ void raise_err(const V2& a, int phi, int code, int step = 0, unsigned long long count = 0, int what = 0,
                           long long need = 0) {
   (void)phi;
@@ -229,10 +235,12 @@ struct ScanJob {
   int32_t* out;
   int n;
   int mode;  // 0 plain, 1 big-status flag, 2 small-status flag, 3 nonzero flag
+  const int32_t* idx = nullptr;  // gather/scatter through this list (status slots) when set
 };
 
 __device__ __forceinline__ int scan_load(const ScanJob& J, int i) {
   if (i >= J.n) return 0;
+  if (J.idx) i = J.idx[i];
   if (J.mode == 0) return J.in[i];
   if (J.mode == 3) return J.in[i] > 0 ? 1 : 0;
   const int uc = J.in[i];
@@ -280,7 +288,7 @@ __device__ int block_scan_tile(const ScanJob& J, int base, int* sm) {
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int i = base + tid * 8 + k;
-    if (i < J.n) J.out[i] = v[k];
+    if (i < J.n) J.out[J.idx ? J.idx[i] : i] = v[k];
   }
   const int agg = sm[64];
   __syncthreads();
@@ -357,7 +365,7 @@ __device__ void multi_scan(const V2& a, const ScanJob* jobs, int njobs, int epoc
     __syncthreads();
     const int excl = s_excl;
     if (excl)
-      for (int i = j * kTile + threadIdx.x; i < min(J.n, (j + 1) * kTile); i += kThreads) J.out[i] += excl;
+      for (int i = j * kTile + threadIdx.x; i < min(J.n, (j + 1) * kTile); i += kThreads) J.out[J.idx ? J.idx[i] : i] += excl;
     __syncthreads();
   }
 }
@@ -379,8 +387,14 @@ __device__ int ns_slot(const V2& a, uint32_t key, int phi, int step) {
   for (int probe = 0; probe <= (a.hmask >> 1); ++probe) {
     const int slot = static_cast<int>((h + static_cast<unsigned>(probe)) & static_cast<unsigned>(a.hmask));
     uint32_t w = a.hash[slot];
-    if (w == 0) w = atomicCAS(&a.hash[slot], 0u, want);
-    if (w == 0 || w == want) return slot;
+    if (w == 0) {
+      w = atomicCAS(&a.hash[slot], 0u, want);
+      if (w == 0) {  // this thread claimed the slot: list it for the step's status loops
+        a.ns_used[atomicAdd(&a.ctl->sc[step & 1].n_ns, 1)] = slot;
+        return slot;
+      }
+    }
+    if (w == want) return slot;
   }
   raise_err(a, phi, kOverflow, step, 0, 2, 0);  // table too full
   return -1;
@@ -545,7 +559,9 @@ __device__ void phase_place(const V2& a, int s) {
       a.it_b_chunk[bb + c] = c;
     }
   }
-  for (int id = gtid; id <= a.hmask; id += gstride) {
+  const int n_ns = sc.n_ns;
+  for (int k = gtid; k < n_ns; k += gstride) {
+    const int id = a.ns_used[k];
     const int uc = a.ns_ucnt[id];
     if (uc == 0) continue;
     if (uc > 1 || a.ns_ccnt[id] > kBigNs) a.ns_big[a.ns_bigpos[id]] = id;
@@ -847,12 +863,37 @@ __device__ void phase_trans_small(const V2& a, int s) {
   const int lane = threadIdx.x & 31;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const int nis = sc.items_s;
+  constexpr int kFull = (1 << M) - 1;
   for (int item = wid; item < nis; item += nw) {
     const int unit = a.it_s_unit[item], chunk = a.it_s_chunk[item];
     const int g = a.u_group[unit], sig = a.u_sig[unit];
     const int gs = F.g_start[g], gn = F.g_size[g];
     const int sb = a.sp.sig_off[sig], L = a.sp.sig_off[sig + 1] - sb;
     const int ti = chunk * kChunkS + lane;
+    // empty subset: the group's best state, one warp-cooperative pass
+    double v0 = 0.0;
+    uint32_t r0 = 0xffffffffu;
+    int i0 = -1;
+    for (int j = lane; j < gn; j += 32) {
+      if (!F.alive[gs + j]) continue;
+      const double vj = F.value[gs + j];
+      const uint32_t rj = F.rank[gs + j];
+      if (i0 < 0 || better(vj, rj, v0, r0)) {
+        v0 = vj;
+        r0 = rj;
+        i0 = j;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v0, o);
+      const uint32_t orr = __shfl_xor_sync(0xffffffffu, r0, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, i0, o);
+      if (oi >= 0 && (i0 < 0 || better(ov, orr, v0, r0))) {
+        v0 = ov;
+        r0 = orr;
+        i0 = oi;
+      }
+    }
     if (ti >= L) continue;
     double acc[M];
     group_acc<M>(a, F.g_status[g], acc);
@@ -861,23 +902,32 @@ __device__ void phase_trans_small(const V2& a, int s) {
     const uint32_t ids_p = static_cast<uint32_t>(a.sp.pl_ids[p]);
     BestT<M> b;
 #pragma unroll
-    for (int k = 0; k < (1 << M); ++k) {
+    for (int k = 1; k < (1 << M); ++k) {
       b.i[k] = -1;
       b.v[k] = 0.0;
       b.r[k] = 0xffffffffu;
     }
+    b.i[0] = i0;
+    b.v[0] = v0;
+    b.r[0] = r0;
+    // non-empty subsets: only states that agree with the target on the
+    // subset's tenants can represent it (solvers.hpp:367-378)
 #pragma unroll 4
     for (int j = 0; j < gn; ++j) {
-      const bool al = F.alive[gs + j];
-      const double vj = F.value[gs + j];
-      const uint32_t rj = F.rank[gs + j];
-      const uint32_t idj = F.ids[gs + j];
-      if (!al) continue;
+      const uint32_t x = F.ids[gs + j] ^ ids_p;
       int mt = 0;
 #pragma unroll
-      for (int m = 0; m < M; ++m) mt |= (((idj ^ ids_p) >> (16 * m)) & 0xffff) == 0 ? (1 << m) : 0;
+      for (int m = 0; m < M; ++m) mt |= ((x >> (16 * m)) & 0xffff) == 0 ? (1 << m) : 0;
+      if (mt == 0 || !F.alive[gs + j]) continue;
+      const double vj = F.value[gs + j];
+      const uint32_t rj = F.rank[gs + j];
+      if (mt == kFull) {  // the full subset's key is the state's own placement: unique in the group
+        b.v[kFull] = vj;
+        b.r[kFull] = rj;
+        b.i[kFull] = j;
+      }
 #pragma unroll
-      for (int sub = 0; sub < (1 << M); ++sub) {
+      for (int sub = 1; sub < kFull; ++sub) {
         if ((sub & ~mt) != 0) continue;
         if (b.i[sub] < 0 || better(vj, rj, b.v[sub], b.r[sub])) {
           b.v[sub] = vj;
@@ -1183,11 +1233,11 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
       if (static_cast<unsigned long long>(alive_cur) > ctl->fpeak) ctl->fpeak = alive_cur;
     }
   }
-  const int H = a.hmask + 1;
-  const ScanJob jobs[kNumScans] = {{a.ns_ccnt, nullptr, a.ns_cbase, H, 0},
-                                   {a.ns_ucnt, nullptr, a.ns_ubase, H, 0},
-                                   {a.ns_ucnt, a.ns_ccnt, a.ns_bigpos, H, 1},
-                                   {a.ns_ucnt, a.ns_ccnt, a.ns_smallpos, H, 2},
+  const int H = sc.n_ns;  // per-status scans run over the step's claimed slots only
+  const ScanJob jobs[kNumScans] = {{a.ns_ccnt, nullptr, a.ns_cbase, H, 0, a.ns_used},
+                                   {a.ns_ucnt, nullptr, a.ns_ubase, H, 0, a.ns_used},
+                                   {a.ns_ucnt, a.ns_ccnt, a.ns_bigpos, H, 1, a.ns_used},
+                                   {a.ns_ucnt, a.ns_ccnt, a.ns_smallpos, H, 2, a.ns_used},
                                    {a.u_chs, nullptr, a.u_sbase, sc.n_units, 0},
                                    {a.u_chb, nullptr, a.u_bbase, sc.n_units, 0},
                                    {a.kid_cnt[cur], nullptr, a.kid_base, ctl->ranks_prev[s & 1], 0}};
@@ -1270,8 +1320,9 @@ __global__ void __launch_bounds__(kThreads) k_band(const V2* __restrict__ ap, in
 __global__ void __launch_bounds__(kThreads) k_outscan(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (failed(a)) return;
-  const int H = a.hmask + 1;
-  const ScanJob jobs[2] = {{a.ns_out, nullptr, a.ns_obase, H, 0}, {a.ns_out, nullptr, a.ns_gbase, H, 3}};
+  const int H = a.ctl->sc[s & 1].n_ns;
+  const ScanJob jobs[2] = {{a.ns_out, nullptr, a.ns_obase, H, 0, a.ns_used},
+                           {a.ns_out, nullptr, a.ns_gbase, H, 3, a.ns_used}};
   multi_scan(a, jobs, 2, 2 * (s + 1) + 1, &a.ctl->sc[s & 1].ticket2, a.ctl->out_total);
 }
 
@@ -1299,7 +1350,9 @@ __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int
   Ctl* ctl = a.ctl;
   if (a.dominance_ok) phase_dominance(a, s);
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
-  for (int i = gtid; i <= a.hmask; i += gstride) {  // S6 read the keys from the hash: clear now
+  const int n_ns = ctl->sc[s & 1].n_ns;
+  for (int k = gtid; k < n_ns; k += gstride) {  // S6 read the keys from the hash: clear the claimed slots
+    const int i = a.ns_used[k];
     a.hash[i] = 0u;
     a.ns_out[i] = 0;
     a.ns_ucnt[i] = 0;
@@ -1532,6 +1585,7 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, double band, int dominan
   a.ns_gbase = c.buf<int32_t>("v2_nsgbase", H);
   a.ns_big = c.buf<int32_t>("v2_nsbig", H);
   a.ns_small = c.buf<int32_t>("v2_nssmall", H);
+  a.ns_used = c.buf<int32_t>("v2_nsused", H);
   for (void* z : {static_cast<void*>(a.hash), static_cast<void*>(a.ns_ucnt), static_cast<void*>(a.ns_ccnt),
                   static_cast<void*>(a.ns_ucur), static_cast<void*>(a.ns_ccur), static_cast<void*>(a.ns_out)})
     MGS_CUDA_OK(cudaMemsetAsync(z, 0, H * 4, c.stream));

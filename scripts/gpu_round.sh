@@ -13,7 +13,7 @@ if [ -n "$REF" ]; then
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "rc $?" >> $OUT/bench_ref.err
 fi
 if [ -n "$NCU" ]; then
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python scripts/solve_once.py tests/golden/c1/c1_S200_100001.scn 2 > $OUT/ncu_launches.log 2>&1; echo "rc $?" >> $OUT/ncu_launches.log
 for K in ${NCU_KERNELS:-k_trans_big k_write}; do
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:$K --launch-skip ${NCU_SKIP:-300} --launch-count 1 \
