@@ -44,7 +44,7 @@ for k, d in sorted(per.items(), key=lambda x: -x[1]["gpu__time_duration.sum"]):
 print("per window: %.2f ms kernel time, %.1f MB DRAM" % (tot_t / W / 1e3, tot_b / W / 1e6))
 if len(sys.argv) > 3:
     json.dump({"bytes_per_window": int(tot_b / W), "kernel_us_per_window": tot_t / W,
-               "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over %g C1 windows (%s)"
+               "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over %g C1 windows (%s); ncu flushes caches before each kernel, so this over-counts live traffic"
                          % (W, sys.argv[1].split("/")[-1]),
                "per_kernel": {k: {"launches": counts[k], "time_us": d["gpu__time_duration.sum"],
                                   "dram_bytes": d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]}
