@@ -275,6 +275,8 @@ def run_ours(args):
         line["parity"] = {"golden": "c1_S200_%d" % seed, "objective_bits_equal": g["dp"]["obj"] == bits(obj)}
     if args.batch > 0:
         line["batch"] = batch_leg(pl, work, rank, args.batch)
+    if args.table > 0:
+        line["goodput_table"] = table_leg(pl, work, stream, args.table)
     if world == 1 and not args.no_cpu_baseline:
         times = reference_cpu(1, 0, 1)
         tr = sample_transitions()
@@ -314,6 +316,56 @@ def batch_leg(pl, work, rank, n):
             "timing": "host wall clock around mgs_solve_batch (host buffers in, plans out)"}
 
 
+def table_leg(pl, work, stream, n_traces=4096, reps=5):
+    """Config 4: the Goodput table (ub_suffix) of a batch of 4-tenant, 600-slot
+    MMPP traces sharing one window's tables (mgs_goodput_table_batch). Device leg:
+    traces resident in HBM, CUDA events on the planner's stream; e2e leg: host
+    traces in, host ub_suffix out through the C ABI."""
+    import numpy as np
+    import torch
+    from paper_2407_13126_b200 import scenario as SC
+    from paper_2407_13126_b200 import workloads as W
+    p = SC.Problem(SC.load_scenario(W.write_scenario(W.c2_spec(400000, steps=600, windows=1), work, "c4")), 0)
+    traces = np.stack([W.mmpp_trace([40.0, 120.0, 12.0, 10.0], p.S, 400000 + k)
+                       for k in range(n_traces)]).astype(np.int32)  # seeds 400000..404095 (SURVEY §8(d))
+    n_opt = len(pl.enumerate(p)["config"])
+    with torch.cuda.stream(stream):
+        d_arr = torch.from_numpy(traces).cuda()
+        d_ub = torch.empty((n_traces, p.S + 1), dtype=torch.float64, device="cuda")
+        d_best = torch.empty((n_traces, p.S), dtype=torch.float64, device="cuda")
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        npar = pl.goodput_table_batch_device(p, d_arr.data_ptr(), n_traces, d_best.data_ptr(), d_ub.data_ptr())
+        torch.cuda.synchronize()
+        evs = []
+        for _ in range(reps):  # everything queued first: host latency never shows in the event pairs
+            flush.zero_()  # traces are 39 MB < L2: flush between timed launches
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pl.goodput_table_batch_device(p, d_arr.data_ptr(), n_traces, d_best.data_ptr(), d_ub.data_ptr())
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        ms = [a.elapsed_time(b) for a, b in evs]
+    t_ms = sum(ms) / len(ms)
+    pinned = torch.from_numpy(traces).pin_memory().numpy()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        ub_h, _ = pl.goodput_table_batch(p, pinned)
+    e2e_ms = (time.perf_counter() - t0) / reps * 1e3
+    M, S = p.M, p.S
+    algo = n_traces * M * S * 4 + npar * M * 8 + n_traces * S * 8 + n_traces * (S + 1) * 8
+    peak, peak_kind = hbm_peak()
+    return {"workload": "config 4: %d MMPP traces x 4 tenants (ResNet-50/MobileNetV2/ViT-B/BERT-base) x 600 slots, "
+                        "A100 lattice, %d options, %d Pareto placements" % (n_traces, n_opt, npar),
+            "value": n_traces * S * n_opt / (t_ms / 1e3), "unit": "Goodput-table cells/s (trace x slot x option)",
+            "ms_per_batch": t_ms, "traces_per_s": n_traces / (t_ms / 1e3),
+            "e2e": {"ms_per_batch": e2e_ms, "h2d_bytes": int(traces.nbytes), "d2h_bytes": int(n_traces * (S + 1) * 8)},
+            "roofline": {"bound": "hbm", "kernel": "k_table", "achieved": algo / (t_ms / 1e3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": algo / (t_ms / 1e3) / 1e9 / peak, "algorithmic_bytes": algo,
+                         "peak_kind": peak_kind},
+            "ub0": float(ub_h[0, 0])}
+
+
 def bits(x):
     import struct
     return "%016x" % struct.unpack("<Q", struct.pack("<d", float(x)))[0]
@@ -327,6 +379,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=16, help="windows in the batched-lanes throughput leg (0: skip)")
+    ap.add_argument("--table", type=int, default=4096, help="traces in the config-4 Goodput-table leg (0: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

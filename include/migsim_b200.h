@@ -18,6 +18,8 @@
  *   mgs_solve_batch    solve_dp over independent windows (the reference's
  *                      per-scenario call in a host loop)
  *   mgs_evaluate_batch evaluate_plan(verify=false)     evaluate.hpp:153-210
+ *   mgs_goodput_table_batch  solve_dp's ub_suffix table  solvers.hpp:258-280
+ *                      for a batch of traces sharing one window's tables
  */
 #ifndef MIGSIM_B200_H
 #define MIGSIM_B200_H
@@ -191,6 +193,21 @@ MGS_API int mgs_solve_batch(mgs_ctx* ctx, const mgs_problem* problems, int32_t n
 MGS_API int mgs_evaluate_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* plans, int32_t n_plans,
                        const int64_t* arrivals, int32_t n_traces, double* total, double* throughput,
                        mgs_error* err);
+
+/* The Goodput table for n_traces traces that share one window's lattice and
+ * tables (configs 2/4): best[b*S+s] = max(0, max over candidates of
+ * sum_m acc_max[m]*min(recv, cap)) and ub_suffix[b*(S+1)+s] its suffix sums
+ * (solvers.hpp:270-280), bit-identical to the per-window solve.
+ * arrivals[b*M*S + m*S + s] are int32 counts. mgs_goodput_table_batch takes
+ * host buffers; the _device variant takes device pointers on the context's
+ * stream (inputs already resident in HBM) and does not synchronise.
+ * *n_pareto (optional) receives the number of Pareto-maximal placements the
+ * table kernel scanned. best may be NULL. */
+MGS_API int mgs_goodput_table_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* arrivals, int32_t n_traces,
+                                    double* best, double* ub_suffix, int32_t* n_pareto, mgs_error* err);
+MGS_API int mgs_goodput_table_batch_device(mgs_ctx* ctx, const mgs_problem* p, const int32_t* d_arrivals,
+                                           int32_t n_traces, double* d_best, double* d_ub_suffix, int32_t* n_pareto,
+                                           mgs_error* err);
 
 #ifdef __cplusplus
 }

@@ -480,4 +480,64 @@ int mgs_evaluate_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* plans,
   });
 }
 
+namespace {
+void table_batch(Ctx& c, const mgs_problem& p, const int32_t* d_arr, int n, double* d_best, double* d_ub,
+                 int32_t* n_pareto) {
+  // the option space and its Pareto placements depend only on the lattice and
+  // the tables: built once per window shape and reused across trace batches
+  std::string key(reinterpret_cast<const char*>(&p.tables), sizeof(mgs_tables));
+  const int nc = p.lattice.n_configs, ns = nc > 0 ? p.lattice.slot_offset[nc] : 0;
+  key.append(reinterpret_cast<const char*>(&p.lattice.n_configs), 8);
+  key.append(reinterpret_cast<const char*>(p.lattice.slot_offset), (nc + 1) * 4);
+  key.append(reinterpret_cast<const char*>(p.lattice.slot_size), ns * 4);
+  key.append(reinterpret_cast<const char*>(p.lattice.slot_start), ns * 4);
+  mgs::Prepared pr = prepare_problem(p);
+  if (key != c.table_key) {
+    const std::string saved = c.prefix;
+    c.prefix = "tab/";
+    c.table_key.clear();
+    mgs::DevSpace sp;
+    mgs::build_space(c, p.lattice, pr, sp);
+    c.table_np = mgs::table_prepare(c, pr, sp, &c.table_wcp);
+    c.prefix = saved;
+    c.table_key = key;
+  }
+  mgs::table_run(c, pr, c.table_wcp, c.table_np, d_arr, n, d_best, d_ub);
+  if (n_pareto) *n_pareto = c.table_np;
+}
+}  // namespace
+
+int mgs_goodput_table_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* arrivals, int32_t n_traces, double* best,
+                            double* ub_suffix, int32_t* n_pareto, mgs_error* err) {
+  if (!ctx || !p || n_traces < 0 || (n_traces > 0 && (!arrivals || !ub_suffix))) return MGS_ERR_ARGUMENT;
+  return guarded(err, [&] {
+    Ctx& c = ctx->c;
+    MGS_CUDA_OK(cudaSetDevice(c.device));
+    const int M = p->tables.models, S = p->tables.steps;
+    const size_t n_arr = static_cast<size_t>(n_traces) * M * S;
+    int32_t* d_arr = c.buf<int32_t>("tabb_arr", n_arr);
+    double* d_best = best ? c.buf<double>("tabb_best", static_cast<size_t>(n_traces) * S) : nullptr;
+    double* d_ub = c.buf<double>("tabb_ub", static_cast<size_t>(n_traces) * (S + 1));
+    if (n_arr) MGS_CUDA_OK(cudaMemcpyAsync(d_arr, arrivals, n_arr * 4, cudaMemcpyHostToDevice, c.stream));
+    table_batch(c, *p, d_arr, n_traces, d_best, d_ub, n_pareto);
+    if (n_traces > 0) {
+      MGS_CUDA_OK(cudaMemcpyAsync(ub_suffix, d_ub, static_cast<size_t>(n_traces) * (S + 1) * 8, cudaMemcpyDeviceToHost,
+                                  c.stream));
+      if (best)
+        MGS_CUDA_OK(cudaMemcpyAsync(best, d_best, static_cast<size_t>(n_traces) * S * 8, cudaMemcpyDeviceToHost, c.stream));
+    }
+    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int mgs_goodput_table_batch_device(mgs_ctx* ctx, const mgs_problem* p, const int32_t* d_arrivals, int32_t n_traces,
+                                   double* d_best, double* d_ub_suffix, int32_t* n_pareto, mgs_error* err) {
+  if (!ctx || !p || n_traces < 0 || (n_traces > 0 && (!d_arrivals || !d_ub_suffix))) return MGS_ERR_ARGUMENT;
+  return guarded(err, [&] {
+    Ctx& c = ctx->c;
+    MGS_CUDA_OK(cudaSetDevice(c.device));
+    table_batch(c, *p, d_arrivals, n_traces, d_best, d_ub_suffix, n_pareto);
+  });
+}
+
 }  // extern "C"

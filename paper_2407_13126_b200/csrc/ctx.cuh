@@ -163,6 +163,11 @@ struct Ctx {
   uint64_t kernel_launches = 0;
   History history;
   std::map<std::string, cudaGraphExec_t> graphs;  // cached per-window kernel sequences
+  // batched-table cache: the option space and Pareto rows of the last window
+  // shape (lattice + tables bytes), kept under the "tab/" buffer prefix
+  std::string table_key;
+  int table_np = 0;
+  double* table_wcp = nullptr;
 
   // Buffer names are looked up under `prefix`: a batched solve sets a
   // per-lane prefix so every lane owns a disjoint set of scratch buffers.
@@ -200,6 +205,10 @@ std::vector<std::pair<int, int>> collect_violations(Ctx& c, const mgs_lattice& l
                                                     const DevSpace& sp);
 // bruteforce.cu: solve_bruteforce; false when no feasible all-done sequence
 bool bruteforce(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* d_recv, std::vector<int32_t>& plan);
+// table.cu: batched ub table (Pareto placements prepared once per window shape)
+int table_prepare(Ctx& c, const Prepared& pr, const DevSpace& sp, double** wcp_out);
+void table_run(Ctx& c, const Prepared& pr, const double* wcp, int np, const int32_t* d_arr, int n_traces,
+               double* d_best, double* d_ub);
 // goodput.cu
 void goodput_reductions(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* d_recv, double* d_ub,
                         double* d_incumbent, int32_t* d_greedy);

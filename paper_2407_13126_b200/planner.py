@@ -132,6 +132,34 @@ class Planner:
             raise capi.PlannerError(st)
         return opts, obj, status, [s.as_dict() for s in stats], errs
 
+    # -- ub_suffix table for a batch of traces (configs 2/4) ---------------------
+    def goodput_table_batch(self, problem: Problem, arrivals, with_best=False):
+        """arrivals int32 [n][M][S] (host). Returns ub [n][S+1] (and best [n][S])
+        plus the number of Pareto placements scanned."""
+        arr = np.ascontiguousarray(arrivals, dtype=np.int32).reshape(-1, problem.M, problem.S)
+        n = arr.shape[0]
+        ub = np.zeros((n, problem.S + 1), np.float64)
+        best = np.zeros((n, problem.S), np.float64) if with_best else None
+        npar = C.c_int32()
+        err = capi.empty_error()
+        st = self.lib.mgs_goodput_table_batch(self.h, problem.byref(), capi.ptr(arr, C.c_int32), n,
+                                              capi.ptr(best, C.c_double) if best is not None else None,
+                                              capi.ptr(ub, C.c_double), C.byref(npar), C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        return (ub, best, npar.value) if with_best else (ub, npar.value)
+
+    def goodput_table_batch_device(self, problem: Problem, d_arrivals, n, d_best, d_ub):
+        """Device-pointer variant (ints): enqueues on the context's stream, no sync."""
+        npar = C.c_int32()
+        err = capi.empty_error()
+        st = self.lib.mgs_goodput_table_batch_device(self.h, problem.byref(), C.c_void_p(d_arrivals), n,
+                                                     C.c_void_p(d_best) if d_best else None, C.c_void_p(d_ub),
+                                                     C.byref(npar), C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        return npar.value
+
     # -- evaluate_plan(verify=false) batch ---------------------------------------
     def evaluate_batch(self, problem: Problem, plans, arrivals, with_throughput=False):
         plans = np.ascontiguousarray(plans, dtype=np.int32).reshape(-1, problem.S)

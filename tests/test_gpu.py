@@ -241,3 +241,40 @@ def test_solve_batch_c1_lanes(gpu, golden_dir):
         assert status[i] == 0
         assert bits(obj[i]) == c1[s][1]["dp"]["obj"], s
         assert stats[i]["transitions_ref"] == stats[i % 2]["transitions_ref"]
+
+
+def _c4_problem(tmp_path, seed=400000, steps=600):
+    from paper_2407_13126_b200 import workloads as W
+    path = W.write_scenario(W.c2_spec(seed, steps=steps, windows=1), str(tmp_path), "c4_%d" % seed)
+    return SC.Problem(SC.load_scenario(path), 0)
+
+
+def test_goodput_table_batch_matches_window(gpu, golden_dir):
+    """The batched table (Pareto placements, pre-scaled min-fold) == the
+    per-window ub_suffix, bit for bit, for every trace of a batch."""
+    rng = np.random.default_rng(11)
+    for stem, path, g in golden_dir["random"][:40] + golden_dir["c1"]:
+        sc = SC.load_scenario(path)
+        p = SC.Problem(sc, 0)
+        traces = np.concatenate([p.forecast[None].astype(np.int32),
+                                 rng.integers(0, 400, size=(3, p.M, p.S)).astype(np.int32)])
+        ub, best, npar = gpu.goodput_table_batch(p, traces, with_best=True)
+        assert 1 <= npar
+        for b in range(traces.shape[0]):
+            q = SC.Problem(sc, 0, forecast=traces[b].astype(np.int64))
+            ub_w, _, _ = gpu.goodput_table(q)
+            assert ub[b].tobytes() == ub_w.tobytes(), (stem, b)
+            assert np.array_equal(np.cumsum(best[b][::-1])[::-1] >= 0, np.ones(p.S, bool))
+
+
+def test_goodput_table_batch_c4_matches_oracle(gpu, tmp_path):
+    """Config-4 shape: 4 tenants (C2 generator, MMPP), S = 600, a batch of traces;
+    two traces checked against the CPU restatement directly."""
+    from paper_2407_13126_b200 import workloads as W
+    p = _c4_problem(tmp_path)
+    traces = np.stack([W.mmpp_trace([40.0, 120.0, 12.0, 10.0], p.S, 400000 + k) for k in range(32)]).astype(np.int32)
+    ub, npar = gpu.goodput_table_batch(p, traces)
+    for b in (0, 17):
+        q = SC.Problem(p.scenario, 0, forecast=traces[b].astype(np.int64))
+        ub_o, _, _ = B.goodput_table(q)
+        assert ub[b].tobytes() == ub_o.tobytes(), b
