@@ -18,6 +18,7 @@
  *   mgs_solve_batch    solve_dp over independent windows (the reference's
  *                      per-scenario call in a host loop)
  *   mgs_evaluate_batch evaluate_plan(verify=false)     evaluate.hpp:153-210
+ *   mgs_window_boundary plan_window_boundary         baselines.hpp:139-289
  *   mgs_goodput_table_batch  solve_dp's ub_suffix table  solvers.hpp:258-280
  *                      for a batch of traces sharing one window's tables
  */
@@ -57,7 +58,8 @@ typedef enum {
   MGS_ERR_PLAN_INFEASIBLE = 10,        /* "plan.infeasible" evaluate.hpp:165 */
   MGS_ERR_CUDA = 11,                   /* device failure (no reference analogue) */
   MGS_ERR_ARGUMENT = 12,               /* null pointer / size out of range */
-  MGS_ERR_BRUTEFORCE_CAP = 13          /* "planner.bruteforce-cap" solvers.hpp:153-158 */
+  MGS_ERR_BRUTEFORCE_CAP = 13,         /* "planner.bruteforce-cap" solvers.hpp:153-158 */
+  MGS_ERR_WINDOW_BOUNDARY = 14         /* "infeasible.window-boundary" baselines.hpp:280-281 */
 } mgs_status;
 
 typedef struct {
@@ -193,6 +195,13 @@ MGS_API int mgs_solve_batch(mgs_ctx* ctx, const mgs_problem* problems, int32_t n
 MGS_API int mgs_evaluate_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* plans, int32_t n_plans,
                        const int64_t* arrivals, int32_t n_traces, double* total, double* throughput,
                        mgs_error* err);
+
+/* plan_window_boundary (the Ekya-like comparison planner): retraining starts
+ * at step 0, the allocation changes only at step 0 and at retraining
+ * completions; exhaustive over per-tenant GPC counts with a phase DP on the
+ * device. Outputs as for mgs_solve_window (objective = evaluate_plan total). */
+MGS_API int mgs_window_boundary(mgs_ctx* ctx, const mgs_problem* p, int32_t* out_option, int32_t* out_config,
+                                int8_t* out_labels, double* out_objective, mgs_error* err);
 
 /* The Goodput table for n_traces traces that share one window's lattice and
  * tables (configs 2/4): best[b*S+s] = max(0, max over candidates of

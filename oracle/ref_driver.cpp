@@ -10,6 +10,7 @@
 //       solve_bruteforce (:143)] -> evaluate_plan (evaluate.hpp:153); prints
 //       one JSON object: plan encoding (space.hpp:231), objective bits, per-(s,m)
 //       SLO-attained throughput bits, wall time, or the Error code.
+//       --wb adds plan_window_boundary (baselines.hpp:139-289) under "wb".
 //       --chain re-plans with initial = final_ranges(first plan)
 //       (solver_test.cpp:130-147 semantics).
 //   migref gen-random <seed> <count> <outdir> [--no-drop]
@@ -29,6 +30,7 @@
 #ifndef MIGSIM_DATA_DIR
 #define MIGSIM_DATA_DIR "/nonexistent"
 #endif
+#include "migsim/baselines.hpp"
 #include "migsim/solvers.hpp"
 #include "test_util.hpp"  // reference tests/test_util.hpp (via -I)
 
@@ -99,13 +101,14 @@ int cmd_solve(int argc, char** argv) {
   std::string path = argv[2];
   int window = 0;
   SolveOptions opt;
-  bool chain = false, bf = false;
+  bool chain = false, bf = false, wb = false;
   for (int i = 3; i < argc; ++i) {
     std::string a = argv[i];
     if (a == "--workers") opt.workers = std::atoi(argv[++i]);
     else if (a == "--budget") opt.state_budget = std::strtoull(argv[++i], nullptr, 10);
     else if (a == "--chain") chain = true;
     else if (a == "--bf") bf = true;
+    else if (a == "--wb") wb = true;
     else window = std::atoi(a.c_str());
   }
   std::string out = guarded([&] {
@@ -118,12 +121,14 @@ int cmd_solve(int argc, char** argv) {
     std::string o = "{\"dp\":" + plan_json(ctx, dp, fc) + ",\"seconds\":" + fmt_real(secs) +
                     ",\"options\":" + std::to_string(engine::Space::build(ctx).options.size());
     if (bf) o += ",\"bf\":" + guarded([&] { return plan_json(ctx, solve_bruteforce(ctx, fc, opt), fc); });
+    if (wb) o += ",\"wb\":" + guarded([&] { return plan_json(ctx, plan_window_boundary(ctx, fc), fc); });
     if (chain) {
       PlanContext chained = ctx;
       chained.initial = final_ranges(sc, dp);
       o += ",\"chain\":{\"initial\":" + initial_json(*chained.initial) +
            ",\"dp\":" + guarded([&] { return plan_json(chained, solve_dp(chained, fc, opt), fc); });
       if (bf) o += ",\"bf\":" + guarded([&] { return plan_json(chained, solve_bruteforce(chained, fc, opt), fc); });
+      if (wb) o += ",\"wb\":" + guarded([&] { return plan_json(chained, plan_window_boundary(chained, fc), fc); });
       o += "}";
     }
     return o + "}";

@@ -34,6 +34,7 @@ STATUS_CODES = {
     11: "device.cuda",
     12: "input.argument",
     13: "planner.bruteforce-cap",
+    14: "infeasible.window-boundary",
 }
 
 
@@ -134,13 +135,16 @@ def load():
                                             P(C.c_double), P(C.c_int32), P(mgs_error)]
     lib.mgs_goodput_table_batch_device.argtypes = [C.c_void_p, P(mgs_problem), C.c_void_p, C.c_int32, C.c_void_p,
                                                    C.c_void_p, P(C.c_int32), P(mgs_error)]
+    lib.mgs_window_boundary.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_int32), P(C.c_int32), P(C.c_int8),
+                                        P(C.c_double), P(mgs_error)]
     _LIB = lib
     return lib
 
 
 EXPORTED_SYMBOLS = ["mgs_open", "mgs_close", "mgs_status_code", "mgs_version", "mgs_set_stream", "mgs_enumerate",
                     "mgs_goodput_table", "mgs_solve_window", "mgs_solve_batch", "mgs_evaluate_batch",
-                    "mgs_precheck", "mgs_bruteforce", "mgs_goodput_table_batch", "mgs_goodput_table_batch_device"]
+                    "mgs_precheck", "mgs_bruteforce", "mgs_goodput_table_batch", "mgs_goodput_table_batch_device",
+                    "mgs_window_boundary"]
 
 
 def empty_error():

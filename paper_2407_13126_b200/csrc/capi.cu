@@ -195,6 +195,7 @@ const char* mgs_status_code(int status) {
     case MGS_ERR_CUDA: return "device.cuda";
     case MGS_ERR_ARGUMENT: return "input.argument";
     case MGS_ERR_BRUTEFORCE_CAP: return "planner.bruteforce-cap";
+    case MGS_ERR_WINDOW_BOUNDARY: return "infeasible.window-boundary";
     default: return "unknown";
   }
 }
@@ -318,6 +319,31 @@ int mgs_bruteforce(mgs_ctx* ctx, const mgs_problem* p, double bruteforce_cap, in
     std::vector<int32_t> plan;
     if (!mgs::bruteforce(c, pr, sp, d_recv, plan))
       throw PlanFail{MGS_ERR_INFEASIBLE_JOINT, "no feasible allocation sequence exists for this window"};
+    const double total = plan_total(c, pr, sp, plan);
+    copy_plan_labels(c, sp, plan, out_config, out_labels);
+    if (out_option)
+      for (int s = 0; s < S; ++s) out_option[s] = plan[s];
+    if (out_objective) *out_objective = total;
+  });
+}
+
+int mgs_window_boundary(mgs_ctx* ctx, const mgs_problem* p, int32_t* out_option, int32_t* out_config,
+                        int8_t* out_labels, double* out_objective, mgs_error* err) {
+  if (!ctx || !p) return MGS_ERR_ARGUMENT;
+  return guarded(err, [&] {
+    Ctx& c = ctx->c;
+    MGS_CUDA_OK(cudaSetDevice(c.device));
+    c.kernel_launches = 0;
+    mgs::Prepared pr = prepare_problem(*p);
+    mgs::DevSpace sp;
+    mgs::build_space(c, p->lattice, pr, sp);
+    mgs::precheck_space(c, p->lattice, pr, sp);  // throw_if_infeasible(precheck_scenario) (baselines.hpp:141)
+    const int M = pr.t.M, S = pr.t.S;
+    if (p->forecast_len != S) throw PlanFail{MGS_ERR_INPUT_FORECAST, "forecast horizon != window size"};
+    double* d_recv = upload_forecast(c, *p, M, S);
+    std::vector<int32_t> plan;
+    if (!mgs::window_boundary(c, pr, sp, p->lattice, d_recv, plan))
+      throw PlanFail{MGS_ERR_WINDOW_BOUNDARY, "no window-boundary plan can complete every retraining"};
     const double total = plan_total(c, pr, sp, plan);
     copy_plan_labels(c, sp, plan, out_config, out_labels);
     if (out_option)

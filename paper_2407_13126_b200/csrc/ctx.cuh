@@ -205,6 +205,9 @@ std::vector<std::pair<int, int>> collect_violations(Ctx& c, const mgs_lattice& l
                                                     const DevSpace& sp);
 // bruteforce.cu: solve_bruteforce; false when no feasible all-done sequence
 bool bruteforce(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* d_recv, std::vector<int32_t>& plan);
+// wb.cu: plan_window_boundary; false when no k-vector is realizable
+bool window_boundary(Ctx& c, const Prepared& pr, const DevSpace& sp, const mgs_lattice& lat, const double* d_recv,
+                     std::vector<int32_t>& plan);
 // table.cu: batched ub table (Pareto placements prepared once per window shape)
 int table_prepare(Ctx& c, const Prepared& pr, const DevSpace& sp, double** wcp_out);
 void table_run(Ctx& c, const Prepared& pr, const double* wcp, int np, const int32_t* d_arr, int n_traces,

@@ -117,6 +117,21 @@ class Planner:
             raise capi.PlannerError(st, err)
         return opt, cfg, lab, obj.value
 
+    # -- plan_window_boundary (baselines.hpp:139-289) ----------------------------
+    def window_boundary(self, problem: Problem):
+        """Returns (options[S], config[S], labels[S][8], objective)."""
+        S = problem.S
+        opt = np.zeros(S, np.int32)
+        cfg = np.zeros(S, np.int32)
+        lab = np.zeros((S, capi.MAX_SLOTS), np.int8)
+        obj = C.c_double()
+        err = capi.empty_error()
+        st = self.lib.mgs_window_boundary(self.h, problem.byref(), capi.ptr(opt, C.c_int32), capi.ptr(cfg, C.c_int32),
+                                          capi.ptr(lab, C.c_int8), C.byref(obj), C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        return opt, cfg, lab, obj.value
+
     def solve_batch(self, problems):
         n = len(problems)
         s_max = max(p.S for p in problems)

@@ -278,3 +278,33 @@ def test_goodput_table_batch_c4_matches_oracle(gpu, tmp_path):
         q = SC.Problem(p.scenario, 0, forecast=traces[b].astype(np.int64))
         ub_o, _, _ = B.goodput_table(q)
         assert ub[b].tobytes() == ub_o.tobytes(), b
+
+
+def test_window_boundary_matches_reference(gpu, golden_dir):
+    """plan_window_boundary (the Ekya-like baseline, §8(f) row 1) on the GPU ==
+    the unmodified reference: plan encoding and evaluate_plan objective bits,
+    cold and chained, on the random corpus, the config-1 fixtures and the KATs."""
+    import json
+    import os
+    wb = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "wb_golden.json")))
+    n = 0
+    for kind in ("random", "c1", "kat"):
+        for stem, path, g in golden_dir[kind]:
+            if stem not in wb:
+                continue
+            sc = SC.load_scenario(path)
+            runs = [(None, wb[stem]["wb"])]
+            if "chain" in wb[stem]:
+                runs.append(([tuple(x) for x in wb[stem]["chain"]["initial"]], wb[stem]["chain"]["wb"]))
+            for initial, want in runs:
+                p = SC.Problem(sc, 0, initial=initial)
+                if "error" in want:
+                    with pytest.raises(capi.PlannerError) as e:
+                        gpu.window_boundary(p)
+                    assert e.value.code == want["error"], stem
+                    continue
+                opt, cfg, lab, obj = gpu.window_boundary(p)
+                assert planner.encode(cfg, lab, nslots(sc)) == want["encode"], (stem, initial is not None)
+                assert bits(obj) == want["obj"], stem
+                n += 1
+    assert n >= 150
