@@ -19,6 +19,7 @@
  *                      per-scenario call in a host loop)
  *   mgs_evaluate_batch evaluate_plan(verify=false)     evaluate.hpp:153-210
  *   mgs_window_boundary plan_window_boundary         baselines.hpp:139-289
+ *   mgs_replay_requests run_requests (one window)      simulator.hpp:209-275
  *   mgs_goodput_table_batch  solve_dp's ub_suffix table  solvers.hpp:258-280
  *                      for a batch of traces sharing one window's tables
  */
@@ -134,6 +135,14 @@ typedef struct {
   int32_t model;
 } mgs_violation;
 
+/* JobMetrics counters of one tenant (simulator.hpp:17-32); the fractions
+ * (goodput, slo_attainment, accuracy) follow from them (finalize_fractions). */
+typedef struct {
+  double received, served, timely, correct, valid, dropped, queued_at_end;
+  int32_t reconfigurations;
+  double overhead_seconds;
+} mgs_job_metrics;
+
 typedef struct mgs_ctx mgs_ctx;
 
 MGS_API int mgs_open(int device, mgs_ctx** out);
@@ -202,6 +211,15 @@ MGS_API int mgs_evaluate_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t
  * device. Outputs as for mgs_solve_window (objective = evaluate_plan total). */
 MGS_API int mgs_window_boundary(mgs_ctx* ctx, const mgs_problem* p, int32_t* out_option, int32_t* out_config,
                                 int8_t* out_labels, double* out_objective, mgs_error* err);
+
+/* Request-mode replay (run_requests, single-window scenario, no pre-init
+ * overrides) of n_plans x n_traces x n_seeds runs on the device:
+ * plans[i*S+s] option indices, arrivals[t*M*S+m*S+s], seeds[k];
+ * slo[m] = 2*latency_full (seconds), step_seconds = Scenario::step_seconds.
+ * out[((i*n_traces + t)*n_seeds + k)*M + m]. */
+MGS_API int mgs_replay_requests(mgs_ctx* ctx, const mgs_problem* p, const double* slo, double step_seconds,
+                                const int32_t* plans, int32_t n_plans, const int64_t* arrivals, int32_t n_traces,
+                                const uint64_t* seeds, int32_t n_seeds, mgs_job_metrics* out, mgs_error* err);
 
 /* The Goodput table for n_traces traces that share one window's lattice and
  * tables (configs 2/4): best[b*S+s] = max(0, max over candidates of

@@ -13,6 +13,10 @@
 //       --wb adds plan_window_boundary (baselines.hpp:139-289) under "wb".
 //       --chain re-plans with initial = final_ranges(first plan)
 //       (solver_test.cpp:130-147 semantics).
+//   migref replay <scenario.scn> <seed>...
+//       run_requests (simulator.hpp:209-275) of the window-0 solve_dp plan
+//       (no pre-initialisation overrides) for each seed; prints per-model
+//       JobMetrics counters as hex bits.
 //   migref gen-random <seed> <count> <outdir> [--no-drop]
 //       the reference's own randomized oracle corpus generator
 //       (tests/test_util.hpp:104-181), written to files with
@@ -31,6 +35,7 @@
 #define MIGSIM_DATA_DIR "/nonexistent"
 #endif
 #include "migsim/baselines.hpp"
+#include "migsim/simulator.hpp"
 #include "migsim/solvers.hpp"
 #include "test_util.hpp"  // reference tests/test_util.hpp (via -I)
 
@@ -137,6 +142,34 @@ int cmd_solve(int argc, char** argv) {
   return 0;
 }
 
+int cmd_replay(int argc, char** argv) {
+  if (argc < 4) return 2;
+  std::string out = guarded([&] {
+    Scenario sc = load_scenario(argv[2]);
+    PlanContext ctx{&sc, 0, std::nullopt};
+    ArrivalForecast fc = window_forecast(sc, 0);
+    AllocationSequence dp = solve_dp(ctx, fc);
+    std::vector<EffectivePlan> plans{EffectivePlan{dp, {}}};
+    std::string o = "{\"runs\":[";
+    for (int i = 3; i < argc; ++i) {
+      const uint64_t seed = std::strtoull(argv[i], nullptr, 10);
+      Metrics mt = run_requests(sc, plans, seed);
+      o += std::string(i > 3 ? "," : "") + "{\"seed\":" + std::to_string(seed) + ",\"jobs\":[";
+      for (size_t m = 0; m < mt.jobs.size(); ++m) {
+        const JobMetrics& j = mt.jobs[m];
+        o += std::string(m ? "," : "") + "[\"" + hexbits(j.received) + "\",\"" + hexbits(j.served) + "\",\"" +
+             hexbits(j.timely) + "\",\"" + hexbits(j.correct) + "\",\"" + hexbits(j.valid) + "\",\"" +
+             hexbits(j.dropped) + "\",\"" + hexbits(j.queued_at_end) + "\"," + std::to_string(j.reconfigurations) +
+             ",\"" + hexbits(j.overhead_seconds) + "\"]";
+      }
+      o += "]}";
+    }
+    return o + "]}";
+  });
+  std::printf("%s\n", out.c_str());
+  return 0;
+}
+
 int cmd_gen_random(int argc, char** argv) {
   if (argc < 5) return 2;
   unsigned seed = static_cast<unsigned>(std::strtoul(argv[2], nullptr, 10));
@@ -190,6 +223,7 @@ int main(int argc, char** argv) {
   std::string cmd = argv[1];
   if (cmd == "solve") return cmd_solve(argc, argv);
   if (cmd == "gen-random") return cmd_gen_random(argc, argv);
+  if (cmd == "replay") return cmd_replay(argc, argv);
   std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
   return 2;
 }

@@ -66,6 +66,12 @@ class mgs_violation(C.Structure):
     _fields_ = [("code", C.c_int32), ("model", C.c_int32)]
 
 
+class mgs_job_metrics(C.Structure):
+    _fields_ = [("received", C.c_double), ("served", C.c_double), ("timely", C.c_double), ("correct", C.c_double),
+                ("valid", C.c_double), ("dropped", C.c_double), ("queued_at_end", C.c_double),
+                ("reconfigurations", C.c_int32), ("overhead_seconds", C.c_double)]
+
+
 class mgs_stats(C.Structure):
     _fields_ = [("options", C.c_uint64), ("candidates", C.c_uint64), ("transitions_ref", C.c_uint64),
                 ("transitions", C.c_uint64), ("frontier_total", C.c_uint64), ("frontier_peak", C.c_uint64),
@@ -137,6 +143,9 @@ def load():
                                                    C.c_void_p, P(C.c_int32), P(mgs_error)]
     lib.mgs_window_boundary.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_int32), P(C.c_int32), P(C.c_int8),
                                         P(C.c_double), P(mgs_error)]
+    lib.mgs_replay_requests.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_double), C.c_double, P(C.c_int32),
+                                        C.c_int32, P(C.c_int64), C.c_int32, P(C.c_uint64), C.c_int32,
+                                        P(mgs_job_metrics), P(mgs_error)]
     _LIB = lib
     return lib
 
@@ -144,7 +153,7 @@ def load():
 EXPORTED_SYMBOLS = ["mgs_open", "mgs_close", "mgs_status_code", "mgs_version", "mgs_set_stream", "mgs_enumerate",
                     "mgs_goodput_table", "mgs_solve_window", "mgs_solve_batch", "mgs_evaluate_batch",
                     "mgs_precheck", "mgs_bruteforce", "mgs_goodput_table_batch", "mgs_goodput_table_batch_device",
-                    "mgs_window_boundary"]
+                    "mgs_window_boundary", "mgs_replay_requests"]
 
 
 def empty_error():

@@ -208,6 +208,10 @@ bool bruteforce(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* d_
 // wb.cu: plan_window_boundary; false when no k-vector is realizable
 bool window_boundary(Ctx& c, const Prepared& pr, const DevSpace& sp, const mgs_lattice& lat, const double* d_recv,
                      std::vector<int32_t>& plan);
+// replay.cu: run_requests for plans x traces x seeds
+void replay_requests(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* psi, const double* slo,
+                     double step_seconds, const int32_t* d_plans, int n_plans, const int64_t* d_arr, int n_traces,
+                     const uint64_t* d_seeds, int n_seeds, mgs_job_metrics* d_out);
 // table.cu: batched ub table (Pareto placements prepared once per window shape)
 int table_prepare(Ctx& c, const Prepared& pr, const DevSpace& sp, double** wcp_out);
 void table_run(Ctx& c, const Prepared& pr, const double* wcp, int np, const int32_t* d_arr, int n_traces,

@@ -132,6 +132,26 @@ class Planner:
             raise capi.PlannerError(st, err)
         return opt, cfg, lab, obj.value
 
+    # -- run_requests (simulator.hpp:209-275), one window ----------------------------
+    def replay_requests(self, problem: Problem, plans, arrivals, seeds, step_seconds=1.0):
+        """plans [n_p][S] option indices, arrivals [n_t][M][S], seeds [n_s].
+        Returns mgs_job_metrics as a structured numpy array [n_p][n_t][n_s][M]."""
+        plans = np.ascontiguousarray(plans, dtype=np.int32).reshape(-1, problem.S)
+        arrivals = np.ascontiguousarray(arrivals, dtype=np.int64).reshape(-1, problem.M, problem.S)
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64).reshape(-1)
+        slo = np.asarray([2.0 * m.latency_full for m in problem.scenario.models], dtype=np.float64)  # slo_target
+        n = plans.shape[0] * arrivals.shape[0] * seeds.shape[0] * problem.M
+        out = (capi.mgs_job_metrics * max(1, n))()
+        err = capi.empty_error()
+        st = self.lib.mgs_replay_requests(self.h, problem.byref(), capi.ptr(slo, C.c_double), float(step_seconds),
+                                          capi.ptr(plans, C.c_int32), plans.shape[0], capi.ptr(arrivals, C.c_int64),
+                                          arrivals.shape[0], capi.ptr(seeds, C.c_uint64), seeds.shape[0], out,
+                                          C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        arr = np.ctypeslib.as_array(out)[:n]
+        return arr.reshape(plans.shape[0], arrivals.shape[0], seeds.shape[0], problem.M)
+
     def solve_batch(self, problems):
         n = len(problems)
         s_max = max(p.S for p in problems)

@@ -308,3 +308,31 @@ def test_window_boundary_matches_reference(gpu, golden_dir):
                 assert bits(obj) == want["obj"], stem
                 n += 1
     assert n >= 150
+
+
+def test_replay_requests_matches_reference(gpu, golden_dir):
+    """Request-mode replay (run_requests, §8(f) row 2) of each window's solve_dp
+    plan: every tenant's counters bit-equal to the unmodified reference
+    (per-request mt19937_64 correctness draws, FIFO deadlines, psi spill)."""
+    import json
+    import os
+    rp = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "replay_golden.json")))
+    fields = ("received", "served", "timely", "correct", "valid", "dropped", "queued_at_end")
+    n = 0
+    for kind in ("random", "c1", "kat"):
+        for stem, path, g in golden_dir[kind]:
+            want = rp.get(stem)
+            if not want or "runs" not in want:
+                continue
+            p = SC.Problem(SC.load_scenario(path), 0)
+            opt = gpu.solve_window(p)[0]
+            seeds = [r["seed"] for r in want["runs"]]
+            got = gpu.replay_requests(p, opt[None], p.forecast[None], seeds)
+            for k, run in enumerate(want["runs"]):
+                for m, job in enumerate(run["jobs"]):
+                    r = got[0, 0, k, m]
+                    assert [bits(r[f]) for f in fields] == job[:7], (stem, run["seed"], m)
+                    assert int(r["reconfigurations"]) == job[7], (stem, m)
+                    assert bits(r["overhead_seconds"]) == job[8], (stem, m)
+                    n += 1
+    assert n >= 300
