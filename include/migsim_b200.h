@@ -20,6 +20,7 @@
  *   mgs_evaluate_batch evaluate_plan(verify=false)     evaluate.hpp:153-210
  *   mgs_window_boundary plan_window_boundary         baselines.hpp:139-289
  *   mgs_replay_requests run_requests (one window)      simulator.hpp:209-275
+ *   mgs_preinit        plan_preinit + apply_preinit    preinit.hpp:41-114
  *   mgs_goodput_table_batch  solve_dp's ub_suffix table  solvers.hpp:258-280
  *                      for a batch of traces sharing one window's tables
  */
@@ -200,10 +201,21 @@ MGS_API int mgs_solve_batch(mgs_ctx* ctx, const mgs_problem* problems, int32_t n
 /* evaluate_plan(verify_feasibility=false) for n_plans plans x n_traces traces
  * sharing one window's tables: plans[i*S+s] = option index,
  * arrivals[t*M*S + m*S + s]. total[i*n_traces+t] = objective;
- * throughput (optional, [i][t][s][m]) = SLO-attained counts. */
+ * throughput (optional, [i][t][s][m]) = SLO-attained counts. overrides
+ * (optional, [i][s][m], nonzero = psi_eff 0) are OverheadOverrides, e.g. the
+ * pre-initialisation result of mgs_preinit. */
 MGS_API int mgs_evaluate_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* plans, int32_t n_plans,
-                       const int64_t* arrivals, int32_t n_traces, double* total, double* throughput,
-                       mgs_error* err);
+                       const uint8_t* overrides, const int64_t* arrivals, int32_t n_traces, double* total,
+                       double* throughput, mgs_error* err);
+
+/* Pre-initialisation (plan_preinit + apply_preinit, preinit.hpp:41-114) of
+ * n_plans plans: overrides[i*S*M + s*M + m] = 1 where tenant m's overhead at
+ * step s drops to 0 (every instance it acquires was created early on unused
+ * slices during s-1); fired (optional) [i*S+s] = universe-id bitmask
+ * (instances in first-appearance order over the lattice) created early during
+ * step s. */
+MGS_API int mgs_preinit(mgs_ctx* ctx, const mgs_problem* p, const int32_t* plans, int32_t n_plans, uint8_t* overrides,
+                        uint32_t* fired, mgs_error* err);
 
 /* plan_window_boundary (the Ekya-like comparison planner): retraining starts
  * at step 0, the allocation changes only at step 0 and at retraining
@@ -215,10 +227,12 @@ MGS_API int mgs_window_boundary(mgs_ctx* ctx, const mgs_problem* p, int32_t* out
 /* Request-mode replay (run_requests, single-window scenario, no pre-init
  * overrides) of n_plans x n_traces x n_seeds runs on the device:
  * plans[i*S+s] option indices, arrivals[t*M*S+m*S+s], seeds[k];
- * slo[m] = 2*latency_full (seconds), step_seconds = Scenario::step_seconds.
+ * slo[m] = 2*latency_full (seconds), step_seconds = Scenario::step_seconds;
+ * overrides as for mgs_evaluate_batch (EffectivePlan::overrides) or NULL.
  * out[((i*n_traces + t)*n_seeds + k)*M + m]. */
 MGS_API int mgs_replay_requests(mgs_ctx* ctx, const mgs_problem* p, const double* slo, double step_seconds,
-                                const int32_t* plans, int32_t n_plans, const int64_t* arrivals, int32_t n_traces,
+                                const int32_t* plans, int32_t n_plans, const uint8_t* overrides,
+                                const int64_t* arrivals, int32_t n_traces,
                                 const uint64_t* seeds, int32_t n_seeds, mgs_job_metrics* out, mgs_error* err);
 
 /* The Goodput table for n_traces traces that share one window's lattice and

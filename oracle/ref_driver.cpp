@@ -17,6 +17,10 @@
 //       run_requests (simulator.hpp:209-275) of the window-0 solve_dp plan
 //       (no pre-initialisation overrides) for each seed; prints per-model
 //       JobMetrics counters as hex bits.
+//   migref preinit <scenario.scn> <seed>
+//       plan_preinit + apply_preinit (preinit.hpp:41-114) of the window-0
+//       solve_dp plan: overrides, evaluate_plan total with them,
+//       overhead_summary, and run_requests of the EffectivePlan.
 //   migref gen-random <seed> <count> <outdir> [--no-drop]
 //       the reference's own randomized oracle corpus generator
 //       (tests/test_util.hpp:104-181), written to files with
@@ -170,6 +174,59 @@ int cmd_replay(int argc, char** argv) {
   return 0;
 }
 
+std::string jobs_json(const Metrics& mt) {
+  std::string o = "[";
+  for (size_t m = 0; m < mt.jobs.size(); ++m) {
+    const JobMetrics& j = mt.jobs[m];
+    o += std::string(m ? "," : "") + "[\"" + hexbits(j.received) + "\",\"" + hexbits(j.served) + "\",\"" +
+         hexbits(j.timely) + "\",\"" + hexbits(j.correct) + "\",\"" + hexbits(j.valid) + "\",\"" +
+         hexbits(j.dropped) + "\",\"" + hexbits(j.queued_at_end) + "\"," + std::to_string(j.reconfigurations) +
+         ",\"" + hexbits(j.overhead_seconds) + "\"]";
+  }
+  return o + "]";
+}
+
+std::string preinit_json(const Scenario& sc, const PlanContext& ctx, const ArrivalForecast& fc,
+                         const AllocationSequence& seq, uint64_t seed) {
+  auto actions = plan_preinit(sc.catalog, seq);
+  EffectivePlan eff = apply_preinit(ctx, seq, actions);
+  engine::Space sp = engine::Space::build(ctx);
+  auto enc = sp.encode(seq);
+  std::string o = "{\"encode\":[";
+  for (size_t i = 0; i < enc.size(); ++i) o += (i ? "," : "") + std::to_string(enc[i]);
+  o += "],\"overrides\":[";
+  bool first = true;
+  for (const auto& [key, v] : eff.overrides) {
+    o += std::string(first ? "" : ",") + "[" + std::to_string(key.first) + "," + std::to_string(key.second) + "]";
+    first = false;
+  }
+  PlanScore ps = evaluate_plan(ctx, seq, fc.counts, &eff.overrides);
+  OverheadSummary os = overhead_summary(ctx, seq, &eff.overrides);
+  o += "],\"actions\":" + std::to_string(actions.size()) + ",\"obj\":\"" + hexbits(ps.total) +
+       "\",\"reconfigurations\":" + std::to_string(os.reconfigurations) + ",\"overhead\":\"" +
+       hexbits(os.total_overhead) + "\",\"seed\":" + std::to_string(seed) +
+       ",\"jobs\":" + jobs_json(run_requests(sc, {eff}, seed)) + "}";
+  return o;
+}
+
+int cmd_preinit(int argc, char** argv) {
+  if (argc < 4) return 2;
+  const int n_random = argc > 4 ? std::atoi(argv[4]) : 0;
+  std::string out = guarded([&] {
+    Scenario sc = load_scenario(argv[2]);
+    const uint64_t seed = std::strtoull(argv[3], nullptr, 10);
+    PlanContext ctx{&sc, 0, std::nullopt};
+    ArrivalForecast fc = window_forecast(sc, 0);
+    std::string o = "{\"dp\":" + preinit_json(sc, ctx, fc, solve_dp(ctx, fc), seed) + ",\"random\":[";
+    std::mt19937 rng(static_cast<unsigned>(seed));
+    for (int k = 0; k < n_random; ++k)  // sparse random feasible plans leave pre-initialisation room to act
+      o += std::string(k ? "," : "") + preinit_json(sc, ctx, fc, testutil::random_feasible_plan(sc, rng, true), seed);
+    return o + "]}";
+  });
+  std::printf("%s\n", out.c_str());
+  return 0;
+}
+
 int cmd_gen_random(int argc, char** argv) {
   if (argc < 5) return 2;
   unsigned seed = static_cast<unsigned>(std::strtoul(argv[2], nullptr, 10));
@@ -224,6 +281,7 @@ int main(int argc, char** argv) {
   if (cmd == "solve") return cmd_solve(argc, argv);
   if (cmd == "gen-random") return cmd_gen_random(argc, argv);
   if (cmd == "replay") return cmd_replay(argc, argv);
+  if (cmd == "preinit") return cmd_preinit(argc, argv);
   std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
   return 2;
 }

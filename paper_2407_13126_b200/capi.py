@@ -131,8 +131,10 @@ def load():
                                      P(C.c_double), P(mgs_stats), P(mgs_error)]
     lib.mgs_solve_batch.argtypes = [C.c_void_p, P(mgs_problem), C.c_int32, C.c_int32, P(C.c_int32),
                                     P(C.c_double), P(C.c_int32), P(mgs_stats), P(mgs_error)]
-    lib.mgs_evaluate_batch.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_int32), C.c_int32, P(C.c_int64),
-                                       C.c_int32, P(C.c_double), P(C.c_double), P(mgs_error)]
+    lib.mgs_evaluate_batch.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_int32), C.c_int32, P(C.c_uint8),
+                                       P(C.c_int64), C.c_int32, P(C.c_double), P(C.c_double), P(mgs_error)]
+    lib.mgs_preinit.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_int32), C.c_int32, P(C.c_uint8), P(C.c_uint32),
+                                P(mgs_error)]
     lib.mgs_precheck.argtypes = [C.c_void_p, P(mgs_lattice), P(mgs_tables), P(mgs_violation), C.c_int32,
                                  P(C.c_int32), P(mgs_error)]
     lib.mgs_bruteforce.argtypes = [C.c_void_p, P(mgs_problem), C.c_double, P(C.c_int32), P(C.c_int32), P(C.c_int8),
@@ -144,7 +146,7 @@ def load():
     lib.mgs_window_boundary.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_int32), P(C.c_int32), P(C.c_int8),
                                         P(C.c_double), P(mgs_error)]
     lib.mgs_replay_requests.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_double), C.c_double, P(C.c_int32),
-                                        C.c_int32, P(C.c_int64), C.c_int32, P(C.c_uint64), C.c_int32,
+                                        C.c_int32, P(C.c_uint8), P(C.c_int64), C.c_int32, P(C.c_uint64), C.c_int32,
                                         P(mgs_job_metrics), P(mgs_error)]
     _LIB = lib
     return lib
@@ -153,7 +155,7 @@ def load():
 EXPORTED_SYMBOLS = ["mgs_open", "mgs_close", "mgs_status_code", "mgs_version", "mgs_set_stream", "mgs_enumerate",
                     "mgs_goodput_table", "mgs_solve_window", "mgs_solve_batch", "mgs_evaluate_batch",
                     "mgs_precheck", "mgs_bruteforce", "mgs_goodput_table_batch", "mgs_goodput_table_batch_device",
-                    "mgs_window_boundary", "mgs_replay_requests"]
+                    "mgs_window_boundary", "mgs_replay_requests", "mgs_preinit"]
 
 
 def empty_error():

@@ -17,7 +17,7 @@ bool solve_dp_v2_supported(const Prepared& pr, const DevSpace& sp);
 void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& sp, const double* d_recv,
                  const double* d_ub, const double* d_incumbent, SolveOut& out);
 void evaluate_batch(Ctx& c, const Prepared& pr, const DevSpace& sp, const int32_t* d_plans, int n_plans,
-                    const int64_t* d_arr, int n_traces, double* d_total, double* d_thr);
+                    const int64_t* d_arr, int n_traces, double* d_total, double* d_thr, const uint8_t* d_overrides);
 }
 
 namespace {
@@ -88,7 +88,7 @@ double plan_total(Ctx& c, const mgs::Prepared& pr, const mgs::DevSpace& sp, cons
   double* d_total = c.buf<double>("plan_total", 1);
   MGS_CUDA_OK(cudaMemcpyAsync(d_plan, plan.data(), S * 4, cudaMemcpyHostToDevice, c.stream));
   int64_t* d_arr = c.buf<int64_t>("forecast_i64", static_cast<size_t>(M) * S);
-  mgs::evaluate_batch(c, pr, sp, d_plan, 1, d_arr, 1, d_total, nullptr);
+  mgs::evaluate_batch(c, pr, sp, d_plan, 1, d_arr, 1, d_total, nullptr, nullptr);
   double* h = c.pinned.get<double>(1);
   MGS_CUDA_OK(cudaMemcpyAsync(h, d_total, 8, cudaMemcpyDeviceToHost, c.stream));
   MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
@@ -143,7 +143,7 @@ void solve_one(Ctx& c, const mgs_problem& p, int32_t* out_option, int32_t* out_c
   double* d_total = c.buf<double>("plan_total", 1);
   MGS_CUDA_OK(cudaMemcpyAsync(d_plan, out.options.data(), S * 4, cudaMemcpyHostToDevice, c.stream));
   int64_t* d_arr = c.buf<int64_t>("forecast_i64", static_cast<size_t>(M) * S);
-  mgs::evaluate_batch(c, pr, sp, d_plan, 1, d_arr, 1, d_total, nullptr);
+  mgs::evaluate_batch(c, pr, sp, d_plan, 1, d_arr, 1, d_total, nullptr, nullptr);
   double total = 0.0;
   MGS_CUDA_OK(cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, c.stream));
   if (out_config || out_labels) {
@@ -353,7 +353,7 @@ int mgs_window_boundary(mgs_ctx* ctx, const mgs_problem* p, int32_t* out_option,
 }
 
 int mgs_replay_requests(mgs_ctx* ctx, const mgs_problem* p, const double* slo, double step_seconds, const int32_t* plans,
-                        int32_t n_plans, const int64_t* arrivals, int32_t n_traces, const uint64_t* seeds,
+                        int32_t n_plans, const uint8_t* overrides, const int64_t* arrivals, int32_t n_traces, const uint64_t* seeds,
                         int32_t n_seeds, mgs_job_metrics* out, mgs_error* err) {
   if (!ctx || !p || !slo || n_plans < 0 || n_traces < 0 || n_seeds < 0 || !(step_seconds > 0)) return MGS_ERR_ARGUMENT;
   const long long runs = static_cast<long long>(n_plans) * n_traces * n_seeds;
@@ -377,10 +377,38 @@ int mgs_replay_requests(mgs_ctx* ctx, const mgs_problem* p, const double* slo, d
     MGS_CUDA_OK(cudaMemcpyAsync(d_plans, plans, static_cast<size_t>(n_plans) * S * 4, cudaMemcpyHostToDevice, c.stream));
     MGS_CUDA_OK(cudaMemcpyAsync(d_arr, arrivals, static_cast<size_t>(n_traces) * M * S * 8, cudaMemcpyHostToDevice, c.stream));
     MGS_CUDA_OK(cudaMemcpyAsync(d_seeds, seeds, static_cast<size_t>(n_seeds) * 8, cudaMemcpyHostToDevice, c.stream));
-    mgs::replay_requests(c, pr, sp, p->tables.psi, slo, step_seconds, d_plans, n_plans, d_arr, n_traces, d_seeds,
-                         n_seeds, d_out);
+    uint8_t* d_ov = overrides ? c.buf<uint8_t>("rp_ov", static_cast<size_t>(n_plans) * S * M) : nullptr;
+    if (overrides)
+      MGS_CUDA_OK(cudaMemcpyAsync(d_ov, overrides, static_cast<size_t>(n_plans) * S * M, cudaMemcpyHostToDevice, c.stream));
+    mgs::replay_requests(c, pr, sp, p->tables.psi, slo, step_seconds, d_plans, d_ov, n_plans, d_arr, n_traces,
+                         d_seeds, n_seeds, d_out);
     MGS_CUDA_OK(cudaMemcpyAsync(out, d_out, static_cast<size_t>(runs) * M * sizeof(mgs_job_metrics),
                                 cudaMemcpyDeviceToHost, c.stream));
+    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int mgs_preinit(mgs_ctx* ctx, const mgs_problem* p, const int32_t* plans, int32_t n_plans, uint8_t* overrides,
+                uint32_t* fired, mgs_error* err) {
+  if (!ctx || !p || n_plans < 0 || (n_plans > 0 && (!plans || !overrides))) return MGS_ERR_ARGUMENT;
+  return guarded(err, [&] {
+    Ctx& c = ctx->c;
+    MGS_CUDA_OK(cudaSetDevice(c.device));
+    mgs::Prepared pr = prepare_problem(*p);
+    mgs::DevSpace sp;
+    mgs::build_space(c, p->lattice, pr, sp);
+    const int M = pr.t.M, S = pr.t.S;
+    for (long long k = 0; k < static_cast<long long>(n_plans) * S; ++k)
+      if (plans[k] < 0 || plans[k] >= sp.n_opt) throw PlanFail{MGS_ERR_PLAN_INFEASIBLE, "plan names an unknown option"};
+    if (n_plans == 0) return;
+    int32_t* d_plans = c.buf<int32_t>("pi_plans", static_cast<size_t>(n_plans) * S);
+    uint8_t* d_ov = c.buf<uint8_t>("pi_ov", static_cast<size_t>(n_plans) * S * M);
+    uint32_t* d_fired = fired ? c.buf<uint32_t>("pi_fired", static_cast<size_t>(n_plans) * S) : nullptr;
+    MGS_CUDA_OK(cudaMemcpyAsync(d_plans, plans, static_cast<size_t>(n_plans) * S * 4, cudaMemcpyHostToDevice, c.stream));
+    mgs::preinit_overrides(c, pr, sp, p->lattice, d_plans, n_plans, d_ov, d_fired);
+    MGS_CUDA_OK(cudaMemcpyAsync(overrides, d_ov, static_cast<size_t>(n_plans) * S * M, cudaMemcpyDeviceToHost, c.stream));
+    if (fired)
+      MGS_CUDA_OK(cudaMemcpyAsync(fired, d_fired, static_cast<size_t>(n_plans) * S * 4, cudaMemcpyDeviceToHost, c.stream));
     MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
   });
 }
@@ -512,7 +540,8 @@ int mgs_solve_batch(mgs_ctx* ctx, const mgs_problem* problems, int32_t n, int32_
 }
 
 int mgs_evaluate_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* plans, int32_t n_plans,
-                       const int64_t* arrivals, int32_t n_traces, double* total, double* throughput, mgs_error* err) {
+                       const uint8_t* overrides, const int64_t* arrivals, int32_t n_traces, double* total,
+                       double* throughput, mgs_error* err) {
   if (!ctx || !p || !plans || !arrivals || !total || n_plans < 0 || n_traces < 0) return MGS_ERR_ARGUMENT;
   return guarded(err, [&] {
     Ctx& c = ctx->c;
@@ -528,9 +557,12 @@ int mgs_evaluate_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* plans,
     int64_t* d_arr = c.buf<int64_t>("eval_arr", static_cast<size_t>(n_traces) * M * S);
     double* d_total = c.buf<double>("eval_total", static_cast<size_t>(n_plans) * n_traces);
     double* d_thr = throughput ? c.buf<double>("eval_thr", static_cast<size_t>(n_plans) * n_traces * S * M) : nullptr;
+    uint8_t* d_ov = overrides ? c.buf<uint8_t>("eval_ov", static_cast<size_t>(n_plans) * S * M) : nullptr;
+    if (overrides)
+      MGS_CUDA_OK(cudaMemcpyAsync(d_ov, overrides, static_cast<size_t>(n_plans) * S * M, cudaMemcpyHostToDevice, c.stream));
     MGS_CUDA_OK(cudaMemcpyAsync(d_plans, plans, static_cast<size_t>(n_plans) * S * 4, cudaMemcpyHostToDevice, c.stream));
     MGS_CUDA_OK(cudaMemcpyAsync(d_arr, arrivals, static_cast<size_t>(n_traces) * M * S * 8, cudaMemcpyHostToDevice, c.stream));
-    mgs::evaluate_batch(c, pr, sp, d_plans, n_plans, d_arr, n_traces, d_total, d_thr);
+    mgs::evaluate_batch(c, pr, sp, d_plans, n_plans, d_arr, n_traces, d_total, d_thr, d_ov);
     MGS_CUDA_OK(cudaMemcpyAsync(total, d_total, static_cast<size_t>(n_plans) * n_traces * 8, cudaMemcpyDeviceToHost, c.stream));
     if (throughput)
       MGS_CUDA_OK(cudaMemcpyAsync(throughput, d_thr, static_cast<size_t>(n_plans) * n_traces * S * M * 8,

@@ -210,8 +210,11 @@ bool window_boundary(Ctx& c, const Prepared& pr, const DevSpace& sp, const mgs_l
                      std::vector<int32_t>& plan);
 // replay.cu: run_requests for plans x traces x seeds
 void replay_requests(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* psi, const double* slo,
-                     double step_seconds, const int32_t* d_plans, int n_plans, const int64_t* d_arr, int n_traces,
-                     const uint64_t* d_seeds, int n_seeds, mgs_job_metrics* d_out);
+                     double step_seconds, const int32_t* d_plans, const uint8_t* d_overrides, int n_plans,
+                     const int64_t* d_arr, int n_traces, const uint64_t* d_seeds, int n_seeds, mgs_job_metrics* d_out);
+// preinit.cu: plan_preinit + apply_preinit overrides [n_plans][S][M], fired [n_plans][S]
+void preinit_overrides(Ctx& c, const Prepared& pr, const DevSpace& sp, const mgs_lattice& lat, const int32_t* d_plans,
+                       int n_plans, uint8_t* d_overrides, uint32_t* d_fired);
 // table.cu: batched ub table (Pareto placements prepared once per window shape)
 int table_prepare(Ctx& c, const Prepared& pr, const DevSpace& sp, double** wcp_out);
 void table_run(Ctx& c, const Prepared& pr, const double* wcp, int np, const int32_t* d_arr, int n_traces,

@@ -175,8 +175,9 @@ void goodput_reductions(Ctx& c, const Prepared& pr, const DevSpace& sp, const do
 
 // ---------------------------------------------------------------------------
 // evaluate_plan(verify=false) batch: thread per (plan, trace).
-__global__ void k_evaluate(DevSpace sp, HostTables t, const int32_t* plans, int n_plans, const int64_t* arrivals,
-                           int n_traces, int has_initial, uint4 init_lo, double* total, double* thr_out) {
+__global__ void k_evaluate(DevSpace sp, HostTables t, const int32_t* plans, int n_plans, const uint8_t* overrides,
+                           const int64_t* arrivals, int n_traces, int has_initial, uint4 init_lo, double* total,
+                           double* thr_out) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= (long long)n_plans * n_traces) return;
   const int i = static_cast<int>(idx / n_traces), j = static_cast<int>(idx % n_traces);
@@ -199,7 +200,9 @@ __global__ void k_evaluate(DevSpace sp, HostTables t, const int32_t* plans, int 
     for (int m = 0; m < M; ++m) {
       const uint32_t mask = sp.opt_mask[o * KM + m];
       const bool changed = s == 0 ? (has_initial && mask != init[m]) : (mask != sp.opt_mask[plan[s - 1] * KM + m]);
-      const double eff = eff_cap(sp.opt_cap[o * KM + m], changed ? t.loss[m] : 0.0);
+      // an override (pre-initialisation, psi_eff = 0) replaces psi (evaluate.hpp:193-197)
+      const bool zero_psi = overrides && overrides[(static_cast<size_t>(i) * S + s) * M + m];
+      const double eff = eff_cap(sp.opt_cap[o * KM + m], changed && !zero_psi ? t.loss[m] : 0.0);
       const double thr = thr_of(static_cast<double>(arr[m * S + s]), eff);
       const double acc = s >= finish_after[m] ? t.post[m] : t.pre[m];
       tot = dadd(tot, dmul(thr, acc));
@@ -210,10 +213,10 @@ __global__ void k_evaluate(DevSpace sp, HostTables t, const int32_t* plans, int 
 }
 
 void evaluate_batch(Ctx& c, const Prepared& pr, const DevSpace& sp, const int32_t* d_plans, int n_plans,
-                    const int64_t* d_arr, int n_traces, double* d_total, double* d_thr) {
+                    const int64_t* d_arr, int n_traces, double* d_total, double* d_thr, const uint8_t* d_overrides) {
   const long long n = (long long)n_plans * n_traces;
   uint4 init{pr.init_mask[0], pr.init_mask[1], pr.init_mask[2], pr.init_mask[3]};
-  k_evaluate<<<ceil_div(n, 128), 128, 0, c.stream>>>(sp, pr.t, d_plans, n_plans, d_arr, n_traces, pr.has_initial,
+  k_evaluate<<<ceil_div(n, 128), 128, 0, c.stream>>>(sp, pr.t, d_plans, n_plans, d_overrides, d_arr, n_traces, pr.has_initial,
                                                      init, d_total, d_thr);
   MGS_CUDA_OK(cudaGetLastError());
 }

@@ -60,6 +60,7 @@ struct ReplayArgs {
   DevSpace sp;
   HostTables t;
   const int32_t* plans;    // [n_plans][S]
+  const uint8_t* overrides;  // [n_plans][S][M] psi_eff = 0 (pre-initialisation), or null
   const int64_t* arrivals; // [n_traces][M][S]
   const uint64_t* seeds;   // [n_seeds]
   int n_plans, n_traces, n_seeds;
@@ -107,7 +108,8 @@ __global__ void k_replay(ReplayArgs a) {
     const bool changed = s > 0 && a.sp.opt_mask[o * KM + m] != a.sp.opt_mask[plan[s - 1] * KM + m];
     double applied = 0.0;
     if (changed) {
-      applied = a.psi[m];
+      const bool zero = a.overrides && a.overrides[(static_cast<size_t>(pi) * S + s) * M + m];
+      applied = zero ? 0.0 : a.psi[m];  // EffectivePlan overrides (simulator.hpp:112-114)
       spill = dadd(spill, applied);
     }
     const double consumed = spill < 1.0 ? spill : 1.0;
@@ -160,14 +162,14 @@ __global__ void k_replay(ReplayArgs a) {
 }  // namespace
 
 void replay_requests(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* psi, const double* slo,
-                     double step_seconds,
-                     const int32_t* d_plans, int n_plans, const int64_t* d_arr, int n_traces, const uint64_t* d_seeds,
+                     double step_seconds, const int32_t* d_plans, const uint8_t* d_overrides, int n_plans, const int64_t* d_arr, int n_traces, const uint64_t* d_seeds,
                      int n_seeds, mgs_job_metrics* d_out) {
   const HostTables& t = pr.t;
   ReplayArgs a{};
   a.sp = sp;
   a.t = t;
   a.plans = d_plans;
+  a.overrides = d_overrides;
   a.arrivals = d_arr;
   a.seeds = d_seeds;
   a.n_plans = n_plans;

@@ -133,10 +133,13 @@ class Planner:
         return opt, cfg, lab, obj.value
 
     # -- run_requests (simulator.hpp:209-275), one window ----------------------------
-    def replay_requests(self, problem: Problem, plans, arrivals, seeds, step_seconds=1.0):
-        """plans [n_p][S] option indices, arrivals [n_t][M][S], seeds [n_s].
+    def replay_requests(self, problem: Problem, plans, arrivals, seeds, step_seconds=1.0, overrides=None):
+        """plans [n_p][S] option indices, arrivals [n_t][M][S], seeds [n_s],
+        overrides (optional) [n_p][S][M] psi_eff-zero flags (mgs_preinit).
         Returns mgs_job_metrics as a structured numpy array [n_p][n_t][n_s][M]."""
         plans = np.ascontiguousarray(plans, dtype=np.int32).reshape(-1, problem.S)
+        ov = None if overrides is None else np.ascontiguousarray(overrides, dtype=np.uint8).reshape(
+            plans.shape[0], problem.S, problem.M)
         arrivals = np.ascontiguousarray(arrivals, dtype=np.int64).reshape(-1, problem.M, problem.S)
         seeds = np.ascontiguousarray(seeds, dtype=np.uint64).reshape(-1)
         slo = np.asarray([2.0 * m.latency_full for m in problem.scenario.models], dtype=np.float64)  # slo_target
@@ -144,13 +147,29 @@ class Planner:
         out = (capi.mgs_job_metrics * max(1, n))()
         err = capi.empty_error()
         st = self.lib.mgs_replay_requests(self.h, problem.byref(), capi.ptr(slo, C.c_double), float(step_seconds),
-                                          capi.ptr(plans, C.c_int32), plans.shape[0], capi.ptr(arrivals, C.c_int64),
+                                          capi.ptr(plans, C.c_int32), plans.shape[0],
+                                          capi.ptr(ov, C.c_uint8) if ov is not None else None,
+                                          capi.ptr(arrivals, C.c_int64),
                                           arrivals.shape[0], capi.ptr(seeds, C.c_uint64), seeds.shape[0], out,
                                           C.byref(err))
         if st:
             raise capi.PlannerError(st, err)
         arr = np.ctypeslib.as_array(out)[:n]
         return arr.reshape(plans.shape[0], arrivals.shape[0], seeds.shape[0], problem.M)
+
+    # -- plan_preinit + apply_preinit (preinit.hpp:41-114) ------------------------
+    def preinit(self, problem: Problem, plans):
+        """Returns (overrides uint8 [n][S][M], fired uint32 [n][S] universe masks)."""
+        plans = np.ascontiguousarray(plans, dtype=np.int32).reshape(-1, problem.S)
+        n = plans.shape[0]
+        ov = np.zeros((n, problem.S, problem.M), np.uint8)
+        fired = np.zeros((n, problem.S), np.uint32)
+        err = capi.empty_error()
+        st = self.lib.mgs_preinit(self.h, problem.byref(), capi.ptr(plans, C.c_int32), n, capi.ptr(ov, C.c_uint8),
+                                  capi.ptr(fired, C.c_uint32), C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        return ov, fired
 
     def solve_batch(self, problems):
         n = len(problems)
@@ -196,14 +215,17 @@ class Planner:
         return npar.value
 
     # -- evaluate_plan(verify=false) batch ---------------------------------------
-    def evaluate_batch(self, problem: Problem, plans, arrivals, with_throughput=False):
+    def evaluate_batch(self, problem: Problem, plans, arrivals, with_throughput=False, overrides=None):
         plans = np.ascontiguousarray(plans, dtype=np.int32).reshape(-1, problem.S)
+        ov = None if overrides is None else np.ascontiguousarray(overrides, dtype=np.uint8).reshape(
+            plans.shape[0], problem.S, problem.M)
         arrivals = np.ascontiguousarray(arrivals, dtype=np.int64).reshape(-1, problem.M, problem.S)
         n_p, n_t = plans.shape[0], arrivals.shape[0]
         total = np.zeros((n_p, n_t), np.float64)
         thr = np.zeros((n_p, n_t, problem.S, problem.M), np.float64) if with_throughput else None
         err = capi.empty_error()
         st = self.lib.mgs_evaluate_batch(self.h, problem.byref(), capi.ptr(plans, C.c_int32), n_p,
+                                         capi.ptr(ov, C.c_uint8) if ov is not None else None,
                                          capi.ptr(arrivals, C.c_int64), n_t, capi.ptr(total, C.c_double),
                                          capi.ptr(thr, C.c_double) if thr is not None else None, C.byref(err))
         if st:

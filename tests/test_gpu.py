@@ -336,3 +336,52 @@ def test_replay_requests_matches_reference(gpu, golden_dir):
                     assert bits(r["overhead_seconds"]) == job[8], (stem, m)
                     n += 1
     assert n >= 300
+
+
+def test_preinit_matches_reference(gpu, golden_dir):
+    """Pre-initialisation (§8(f) row 4) on the GPU == the reference's
+    plan_preinit + apply_preinit: override sets, evaluate_plan totals with the
+    overrides, and request-mode replays of the EffectivePlan, for the solve_dp
+    plan and three sparse random feasible plans of every scenario."""
+    import json
+    import os
+    pg = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "preinit_golden.json")))
+    fields = ("received", "served", "timely", "correct", "valid", "dropped", "queued_at_end")
+    n_plans = n_ov = 0
+    for kind in ("random", "c1", "kat"):
+        for stem, path, g in golden_dir[kind]:
+            want = pg.get(stem)
+            if not want or "dp" not in want:
+                continue
+            sc = SC.load_scenario(path)
+            p = SC.Problem(sc, 0)
+            en = gpu.enumerate(p)
+            ns = nslots(sc)
+            index = {}
+            for o in range(len(en["config"])):
+                c = int(en["config"][o])
+                index.setdefault((c,) + tuple(int(x) for x in en["labels"][o][:ns[c]]), o)
+            cases = [want["dp"]] + want["random"]
+            plans = []
+            for w in cases:
+                enc, plan, i = w["encode"], [], 0
+                while i < len(enc):
+                    c = enc[i]
+                    plan.append(index[tuple(enc[i:i + 1 + ns[c]])])
+                    i += 1 + ns[c]
+                plans.append(plan)
+            plans = np.asarray(plans, np.int32)
+            ov, fired = gpu.preinit(p, plans)
+            totals = gpu.evaluate_batch(p, plans, p.forecast[None], overrides=ov)
+            runs = gpu.replay_requests(p, plans, p.forecast[None], [want["dp"]["seed"]], overrides=ov)
+            for k, w in enumerate(cases):
+                got = sorted((int(m), int(s)) for s, m in zip(*np.nonzero(ov[k])))
+                assert got == sorted(tuple(x) for x in w["overrides"]), (stem, k)
+                assert bits(totals[k, 0]) == w["obj"], (stem, k)
+                for m, job in enumerate(w["jobs"]):
+                    r = runs[k, 0, 0, m]
+                    assert [bits(r[f]) for f in fields] == job[:7], (stem, k, m)
+                    assert int(r["reconfigurations"]) == job[7] and bits(r["overhead_seconds"]) == job[8]
+                n_plans += 1
+                n_ov += len(w["overrides"])
+    assert n_plans >= 600 and n_ov >= 500
