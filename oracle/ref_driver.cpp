@@ -21,6 +21,10 @@
 //       plan_preinit + apply_preinit (preinit.hpp:41-114) of the window-0
 //       solve_dp plan: overrides, evaluate_plan total with them,
 //       overhead_summary, and run_requests of the EffectivePlan.
+//   migref drive <scenario.scn> <predictor>
+//       the per-window planning loop from the reference's
+//       pieces: predict_arrivals (oracle for window 0) -> solve_dp with the
+//       carried final_ranges -> evaluate_plan on forecast and actual counts.
 //   migref gen-random <seed> <count> <outdir> [--no-drop]
 //       the reference's own randomized oracle corpus generator
 //       (tests/test_util.hpp:104-181), written to files with
@@ -227,6 +231,47 @@ int cmd_preinit(int argc, char** argv) {
   return 0;
 }
 
+int cmd_drive(int argc, char** argv) {
+  if (argc < 4) return 2;
+  std::string out = guarded([&] {
+    Scenario sc = load_scenario(argv[2]);
+    PredictorSpec spec = parse_predictor_spec(argv[3]);
+    const int S = sc.window_size, M = static_cast<int>(sc.models.size());
+    std::optional<std::map<TaskId, std::set<SlotRange>>> initial;
+    std::string o = "{\"windows\":[";
+    for (int w = 0; w < sc.window_count; ++w) {
+      ArrivalForecast actual = window_forecast(sc, w);
+      ArrivalForecast fc;
+      if (spec.kind == PredictorKind::Oracle || w == 0) {
+        fc = predict_arrivals(PredictorSpec{}, {}, S, S, &actual.counts);
+      } else {
+        std::vector<std::vector<long long>> history(M);
+        for (int m = 0; m < M; ++m)
+          history[m].assign(sc.trace.counts[m].begin(), sc.trace.counts[m].begin() + static_cast<long>(w) * S);
+        fc = predict_arrivals(spec, history, S, S, &actual.counts);
+      }
+      PlanContext ctx{&sc, w, initial};
+      AllocationSequence dp = solve_dp(ctx, fc);
+      engine::Space sp = engine::Space::build(ctx);
+      auto enc = sp.encode(dp);
+      o += std::string(w ? "," : "") + "{\"encode\":[";
+      for (size_t i = 0; i < enc.size(); ++i) o += (i ? "," : "") + std::to_string(enc[i]);
+      o += "],\"forecast\":[";
+      for (int m = 0; m < M; ++m) {
+        o += std::string(m ? "," : "") + "[";
+        for (int s = 0; s < S; ++s) o += (s ? "," : "") + std::to_string(fc.counts[m][s]);
+        o += "]";
+      }
+      o += "],\"obj\":\"" + hexbits(evaluate_plan(ctx, dp, fc.counts).total) + "\",\"realized\":\"" +
+           hexbits(evaluate_plan(ctx, dp, actual.counts).total) + "\"}";
+      initial = final_ranges(sc, dp);
+    }
+    return o + "]}";
+  });
+  std::printf("%s\n", out.c_str());
+  return 0;
+}
+
 int cmd_gen_random(int argc, char** argv) {
   if (argc < 5) return 2;
   unsigned seed = static_cast<unsigned>(std::strtoul(argv[2], nullptr, 10));
@@ -282,6 +327,7 @@ int main(int argc, char** argv) {
   if (cmd == "gen-random") return cmd_gen_random(argc, argv);
   if (cmd == "replay") return cmd_replay(argc, argv);
   if (cmd == "preinit") return cmd_preinit(argc, argv);
+  if (cmd == "drive") return cmd_drive(argc, argv);
   std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
   return 2;
 }

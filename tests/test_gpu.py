@@ -385,3 +385,30 @@ def test_preinit_matches_reference(gpu, golden_dir):
                 n_plans += 1
                 n_ov += len(w["overrides"])
     assert n_plans >= 600 and n_ov >= 500
+
+
+def test_per_window_driver_matches_reference(gpu):
+    """The per-window planning loop (§8(f) row 3): predictor -> GPU solve_dp with
+    the carried final ranges -> realized evaluate_plan, window after window,
+    for several scenarios advanced together as batched lanes; == the loop
+    built from the unmodified reference's own pieces (`migref drive`)."""
+    import json
+    import os
+    from paper_2407_13126_b200 import driver
+    d = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "drive")
+    gold = json.load(open(os.path.join(d, "drive_golden.json")))
+    feasible = ["d_c1_40", "d_c1_40v"]
+    for pred in ("oracle", "persistence", "ewma:0.3"):
+        scs = [SC.load_scenario(os.path.join(d, stem + ".scn")) for stem in feasible]
+        plans = driver.plan_scenarios(gpu, scs, pred)
+        for stem, sc, wins in zip(feasible, scs, plans):
+            want = gold[stem][pred]["windows"]
+            assert len(wins) == len(want)
+            for wp, w in zip(wins, want):
+                assert planner.encode(wp.config, wp.labels, nslots(sc)) == w["encode"], (stem, pred, wp.window)
+                assert wp.forecast.tolist() == w["forecast"], (stem, pred, wp.window)
+                assert bits(wp.objective) == w["obj"] and bits(wp.realized) == w["realized"], (stem, pred)
+        sc = SC.load_scenario(os.path.join(d, "d_c2_100.scn"))
+        with pytest.raises(capi.PlannerError) as e:
+            driver.plan_scenarios(gpu, [sc], pred)
+        assert e.value.code == gold["d_c2_100"][pred]["error"]
