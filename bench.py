@@ -151,9 +151,16 @@ def run_ours(args):
     import torch.distributed as dist
     from paper_2407_13126_b200 import planner
     rank, world, local = env_rank()
+    # one rank per GPU; --dist-backend gloo lets a functional N>1 check share
+    # fewer GPUs (ranks wrap around the visible devices)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    coll_dev = "cuda" if args.dist_backend == "nccl" else "cpu"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     work = tempfile.mkdtemp(prefix="mgs_bench_")
     seed = 100001 + rank
     prob = c1_problem(seed, work)
@@ -167,7 +174,7 @@ def run_ours(args):
     def combine(obj):
         # per-shard best (objective, shard) -> NCCL all-reduce(max): the only collective
         if world > 1:
-            shard.combine_best(obj, rank, world, device="cuda")
+            shard.combine_best(obj, rank, world, device=coll_dev)
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -212,10 +219,10 @@ def run_ours(args):
     trans_bytes = sum(s["transition_bytes"] for s in stats)
     launches = sum(s["kernel_launches"] for s in stats)
     if world > 1:
-        t = torch.tensor([dev_s, e2e_s], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dev_s, e2e_s], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_s, e2e_s = t.tolist()
-        n = torch.tensor([float(tr_window)], dtype=torch.float64, device="cuda")
+        n = torch.tensor([float(tr_window)], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(n, op=dist.ReduceOp.SUM)
         total_tr = n.item() * args.steps
     else:
@@ -378,6 +385,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="collective backend for N>1 (gloo only for functional checks on fewer GPUs)")
     ap.add_argument("--batch", type=int, default=16, help="windows in the batched-lanes throughput leg (0: skip)")
     ap.add_argument("--table", type=int, default=4096, help="traces in the config-4 Goodput-table leg (0: skip)")
     args = ap.parse_args()

@@ -57,6 +57,7 @@ constexpr int kBucketSmall = 256;    // child buckets up to this size: thread pe
 constexpr int kSortItems = 16;       // big child buckets: CTA radix sort of up to 256*16 keys
 constexpr int kBatch = 512;          // groups / statuses per CTA allocation batch
 constexpr int kNumScans = 7;
+constexpr int kDbg = 10;  // per-step debug counters
 
 enum Err : int { kOk = 0, kOverflow = 100 };
 
@@ -149,7 +150,7 @@ struct V2 {
   int sc_big_ctas;               // CTAs of k_trans that may take big-group items
   int oi_bits;                   // bits of an option index (radix sort width)
   int merge_win;                 // placement window of the CTA merge table
-  long long* dbg;                // [S][6] per-step counters (debug dump)
+  long long* dbg;                // [S][kDbg] per-step counters (debug dump)
   unsigned long long* dbg_time;  // barrier timestamps (debug)
 };
 
@@ -1097,6 +1098,11 @@ __device__ void phase_write(const V2& a, int s) {
     const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
     const int q0 = a.ns_obase[id], gi = a.ns_gbase[id];
     const uint32_t key = a.hash[id] - 1u;
+    if (threadIdx.x == 0 && a.dbg) {
+      atomicMax(reinterpret_cast<unsigned long long*>(a.dbg + kDbg * (s + 1 < a.S ? s + 1 : s) + 8),
+                static_cast<unsigned long long>(total));
+      if (total > kSmall) atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + kDbg * (s + 1 < a.S ? s + 1 : s) + 9), 1ull);
+    }
     if (threadIdx.x == 0) {
       N.g_start[gi] = q0;
       N.g_size[gi] = total;
@@ -1370,7 +1376,9 @@ __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int
     StepCounters& sc = ctl->sc[s & 1];
     a.hist_base[s + 2] = a.hist_base[s + 1] + ctl->n_store[nxt];  // array has S+2 entries
     if (a.dbg) {
-      long long* d = a.dbg + 6ll * s;
+      long long* d = a.dbg + static_cast<long long>(kDbg) * s;
+      d[6] = sc.items_b;
+      d[7] = sc.items_s;
       d[0] = sc.n_units;
       d[1] = sc.n_big + sc.n_small;
       d[2] = sc.T;
@@ -1615,7 +1623,8 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, double band, int dominan
   a.chosen = c.buf<int32_t>("v2_chosen", S);
   a.n_partial = sp.proj_base[(1 << t.M) - 1];  // all subsets but the full one
   const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr || std::getenv("MGS_TRACE") != nullptr;
-  a.dbg = debug ? c.buf<long long>("v2_dbg", 6 * S) : nullptr;
+  a.dbg = debug ? c.buf<long long>("v2_dbg", kDbg * S) : nullptr;
+  if (a.dbg) MGS_CUDA_OK(cudaMemsetAsync(a.dbg, 0, sizeof(long long) * kDbg * S, c.stream));
   a.dbg_time = nullptr;
   a.sc_big_ctas = grid_term;
   a.merge_win = merge_win;
@@ -1860,11 +1869,15 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
       V2Lane& L = lanes[l];
       const Ctl& hc = h[l];
       if (debug && args[l].dbg && l == 0) {
-        std::vector<long long> d(6 * S);
+        std::vector<long long> d(kDbg * S);
         MGS_CUDA_OK(cudaMemcpy(d.data(), args[l].dbg, d.size() * 8, cudaMemcpyDeviceToHost));
-        for (int s = 0; s < S; ++s)
-          std::fprintf(stderr, "v2 step %d units %lld ns %lld T %lld store %lld groups %lld alive_in %lld\n", s, d[6 * s],
-                       d[6 * s + 1], d[6 * s + 2], d[6 * s + 3], d[6 * s + 4], d[6 * s + 5]);
+        for (int s = 0; s < S; ++s) {
+          const long long* q = d.data() + kDbg * s;
+          std::fprintf(stderr,
+                       "v2 step %d units %lld ns %lld T %lld store %lld groups %lld alive_in %lld items_b %lld "
+                       "items_s %lld max_group %lld big_groups %lld\n",
+                       s, q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8], q[9]);
+        }
       }
       L.status = MGS_OK;
       if (hc.err_code == MGS_ERR_STATE_BUDGET) {

@@ -412,3 +412,31 @@ def test_per_window_driver_matches_reference(gpu):
         with pytest.raises(capi.PlannerError) as e:
             driver.plan_scenarios(gpu, [sc], pred)
         assert e.value.code == gold["d_c2_100"][pred]["error"]
+
+
+def test_edge_cases(gpu, tmp_path):
+    """The shortest windows the grammar allows (S = 2; every retraining finishes
+    in a single slot), empty batches, and an all-zero trace: GPU DP == GPU brute force == the CPU
+    restatement; empty inputs return empty outputs without error."""
+    from paper_2407_13126_b200 import workloads as W
+    ts = [W.Tenant("a", 40.0, [0.6], [0.9], rt={k: 1 for k in range(1, 8)}, psi=0.5),
+          W.Tenant("b", 50.0, [0.62], [0.89], rt={k: 1 for k in range(1, 8)}, psi=1.5)]
+    for S, counts in ((2, [[120, 30], [150, 9]]), (2, [[0, 0], [0, 0]]), (3, [[500, 0, 900], [7, 3000, 1]])):
+        spec = W.ScenarioSpec(ts, S, 1)
+        spec.counts = np.asarray(counts, np.int64)
+        p = SC.Problem(SC.load_scenario(W.write_scenario(spec, str(tmp_path), "edge%d_%d" % (S, sum(map(sum, counts))))), 0)
+        opt, cfg, lab, obj, _ = gpu.solve_window(p)
+        want, want_obj, _ = B.solve_window(p)
+        assert list(opt) == list(want), S
+        assert bits(obj) == bits(want_obj), S
+        if S == 2:  # |O|^2 ~ 6e8 sequences: the GPU brute force takes it with a raised cap
+            bopt, _, _, bobj = gpu.solve_bruteforce(p, bruteforce_cap=1e9)
+            assert list(bopt) == list(want) and bits(bobj) == bits(want_obj)
+    opts, obj, status, stats, errs = gpu.solve_batch([p])
+    assert status[0] == 0 and bits(obj[0]) == bits(want_obj)
+    assert gpu.evaluate_batch(p, np.zeros((0, p.S), np.int32), p.forecast[None]).shape == (0, 1)
+    ub, npar = gpu.goodput_table_batch(p, np.zeros((0, p.M, p.S), np.int32))
+    assert ub.shape == (0, p.S + 1)
+    assert gpu.replay_requests(p, opt[None], p.forecast[None], []).shape == (1, 1, 0, p.M)
+    ov, fired = gpu.preinit(p, np.zeros((0, p.S), np.int32))
+    assert ov.shape == (0, p.S, p.M)
