@@ -19,7 +19,7 @@
  *                      per-scenario call in a host loop)
  *   mgs_evaluate_batch evaluate_plan(verify=false)     evaluate.hpp:153-210
  *   mgs_window_boundary plan_window_boundary         baselines.hpp:139-289
- *   mgs_replay_requests run_requests (one window)      simulator.hpp:209-275
+ *   mgs_replay_requests run_requests                   simulator.hpp:209-275
  *   mgs_preinit        plan_preinit + apply_preinit    preinit.hpp:41-114
  *   mgs_goodput_table_batch  solve_dp's ub_suffix table  solvers.hpp:258-280
  *                      for a batch of traces sharing one window's tables
@@ -224,15 +224,20 @@ MGS_API int mgs_preinit(mgs_ctx* ctx, const mgs_problem* p, const int32_t* plans
 MGS_API int mgs_window_boundary(mgs_ctx* ctx, const mgs_problem* p, int32_t* out_option, int32_t* out_config,
                                 int8_t* out_labels, double* out_objective, mgs_error* err);
 
-/* Request-mode replay (run_requests, single-window scenario, no pre-init
- * overrides) of n_plans x n_traces x n_seeds runs on the device:
- * plans[i*S+s] option indices, arrivals[t*M*S+m*S+s], seeds[k];
- * slo[m] = 2*latency_full (seconds), step_seconds = Scenario::step_seconds;
- * overrides as for mgs_evaluate_batch (EffectivePlan::overrides) or NULL.
- * out[((i*n_traces + t)*n_seeds + k)*M + m]. */
-MGS_API int mgs_replay_requests(mgs_ctx* ctx, const mgs_problem* p, const double* slo, double step_seconds,
-                                const int32_t* plans, int32_t n_plans, const uint8_t* overrides,
-                                const int64_t* arrivals, int32_t n_traces,
+/* Request-mode replay (run_requests, simulator.hpp:209-275) of a scenario's
+ * `windows` consecutive windows (one window's tables in p; queues, psi spill
+ * and inference masks carry across windows) for n_plans x n_traces x n_seeds
+ * runs on the device. plans[(i*windows + w)*S + s] option indices;
+ * arrivals[t*M*windows*S + m*windows*S + g] (g = w*S + s); seeds[k];
+ * acc_pre/acc_post [w*M + m] per-window accuracies (NULL with windows == 1:
+ * p's tables); slo[m] = 2*latency_full (seconds); step_seconds =
+ * Scenario::step_seconds; overrides [(i*windows + w)*S + s][m] as for
+ * mgs_evaluate_batch (EffectivePlan::overrides) or NULL.
+ * out[((run*windows + w)*M + m)], run = (i*n_traces + t)*n_seeds + k: the
+ * per-window JobMetrics (totals = their sums in window order). */
+MGS_API int mgs_replay_requests(mgs_ctx* ctx, const mgs_problem* p, int32_t windows, const double* acc_pre,
+                                const double* acc_post, const double* slo, double step_seconds, const int32_t* plans,
+                                int32_t n_plans, const uint8_t* overrides, const int64_t* arrivals, int32_t n_traces,
                                 const uint64_t* seeds, int32_t n_seeds, mgs_job_metrics* out, mgs_error* err);
 
 /* The Goodput table for n_traces traces that share one window's lattice and

@@ -4,6 +4,9 @@ per-window planning loop's results from the UNMODIFIED reference's pieces
 evaluate_plan), for the oracle, persistence and ewma:0.3 predictors.
 
     python oracle/make_drive_goldens.py   -> tests/golden/drive/*
+
+Also the multi-window request replay of the loop's plans (`migref replay-windows`,
+run_requests over all windows with queues and psi spill carried across them).
 """
 import dataclasses
 import json
@@ -40,6 +43,14 @@ def main():
             gold[stem][pred] = json.loads(r.stdout)
             print(stem, pred, list(gold[stem][pred].keys()), flush=True)
     json.dump(gold, open(os.path.join(OUT, "drive_golden.json"), "w"), sort_keys=True)
+    # multi-window request replay of the loop's plans (run_requests over all windows)
+    rw = {}
+    for stem in ("d_c1_40", "d_c1_40v"):
+        for seed in ("5", "77"):
+            r = subprocess.run([os.path.join(HERE, "_ref", "migref"), "replay-windows", os.path.join(OUT, stem + ".scn"),
+                                seed], capture_output=True, text=True, timeout=900)
+            rw["%s:%s" % (stem, seed)] = json.loads(r.stdout)
+    json.dump(rw, open(os.path.join(OUT, "replay_windows_golden.json"), "w"), sort_keys=True)
 
 
 if __name__ == "__main__":

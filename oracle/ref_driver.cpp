@@ -25,6 +25,10 @@
 //       the per-window planning loop from the reference's
 //       pieces: predict_arrivals (oracle for window 0) -> solve_dp with the
 //       carried final_ranges -> evaluate_plan on forecast and actual counts.
+//   migref replay-windows <scenario.scn> <seed>
+//       run_requests over every window of the scenario for the plans of the
+//       per-window loop (oracle forecasts, carried final_ranges); prints the
+//       per-window JobMetrics counters and each window's plan encoding.
 //   migref gen-random <seed> <count> <outdir> [--no-drop]
 //       the reference's own randomized oracle corpus generator
 //       (tests/test_util.hpp:104-181), written to files with
@@ -272,6 +276,38 @@ int cmd_drive(int argc, char** argv) {
   return 0;
 }
 
+int cmd_replay_windows(int argc, char** argv) {
+  if (argc < 4) return 2;
+  std::string out = guarded([&] {
+    Scenario sc = load_scenario(argv[2]);
+    const uint64_t seed = std::strtoull(argv[3], nullptr, 10);
+    std::optional<std::map<TaskId, std::set<SlotRange>>> initial;
+    std::vector<EffectivePlan> plans;
+    std::string o = "{\"encode\":[";
+    for (int w = 0; w < sc.window_count; ++w) {
+      PlanContext ctx{&sc, w, initial};
+      ArrivalForecast fc = window_forecast(sc, w);
+      AllocationSequence dp = solve_dp(ctx, fc);
+      auto enc = engine::Space::build(ctx).encode(dp);
+      o += std::string(w ? "," : "") + "[";
+      for (size_t i = 0; i < enc.size(); ++i) o += (i ? "," : "") + std::to_string(enc[i]);
+      o += "]";
+      plans.push_back(EffectivePlan{dp, {}});
+      initial = final_ranges(sc, dp);
+    }
+    Metrics mt = run_requests(sc, plans, seed);
+    o += "],\"windows\":[";
+    for (size_t w = 0; w < mt.windows.size(); ++w) {
+      Metrics one;
+      one.jobs = mt.windows[w].jobs;
+      o += std::string(w ? "," : "") + jobs_json(one);
+    }
+    return o + "],\"totals\":" + jobs_json(mt) + "}";
+  });
+  std::printf("%s\n", out.c_str());
+  return 0;
+}
+
 int cmd_gen_random(int argc, char** argv) {
   if (argc < 5) return 2;
   unsigned seed = static_cast<unsigned>(std::strtoul(argv[2], nullptr, 10));
@@ -328,6 +364,7 @@ int main(int argc, char** argv) {
   if (cmd == "replay") return cmd_replay(argc, argv);
   if (cmd == "preinit") return cmd_preinit(argc, argv);
   if (cmd == "drive") return cmd_drive(argc, argv);
+  if (cmd == "replay-windows") return cmd_replay_windows(argc, argv);
   std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
   return 2;
 }

@@ -145,7 +145,8 @@ def load():
                                                    C.c_void_p, P(C.c_int32), P(mgs_error)]
     lib.mgs_window_boundary.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_int32), P(C.c_int32), P(C.c_int8),
                                         P(C.c_double), P(mgs_error)]
-    lib.mgs_replay_requests.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_double), C.c_double, P(C.c_int32),
+    lib.mgs_replay_requests.argtypes = [C.c_void_p, P(mgs_problem), C.c_int32, P(C.c_double), P(C.c_double),
+                                        P(C.c_double), C.c_double, P(C.c_int32),
                                         C.c_int32, P(C.c_uint8), P(C.c_int64), C.c_int32, P(C.c_uint64), C.c_int32,
                                         P(mgs_job_metrics), P(mgs_error)]
     _LIB = lib

@@ -352,10 +352,13 @@ int mgs_window_boundary(mgs_ctx* ctx, const mgs_problem* p, int32_t* out_option,
   });
 }
 
-int mgs_replay_requests(mgs_ctx* ctx, const mgs_problem* p, const double* slo, double step_seconds, const int32_t* plans,
-                        int32_t n_plans, const uint8_t* overrides, const int64_t* arrivals, int32_t n_traces, const uint64_t* seeds,
+int mgs_replay_requests(mgs_ctx* ctx, const mgs_problem* p, int32_t windows, const double* acc_pre, const double* acc_post,
+                        const double* slo, double step_seconds, const int32_t* plans, int32_t n_plans,
+                        const uint8_t* overrides, const int64_t* arrivals, int32_t n_traces, const uint64_t* seeds,
                         int32_t n_seeds, mgs_job_metrics* out, mgs_error* err) {
-  if (!ctx || !p || !slo || n_plans < 0 || n_traces < 0 || n_seeds < 0 || !(step_seconds > 0)) return MGS_ERR_ARGUMENT;
+  if (!ctx || !p || !slo || windows < 1 || n_plans < 0 || n_traces < 0 || n_seeds < 0 || !(step_seconds > 0))
+    return MGS_ERR_ARGUMENT;
+  if ((acc_pre == nullptr) != (acc_post == nullptr) || (windows > 1 && !acc_pre)) return MGS_ERR_ARGUMENT;
   const long long runs = static_cast<long long>(n_plans) * n_traces * n_seeds;
   if (runs > 0 && (!plans || !arrivals || !seeds || !out)) return MGS_ERR_ARGUMENT;
   return guarded(err, [&] {
@@ -364,27 +367,36 @@ int mgs_replay_requests(mgs_ctx* ctx, const mgs_problem* p, const double* slo, d
     mgs::Prepared pr = prepare_problem(*p);
     mgs::DevSpace sp;
     mgs::build_space(c, p->lattice, pr, sp);
-    const int M = pr.t.M, S = pr.t.S;
+    const int M = pr.t.M, S = pr.t.S, W = windows;
     for (int m = 0; m < M; ++m)
       if (!(slo[m] > 0)) throw PlanFail{MGS_ERR_INPUT_SCENARIO, "latency_full must be positive"};  // workload.hpp:90-92
-    for (long long k = 0; k < static_cast<long long>(n_plans) * S; ++k)
+    for (long long k = 0; k < static_cast<long long>(n_plans) * W * S; ++k)
       if (plans[k] < 0 || plans[k] >= sp.n_opt) throw PlanFail{MGS_ERR_PLAN_INFEASIBLE, "plan names an unknown option"};
     if (runs == 0) return;
-    int32_t* d_plans = c.buf<int32_t>("rp_plans", static_cast<size_t>(n_plans) * S);
-    int64_t* d_arr = c.buf<int64_t>("rp_arr", static_cast<size_t>(n_traces) * M * S);
+    std::vector<double> acc(static_cast<size_t>(W) * 2 * M);  // [W][pre|post][M]
+    for (int w = 0; w < W; ++w)
+      for (int m = 0; m < M; ++m) {
+        acc[(w * 2 + 0) * M + m] = acc_pre ? acc_pre[w * M + m] : p->tables.acc_pre[m];
+        acc[(w * 2 + 1) * M + m] = acc_post ? acc_post[w * M + m] : p->tables.acc_post[m];
+      }
+    const size_t G = static_cast<size_t>(W) * S;
+    int32_t* d_plans = c.buf<int32_t>("rp_plans", static_cast<size_t>(n_plans) * G);
+    int64_t* d_arr = c.buf<int64_t>("rp_arr", static_cast<size_t>(n_traces) * M * G);
     uint64_t* d_seeds = c.buf<uint64_t>("rp_seeds", n_seeds);
-    mgs_job_metrics* d_out = c.buf<mgs_job_metrics>("rp_out", static_cast<size_t>(runs) * M);
-    MGS_CUDA_OK(cudaMemcpyAsync(d_plans, plans, static_cast<size_t>(n_plans) * S * 4, cudaMemcpyHostToDevice, c.stream));
-    MGS_CUDA_OK(cudaMemcpyAsync(d_arr, arrivals, static_cast<size_t>(n_traces) * M * S * 8, cudaMemcpyHostToDevice, c.stream));
+    double* d_acc = c.buf<double>("rp_acc", acc.size());
+    mgs_job_metrics* d_out = c.buf<mgs_job_metrics>("rp_out", static_cast<size_t>(runs) * W * M);
+    MGS_CUDA_OK(cudaMemcpyAsync(d_plans, plans, static_cast<size_t>(n_plans) * G * 4, cudaMemcpyHostToDevice, c.stream));
+    MGS_CUDA_OK(cudaMemcpyAsync(d_arr, arrivals, static_cast<size_t>(n_traces) * M * G * 8, cudaMemcpyHostToDevice, c.stream));
     MGS_CUDA_OK(cudaMemcpyAsync(d_seeds, seeds, static_cast<size_t>(n_seeds) * 8, cudaMemcpyHostToDevice, c.stream));
-    uint8_t* d_ov = overrides ? c.buf<uint8_t>("rp_ov", static_cast<size_t>(n_plans) * S * M) : nullptr;
+    MGS_CUDA_OK(cudaMemcpyAsync(d_acc, acc.data(), acc.size() * 8, cudaMemcpyHostToDevice, c.stream));
+    uint8_t* d_ov = overrides ? c.buf<uint8_t>("rp_ov", static_cast<size_t>(n_plans) * G * M) : nullptr;
     if (overrides)
-      MGS_CUDA_OK(cudaMemcpyAsync(d_ov, overrides, static_cast<size_t>(n_plans) * S * M, cudaMemcpyHostToDevice, c.stream));
-    mgs::replay_requests(c, pr, sp, p->tables.psi, slo, step_seconds, d_plans, d_ov, n_plans, d_arr, n_traces,
-                         d_seeds, n_seeds, d_out);
-    MGS_CUDA_OK(cudaMemcpyAsync(out, d_out, static_cast<size_t>(runs) * M * sizeof(mgs_job_metrics),
+      MGS_CUDA_OK(cudaMemcpyAsync(d_ov, overrides, static_cast<size_t>(n_plans) * G * M, cudaMemcpyHostToDevice, c.stream));
+    mgs::replay_requests(c, pr, sp, W, d_acc, p->tables.psi, slo, step_seconds, d_plans, d_ov, n_plans, d_arr,
+                         n_traces, d_seeds, n_seeds, d_out);
+    MGS_CUDA_OK(cudaMemcpyAsync(out, d_out, static_cast<size_t>(runs) * W * M * sizeof(mgs_job_metrics),
                                 cudaMemcpyDeviceToHost, c.stream));
-    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));  // also keeps `acc` alive until its copy has run
   });
 }
 

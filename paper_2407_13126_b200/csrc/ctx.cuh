@@ -209,8 +209,9 @@ bool bruteforce(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* d_
 bool window_boundary(Ctx& c, const Prepared& pr, const DevSpace& sp, const mgs_lattice& lat, const double* d_recv,
                      std::vector<int32_t>& plan);
 // replay.cu: run_requests for plans x traces x seeds
-void replay_requests(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* psi, const double* slo,
-                     double step_seconds, const int32_t* d_plans, const uint8_t* d_overrides, int n_plans,
+void replay_requests(Ctx& c, const Prepared& pr, const DevSpace& sp, int W, const double* d_acc, const double* psi,
+                     const double* slo, double step_seconds, const int32_t* d_plans, const uint8_t* d_overrides,
+                     int n_plans,
                      const int64_t* d_arr, int n_traces, const uint64_t* d_seeds, int n_seeds, mgs_job_metrics* d_out);
 // preinit.cu: plan_preinit + apply_preinit overrides [n_plans][S][M], fired [n_plans][S]
 void preinit_overrides(Ctx& c, const Prepared& pr, const DevSpace& sp, const mgs_lattice& lat, const int32_t* d_plans,

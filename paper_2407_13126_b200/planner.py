@@ -132,30 +132,39 @@ class Planner:
             raise capi.PlannerError(st, err)
         return opt, cfg, lab, obj.value
 
-    # -- run_requests (simulator.hpp:209-275), one window ----------------------------
-    def replay_requests(self, problem: Problem, plans, arrivals, seeds, step_seconds=1.0, overrides=None):
-        """plans [n_p][S] option indices, arrivals [n_t][M][S], seeds [n_s],
-        overrides (optional) [n_p][S][M] psi_eff-zero flags (mgs_preinit).
-        Returns mgs_job_metrics as a structured numpy array [n_p][n_t][n_s][M]."""
-        plans = np.ascontiguousarray(plans, dtype=np.int32).reshape(-1, problem.S)
+    # -- run_requests (simulator.hpp:209-275) ---------------------------------------
+    def replay_requests(self, problem: Problem, plans, arrivals, seeds, step_seconds=1.0, overrides=None,
+                        windows=1):
+        """Request-mode replay of `windows` consecutive windows (queues, psi spill
+        and masks carry across them). plans [n_p][W*S] option indices (window
+        after window), arrivals [n_t][M][W*S], seeds [n_s], overrides (optional)
+        [n_p][W*S][M] psi_eff-zero flags (mgs_preinit). Per-window accuracies
+        come from problem.scenario. Returns mgs_job_metrics as a structured
+        numpy array [n_p][n_t][n_s][M] (W = 1) or [n_p][n_t][n_s][W][M]."""
+        W, S, M = windows, problem.S, problem.M
+        plans = np.ascontiguousarray(plans, dtype=np.int32).reshape(-1, W * S)
         ov = None if overrides is None else np.ascontiguousarray(overrides, dtype=np.uint8).reshape(
-            plans.shape[0], problem.S, problem.M)
-        arrivals = np.ascontiguousarray(arrivals, dtype=np.int64).reshape(-1, problem.M, problem.S)
+            plans.shape[0], W * S, M)
+        arrivals = np.ascontiguousarray(arrivals, dtype=np.int64).reshape(-1, M, W * S)
         seeds = np.ascontiguousarray(seeds, dtype=np.uint64).reshape(-1)
-        slo = np.asarray([2.0 * m.latency_full for m in problem.scenario.models], dtype=np.float64)  # slo_target
-        n = plans.shape[0] * arrivals.shape[0] * seeds.shape[0] * problem.M
+        models = problem.scenario.models
+        slo = np.asarray([2.0 * m.latency_full for m in models], dtype=np.float64)  # slo_target
+        w0 = problem.window
+        acc_pre = np.asarray([[m.acc_pre[w0 + w] for m in models] for w in range(W)], np.float64)
+        acc_post = np.asarray([[m.acc_post[w0 + w] for m in models] for w in range(W)], np.float64)
+        n = plans.shape[0] * arrivals.shape[0] * seeds.shape[0] * W * M
         out = (capi.mgs_job_metrics * max(1, n))()
         err = capi.empty_error()
-        st = self.lib.mgs_replay_requests(self.h, problem.byref(), capi.ptr(slo, C.c_double), float(step_seconds),
-                                          capi.ptr(plans, C.c_int32), plans.shape[0],
+        st = self.lib.mgs_replay_requests(self.h, problem.byref(), W, capi.ptr(acc_pre, C.c_double),
+                                          capi.ptr(acc_post, C.c_double), capi.ptr(slo, C.c_double),
+                                          float(step_seconds), capi.ptr(plans, C.c_int32), plans.shape[0],
                                           capi.ptr(ov, C.c_uint8) if ov is not None else None,
-                                          capi.ptr(arrivals, C.c_int64),
-                                          arrivals.shape[0], capi.ptr(seeds, C.c_uint64), seeds.shape[0], out,
-                                          C.byref(err))
+                                          capi.ptr(arrivals, C.c_int64), arrivals.shape[0],
+                                          capi.ptr(seeds, C.c_uint64), seeds.shape[0], out, C.byref(err))
         if st:
             raise capi.PlannerError(st, err)
-        arr = np.ctypeslib.as_array(out)[:n]
-        return arr.reshape(plans.shape[0], arrivals.shape[0], seeds.shape[0], problem.M)
+        arr = np.ctypeslib.as_array(out)[:n].reshape(plans.shape[0], arrivals.shape[0], seeds.shape[0], W, M)
+        return arr[:, :, :, 0, :] if W == 1 else arr
 
     # -- plan_preinit + apply_preinit (preinit.hpp:41-114) ------------------------
     def preinit(self, problem: Problem, plans):

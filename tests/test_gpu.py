@@ -440,3 +440,35 @@ def test_edge_cases(gpu, tmp_path):
     assert gpu.replay_requests(p, opt[None], p.forecast[None], []).shape == (1, 1, 0, p.M)
     ov, fired = gpu.preinit(p, np.zeros((0, p.S), np.int32))
     assert ov.shape == (0, p.S, p.M)
+
+
+def test_replay_requests_multi_window(gpu):
+    """run_requests over a 3-window scenario (queues, psi spill and masks carried
+    across windows) for the per-window loop's plans: per-window counters bit-equal
+    to the reference's, and their window-order sums equal its totals."""
+    import json
+    import os
+    from paper_2407_13126_b200 import driver
+    d = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "drive")
+    gold = json.load(open(os.path.join(d, "replay_windows_golden.json")))
+    fields = ("received", "served", "timely", "correct", "valid", "dropped", "queued_at_end")
+    for stem in ("d_c1_40", "d_c1_40v"):
+        sc = SC.load_scenario(os.path.join(d, stem + ".scn"))
+        wins = driver.plan_scenarios(gpu, [sc], "oracle")[0]
+        for w, wp in enumerate(wins):
+            assert planner.encode(wp.config, wp.labels, nslots(sc)) == gold[stem + ":5"]["encode"][w]
+        plans = np.concatenate([wp.options for wp in wins])[None]
+        p = SC.Problem(sc, 0)
+        got = gpu.replay_requests(p, plans, sc.counts[None], [5, 77], windows=sc.window_count)
+        for k, seed in enumerate((5, 77)):
+            want = gold["%s:%d" % (stem, seed)]
+            for w in range(sc.window_count):
+                for m, job in enumerate(want["windows"][w]):
+                    r = got[0, 0, k, w, m]
+                    assert [bits(r[f]) for f in fields] == job[:7], (stem, seed, w, m)
+                    assert int(r["reconfigurations"]) == job[7] and bits(r["overhead_seconds"]) == job[8]
+            for m, job in enumerate(want["totals"]):
+                tot = 0.0
+                for w in range(sc.window_count):
+                    tot += float(got[0, 0, k, w, m]["valid"])
+                assert bits(tot) == job[4]
