@@ -1,4 +1,5 @@
-"""The reference's OWN Catch2 suites, compiled unchanged against the B200
+"""The reference's OWN Catch2 suites (plus our extras_test of the widened C++ API
+against the reference functions), compiled unchanged against the B200
 drop-in header (paper_2407_13126_b200/host/migsim/solvers.hpp) and run on the
 GPU: solve_dp / solve_bruteforce / precheck_scenario go through the C ABI to
 the sm_100a kernels. Binaries are built by tests/dropin/Makefile (from
@@ -13,7 +14,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "paper_2407_13126_b200", "lib", "dropin")
-SUITES = ["solver_test", "eval_test", "baseline_test", "simulator_test", "preinit_test"]
+SUITES = ["solver_test", "eval_test", "baseline_test", "simulator_test", "preinit_test", "extras_test"]
 
 
 @pytest.fixture(scope="module")
