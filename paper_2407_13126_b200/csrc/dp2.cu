@@ -79,6 +79,7 @@ struct FrontierV2 {
 struct StepCounters {  // double buffered; zeroed one step ahead
   int n_units, T, items_s, items_b, n_big, n_small, n_big_bucket, ticket, kids, ticket2;
   int n_ns;  // successor statuses of the step = entries of the used-slot list
+  int n_tab;  // big status groups of F_s whose subset tables k_tables builds
 };
 
 struct Ctl {
@@ -121,6 +122,14 @@ struct V2 {
   uint32_t* hash;  // key+1 per slot; the slot index is the successor-status id
   int hmask;
   int32_t* ns_used;  // hash slots claimed this step (list order = claim order)
+  // per big group of F_s (> kSmall states): subset tables built once per step
+  int tcap;                 // table slots
+  int32_t* g_tab;           // [gcap] group -> slot (valid for big groups)
+  int32_t* tab_group;       // [tcap] slot -> group
+  unsigned long long* tab_vb;   // [tcap][n_partial] max value bits per (subset, projection)
+  unsigned long long* tab_rx;   // [tcap][n_partial] (rank << 32 | j) of the best among the max
+  uint32_t* tab_ex;         // [tcap][P1] j + 1 of the group's state at each placement (0 = none)
+  unsigned long long* tab_hdr;  // [tcap][2] empty subset: value bits, (rank << 32 | j)
   int32_t *ns_ucnt, *ns_ccnt, *ns_ubase, *ns_cbase, *ns_ucur, *ns_ccur, *ns_units, *ns_bigpos, *ns_smallpos;
   int32_t *ns_big, *ns_small;
   int32_t *ns_out, *ns_obase, *ns_gbase;  // survivors per status, their offsets and group index
@@ -492,6 +501,15 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
       for (int g = bs + warp; g < be; g += kWarps) {
         if (F.g_alive[g] <= 0) continue;
         const bool small = F.g_size[g] <= kSmall;
+        if (!small && lane == 0) {  // big group: one subset-table slot, built once by k_tables
+          const int slot = atomicAdd(&sc.n_tab, 1);
+          if (slot < a.tcap) {
+            a.g_tab[g] = slot;
+            a.tab_group[slot] = g;
+          } else {
+            raise_err(a, phi, kOverflow, s, 0, 9, slot + 1);
+          }
+        }
         UnitSpace<M> us;
         us.init(a, F.g_status[g], s);
         int run = base + s_cnt[g - bs];
@@ -721,55 +739,45 @@ __device__ __forceinline__ void group_acc(const V2& a, uint32_t gstat, double* a
     acc[m] = static_cast<int>((gstat >> (16 * m)) & 0xffff) == Codec::done() ? a.t.post[m] : a.t.pre[m];
 }
 
-struct TransSmem {
-  unsigned long long* ex;  // [P1] (tag << 32) | idx of the group's state at that placement
-  unsigned long long* vb;  // [n_partial] max value bits per (subset, projection)
-  unsigned long long* rx;  // [n_partial] (rank << 32) | idx: min rank among the max
-  uint32_t* tg;            // [n_partial] entry owner tag
-};
-
-// Big groups: one CTA per (unit, chunk) item. The group's best representative
-// per (subset, projected placement) is built in shared memory: the empty subset
-// by a block reduction, the others by a max-value then min-(rank,idx) atomic
-// pass; the full subset is the state at that placement itself.
-template <int M>
-__device__ void phase_trans_big(const V2& a, int s, TransSmem& T) {
+// Subset tables of every big group of F_s, built once per step (one CTA per
+// group) into L2-resident global slots: the best representative per (subset,
+// projected placement) by a max-value then min-(rank, idx) pass (solvers.hpp:
+// 363-378), the state at each placement (the full subset), and the group's
+// best state (the empty subset). k_trans_big items then only read them.
+__device__ void phase_tables(const V2& a, int s) {
   const int cur = s & 1;
   StepCounters& sc = a.ctl->sc[s & 1];
   const FrontierV2& F = a.f[cur];
-  const int charge = (s > 0 || a.has_initial) ? 1 : 0;
-  const int P1 = a.sp.P1;
+  const int P1 = a.sp.P1, np = a.n_partial, M = a.t.M;
+  const int nsub = 1 << M;
   __shared__ unsigned long long s_bv[kWarps], s_brx[kWarps];
-  __shared__ unsigned long long s_v0, s_rx0;
-  uint32_t tag = 0;
-  const int nib = sc.items_b;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int item = blockIdx.x; item < nib; item += gridDim.x) {
-    ++tag;
-    const int unit = a.it_b_unit[item], chunk = a.it_b_chunk[item];
-    const int g = a.u_group[unit], sig = a.u_sig[unit];
+  const int nt = min(sc.n_tab, a.tcap);
+  for (int b = blockIdx.x; b < nt; b += gridDim.x) {
+    const int g = a.tab_group[b];
     const int gs = F.g_start[g], gn = F.g_size[g];
-    double acc[M];
-    group_acc<M>(a, F.g_status[g], acc);
-    // claim entries + empty-subset best (value desc, rank asc)
+    unsigned long long* vb = a.tab_vb + static_cast<size_t>(b) * np;
+    unsigned long long* rxs = a.tab_rx + static_cast<size_t>(b) * np;
+    uint32_t* ex = a.tab_ex + static_cast<size_t>(b) * P1;
+    for (int i = threadIdx.x; i < P1; i += kThreads) ex[i] = 0u;
+    for (int i = threadIdx.x; i < np; i += kThreads) {
+      vb[i] = 0ull;
+      rxs[i] = ~0ull;
+    }
+    __syncthreads();
     unsigned long long bv = 0, brx = ~0ull;
-    for (int j = threadIdx.x; j < gn; j += kThreads) {
+    for (int j = threadIdx.x; j < gn; j += kThreads) {  // claim placements, max value per entry, group best
       if (!F.alive[gs + j]) continue;
       const int pj = F.pid[gs + j];
-      const unsigned long long vb = vbits(F.value[gs + j]);
+      const unsigned long long v = vbits(F.value[gs + j]);
       const unsigned long long rx = (static_cast<unsigned long long>(F.rank[gs + j]) << 32) | static_cast<uint32_t>(j);
-      if (brx == ~0ull || vb > bv || (vb == bv && rx < brx)) {
-        bv = vb;
+      if (brx == ~0ull || v > bv || (v == bv && rx < brx)) {
+        bv = v;
         brx = rx;
       }
-      T.ex[pj] = (static_cast<unsigned long long>(tag) << 32) | static_cast<uint32_t>(j);
-#pragma unroll
-      for (int sub = 1; sub < (1 << M) - 1; ++sub) {
-        const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj];
-        T.tg[e] = tag;
-        T.vb[e] = 0ull;
-        T.rx[e] = ~0ull;
-      }
+      ex[pj] = static_cast<uint32_t>(j) + 1u;
+      for (int sub = 1; sub < nsub - 1; ++sub)
+        atomicMax(&vb[a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj]], v);
     }
     for (int o = 16; o > 0; o >>= 1) {
       const unsigned long long ov = __shfl_down_sync(0xffffffffu, bv, o);
@@ -783,73 +791,86 @@ __device__ void phase_trans_big(const V2& a, int s, TransSmem& T) {
       s_bv[warp] = bv;
       s_brx[warp] = brx;
     }
-    __syncthreads();
+    __syncthreads();  // also orders the vb maxima before the min pass (block-scope visibility)
     if (threadIdx.x == 0) {
       for (int w = 1; w < kWarps; ++w)
         if (s_brx[w] != ~0ull && (brx == ~0ull || s_bv[w] > bv || (s_bv[w] == bv && s_brx[w] < brx))) {
           bv = s_bv[w];
           brx = s_brx[w];
         }
-      s_v0 = bv;
-      s_rx0 = brx;
+      a.tab_hdr[2 * b] = bv;
+      a.tab_hdr[2 * b + 1] = brx;
     }
-    if (M > 1) {
-      for (int j = threadIdx.x; j < gn; j += kThreads) {  // max value per entry
-        if (!F.alive[gs + j]) continue;
-        const int pj = F.pid[gs + j];
-        const unsigned long long vb = vbits(F.value[gs + j]);
-#pragma unroll
-        for (int sub = 1; sub < (1 << M) - 1; ++sub)
-          atomicMax(&T.vb[a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj]], vb);
-      }
-      __syncthreads();
+    if (nsub > 2)
       for (int j = threadIdx.x; j < gn; j += kThreads) {  // min (rank, idx) among the max
         if (!F.alive[gs + j]) continue;
         const int pj = F.pid[gs + j];
-        const unsigned long long vb = vbits(F.value[gs + j]);
+        const unsigned long long v = vbits(F.value[gs + j]);
         const unsigned long long rx = (static_cast<unsigned long long>(F.rank[gs + j]) << 32) | static_cast<uint32_t>(j);
-#pragma unroll
-        for (int sub = 1; sub < (1 << M) - 1; ++sub) {
+        for (int sub = 1; sub < nsub - 1; ++sub) {
           const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj];
-          if (T.vb[e] == vb) atomicMin(&T.rx[e], rx);
+          if (vb[e] == v) atomicMin(&rxs[e], rx);
         }
       }
-    }
     __syncthreads();
+  }
+}
+
+// Big groups: one CTA per (unit, chunk) item; every thread owns targets and
+// reads its group's subset tables (phase_tables) from L2.
+template <int M>
+__device__ void phase_trans_big(const V2& a, int s) {
+  const int cur = s & 1;
+  StepCounters& sc = a.ctl->sc[s & 1];
+  const FrontierV2& F = a.f[cur];
+  const int charge = (s > 0 || a.has_initial) ? 1 : 0;
+  const int P1 = a.sp.P1, np = a.n_partial;
+  const int nib = sc.items_b;
+  for (int item = blockIdx.x; item < nib; item += gridDim.x) {
+    const int unit = a.it_b_unit[item], chunk = a.it_b_chunk[item];
+    const int g = a.u_group[unit], sig = a.u_sig[unit];
+    const int gs = F.g_start[g];
+    const int b = a.g_tab[g];
+    const unsigned long long* vb = a.tab_vb + static_cast<size_t>(b) * np;
+    const unsigned long long* rxs = a.tab_rx + static_cast<size_t>(b) * np;
+    const uint32_t* ex = a.tab_ex + static_cast<size_t>(b) * P1;
+    const unsigned long long v0 = a.tab_hdr[2 * b], rx0 = a.tab_hdr[2 * b + 1];
+    double acc[M];
+    group_acc<M>(a, F.g_status[g], acc);
     const int sb = a.sp.sig_off[sig], L = a.sp.sig_off[sig + 1] - sb;
     const int t0 = chunk * kChunkB, t1 = min(L, t0 + kChunkB);
     for (int ti = t0 + threadIdx.x; ti < t1; ti += kThreads) {
       const int p = a.sp.cand_pid[sb + ti];
       const int oi = a.sp.cand_oi[sb + ti];
-      BestT<M> b;
-      b.i[0] = s_rx0 == ~0ull ? -1 : static_cast<int>(s_rx0 & 0xffffffffu);
-      b.v[0] = __longlong_as_double(static_cast<long long>(s_v0));
-      b.r[0] = static_cast<uint32_t>(s_rx0 >> 32);
+      BestT<M> bt;
+      bt.i[0] = rx0 == ~0ull ? -1 : static_cast<int>(rx0 & 0xffffffffu);
+      bt.v[0] = __longlong_as_double(static_cast<long long>(v0));
+      bt.r[0] = static_cast<uint32_t>(rx0 >> 32);
 #pragma unroll
       for (int sub = 1; sub < (1 << M) - 1; ++sub) {
         const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + p];
-        const bool hit = T.tg[e] == tag && T.rx[e] != ~0ull;
-        b.i[sub] = hit ? static_cast<int>(T.rx[e] & 0xffffffffu) : -1;
-        b.v[sub] = hit ? __longlong_as_double(static_cast<long long>(T.vb[e])) : 0.0;
-        b.r[sub] = hit ? static_cast<uint32_t>(T.rx[e] >> 32) : 0u;
+        const unsigned long long rx = rxs[e];
+        const bool hit = rx != ~0ull;
+        bt.i[sub] = hit ? static_cast<int>(rx & 0xffffffffu) : -1;
+        bt.v[sub] = hit ? __longlong_as_double(static_cast<long long>(vb[e])) : 0.0;
+        bt.r[sub] = hit ? static_cast<uint32_t>(rx >> 32) : 0u;
       }
       {
-        const unsigned long long w = T.ex[p];
+        const uint32_t w = ex[p];
         const int full = (1 << M) - 1;
-        if ((w >> 32) == tag) {
-          const int j = static_cast<int>(w & 0xffffffffu);
-          b.i[full] = j;
-          b.v[full] = F.value[gs + j];
-          b.r[full] = F.rank[gs + j];
+        if (w) {
+          const int j = static_cast<int>(w) - 1;
+          bt.i[full] = j;
+          bt.v[full] = F.value[gs + j];
+          bt.r[full] = F.rank[gs + j];
         } else {
-          b.i[full] = -1;
-          b.v[full] = 0.0;
-          b.r[full] = 0u;
+          bt.i[full] = -1;
+          bt.v[full] = 0.0;
+          bt.r[full] = 0u;
         }
       }
-      emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, static_cast<uint32_t>(a.sp.pl_ids[p]), b, F);
+      emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, static_cast<uint32_t>(a.sp.pl_ids[p]), bt, F);
     }
-    __syncthreads();
   }
 }
 
@@ -1286,22 +1307,18 @@ __global__ void __launch_bounds__(kThreads) k_ranks_small(const V2* __restrict__
   phase_ranks_small(a, s);
 }
 
+__global__ void __launch_bounds__(kThreads) k_tables(const V2* __restrict__ ap, int s) {
+  const V2& a = c_v2;
+  if (failed(a)) return;
+  phase_tables(a, s);
+}
+
 template <int M>
 __global__ void __launch_bounds__(kThreads) k_trans_big(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
   if (static_cast<int>(blockIdx.x) >= a.ctl->sc[s & 1].items_b) return;  // no item for this CTA
-  const int P1 = a.sp.P1;
-  TransSmem T;
-  T.ex = smem_u64;
-  T.vb = smem_u64 + P1;
-  T.rx = T.vb + a.n_partial;
-  T.tg = reinterpret_cast<uint32_t*>(T.rx + a.n_partial);
-  for (int i = threadIdx.x; i < P1; i += kThreads) T.ex[i] = 0ull;  // tags start at 1
-  for (int i = threadIdx.x; i < a.n_partial; i += kThreads) T.tg[i] = 0u;
-  __syncthreads();
-  phase_trans_big<M>(a, s, T);
+  phase_trans_big<M>(a, s);
 }
 
 template <int M>
@@ -1502,7 +1519,7 @@ __global__ void k_sig_len(const int32_t* sig_off, int n_sig, int32_t* sig_len) {
 }
 
 struct Caps {
-  int fcap, gcap, ucap, itcap, ccap, hbits;
+  int fcap, gcap, ucap, itcap, ccap, hbits, tcap;
   long long hcap;
 };
 
@@ -1594,6 +1611,14 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, double band, int dominan
   a.ns_big = c.buf<int32_t>("v2_nsbig", H);
   a.ns_small = c.buf<int32_t>("v2_nssmall", H);
   a.ns_used = c.buf<int32_t>("v2_nsused", H);
+  a.tcap = caps.tcap;
+  const int n_partial_l = sp.proj_base[(1 << t.M) - 1];
+  a.g_tab = c.buf<int32_t>("v2_gtab", caps.gcap);
+  a.tab_group = c.buf<int32_t>("v2_tabgroup", caps.tcap);
+  a.tab_vb = c.buf<unsigned long long>("v2_tabvb", static_cast<size_t>(caps.tcap) * std::max(1, n_partial_l));
+  a.tab_rx = c.buf<unsigned long long>("v2_tabrx", static_cast<size_t>(caps.tcap) * std::max(1, n_partial_l));
+  a.tab_ex = c.buf<uint32_t>("v2_tabex", static_cast<size_t>(caps.tcap) * sp.P1);
+  a.tab_hdr = c.buf<unsigned long long>("v2_tabhdr", static_cast<size_t>(caps.tcap) * 2);
   for (void* z : {static_cast<void*>(a.hash), static_cast<void*>(a.ns_ucnt), static_cast<void*>(a.ns_ccnt),
                   static_cast<void*>(a.ns_ucur), static_cast<void*>(a.ns_ccur), static_cast<void*>(a.ns_out)})
     MGS_CUDA_OK(cudaMemsetAsync(z, 0, H * 4, c.stream));
@@ -1646,7 +1671,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   // per-lane scalars: band (solvers.hpp:258-267), dominance validity, tables' smem
   std::vector<double> band(K);
   std::vector<int> dom_ok(K), merge_win(K);
-  size_t smem_trans = 0, smem_merge = 0;
+  size_t smem_merge = 0;
   for (int l = 0; l < K; ++l) {
     const HostTables& t = lanes[l].pr->t;
     const DevSpace& sp = *lanes[l].sp;
@@ -1665,8 +1690,6 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     band[l] = 1e-9;
     for (int m = 0; m < M; ++m) band[l] += t.loss[m] * cap_max[m] * acc_max[m];
     dom_ok[l] = dominance_ok ? 1 : 0;
-    const int n_partial = sp.proj_base[(1 << M) - 1];
-    smem_trans = std::max(smem_trans, static_cast<size_t>(sp.P1) * 8 + static_cast<size_t>(n_partial) * 20);
     merge_win[l] = std::min(sp.P1, 8192);  // whole placement range in one window when it fits
     smem_merge = std::max(smem_merge, static_cast<size_t>(2 * merge_win[l]) * 8);
   }
@@ -1674,7 +1697,6 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   auto ktbig = M == 1 ? k_trans_big<1> : k_trans_big<2>;
   auto ktsmall = M == 1 ? k_trans_small<1> : k_trans_small<2>;
   auto kunits = M == 1 ? k_units<1> : k_units<2>;
-  MGS_CUDA_OK(cudaFuncSetAttribute(ktbig, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_trans)));
   MGS_CUDA_OK(cudaFuncSetAttribute(k_ranks_big, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_rank)));
   MGS_CUDA_OK(cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_merge)));
   // One resident wave per kernel (SMs x max co-resident CTAs), shared by the
@@ -1694,17 +1716,18 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   const dim3 g_place = wave(reinterpret_cast<const void*>(k_place), 0);
   const dim3 g_rbig = wave(reinterpret_cast<const void*>(k_ranks_big), smem_rank);
   const dim3 g_rsmall = wave(reinterpret_cast<const void*>(k_ranks_small), 0);
-  const dim3 g_tbig = wave(reinterpret_cast<const void*>(ktbig), smem_trans);
+  const dim3 g_tbig = wave(reinterpret_cast<const void*>(ktbig), 0);
+  const dim3 g_tables = wave(reinterpret_cast<const void*>(k_tables), 0);
   const dim3 g_tsmall = wave(reinterpret_cast<const void*>(ktsmall), 0);
   const dim3 g_band = wave(reinterpret_cast<const void*>(k_band), smem_merge);
   const dim3 g_oscan = wave(reinterpret_cast<const void*>(k_outscan), 0);
   const dim3 g_write = wave(reinterpret_cast<const void*>(k_write), 0);
   const dim3 g_dom = wave(reinterpret_cast<const void*>(k_dom), 0);
-  static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 128ll << 20};
+  static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 2048, 128ll << 20};
   const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr || std::getenv("MGS_TRACE") != nullptr;
   if (std::getenv("MGS_TRACE"))
     std::fprintf(stderr, "trace v2 setup: lanes %d S %d M %d smem trans %zu rank %zu merge %zu grid.x %u %u %u %u %u %u %u %u %u %u %u\n",
-                 K, S, M, smem_trans, smem_rank, smem_merge, g_units.x, g_scans.x, g_place.x, g_rbig.x, g_rsmall.x,
+                 K, S, M, size_t(0), smem_rank, smem_merge, g_units.x, g_scans.x, g_place.x, g_rbig.x, g_rsmall.x,
                  g_tbig.x, g_tsmall.x, g_band.x, g_oscan.x, g_write.x, g_dom.x);
   for (int attempt = 0; attempt < 10; ++attempt) {
     std::vector<V2> args(K);
@@ -1716,8 +1739,8 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     // The window's kernel sequence depends only on S, M, the lane count and
     // launch shapes (all problem data lives behind d_args), so it is captured
     // once into a CUDA graph and replayed; MGS_DEBUG_STEPS launches eagerly.
-    constexpr int kK = 11;
-    static const char* kNames[kK] = {"units", "scans", "place", "ranks_big", "ranks_small", "trans_big",
+    constexpr int kK = 12;
+    static const char* kNames[kK] = {"units", "scans", "place", "ranks_big", "ranks_small", "tables", "trans_big",
                                      "trans_small", "band", "outscan", "write", "dom"};
     std::vector<cudaEvent_t> evs;
     auto enqueue = [&](cudaStream_t st_, bool timed) {
@@ -1782,7 +1805,9 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         after("ranks_big", st);
         k_ranks_small<<<g_rsmall, kThreads, 0, st_>>>(d_args, st);
         after("ranks_small", st);
-        ktbig<<<g_tbig, kThreads, smem_trans, st_>>>(d_args, st);
+        k_tables<<<g_tables, kThreads, 0, st_>>>(d_args, st);
+        after("tables", st);
+        ktbig<<<g_tbig, kThreads, 0, st_>>>(d_args, st);
         after("trans_big", st);
         ktsmall<<<g_tsmall, kThreads, 0, st_>>>(d_args, st);
         after("trans_small", st);
@@ -1800,7 +1825,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
       k_term3<<<g_term, kThreads, 0, st_>>>(d_args);
       k_backtrack2<<<g_one, 32, 0, st_>>>(d_args);
     };
-    c.kernel_launches += 11ull * S + 4;
+    c.kernel_launches += 12ull * S + 4;
     if (debug) {
       const auto host_t0 = std::chrono::steady_clock::now();
       enqueue(c.stream, true);
@@ -1821,7 +1846,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
       std::fprintf(stderr, "\n");
     } else {
       char key[256];
-      std::snprintf(key, sizeof key, "v2:%d:%d:%d:%zu:%zu:%zu:%p", K, S, M, smem_trans, smem_merge, smem_rank,
+      std::snprintf(key, sizeof key, "v2:%d:%d:%d:%zu:%zu:%p", K, S, M, smem_merge, smem_rank,
                     static_cast<void*>(d_args));
       auto it = c.graphs.find(key);
       if (it == c.graphs.end()) {
@@ -1861,6 +1886,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         case 6: caps.hcap = std::max<long long>(need * 2, caps.hcap * 2); break;
         case 7: caps.ccap = static_cast<int>(std::max<long long>(need * 2, caps.ccap * 2ll)); break;
         case 8: caps.itcap = static_cast<int>(std::max<long long>(need * 2, caps.itcap * 2ll)); break;
+        case 9: caps.tcap = static_cast<int>(std::max<long long>(need * 2, caps.tcap * 2ll)); break;
         default: throw PlanFail{MGS_ERR_CUDA, "persistent DP: unknown capacity overflow"};
       }
     }
