@@ -1723,7 +1723,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   const dim3 g_oscan = wave(reinterpret_cast<const void*>(k_outscan), 0);
   const dim3 g_write = wave(reinterpret_cast<const void*>(k_write), 0);
   const dim3 g_dom = wave(reinterpret_cast<const void*>(k_dom), 0);
-  static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 2048, 128ll << 20};
+  static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 8192, 128ll << 20};
   const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr || std::getenv("MGS_TRACE") != nullptr;
   if (std::getenv("MGS_TRACE"))
     std::fprintf(stderr, "trace v2 setup: lanes %d S %d M %d smem trans %zu rank %zu merge %zu grid.x %u %u %u %u %u %u %u %u %u %u %u\n",
@@ -1878,6 +1878,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
       if (h[l].err_code != kOverflow) continue;
       grow = true;
       const long long need = h[l].need;
+      if (debug) std::fprintf(stderr, "v2 capacity growth: what %d need %lld at step %d\n", h[l].need_what, need, h[l].err_step);
       switch (h[l].need_what) {
         case 2: caps.hbits += 1; break;
         case 3: caps.ucap = static_cast<int>(std::max<long long>(need * 2, caps.ucap * 2ll)); break;

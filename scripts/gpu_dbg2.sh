@@ -1,3 +1,3 @@
 #!/bin/bash
-OUT=gpurun_out/dbg5; mkdir -p $OUT
+OUT=gpurun_out/dbg6; mkdir -p $OUT
 timeout 120 env MGS_DEBUG_STEPS=1 python -u scripts/solve_once.py > $OUT/steps.log 2>&1
