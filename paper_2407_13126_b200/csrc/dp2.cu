@@ -77,9 +77,10 @@ struct FrontierV2 {
 };
 
 struct StepCounters {  // double buffered; zeroed one step ahead
-  int n_units, T, items_s, items_b, n_big, n_small, n_big_bucket, ticket, kids, ticket2;
+  int n_units, T, items_s, items_b, n_big, n_small, n_big_bucket, ticket, kids;
   int n_ns;  // successor statuses of the step = entries of the used-slot list
   int n_tab;  // big status groups of F_s whose subset tables k_tables builds
+  int out_states, out_groups;  // F_{s+1} allocation cursors (k_write, one atomic per CTA batch)
 };
 
 struct Ctl {
@@ -97,7 +98,6 @@ struct Ctl {
   int best_idx;
   int ranks_prev[2];  // [s&1]: live states of F_{s-1}, the parent-rank space of F_s
   int scan_total[kNumScans];
-  int out_total[2];  // survivors, groups of F_{s+1}
 };
 
 struct V2 {
@@ -132,7 +132,7 @@ struct V2 {
   unsigned long long* tab_hdr;  // [tcap][2] empty subset: value bits, (rank << 32 | j)
   int32_t *ns_ucnt, *ns_ccnt, *ns_ubase, *ns_cbase, *ns_ucur, *ns_ccur, *ns_units, *ns_bigpos, *ns_smallpos;
   int32_t *ns_big, *ns_small;
-  int32_t *ns_out, *ns_obase, *ns_gbase;  // survivors per status, their offsets and group index
+  int32_t* ns_out;  // survivors per status
   int32_t *it_s_unit, *it_s_chunk, *it_b_unit, *it_b_chunk;
   int itcap;
   double* c_value;
@@ -1105,24 +1105,59 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
 }
 
 // S6c: survivors of every status written at their scanned offsets
+// Survivors of every status go to F_{s+1} at positions claimed with one
+// atomic per status (big statuses) or per CTA batch of small statuses; the
+// frontier's storage order is therefore arbitrary, which nothing depends on
+// (every comparison uses values and lex ranks, never storage indices).
+__device__ __forceinline__ bool claim_fits(const V2& a, int s, int q0, int total, int gi) {
+  if (q0 + total > a.fcap) {
+    raise_err(a, 0, kOverflow, s, 0, 4, q0 + total);
+    return false;
+  }
+  if (gi >= a.gcap) {
+    raise_err(a, 0, kOverflow, s, 0, 5, gi + 1);
+    return false;
+  }
+  if (a.hist_base[s + 1] + q0 + total > a.hcap) {
+    raise_err(a, 0, kOverflow, s, 0, 6, a.hist_base[s + 1] + q0 + total);
+    return false;
+  }
+  return true;
+}
+
+constexpr int kWriteBatch = kWarps * 4;  // small statuses per CTA allocation batch
+static_assert(kWriteBatch == 32, "warp 0 scans one batch lane-parallel");
+
 __device__ void phase_write(const V2& a, int s) {
   const int nxt = (s + 1) & 1;
   StepCounters& sc = a.ctl->sc[s & 1];
   const FrontierV2& N = a.f[nxt];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ int s_wsum[kWarps];
+  __shared__ int s_q0, s_gi, s_ok;
+  __shared__ int s_bq[kWriteBatch], s_bg[kWriteBatch];
   const int nbig = sc.n_big;
   for (int w = blockIdx.x; w < nbig; w += gridDim.x) {
     const int id = a.ns_big[w];
     const int total = a.ns_out[id];
     if (total == 0) continue;  // uniform
     const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
-    const int q0 = a.ns_obase[id], gi = a.ns_gbase[id];
     const uint32_t key = a.hash[id] - 1u;
-    if (threadIdx.x == 0 && a.dbg) {
-      atomicMax(reinterpret_cast<unsigned long long*>(a.dbg + kDbg * (s + 1 < a.S ? s + 1 : s) + 8),
-                static_cast<unsigned long long>(total));
-      if (total > kSmall) atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + kDbg * (s + 1 < a.S ? s + 1 : s) + 9), 1ull);
+    if (threadIdx.x == 0) {
+      s_q0 = atomicAdd(&sc.out_states, total);
+      s_gi = atomicAdd(&sc.out_groups, 1);
+      s_ok = claim_fits(a, s, s_q0, total, s_gi) ? 1 : 0;
+      if (a.dbg) {
+        atomicMax(reinterpret_cast<unsigned long long*>(a.dbg + kDbg * (s + 1 < a.S ? s + 1 : s) + 8),
+                  static_cast<unsigned long long>(total));
+        if (total > kSmall) atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + kDbg * (s + 1 < a.S ? s + 1 : s) + 9), 1ull);
+      }
+    }
+    __syncthreads();
+    const int q0 = s_q0, gi = s_gi;
+    if (!s_ok) {
+      __syncthreads();
+      continue;
     }
     if (threadIdx.x == 0) {
       N.g_start[gi] = q0;
@@ -1147,29 +1182,60 @@ __device__ void phase_write(const V2& a, int s) {
       if (a.c_live[k]) write_state(a, s, nxt, q0 + off++, gi, key, k);
     __syncthreads();
   }
-  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  // small statuses: CTA batches of kWriteBatch, one allocation per batch, a
+  // warp per status
   const int nsm = sc.n_small;
-  for (int i = wid; i < nsm; i += nw) {
-    const int id = a.ns_small[i];
-    const int total = a.ns_out[id];
-    if (total == 0) continue;
-    const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
-    const int q0 = a.ns_obase[id], gi = a.ns_gbase[id];
-    const uint32_t key = a.hash[id] - 1u;
-    if (lane == 0) {
-      N.g_start[gi] = q0;
-      N.g_size[gi] = total;
-      N.g_status[gi] = key;
-      N.g_alive[gi] = total;
+  for (int c0 = blockIdx.x * kWriteBatch; c0 < nsm; c0 += gridDim.x * kWriteBatch) {
+    if (warp == 0) {
+      int tot = 0, grp = 0;  // lanes 0..31 cover the batch (kWriteBatch == 32)
+      if (c0 + lane < nsm) {
+        tot = a.ns_out[a.ns_small[c0 + lane]];
+        grp = tot > 0 ? 1 : 0;
+      }
+      int xt = tot, xg = grp;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int yt = __shfl_up_sync(0xffffffffu, xt, o), yg = __shfl_up_sync(0xffffffffu, xg, o);
+        if (lane >= o) {
+          xt += yt;
+          xg += yg;
+        }
+      }
+      int bq = 0, bgi = 0;
+      if (lane == 31) {
+        bq = atomicAdd(&sc.out_states, xt);
+        bgi = atomicAdd(&sc.out_groups, xg);
+        s_ok = claim_fits(a, s, bq, xt, bgi + xg - 1) ? 1 : 0;
+      }
+      bq = __shfl_sync(0xffffffffu, bq, 31);
+      bgi = __shfl_sync(0xffffffffu, bgi, 31);
+      s_bq[lane] = bq + xt - tot;
+      s_bg[lane] = bgi + xg - grp;
     }
-    int run = 0;
-    for (int k0 = cb; k0 < cb + cc; k0 += 32) {
-      const int k = k0 + lane;
-      const bool keep = k < cb + cc && a.c_live[k];
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
-      run += __popc(bal);
-    }
+    __syncthreads();
+    if (s_ok)
+      for (int t = warp; t < kWriteBatch && c0 + t < nsm; t += kWarps) {
+        const int id = a.ns_small[c0 + t];
+        const int total = a.ns_out[id];
+        if (total == 0) continue;
+        const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
+        const int q0 = s_bq[t], gi = s_bg[t];
+        const uint32_t key = a.hash[id] - 1u;
+        if (lane == 0) {
+          N.g_start[gi] = q0;
+          N.g_size[gi] = total;
+          N.g_status[gi] = key;
+          N.g_alive[gi] = total;
+        }
+        int run = 0;
+        for (int k0 = cb; k0 < cb + cc; k0 += 32) {
+          const int k = k0 + lane;
+          const bool keep = k < cb + cc && a.c_live[k];
+          const unsigned bal = __ballot_sync(0xffffffffu, keep);
+          if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
+          run += __popc(bal);
+        }
+      }
+    __syncthreads();
   }
 }
 
@@ -1340,30 +1406,10 @@ __global__ void __launch_bounds__(kThreads) k_band(const V2* __restrict__ ap, in
   phase_band(a, s, smem_u64, smem_u64 + a.merge_win);
 }
 
-__global__ void __launch_bounds__(kThreads) k_outscan(const V2* __restrict__ ap, int s) {
-  const V2& a = c_v2;
-  if (failed(a)) return;
-  const int H = a.ctl->sc[s & 1].n_ns;
-  const ScanJob jobs[2] = {{a.ns_out, nullptr, a.ns_obase, H, 0, a.ns_used},
-                           {a.ns_out, nullptr, a.ns_gbase, H, 3, a.ns_used}};
-  multi_scan(a, jobs, 2, 2 * (s + 1) + 1, &a.ctl->sc[s & 1].ticket2, a.ctl->out_total);
-}
-
 __global__ void __launch_bounds__(kThreads) k_write(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (failed(a)) return;
-  const int nxt = (s + 1) & 1;
-  Ctl* ctl = a.ctl;
-  const int total = ctl->out_total[0], groups = ctl->out_total[1];
-  const bool fits = total <= a.fcap && groups <= a.gcap && a.hist_base[s + 1] + total <= a.hcap;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    ctl->n_store[nxt] = total;
-    ctl->n_groups[nxt] = groups;
-    if (total > a.fcap) raise_err(a, 0, kOverflow, s, 0, 4, total);
-    else if (groups > a.gcap) raise_err(a, 0, kOverflow, s, 0, 5, groups);
-    else if (a.hist_base[s + 1] + total > a.hcap) raise_err(a, 0, kOverflow, s, 0, 6, a.hist_base[s + 1] + total);
-  }
-  if (fits) phase_write(a, s);
+  phase_write(a, s);
 }
 
 __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int s) {
@@ -1391,6 +1437,8 @@ __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int
   if (gtid == 0) {  // end-of-slot bookkeeping (every value read here is final)
     const int nxt = (s + 1) & 1;
     StepCounters& sc = ctl->sc[s & 1];
+    ctl->n_store[nxt] = sc.out_states;   // F_{s+1} as allocated by k_write
+    ctl->n_groups[nxt] = sc.out_groups;
     a.hist_base[s + 2] = a.hist_base[s + 1] + ctl->n_store[nxt];  // array has S+2 entries
     if (a.dbg) {
       long long* d = a.dbg + static_cast<long long>(kDbg) * s;
@@ -1606,8 +1654,6 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, double band, int dominan
   a.ns_bigpos = c.buf<int32_t>("v2_nsbigpos", H);
   a.ns_smallpos = c.buf<int32_t>("v2_nssmallpos", H);
   a.ns_out = c.buf<int32_t>("v2_nsout", H);
-  a.ns_obase = c.buf<int32_t>("v2_nsobase", H);
-  a.ns_gbase = c.buf<int32_t>("v2_nsgbase", H);
   a.ns_big = c.buf<int32_t>("v2_nsbig", H);
   a.ns_small = c.buf<int32_t>("v2_nssmall", H);
   a.ns_used = c.buf<int32_t>("v2_nsused", H);
@@ -1720,15 +1766,14 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   const dim3 g_tables = wave(reinterpret_cast<const void*>(k_tables), 0);
   const dim3 g_tsmall = wave(reinterpret_cast<const void*>(ktsmall), 0);
   const dim3 g_band = wave(reinterpret_cast<const void*>(k_band), smem_merge);
-  const dim3 g_oscan = wave(reinterpret_cast<const void*>(k_outscan), 0);
   const dim3 g_write = wave(reinterpret_cast<const void*>(k_write), 0);
   const dim3 g_dom = wave(reinterpret_cast<const void*>(k_dom), 0);
   static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 8192, 128ll << 20};
   const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr || std::getenv("MGS_TRACE") != nullptr;
   if (std::getenv("MGS_TRACE"))
-    std::fprintf(stderr, "trace v2 setup: lanes %d S %d M %d smem trans %zu rank %zu merge %zu grid.x %u %u %u %u %u %u %u %u %u %u %u\n",
+    std::fprintf(stderr, "trace v2 setup: lanes %d S %d M %d smem trans %zu rank %zu merge %zu grid.x %u %u %u %u %u %u %u %u %u %u\n",
                  K, S, M, size_t(0), smem_rank, smem_merge, g_units.x, g_scans.x, g_place.x, g_rbig.x, g_rsmall.x,
-                 g_tbig.x, g_tsmall.x, g_band.x, g_oscan.x, g_write.x, g_dom.x);
+                 g_tbig.x, g_tsmall.x, g_band.x, g_write.x, g_dom.x);
   for (int attempt = 0; attempt < 10; ++attempt) {
     std::vector<V2> args(K);
     for (int l = 0; l < K; ++l) args[l] = lane_args(c, lanes[l], caps, band[l], dom_ok[l], merge_win[l], g_term.x);
@@ -1739,9 +1784,9 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     // The window's kernel sequence depends only on S, M, the lane count and
     // launch shapes (all problem data lives behind d_args), so it is captured
     // once into a CUDA graph and replayed; MGS_DEBUG_STEPS launches eagerly.
-    constexpr int kK = 12;
+    constexpr int kK = 11;
     static const char* kNames[kK] = {"units", "scans", "place", "ranks_big", "ranks_small", "tables", "trans_big",
-                                     "trans_small", "band", "outscan", "write", "dom"};
+                                     "trans_small", "band", "write", "dom"};
     std::vector<cudaEvent_t> evs;
     auto enqueue = [&](cudaStream_t st_, bool timed) {
       auto mark = [&]() {
@@ -1772,8 +1817,8 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
             cudaMemcpyAsync(ss, args[0].scan_state, 256 * 8, cudaMemcpyDeviceToHost, side);
             cudaStreamSynchronize(side);
             const StepCounters& q = hp->sc[st & 1];
-            std::fprintf(stderr, "HANG in %s step %d: err %d ticket %d ticket2 %d n_units %d ranks_prev %d %d alive %d %d\n",
-                         name, st, hp->err_code, q.ticket, q.ticket2, q.n_units, hp->ranks_prev[0], hp->ranks_prev[1],
+            std::fprintf(stderr, "HANG in %s step %d: err %d ticket %d n_units %d ranks_prev %d %d alive %d %d\n",
+                         name, st, hp->err_code, q.ticket, q.n_units, hp->ranks_prev[0], hp->ranks_prev[1],
                          hp->alive_now[0], hp->alive_now[1]);
             for (int i = 0; i < 140; ++i)
               std::fprintf(stderr, "  tile %d: ep %llu flag %llu agg %llu\n", i, ss[i] >> 34, (ss[i] >> 32) & 3,
@@ -1790,7 +1835,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
                        " store %d/%d groups %d/%d alive %d/%d out %d/%d\n",
                        st, name, cudaGetErrorString(e), hc.err_code, q.n_units, q.T, q.items_s, q.items_b, q.n_big,
                        q.n_small, q.kids, hc.n_store[0], hc.n_store[1], hc.n_groups[0], hc.n_groups[1],
-                       hc.alive_now[0], hc.alive_now[1], hc.out_total[0], hc.out_total[1]);
+                       hc.alive_now[0], hc.alive_now[1], q.out_states, q.out_groups);
         }
         mark();
       };
@@ -1813,8 +1858,6 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         after("trans_small", st);
         k_band<<<g_band, kThreads, smem_merge, st_>>>(d_args, st);
         after("band", st);
-        k_outscan<<<g_oscan, kThreads, 0, st_>>>(d_args, st);
-        after("outscan", st);
         k_write<<<g_write, kThreads, 0, st_>>>(d_args, st);
         after("write", st);
         k_dom<<<g_dom, kThreads, 0, st_>>>(d_args, st);
@@ -1825,7 +1868,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
       k_term3<<<g_term, kThreads, 0, st_>>>(d_args);
       k_backtrack2<<<g_one, 32, 0, st_>>>(d_args);
     };
-    c.kernel_launches += 12ull * S + 4;
+    c.kernel_launches += 11ull * S + 4;
     if (debug) {
       const auto host_t0 = std::chrono::steady_clock::now();
       enqueue(c.stream, true);
