@@ -78,6 +78,7 @@ struct FrontierV2 {
 
 struct StepCounters {  // double buffered; zeroed one step ahead
   int n_units, T, items_s, items_b, n_big, n_small, n_big_bucket, ticket, kids;
+  int u_cursor;  // unit-list allocation cursor (k_scans)
   int n_ns;  // successor statuses of the step = entries of the used-slot list
   int n_tab;  // big status groups of F_s whose subset tables k_tables builds
   int out_states, out_groups;  // F_{s+1} allocation cursors (k_write, one atomic per CTA batch)
@@ -1311,6 +1312,27 @@ __global__ void __launch_bounds__(kThreads) k_units(const V2* __restrict__ ap, i
   phase_units<M>(a, s, 0, s_cnt, s_red);
 }
 
+// Warp-aggregated reservation of n (>= 0) slots from *cursor; every lane of
+// the warp must call it. Returns the lane's first slot.
+__device__ __forceinline__ int warp_alloc(int* cursor, int n) {
+  const int lane = threadIdx.x & 31;
+  int x = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  int base = 0;
+  if (lane == 31) base = atomicAdd(cursor, x);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  return base + x - n;
+}
+
+// S2: ranges for the step's successor statuses (candidates, units, big/small
+// status lists) and units (work items), reserved with warp-aggregated
+// atomics -- their order is arbitrary and nothing depends on it -- and the
+// one order-bearing scan: children offsets in parent-rank order (the dense
+// lex ranks of F_s).
 __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (failed(a)) return;
@@ -1326,15 +1348,39 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
       if (static_cast<unsigned long long>(alive_cur) > ctl->fpeak) ctl->fpeak = alive_cur;
     }
   }
-  const int H = sc.n_ns;  // per-status scans run over the step's claimed slots only
-  const ScanJob jobs[kNumScans] = {{a.ns_ccnt, nullptr, a.ns_cbase, H, 0, a.ns_used},
-                                   {a.ns_ucnt, nullptr, a.ns_ubase, H, 0, a.ns_used},
-                                   {a.ns_ucnt, a.ns_ccnt, a.ns_bigpos, H, 1, a.ns_used},
-                                   {a.ns_ucnt, a.ns_ccnt, a.ns_smallpos, H, 2, a.ns_used},
-                                   {a.u_chs, nullptr, a.u_sbase, sc.n_units, 0},
-                                   {a.u_chb, nullptr, a.u_bbase, sc.n_units, 0},
-                                   {a.kid_cnt[cur], nullptr, a.kid_base, ctl->ranks_prev[s & 1], 0}};
-  multi_scan(a, jobs, kNumScans, 2 * (s + 1), &sc.ticket, ctl->scan_total);
+  const int lane = threadIdx.x & 31;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  const int n_ns = sc.n_ns;
+  for (int k0 = gtid - lane; k0 < n_ns; k0 += gstride) {  // warp-uniform trip count
+    const int k = k0 + lane;
+    const bool valid = k < n_ns;
+    const int id = valid ? a.ns_used[k] : 0;
+    const int cc = valid ? a.ns_ccnt[id] : 0, uc = valid ? a.ns_ucnt[id] : 0;
+    const bool big = valid && (uc > 1 || cc > kBigNs);
+    const int cb = warp_alloc(&sc.T, cc);
+    const int ub = warp_alloc(&sc.u_cursor, uc);
+    const int bp = warp_alloc(&sc.n_big, big ? 1 : 0);
+    const int sp = warp_alloc(&sc.n_small, valid && !big ? 1 : 0);
+    if (valid) {
+      a.ns_cbase[id] = cb;
+      a.ns_ubase[id] = ub;
+      a.ns_bigpos[id] = bp;
+      a.ns_smallpos[id] = sp;
+    }
+  }
+  const int nu = sc.n_units;
+  for (int u0 = gtid - lane; u0 < nu; u0 += gstride) {
+    const int u = u0 + lane;
+    const bool valid = u < nu;
+    const int sb = warp_alloc(&sc.items_s, valid ? a.u_chs[u] : 0);
+    const int bb = warp_alloc(&sc.items_b, valid ? a.u_chb[u] : 0);
+    if (valid) {
+      a.u_sbase[u] = sb;
+      a.u_bbase[u] = bb;
+    }
+  }
+  const ScanJob jobs[1] = {{a.kid_cnt[cur], nullptr, a.kid_base, ctl->ranks_prev[s & 1], 0}};
+  multi_scan(a, jobs, 1, 2 * (s + 1), &sc.ticket, ctl->scan_total);
 }
 
 __global__ void __launch_bounds__(kThreads) k_place(const V2* __restrict__ ap, int s) {
@@ -1342,20 +1388,14 @@ __global__ void __launch_bounds__(kThreads) k_place(const V2* __restrict__ ap, i
   if (failed(a)) return;
   Ctl* ctl = a.ctl;
   StepCounters& sc = ctl->sc[s & 1];
-  const int T_ = ctl->scan_total[0];
-  const bool fits = T_ <= a.ccap && ctl->scan_total[4] <= a.itcap && ctl->scan_total[5] <= a.itcap;
+  const int T_ = sc.T;
+  const bool fits = T_ <= a.ccap && sc.items_s <= a.itcap && sc.items_b <= a.itcap;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    sc.T = T_;
-    sc.n_big = ctl->scan_total[2];
-    sc.n_small = ctl->scan_total[3];
-    sc.items_s = ctl->scan_total[4];
-    sc.items_b = ctl->scan_total[5];
-    sc.kids = ctl->scan_total[6];
+    sc.kids = ctl->scan_total[0];
     ctl->tr += static_cast<unsigned long long>(T_);
     ctl->tbytes += static_cast<unsigned long long>(ctl->n_store[s & 1]) * 20ull + static_cast<unsigned long long>(T_) * 37ull;
     if (T_ > a.ccap) raise_err(a, 0, kOverflow, s, 0, 7, T_);
-    if (ctl->scan_total[4] > a.itcap || ctl->scan_total[5] > a.itcap)
-      raise_err(a, 0, kOverflow, s, 0, 8, max(ctl->scan_total[4], ctl->scan_total[5]));
+    if (sc.items_s > a.itcap || sc.items_b > a.itcap) raise_err(a, 0, kOverflow, s, 0, 8, max(sc.items_s, sc.items_b));
   }
   if (fits) phase_place(a, s);
 }
