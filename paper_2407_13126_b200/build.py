@@ -24,7 +24,7 @@ FLAGS = [
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
     "-Xptxas", "-warn-spills",
     "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-]
+] + (["-DMGS_MINB=" + os.environ["MGS_MINB"]] if os.environ.get("MGS_MINB") else [])
 
 
 def _stale(target, deps):

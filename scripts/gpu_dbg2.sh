@@ -1,3 +1,3 @@
 #!/bin/bash
-OUT=gpurun_out/dbg6; mkdir -p $OUT
-timeout 120 env MGS_DEBUG_STEPS=1 python -u scripts/solve_once.py > $OUT/steps.log 2>&1
+OUT=gpurun_out/dbg7; mkdir -p $OUT
+timeout 60 env MGS_TRACE=1 python -u scripts/solve_once.py tests/golden/kat/worked_example.scn > $OUT/trace.log 2>&1
