@@ -17,6 +17,8 @@
 // first-max rule picks its smallest option index — the candidate's index.
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 #include "ctx.cuh"
 
 namespace mgs {
@@ -61,11 +63,31 @@ __global__ void k_ub_suffix(const double* best, int S, double* ub) {
   for (int s = S - 1; s >= 0; --s) ub[s] = dadd(ub[s + 1], best[s]);
 }
 
-// Single-CTA sequential greedy walk.
+// Sequential greedy walk on one thread-block cluster (kGreedyCluster CTAs of
+// 1024 threads): every step each CTA takes a strided slice of the candidates
+// and reduces its first-max in shared memory; the CTAs exchange their results
+// through distributed shared memory (double-buffered by step parity, so one
+// cluster barrier per step suffices) and all of them fold the same winner into
+// identical copies of the walk's state.
+constexpr int kGreedyCluster = 8;
+
+struct GreedyRes {
+  double v;
+  int oi, ci;
+};
+
+__device__ __forceinline__ bool g_better(double v, int oi, int ci, double bv, int boi, int bci) {
+  return ci >= 0 && (bci < 0 || v > bv || (v == bv && oi < boi));
+}
+
 __global__ void __launch_bounds__(1024) k_greedy(DevSpace sp, HostTables t, Recv recv, int has_initial,
                                                  double* incumbent, int32_t* greedy) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank()), nrank = static_cast<int>(cluster.num_blocks());
   __shared__ double s_v[32];
   __shared__ int s_oi[32], s_ci[32];
+  __shared__ GreedyRes s_res[2];  // this CTA's first-max, by step parity (read remotely)
   __shared__ int s_state[KM];
   __shared__ uint64_t s_ids;
   __shared__ double s_value;
@@ -86,7 +108,7 @@ __global__ void __launch_bounds__(1024) k_greedy(DevSpace sp, HostTables t, Recv
     for (int m = 0; m < KM; ++m) st[m] = s_state[m];
     double bv = -DBL_MAX;
     int boi = INT_MAX, bci = -1;
-    for (int ci = threadIdx.x; ci < sp.n_cand; ci += blockDim.x) {
+    for (int ci = rank * blockDim.x + threadIdx.x; ci < sp.n_cand; ci += nrank * blockDim.x) {
       const int sig = sp.cand_sig[ci];
       bool ok = true;
       for (int m = 0; m < t.M && ok; ++m) {
@@ -104,17 +126,17 @@ __global__ void __launch_bounds__(1024) k_greedy(DevSpace sp, HostTables t, Recv
         v = dadd(v, dmul(thr_of(recv(m, s), eff), acc));
       }
       const int oi = sp.cand_oi[ci];
-      if (bci < 0 || v > bv || (v == bv && oi < boi)) {
+      if (g_better(v, oi, ci, bv, boi, bci)) {
         bv = v;
         boi = oi;
         bci = ci;
       }
     }
     for (int o = 16; o > 0; o >>= 1) {
-      double ov = __shfl_down_sync(0xffffffffu, bv, o);
-      int ooi = __shfl_down_sync(0xffffffffu, boi, o);
-      int oci = __shfl_down_sync(0xffffffffu, bci, o);
-      if (oci >= 0 && (bci < 0 || ov > bv || (ov == bv && ooi < boi))) {
+      const double ov = __shfl_down_sync(0xffffffffu, bv, o);
+      const int ooi = __shfl_down_sync(0xffffffffu, boi, o);
+      const int oci = __shfl_down_sync(0xffffffffu, bci, o);
+      if (g_better(ov, ooi, oci, bv, boi, bci)) {
         bv = ov;
         boi = ooi;
         bci = oci;
@@ -127,34 +149,38 @@ __global__ void __launch_bounds__(1024) k_greedy(DevSpace sp, HostTables t, Recv
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      double v = -DBL_MAX;
-      int oi = INT_MAX, ci = -1;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-        if (s_ci[w] >= 0 && (ci < 0 || s_v[w] > v || (s_v[w] == v && s_oi[w] < oi))) {
-          v = s_v[w];
-          oi = s_oi[w];
-          ci = s_ci[w];
-        }
+      GreedyRes r{-DBL_MAX, INT_MAX, -1};
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w)
+        if (g_better(s_v[w], s_oi[w], s_ci[w], r.v, r.oi, r.ci)) r = GreedyRes{s_v[w], s_oi[w], s_ci[w]};
+      s_res[s & 1] = r;
+    }
+    cluster.sync();  // every CTA's step-s result is published
+    if (threadIdx.x == 0) {
+      GreedyRes b{-DBL_MAX, INT_MAX, -1};
+      for (int q = 0; q < nrank; ++q) {  // same order in every CTA: identical winners
+        const GreedyRes r = cluster.map_shared_rank(s_res, q)[s & 1];
+        if (g_better(r.v, r.oi, r.ci, b.v, b.oi, b.ci)) b = r;
       }
-      if (ci < 0) {
+      if (b.ci < 0) {
         s_alive = 0;
-        greedy[s] = -1;
+        if (rank == 0) greedy[s] = -1;
       } else {
-        greedy[s] = oi;
-        s_value = v;
-        const int sig = sp.cand_sig[ci];
+        if (rank == 0) greedy[s] = b.oi;
+        s_value = b.v;
+        const int sig = sp.cand_sig[b.ci];
         for (int m = 0; m < t.M; ++m) s_state[m] = codec.advance(t.rt[m], s_state[m], (sig >> (3 * m)) & 7, s);
-        s_ids = sp.pl_ids[sp.cand_pid[ci]];
+        s_ids = sp.pl_ids[sp.cand_pid[b.ci]];
       }
     }
     __syncthreads();
     if (!s_alive) break;
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && rank == 0) {
     bool all_done = s_alive != 0;
     for (int m = 0; m < t.M; ++m) all_done = all_done && s_state[m] == Codec::done();
     *incumbent = all_done ? s_value : -INFINITY;
   }
+  cluster.sync();  // no CTA exits while another may still read its shared memory
 }
 
 }  // namespace
@@ -168,7 +194,18 @@ void goodput_reductions(Ctx& c, const Prepared& pr, const DevSpace& sp, const do
   ++c.kernel_launches;
   k_ub_suffix<<<1, 32, 0, c.stream>>>(best, t.S, d_ub);
   ++c.kernel_launches;
-  k_greedy<<<1, 1024, 0, c.stream>>>(sp, t, recv, pr.has_initial, d_incumbent, d_greedy);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kGreedyCluster);
+  cfg.blockDim = dim3(1024);
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kGreedyCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MGS_CUDA_OK(cudaLaunchKernelEx(&cfg, k_greedy, sp, t, recv, pr.has_initial, d_incumbent, d_greedy));
   ++c.kernel_launches;
   MGS_CUDA_OK(cudaGetLastError());
 }

@@ -1,3 +1,3 @@
 #!/bin/bash
-OUT=gpurun_out/dbg7; mkdir -p $OUT
-timeout 60 env MGS_TRACE=1 python -u scripts/solve_once.py tests/golden/kat/worked_example.scn > $OUT/trace.log 2>&1
+OUT=gpurun_out/dbg8; mkdir -p $OUT
+for T in 1024 512 256 128; do echo "threads $T"; MGS_GREEDY_THREADS=$T python scripts/solve_once.py tests/golden/c1/c1_S200_100001.scn 3 2>&1 | tail -2; done > $OUT/greedy.log 2>&1
