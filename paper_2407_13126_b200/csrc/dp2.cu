@@ -893,6 +893,16 @@ __device__ void phase_trans_small(const V2& a, int s) {
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const int nis = sc.items_s;
   constexpr int kFull = (1 << M) - 1;
+  // the item's group (<= kSmall states) staged once per warp in shared memory:
+  // every lane then scans it from there instead of re-reading global memory
+  __shared__ uint32_t sh_ids[kWarps][kSmall], sh_rank[kWarps][kSmall];
+  __shared__ double sh_val[kWarps][kSmall];
+  __shared__ uint8_t sh_alive[kWarps][kSmall];
+  const int warp = threadIdx.x >> 5;
+  uint32_t* gids = sh_ids[warp];
+  uint32_t* grank = sh_rank[warp];
+  double* gval = sh_val[warp];
+  uint8_t* galive = sh_alive[warp];
   for (int item = wid; item < nis; item += nw) {
     const int unit = a.it_s_unit[item], chunk = a.it_s_chunk[item];
     const int g = a.u_group[unit], sig = a.u_sig[unit];
@@ -903,10 +913,16 @@ __device__ void phase_trans_small(const V2& a, int s) {
     double v0 = 0.0;
     uint32_t r0 = 0xffffffffu;
     int i0 = -1;
+    __syncwarp();  // the previous item's scan is done with the staging arrays
     for (int j = lane; j < gn; j += 32) {
-      if (!F.alive[gs + j]) continue;
+      const uint8_t al = F.alive[gs + j];
       const double vj = F.value[gs + j];
       const uint32_t rj = F.rank[gs + j];
+      gids[j] = F.ids[gs + j];
+      grank[j] = rj;
+      gval[j] = vj;
+      galive[j] = al;
+      if (!al) continue;
       if (i0 < 0 || better(vj, rj, v0, r0)) {
         v0 = vj;
         r0 = rj;
@@ -923,6 +939,7 @@ __device__ void phase_trans_small(const V2& a, int s) {
         i0 = oi;
       }
     }
+    __syncwarp();
     if (ti >= L) continue;
     double acc[M];
     group_acc<M>(a, F.g_status[g], acc);
@@ -943,13 +960,13 @@ __device__ void phase_trans_small(const V2& a, int s) {
     // subset's tenants can represent it (solvers.hpp:367-378)
 #pragma unroll 4
     for (int j = 0; j < gn; ++j) {
-      const uint32_t x = F.ids[gs + j] ^ ids_p;
+      const uint32_t x = gids[j] ^ ids_p;
       int mt = 0;
 #pragma unroll
       for (int m = 0; m < M; ++m) mt |= ((x >> (16 * m)) & 0xffff) == 0 ? (1 << m) : 0;
-      if (mt == 0 || !F.alive[gs + j]) continue;
-      const double vj = F.value[gs + j];
-      const uint32_t rj = F.rank[gs + j];
+      if (mt == 0 || !galive[j]) continue;
+      const double vj = gval[j];
+      const uint32_t rj = grank[j];
       if (mt == kFull) {  // the full subset's key is the state's own placement: unique in the group
         b.v[kFull] = vj;
         b.r[kFull] = rj;
