@@ -1149,17 +1149,17 @@ __device__ __forceinline__ bool claim_fits(const V2& a, int s, int q0, int total
   return true;
 }
 
-constexpr int kWriteBatch = kWarps * 4;  // small statuses per CTA allocation batch
-static_assert(kWriteBatch == 32, "warp 0 scans one batch lane-parallel");
+constexpr int kWriteBatch = 1;  // small statuses per warp allocation batch
 
 __device__ void phase_write(const V2& a, int s) {
   const int nxt = (s + 1) & 1;
   StepCounters& sc = a.ctl->sc[s & 1];
   const FrontierV2& N = a.f[nxt];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ int s_wsum[kWarps];
-  __shared__ int s_q0, s_gi, s_ok;
-  __shared__ int s_bq[kWriteBatch], s_bg[kWriteBatch];
+  const int lane = threadIdx.x & 31;
+  __shared__ int s_q0, s_gi, s_ok, s_run;
+  // big statuses: a CTA each; warps compact coalesced 32-candidate chunks
+  // into the status's range through a shared cursor (order within a group is
+  // irrelevant)
   const int nbig = sc.n_big;
   for (int w = blockIdx.x; w < nbig; w += gridDim.x) {
     const int id = a.ns_big[w];
@@ -1171,6 +1171,7 @@ __device__ void phase_write(const V2& a, int s) {
       s_q0 = atomicAdd(&sc.out_states, total);
       s_gi = atomicAdd(&sc.out_groups, 1);
       s_ok = claim_fits(a, s, s_q0, total, s_gi) ? 1 : 0;
+      s_run = 0;
       if (a.dbg) {
         atomicMax(reinterpret_cast<unsigned long long*>(a.dbg + kDbg * (s + 1 < a.S ? s + 1 : s) + 8),
                   static_cast<unsigned long long>(total));
@@ -1179,87 +1180,77 @@ __device__ void phase_write(const V2& a, int s) {
     }
     __syncthreads();
     const int q0 = s_q0, gi = s_gi;
-    if (!s_ok) {
-      __syncthreads();
-      continue;
+    if (s_ok) {
+      if (threadIdx.x == 0) {
+        N.g_start[gi] = q0;
+        N.g_size[gi] = total;
+        N.g_status[gi] = key;
+        N.g_alive[gi] = total;
+      }
+      for (int k0 = cb + (threadIdx.x & ~31); k0 < cb + cc; k0 += kThreads) {
+        const int k = k0 + lane;
+        const bool keep = k < cb + cc && a.c_live[k];
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (bal == 0) continue;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&s_run, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) write_state(a, s, nxt, q0 + base + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
+      }
     }
-    if (threadIdx.x == 0) {
-      N.g_start[gi] = q0;
-      N.g_size[gi] = total;
-      N.g_status[gi] = key;
-      N.g_alive[gi] = total;
-    }
-    const int per = (cc + kThreads - 1) / kThreads;  // ordered compaction: contiguous ranges + block scan
-    const int lo = cb + threadIdx.x * per, hi = min(cb + cc, lo + per);
-    int mine = 0;
-    for (int k = lo; k < hi; ++k) mine += a.c_live[k];
-    int x = mine;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) s_wsum[warp] = x;
-    __syncthreads();
-    int off = x - mine;
-    for (int w2 = 0; w2 < warp; ++w2) off += s_wsum[w2];
-    for (int k = lo; k < hi; ++k)
-      if (a.c_live[k]) write_state(a, s, nxt, q0 + off++, gi, key, k);
     __syncthreads();
   }
-  // small statuses: CTA batches of kWriteBatch, one allocation per batch, a
-  // warp per status
+  // small statuses: each warp takes batches of kWriteBatch, one allocation
+  // per batch, then writes the batch's statuses one after another (no CTA
+  // barriers)
   const int nsm = sc.n_small;
-  for (int c0 = blockIdx.x * kWriteBatch; c0 < nsm; c0 += gridDim.x * kWriteBatch) {
-    if (warp == 0) {
-      int tot = 0, grp = 0;  // lanes 0..31 cover the batch (kWriteBatch == 32)
-      if (c0 + lane < nsm) {
-        tot = a.ns_out[a.ns_small[c0 + lane]];
-        grp = tot > 0 ? 1 : 0;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int c0 = wid * kWriteBatch; c0 < nsm; c0 += nw * kWriteBatch) {
+    const int my_id = lane < kWriteBatch && c0 + lane < nsm ? a.ns_small[c0 + lane] : -1;
+    const int tot = my_id >= 0 ? a.ns_out[my_id] : 0;
+    const int grp = tot > 0 ? 1 : 0;
+    int xt = tot, xg = grp;
+    for (int o = 1; o < kWriteBatch; o <<= 1) {
+      const int yt = __shfl_up_sync(0xffffffffu, xt, o), yg = __shfl_up_sync(0xffffffffu, xg, o);
+      if (lane >= o) {
+        xt += yt;
+        xg += yg;
       }
-      int xt = tot, xg = grp;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int yt = __shfl_up_sync(0xffffffffu, xt, o), yg = __shfl_up_sync(0xffffffffu, xg, o);
-        if (lane >= o) {
-          xt += yt;
-          xg += yg;
-        }
-      }
-      int bq = 0, bgi = 0;
-      if (lane == 31) {
-        bq = atomicAdd(&sc.out_states, xt);
-        bgi = atomicAdd(&sc.out_groups, xg);
-        s_ok = claim_fits(a, s, bq, xt, bgi + xg - 1) ? 1 : 0;
-      }
-      bq = __shfl_sync(0xffffffffu, bq, 31);
-      bgi = __shfl_sync(0xffffffffu, bgi, 31);
-      s_bq[lane] = bq + xt - tot;
-      s_bg[lane] = bgi + xg - grp;
     }
-    __syncthreads();
-    if (s_ok)
-      for (int t = warp; t < kWriteBatch && c0 + t < nsm; t += kWarps) {
-        const int id = a.ns_small[c0 + t];
-        const int total = a.ns_out[id];
-        if (total == 0) continue;
-        const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
-        const int q0 = s_bq[t], gi = s_bg[t];
-        const uint32_t key = a.hash[id] - 1u;
-        if (lane == 0) {
-          N.g_start[gi] = q0;
-          N.g_size[gi] = total;
-          N.g_status[gi] = key;
-          N.g_alive[gi] = total;
-        }
-        int run = 0;
-        for (int k0 = cb; k0 < cb + cc; k0 += 32) {
-          const int k = k0 + lane;
-          const bool keep = k < cb + cc && a.c_live[k];
-          const unsigned bal = __ballot_sync(0xffffffffu, keep);
-          if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
-          run += __popc(bal);
-        }
+    constexpr int kL = kWriteBatch - 1;
+    int bq = 0, bgi = 0, ok = 0;
+    if (lane == kL && xt > 0) {
+      bq = atomicAdd(&sc.out_states, xt);
+      bgi = atomicAdd(&sc.out_groups, xg);
+      ok = claim_fits(a, s, bq, xt, bgi + xg - 1) ? 1 : 0;
+    }
+    if (!__shfl_sync(0xffffffffu, ok, kL)) continue;
+    const int my_q0 = __shfl_sync(0xffffffffu, bq, kL) + xt - tot;
+    const int my_gi = __shfl_sync(0xffffffffu, bgi, kL) + xg - grp;
+    unsigned todo = __ballot_sync(0xffffffffu, tot > 0);
+    while (todo) {
+      const int t = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int id = __shfl_sync(0xffffffffu, my_id, t);
+      const int total = __shfl_sync(0xffffffffu, tot, t);
+      const int q0 = __shfl_sync(0xffffffffu, my_q0, t), gi = __shfl_sync(0xffffffffu, my_gi, t);
+      const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
+      const uint32_t key = a.hash[id] - 1u;
+      if (lane == 0) {
+        N.g_start[gi] = q0;
+        N.g_size[gi] = total;
+        N.g_status[gi] = key;
+        N.g_alive[gi] = total;
       }
-    __syncthreads();
+      int run = 0;
+      for (int k0 = cb; k0 < cb + cc; k0 += 32) {
+        const int k = k0 + lane;
+        const bool keep = k < cb + cc && a.c_live[k];
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
+        run += __popc(bal);
+      }
+    }
   }
 }
 
