@@ -140,6 +140,7 @@ struct V2 {
   int32_t *ns_ucnt, *ns_ccnt, *ns_ubase, *ns_cbase, *ns_ucur, *ns_ccur, *ns_units, *ns_bigpos, *ns_smallpos;
   int32_t *ns_big, *ns_small;
   int32_t* ns_out;  // survivors per status
+  unsigned long long* ns_vmax;  // vbits of the best bound-passing candidate value per status (band max)
   int32_t *it_s_unit, *it_s_chunk, *it_b_unit, *it_b_chunk;
   int itcap;
   double* c_value;
@@ -688,7 +689,7 @@ struct BestT {
 };
 
 template <int M>
-__device__ __forceinline__ void emit_target(const V2& a, int s, int charge, int unit, int t_idx, int gs,
+__device__ __forceinline__ unsigned long long emit_target(const V2& a, int s, int charge, int unit, int t_idx, int gs,
                                             const double* acc, int p, int oi, uint32_t ids_p, const BestT<M>& b,
                                             const FrontierV2& F) {
   const HostTables& t = a.t;
@@ -720,7 +721,7 @@ __device__ __forceinline__ void emit_target(const V2& a, int s, int charge, int 
   const int slot = a.u_cbase[unit] + t_idx;
   if (chosen < 0) {  // cannot happen: units come from groups with live states
     a.c_ok[slot] = 0;
-    return;
+    return 0ull;
   }
   const int pred = gs + chosen;
   const uint32_t pids = F.ids[pred];
@@ -737,6 +738,7 @@ __device__ __forceinline__ void emit_target(const V2& a, int s, int charge, int 
   a.c_parent[slot] = pred;
   a.c_pid[slot] = p;
   a.c_ok[slot] = ok ? 1 : 0;
+  return ok ? vbits(v) : 0ull;  // values are >= 0: vbits orders them
 }
 
 template <int M>
@@ -846,6 +848,7 @@ __device__ void phase_trans_big(const V2& a, int s) {
     group_acc<M>(a, F.g_status[g], acc);
     const int sb = a.sp.sig_off[sig], L = a.sp.sig_off[sig + 1] - sb;
     const int t0 = chunk * kChunkB, t1 = min(L, t0 + kChunkB);
+    unsigned long long vmax = 0ull;
     for (int ti = t0 + threadIdx.x; ti < t1; ti += kThreads) {
       const int p = a.sp.cand_pid[sb + ti];
       const int oi = a.sp.cand_oi[sb + ti];
@@ -876,8 +879,15 @@ __device__ void phase_trans_big(const V2& a, int s) {
           bt.r[full] = 0u;
         }
       }
-      emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, static_cast<uint32_t>(a.sp.pl_ids[p]), bt, F);
+      const unsigned long long vb_t =
+          emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, static_cast<uint32_t>(a.sp.pl_ids[p]), bt, F);
+      vmax = vb_t > vmax ? vb_t : vmax;
     }
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, vmax, o);
+      vmax = y > vmax ? y : vmax;
+    }
+    if ((threadIdx.x & 31) == 0 && vmax) atomicMax(&a.ns_vmax[a.u_ns[unit]], vmax);
   }
 }
 
@@ -940,7 +950,8 @@ __device__ void phase_trans_small(const V2& a, int s) {
       }
     }
     __syncwarp();
-    if (ti >= L) continue;
+    unsigned long long vb_t = 0ull;
+    if (ti < L) {
     double acc[M];
     group_acc<M>(a, F.g_status[g], acc);
     const int p = a.sp.cand_pid[sb + ti];
@@ -982,7 +993,13 @@ __device__ void phase_trans_small(const V2& a, int s) {
         }
       }
     }
-    emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, ids_p, b, F);
+    vb_t = emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, ids_p, b, F);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, vb_t, o);
+      vb_t = y > vb_t ? y : vb_t;
+    }
+    if (lane == 0 && vb_t) atomicMax(&a.ns_vmax[a.u_ns[unit]], vb_t);
   }
 }
 
@@ -1011,16 +1028,26 @@ __device__ __forceinline__ void write_state(const V2& a, int s, int nxt, int q, 
 // S6a: equal-key merge (multi-unit statuses) + band + survivor count per status
 __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned long long* mlx) {
   StepCounters& sc = a.ctl->sc[s & 1];
-  __shared__ unsigned long long s_max;
   __shared__ int s_cnt;
   const int lane = threadIdx.x & 31;
+  // The band's reference value (solvers.hpp:499-511) is the best value among
+  // the merged survivors, which is the best bound-passing candidate of the
+  // status (the merge keeps each placement's maximum): the transition kernels
+  // already reduced it into ns_vmax, so merge, band and count are one sweep.
   // big statuses (multi-unit or large): one CTA each
   const int nbig = sc.n_big;
   for (int w = blockIdx.x; w < nbig; w += gridDim.x) {
     const int id = a.ns_big[w];
     const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id], ub = a.ns_ubase[id], uc = a.ns_ucnt[id];
+    const double thresh = dsub(__longlong_as_double(static_cast<long long>(a.ns_vmax[id])), a.band);
+    if (threadIdx.x == 0) s_cnt = 0;
+    int mine = 0;
     if (uc == 1) {
-      for (int k = cb + threadIdx.x; k < cb + cc; k += kThreads) a.c_live[k] = a.c_ok[k];
+      for (int k = cb + threadIdx.x; k < cb + cc; k += kThreads) {
+        const bool keep = a.c_ok[k] && a.c_value[k] >= thresh;
+        a.c_live[k] = keep ? 1 : 0;
+        mine += keep;
+      }
     } else {  // equal-key merge (solvers.hpp:467-468): max value, then min lex, per placement
       const int P1 = a.sp.P1;
       const int win = a.merge_win;
@@ -1053,13 +1080,16 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
                 if (pass == 2) a.c_live[k] = 0;
                 continue;
               }
-              const unsigned long long vb = vbits(a.c_value[k]);
+              const double v = a.c_value[k];
+              const unsigned long long vb = vbits(v);
               if (pass == 0) {
                 atomicMax(&mvb[p - w0], vb);
               } else if (pass == 1) {
                 if (mvb[p - w0] == vb) atomicMin(&mlx[p - w0], a.c_lex[k]);
               } else {
-                a.c_live[k] = (mvb[p - w0] == vb && mlx[p - w0] == a.c_lex[k]) ? 1 : 0;
+                const bool keep = mvb[p - w0] == vb && mlx[p - w0] == a.c_lex[k] && v >= thresh;
+                a.c_live[k] = keep ? 1 : 0;
+                mine += keep;
               }
             }
           }
@@ -1067,35 +1097,11 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
         }
       }
     }
-    __syncthreads();
-    // band (solvers.hpp:499-511)
-    unsigned long long mx = 0;
-    bool any = false;
-    for (int k = cb + threadIdx.x; k < cb + cc; k += kThreads)
-      if (a.c_live[k]) {
-        const unsigned long long vb = vbits(a.c_value[k]);
-        mx = vb > mx ? vb : mx;
-        any = true;
-      }
-    if (threadIdx.x == 0) {
-      s_max = 0;
-      s_cnt = 0;
-    }
-    __syncthreads();
-    if (any) atomicMax(&s_max, mx);
-    __syncthreads();
-    const double thresh = dsub(__longlong_as_double(static_cast<long long>(s_max)), a.band);
-    int mine = 0;
-    for (int k = cb + threadIdx.x; k < cb + cc; k += kThreads) {
-      const bool keep = a.c_live[k] && a.c_value[k] >= thresh;
-      a.c_live[k] = keep ? 1 : 0;
-      mine += keep;
-    }
     for (int o = 16; o > 0; o >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, o);
+    __syncthreads();
     if (lane == 0 && mine) atomicAdd(&s_cnt, mine);
     __syncthreads();
     if (threadIdx.x == 0) a.ns_out[id] = s_cnt;
-    __syncthreads();
   }
   // small statuses (single unit, <= kBigNs candidates): a warp each, no merge needed
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -1103,24 +1109,11 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
   for (int i = wid; i < nsm; i += nw) {
     const int id = a.ns_small[i];
     const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
-    unsigned long long mx = 0;
-    bool any = false;
-    for (int k = cb + lane; k < cb + cc; k += 32)
-      if (a.c_ok[k]) {
-        const unsigned long long vb = vbits(a.c_value[k]);
-        mx = vb > mx ? vb : mx;
-        any = true;
-      }
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
-      mx = y > mx ? y : mx;
-    }
-    any = __any_sync(0xffffffffu, any);
-    const double thresh = dsub(__longlong_as_double(static_cast<long long>(mx)), a.band);
+    const double thresh = dsub(__longlong_as_double(static_cast<long long>(a.ns_vmax[id])), a.band);
     int total = 0;
     for (int k0 = cb; k0 < cb + cc; k0 += 32) {
       const int k = k0 + lane;
-      const bool keep = any && k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh;
+      const bool keep = k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh;
       if (k < cb + cc) a.c_live[k] = keep ? 1 : 0;
       total += __popc(__ballot_sync(0xffffffffu, keep));
     }
@@ -1478,6 +1471,7 @@ __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int
     const int i = a.ns_used[k];
     a.hash[i] = 0u;
     a.ns_out[i] = 0;
+    a.ns_vmax[i] = 0ull;
     a.ns_ucnt[i] = 0;
     a.ns_ccnt[i] = 0;
     a.ns_ucur[i] = 0;
@@ -1708,6 +1702,8 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, double band, int dominan
   a.ns_bigpos = c.buf<int32_t>("v2_nsbigpos", H);
   a.ns_smallpos = c.buf<int32_t>("v2_nssmallpos", H);
   a.ns_out = c.buf<int32_t>("v2_nsout", H);
+  a.ns_vmax = c.buf<unsigned long long>("v2_nsvmax", H);
+  MGS_CUDA_OK(cudaMemsetAsync(a.ns_vmax, 0, H * 8, c.stream));
   a.ns_big = c.buf<int32_t>("v2_nsbig", H);
   a.ns_small = c.buf<int32_t>("v2_nssmall", H);
   a.ns_used = c.buf<int32_t>("v2_nsused", H);
