@@ -399,7 +399,11 @@ __device__ __forceinline__ uint32_t mix32(uint32_t h) {  // murmur3 finalizer: a
   return h;
 }
 
-__device__ int ns_slot(const V2& a, uint32_t key, int phi, int step) {
+// Claimed slots are listed for the step's status loops: first in the CTA's
+// shared list (flushed with one global atomic per CTA batch), the global list
+// directly when that is full.
+constexpr int kNewCap = 512;
+__device__ int ns_slot(const V2& a, uint32_t key, int phi, int step, int* s_nnew, int* s_new) {
   const uint32_t want = key + 1u;
   const unsigned h = mix32(key);
   for (int probe = 0; probe <= (a.hmask >> 1); ++probe) {
@@ -407,8 +411,10 @@ __device__ int ns_slot(const V2& a, uint32_t key, int phi, int step) {
     uint32_t w = a.hash[slot];
     if (w == 0) {
       w = atomicCAS(&a.hash[slot], 0u, want);
-      if (w == 0) {  // this thread claimed the slot: list it for the step's status loops
-        a.ns_used[atomicAdd(&a.ctl->sc[step & 1].n_ns, 1)] = slot;
+      if (w == 0) {  // this thread claimed the slot
+        const int i = atomicAdd(s_nnew, 1);
+        if (i < kNewCap) s_new[i] = slot;
+        else a.ns_used[atomicAdd(&a.ctl->sc[step & 1].n_ns, 1)] = slot;
         return slot;
       }
     }
@@ -476,6 +482,8 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
   const int G = a.ctl->n_groups[cur];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ int s_base, s_scan[80];
+  __shared__ int s_nnew, s_new[kNewCap];
+  if (threadIdx.x == 0) s_nnew = 0;
   const int g0 = static_cast<int>(static_cast<long long>(G) * blockIdx.x / gridDim.x);
   const int g1 = static_cast<int>(static_cast<long long>(G) * (blockIdx.x + 1) / gridDim.x);
   long long ref = 0;
@@ -528,7 +536,7 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
           const unsigned bal = __ballot_sync(0xffffffffu, ok);
           if (ok) {
             const int u = run + __popc(bal & ((1u << lane) - 1u));
-            const int id = ns_slot(a, ns, phi, s);
+            const int id = ns_slot(a, ns, phi, s, &s_nnew, s_new);
             if (id >= 0) {
               const int L = a.sig_len[sig];
               a.u_group[u] = g;
@@ -546,6 +554,15 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
       }
     }
     __syncthreads();
+    const int nn = min(s_nnew, kNewCap);
+    if (nn > 0) {  // uniform
+      if (threadIdx.x == 0) s_base = atomicAdd(&sc.n_ns, nn);
+      __syncthreads();
+      for (int i = threadIdx.x; i < nn; i += kThreads) a.ns_used[s_base + i] = s_new[i];
+      __syncthreads();
+      if (threadIdx.x == 0) s_nnew = 0;
+      __syncthreads();
+    }
   }
   // children per parent (rank buckets of F_s) + live-state count
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
