@@ -1120,22 +1120,7 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
     __syncthreads();
     if (threadIdx.x == 0) a.ns_out[id] = s_cnt;
   }
-  // small statuses (single unit, <= kBigNs candidates): a warp each, no merge needed
-  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  const int nsm = sc.n_small;
-  for (int i = wid; i < nsm; i += nw) {
-    const int id = a.ns_small[i];
-    const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
-    const double thresh = dsub(__longlong_as_double(static_cast<long long>(a.ns_vmax[id])), a.band);
-    int total = 0;
-    for (int k0 = cb; k0 < cb + cc; k0 += 32) {
-      const int k = k0 + lane;
-      const bool keep = k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh;
-      if (k < cb + cc) a.c_live[k] = keep ? 1 : 0;
-      total += __popc(__ballot_sync(0xffffffffu, keep));
-    }
-    if (lane == 0) a.ns_out[id] = total;
-  }
+  // small statuses: band fused into phase_write
 }
 
 // S6c: survivors of every status written at their scanned offsets
@@ -1158,8 +1143,6 @@ __device__ __forceinline__ bool claim_fits(const V2& a, int s, int q0, int total
   }
   return true;
 }
-
-constexpr int kWriteBatch = 1;  // small statuses per warp allocation batch
 
 __device__ void phase_write(const V2& a, int s) {
   const int nxt = (s + 1) & 1;
@@ -1210,56 +1193,43 @@ __device__ void phase_write(const V2& a, int s) {
     }
     __syncthreads();
   }
-  // small statuses: each warp takes batches of kWriteBatch, one allocation
-  // per batch, then writes the batch's statuses one after another (no CTA
-  // barriers)
+  // small statuses (single unit, <= kBigNs candidates, so no merge): a warp
+  // each applies the band, claims its range with one atomic and writes
   const int nsm = sc.n_small;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (int c0 = wid * kWriteBatch; c0 < nsm; c0 += nw * kWriteBatch) {
-    const int my_id = lane < kWriteBatch && c0 + lane < nsm ? a.ns_small[c0 + lane] : -1;
-    const int tot = my_id >= 0 ? a.ns_out[my_id] : 0;
-    const int grp = tot > 0 ? 1 : 0;
-    int xt = tot, xg = grp;
-    for (int o = 1; o < kWriteBatch; o <<= 1) {
-      const int yt = __shfl_up_sync(0xffffffffu, xt, o), yg = __shfl_up_sync(0xffffffffu, xg, o);
-      if (lane >= o) {
-        xt += yt;
-        xg += yg;
-      }
+  for (int i = wid; i < nsm; i += nw) {
+    const int id = a.ns_small[i];
+    const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
+    const double thresh = dsub(__longlong_as_double(static_cast<long long>(a.ns_vmax[id])), a.band);
+    int total = 0;
+    for (int k0 = cb; k0 < cb + cc; k0 += 32) {
+      const int k = k0 + lane;
+      total += __popc(__ballot_sync(0xffffffffu, k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh));
     }
-    constexpr int kL = kWriteBatch - 1;
-    int bq = 0, bgi = 0, ok = 0;
-    if (lane == kL && xt > 0) {
-      bq = atomicAdd(&sc.out_states, xt);
-      bgi = atomicAdd(&sc.out_groups, xg);
-      ok = claim_fits(a, s, bq, xt, bgi + xg - 1) ? 1 : 0;
+    if (total == 0) continue;  // uniform
+    int q0 = 0, gi = 0, ok = 0;
+    if (lane == 0) {
+      q0 = atomicAdd(&sc.out_states, total);
+      gi = atomicAdd(&sc.out_groups, 1);
+      ok = claim_fits(a, s, q0, total, gi) ? 1 : 0;
     }
-    if (!__shfl_sync(0xffffffffu, ok, kL)) continue;
-    const int my_q0 = __shfl_sync(0xffffffffu, bq, kL) + xt - tot;
-    const int my_gi = __shfl_sync(0xffffffffu, bgi, kL) + xg - grp;
-    unsigned todo = __ballot_sync(0xffffffffu, tot > 0);
-    while (todo) {
-      const int t = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const int id = __shfl_sync(0xffffffffu, my_id, t);
-      const int total = __shfl_sync(0xffffffffu, tot, t);
-      const int q0 = __shfl_sync(0xffffffffu, my_q0, t), gi = __shfl_sync(0xffffffffu, my_gi, t);
-      const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
-      const uint32_t key = a.hash[id] - 1u;
-      if (lane == 0) {
-        N.g_start[gi] = q0;
-        N.g_size[gi] = total;
-        N.g_status[gi] = key;
-        N.g_alive[gi] = total;
-      }
-      int run = 0;
-      for (int k0 = cb; k0 < cb + cc; k0 += 32) {
-        const int k = k0 + lane;
-        const bool keep = k < cb + cc && a.c_live[k];
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
-        run += __popc(bal);
-      }
+    if (!__shfl_sync(0xffffffffu, ok, 0)) continue;
+    q0 = __shfl_sync(0xffffffffu, q0, 0);
+    gi = __shfl_sync(0xffffffffu, gi, 0);
+    const uint32_t key = a.hash[id] - 1u;
+    if (lane == 0) {
+      N.g_start[gi] = q0;
+      N.g_size[gi] = total;
+      N.g_status[gi] = key;
+      N.g_alive[gi] = total;
+    }
+    int run = 0;
+    for (int k0 = cb; k0 < cb + cc; k0 += 32) {
+      const int k = k0 + lane;
+      const bool keep = k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh;
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
+      run += __popc(bal);
     }
   }
 }
