@@ -924,12 +924,10 @@ __device__ void phase_trans_small(const V2& a, int s) {
   // every lane then scans it from there instead of re-reading global memory
   __shared__ uint32_t sh_ids[kWarps][kSmall], sh_rank[kWarps][kSmall];
   __shared__ double sh_val[kWarps][kSmall];
-  __shared__ uint8_t sh_alive[kWarps][kSmall];
   const int warp = threadIdx.x >> 5;
   uint32_t* gids = sh_ids[warp];
   uint32_t* grank = sh_rank[warp];
   double* gval = sh_val[warp];
-  uint8_t* galive = sh_alive[warp];
   for (int item = wid; item < nis; item += nw) {
     const int unit = a.it_s_unit[item], chunk = a.it_s_chunk[item];
     const int g = a.u_group[unit], sig = a.u_sig[unit];
@@ -945,10 +943,11 @@ __device__ void phase_trans_small(const V2& a, int s) {
       const uint8_t al = F.alive[gs + j];
       const double vj = F.value[gs + j];
       const uint32_t rj = F.rank[gs + j];
-      gids[j] = F.ids[gs + j];
+      // a dead state is staged with all-ones ids: no 16-bit field matches a
+      // placement's (ids are indices < 0xffff, k_proj_keys' wildcard)
+      gids[j] = al ? F.ids[gs + j] : 0xffffffffu;
       grank[j] = rj;
       gval[j] = vj;
-      galive[j] = al;
       if (!al) continue;
       if (i0 < 0 || better(vj, rj, v0, r0)) {
         v0 = vj;
@@ -992,7 +991,7 @@ __device__ void phase_trans_small(const V2& a, int s) {
       int mt = 0;
 #pragma unroll
       for (int m = 0; m < M; ++m) mt |= ((x >> (16 * m)) & 0xffff) == 0 ? (1 << m) : 0;
-      if (mt == 0 || !galive[j]) continue;
+      if (mt == 0) continue;
       const double vj = gval[j];
       const uint32_t rj = grank[j];
       if (mt == kFull) {  // the full subset's key is the state's own placement: unique in the group
@@ -1399,12 +1398,7 @@ __global__ void __launch_bounds__(kThreads) k_ranks_big(const V2* __restrict__ a
   extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
   phase_ranks_big(a, s, smem_u64);
-}
-
-__global__ void __launch_bounds__(kThreads) k_ranks_small(const V2* __restrict__ ap, int s) {
-  const V2& a = c_v2;
-  if (failed(a)) return;
-  phase_ranks_small(a, s);
+  phase_ranks_small(a, s);  // independent of the big buckets: same launch
 }
 
 __global__ void MGS_LB k_tables(const V2* __restrict__ ap, int s) {
@@ -1798,7 +1792,6 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   const dim3 g_scans = wave(reinterpret_cast<const void*>(k_scans), 0);
   const dim3 g_place = wave(reinterpret_cast<const void*>(k_place), 0);
   const dim3 g_rbig = wave(reinterpret_cast<const void*>(k_ranks_big), smem_rank);
-  const dim3 g_rsmall = wave(reinterpret_cast<const void*>(k_ranks_small), 0);
   const dim3 g_tbig = wave(reinterpret_cast<const void*>(ktbig), 0);
   const dim3 g_tables = wave(reinterpret_cast<const void*>(k_tables), 0);
   const dim3 g_tsmall = wave(reinterpret_cast<const void*>(ktsmall), 0);
@@ -1809,7 +1802,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr || std::getenv("MGS_TRACE") != nullptr;
   if (std::getenv("MGS_TRACE"))
     std::fprintf(stderr, "trace v2 setup: lanes %d S %d M %d smem trans %zu rank %zu merge %zu grid.x %u %u %u %u %u %u %u %u %u %u\n",
-                 K, S, M, size_t(0), smem_rank, smem_merge, g_units.x, g_scans.x, g_place.x, g_rbig.x, g_rsmall.x,
+                 K, S, M, size_t(0), smem_rank, smem_merge, g_units.x, g_scans.x, g_place.x, g_rbig.x, 0u,
                  g_tbig.x, g_tsmall.x, g_band.x, g_write.x, g_dom.x);
   for (int attempt = 0; attempt < 10; ++attempt) {
     std::vector<V2> args(K);
@@ -1821,8 +1814,8 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     // The window's kernel sequence depends only on S, M, the lane count and
     // launch shapes (all problem data lives behind d_args), so it is captured
     // once into a CUDA graph and replayed; MGS_DEBUG_STEPS launches eagerly.
-    constexpr int kK = 11;
-    static const char* kNames[kK] = {"units", "scans", "place", "ranks_big", "ranks_small", "tables", "trans_big",
+    constexpr int kK = 10;
+    static const char* kNames[kK] = {"units", "scans", "place", "ranks", "tables", "trans_big",
                                      "trans_small", "band", "write", "dom"};
     std::vector<cudaEvent_t> evs;
     auto enqueue = [&](cudaStream_t st_, bool timed) {
@@ -1885,8 +1878,6 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         after("place", st);
         k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(d_args, st);
         after("ranks_big", st);
-        k_ranks_small<<<g_rsmall, kThreads, 0, st_>>>(d_args, st);
-        after("ranks_small", st);
         k_tables<<<g_tables, kThreads, 0, st_>>>(d_args, st);
         after("tables", st);
         ktbig<<<g_tbig, kThreads, 0, st_>>>(d_args, st);
@@ -1905,7 +1896,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
       k_term3<<<g_term, kThreads, 0, st_>>>(d_args);
       k_backtrack2<<<g_one, 32, 0, st_>>>(d_args);
     };
-    c.kernel_launches += 11ull * S + 4;
+    c.kernel_launches += static_cast<unsigned long long>(kK) * S + 4;
     if (debug) {
       const auto host_t0 = std::chrono::steady_clock::now();
       enqueue(c.stream, true);
