@@ -1818,7 +1818,14 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     static const char* kNames[kK] = {"units", "scans", "place", "ranks", "tables", "trans_big",
                                      "trans_small", "band", "write", "dom"};
     std::vector<cudaEvent_t> evs;
+    // trans_small depends only on the ranks, not on the subset tables (it
+    // writes disjoint candidate slots; the band maxima are atomicMax): in the
+    // captured graph it is a parallel branch (MGS_NO_FORK keeps one chain)
+    static const bool fork_ok = std::getenv("MGS_NO_FORK") == nullptr;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     auto enqueue = [&](cudaStream_t st_, bool timed) {
+      const bool fork = fork_ok && !timed && side != nullptr;
       auto mark = [&]() {
         if (!timed) return;
         cudaEvent_t e;
@@ -1878,12 +1885,22 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         after("place", st);
         k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(d_args, st);
         after("ranks_big", st);
-        k_tables<<<g_tables, kThreads, 0, st_>>>(d_args, st);
-        after("tables", st);
-        ktbig<<<g_tbig, kThreads, 0, st_>>>(d_args, st);
-        after("trans_big", st);
-        ktsmall<<<g_tsmall, kThreads, 0, st_>>>(d_args, st);
-        after("trans_small", st);
+        if (fork) {  // graph: small-group transitions run beside tables -> big-group transitions
+          MGS_CUDA_OK(cudaEventRecord(ev_fork, st_));
+          MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_fork, 0));
+          ktsmall<<<g_tsmall, kThreads, 0, side>>>(d_args, st);
+          MGS_CUDA_OK(cudaEventRecord(ev_join, side));
+          k_tables<<<g_tables, kThreads, 0, st_>>>(d_args, st);
+          ktbig<<<g_tbig, kThreads, 0, st_>>>(d_args, st);
+          MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_join, 0));
+        } else {
+          k_tables<<<g_tables, kThreads, 0, st_>>>(d_args, st);
+          after("tables", st);
+          ktbig<<<g_tbig, kThreads, 0, st_>>>(d_args, st);
+          after("trans_big", st);
+          ktsmall<<<g_tsmall, kThreads, 0, st_>>>(d_args, st);
+          after("trans_small", st);
+        }
         k_band<<<g_band, kThreads, smem_merge, st_>>>(d_args, st);
         after("band", st);
         k_write<<<g_write, kThreads, 0, st_>>>(d_args, st);
@@ -1924,9 +1941,16 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         cudaStream_t cap;
         MGS_CUDA_OK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
         cudaGraph_t graph;
+        MGS_CUDA_OK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
         MGS_CUDA_OK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
         enqueue(cap, false);
         MGS_CUDA_OK(cudaStreamEndCapture(cap, &graph));
+        MGS_CUDA_OK(cudaEventDestroy(ev_fork));
+        MGS_CUDA_OK(cudaEventDestroy(ev_join));
+        MGS_CUDA_OK(cudaStreamDestroy(side));
+        side = nullptr;
         cudaGraphExec_t exec;
         MGS_CUDA_OK(cudaGraphInstantiate(&exec, graph, 0));
         MGS_CUDA_OK(cudaGraphDestroy(graph));
