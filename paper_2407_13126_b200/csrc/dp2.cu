@@ -565,6 +565,14 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
     }
   }
   // children per parent (rank buckets of F_s) + live-state count
+  const long long rs = block_sum(ref, s_red);
+  if (threadIdx.x == 0 && rs) atomicAdd(&a.ctl->tr_ref, static_cast<unsigned long long>(rs));
+}
+
+// R1 (rank branch): children per parent rank + live-state count of F_s
+__device__ void phase_kids(const V2& a, int s, long long* s_red) {
+  const int cur = s & 1;
+  const FrontierV2& F = a.f[cur];
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const int n = a.ctl->n_store[cur];
   long long live = 0;
@@ -573,12 +581,8 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
       atomicAdd(&a.kid_cnt[cur][F.lex[i] >> 32], 1);
       ++live;
     }
-  const long long rs = block_sum(ref, s_red);
   const long long ls = block_sum(live, s_red);
-  if (threadIdx.x == 0) {
-    if (rs) atomicAdd(&a.ctl->tr_ref, static_cast<unsigned long long>(rs));
-    if (ls) atomicAdd(&a.ctl->alive_now[cur], static_cast<int>(ls));
-  }
+  if (threadIdx.x == 0 && ls) atomicAdd(&a.ctl->alive_now[cur], static_cast<int>(ls));
 }
 
 // S3: placement
@@ -611,6 +615,13 @@ __device__ void phase_place(const V2& a, int s) {
     if (uc > 1 || a.ns_ccnt[id] > kBigNs) a.ns_big[a.ns_bigpos[id]] = id;
     else a.ns_small[a.ns_smallpos[id]] = id;
   }
+}
+
+// R3 (rank branch): children into their parent's slots
+__device__ void phase_kid_fill(const V2& a, int s) {
+  const int cur = s & 1;
+  StepCounters& sc = a.ctl->sc[s & 1];
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const FrontierV2& F = a.f[cur];
   const int n = a.ctl->n_store[cur];
   const int lane = threadIdx.x & 31;
@@ -1332,15 +1343,6 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
   const int cur = s & 1;
   Ctl* ctl = a.ctl;
   StepCounters& sc = ctl->sc[s & 1];
-  const int alive_cur = ctl->alive_now[cur];
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // frontier checks for F_s (solvers.hpp:348, :539-542)
-    if (alive_cur == 0) raise_err(a, 0, MGS_ERR_INFEASIBLE_JOINT, s);
-    else if (s > 0 && static_cast<uint64_t>(alive_cur) > a.budget) raise_err(a, 0, MGS_ERR_STATE_BUDGET, s, alive_cur);
-    if (s > 0) {
-      ctl->ftot += alive_cur;
-      if (static_cast<unsigned long long>(alive_cur) > ctl->fpeak) ctl->fpeak = alive_cur;
-    }
-  }
   const int lane = threadIdx.x & 31;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const int n_ns = sc.n_ns;
@@ -1372,8 +1374,41 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
       a.u_bbase[u] = bb;
     }
   }
+}
+
+// R2 (rank branch): frontier checks for F_s and the children offsets in
+// parent-rank order (the one order-bearing scan: the dense lex ranks)
+__global__ void __launch_bounds__(kThreads) k_kid_scan(const V2* __restrict__ ap, int s) {
+  const V2& a = c_v2;
+  if (failed(a)) return;
+  const int cur = s & 1;
+  Ctl* ctl = a.ctl;
+  StepCounters& sc = ctl->sc[s & 1];
+  const int alive_cur = ctl->alive_now[cur];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // frontier checks for F_s (solvers.hpp:348, :539-542)
+    if (alive_cur == 0) raise_err(a, 0, MGS_ERR_INFEASIBLE_JOINT, s);
+    else if (s > 0 && static_cast<uint64_t>(alive_cur) > a.budget) raise_err(a, 0, MGS_ERR_STATE_BUDGET, s, alive_cur);
+    if (s > 0) {
+      ctl->ftot += alive_cur;
+      if (static_cast<unsigned long long>(alive_cur) > ctl->fpeak) ctl->fpeak = alive_cur;
+    }
+  }
   const ScanJob jobs[1] = {{a.kid_cnt[cur], nullptr, a.kid_base, ctl->ranks_prev[s & 1], 0}};
   multi_scan(a, jobs, 1, 2 * (s + 1), &sc.ticket, ctl->scan_total);
+}
+
+__global__ void __launch_bounds__(kThreads) k_kids(const V2* __restrict__ ap, int s) {
+  const V2& a = c_v2;
+  __shared__ long long s_red[32];
+  if (failed(a)) return;
+  phase_kids(a, s, s_red);
+}
+
+__global__ void __launch_bounds__(kThreads) k_kid_fill(const V2* __restrict__ ap, int s) {
+  const V2& a = c_v2;
+  if (failed(a)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->sc[s & 1].kids = a.ctl->scan_total[0];
+  phase_kid_fill(a, s);
 }
 
 __global__ void __launch_bounds__(kThreads) k_place(const V2* __restrict__ ap, int s) {
@@ -1384,7 +1419,6 @@ __global__ void __launch_bounds__(kThreads) k_place(const V2* __restrict__ ap, i
   const int T_ = sc.T;
   const bool fits = T_ <= a.ccap && sc.items_s <= a.itcap && sc.items_b <= a.itcap;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    sc.kids = ctl->scan_total[0];
     ctl->tr += static_cast<unsigned long long>(T_);
     ctl->tbytes += static_cast<unsigned long long>(ctl->n_store[s & 1]) * 20ull + static_cast<unsigned long long>(T_) * 37ull;
     if (T_ > a.ccap) raise_err(a, 0, kOverflow, s, 0, 7, T_);
@@ -1791,6 +1825,9 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   const dim3 g_units = wave(reinterpret_cast<const void*>(kunits), 0);
   const dim3 g_scans = wave(reinterpret_cast<const void*>(k_scans), 0);
   const dim3 g_place = wave(reinterpret_cast<const void*>(k_place), 0);
+  const dim3 g_kids = wave(reinterpret_cast<const void*>(k_kids), 0);
+  const dim3 g_kscan = wave(reinterpret_cast<const void*>(k_kid_scan), 0);
+  const dim3 g_kfill = wave(reinterpret_cast<const void*>(k_kid_fill), 0);
   const dim3 g_rbig = wave(reinterpret_cast<const void*>(k_ranks_big), smem_rank);
   const dim3 g_tbig = wave(reinterpret_cast<const void*>(ktbig), 0);
   const dim3 g_tables = wave(reinterpret_cast<const void*>(k_tables), 0);
@@ -1814,16 +1851,16 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     // The window's kernel sequence depends only on S, M, the lane count and
     // launch shapes (all problem data lives behind d_args), so it is captured
     // once into a CUDA graph and replayed; MGS_DEBUG_STEPS launches eagerly.
-    constexpr int kK = 10;
-    static const char* kNames[kK] = {"units", "scans", "place", "ranks", "tables", "trans_big",
-                                     "trans_small", "band", "write", "dom"};
+    constexpr int kK = 13;
+    static const char* kNames[kK] = {"kids", "kid_scan", "kid_fill", "ranks", "units", "scans", "place", "tables",
+                                     "trans_big", "trans_small", "band", "write", "dom"};
     std::vector<cudaEvent_t> evs;
     // trans_small depends only on the ranks, not on the subset tables (it
     // writes disjoint candidate slots; the band maxima are atomicMax): in the
     // captured graph it is a parallel branch (MGS_NO_FORK keeps one chain)
     static const bool fork_ok = std::getenv("MGS_NO_FORK") == nullptr;
     cudaStream_t side = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_rank_fork = nullptr, ev_rank_join = nullptr;
     auto enqueue = [&](cudaStream_t st_, bool timed) {
       const bool fork = fork_ok && !timed && side != nullptr;
       auto mark = [&]() {
@@ -1877,14 +1914,29 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         mark();
       };
       for (int st = 0; st < S; ++st) {
+        // rank branch (F_s's dense lex ranks) beside the unit branch
+        // (successor statuses and candidate ranges): they meet at the transitions
+        cudaStream_t rs_ = fork ? side : st_;
+        if (fork) {
+          MGS_CUDA_OK(cudaEventRecord(ev_rank_fork, st_));
+          MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_rank_fork, 0));
+        }
+        k_kids<<<g_kids, kThreads, 0, rs_>>>(d_args, st);
+        after("kids", st);
+        k_kid_scan<<<g_kscan, kThreads, 0, rs_>>>(d_args, st);
+        after("kid_scan", st);
+        k_kid_fill<<<g_kfill, kThreads, 0, rs_>>>(d_args, st);
+        after("kid_fill", st);
+        k_ranks_big<<<g_rbig, kThreads, smem_rank, rs_>>>(d_args, st);
+        after("ranks", st);
+        if (fork) MGS_CUDA_OK(cudaEventRecord(ev_rank_join, side));
         kunits<<<g_units, kThreads, 0, st_>>>(d_args, st);
         after("units", st);
         k_scans<<<g_scans, kThreads, 0, st_>>>(d_args, st);
         after("scans", st);
         k_place<<<g_place, kThreads, 0, st_>>>(d_args, st);
         after("place", st);
-        k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(d_args, st);
-        after("ranks_big", st);
+        if (fork) MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rank_join, 0));
         if (fork) {  // graph: small-group transitions run beside tables -> big-group transitions
           MGS_CUDA_OK(cudaEventRecord(ev_fork, st_));
           MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_fork, 0));
@@ -1944,11 +1996,15 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         MGS_CUDA_OK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
         MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
         MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_rank_fork, cudaEventDisableTiming));
+        MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_rank_join, cudaEventDisableTiming));
         MGS_CUDA_OK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
         enqueue(cap, false);
         MGS_CUDA_OK(cudaStreamEndCapture(cap, &graph));
         MGS_CUDA_OK(cudaEventDestroy(ev_fork));
         MGS_CUDA_OK(cudaEventDestroy(ev_join));
+        MGS_CUDA_OK(cudaEventDestroy(ev_rank_fork));
+        MGS_CUDA_OK(cudaEventDestroy(ev_rank_join));
         MGS_CUDA_OK(cudaStreamDestroy(side));
         side = nullptr;
         cudaGraphExec_t exec;
