@@ -569,20 +569,19 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
   if (threadIdx.x == 0 && rs) atomicAdd(&a.ctl->tr_ref, static_cast<unsigned long long>(rs));
 }
 
-// R1 (rank branch): children per parent rank + live-state count of F_s
+// R1 (rank branch): children per parent rank + live-state count of F_s.
+// Every stored state is counted; k_dom of the previous step takes the states
+// it kills off both counters (atomics on both sides, so the two kernels may
+// run in either order or concurrently: in the graph this one runs beside
+// k_dom, straight after k_write).
 __device__ void phase_kids(const V2& a, int s, long long* s_red) {
   const int cur = s & 1;
   const FrontierV2& F = a.f[cur];
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
-  const int n = a.ctl->n_store[cur];
-  long long live = 0;
-  for (int i = gtid; i < n; i += gstride)
-    if (F.alive[i]) {
-      atomicAdd(&a.kid_cnt[cur][F.lex[i] >> 32], 1);
-      ++live;
-    }
-  const long long ls = block_sum(live, s_red);
-  if (threadIdx.x == 0 && ls) atomicAdd(&a.ctl->alive_now[cur], static_cast<int>(ls));
+  const int n = s == 0 ? a.ctl->n_store[0] : a.ctl->sc[(s - 1) & 1].out_states;  // k_dom may not have published n_store yet
+  for (int i = gtid; i < n; i += gstride) atomicAdd(&a.kid_cnt[cur][F.lex[i] >> 32], 1);
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.ctl->alive_now[cur], n);
+  (void)s_red;
 }
 
 // S3: placement
@@ -1294,11 +1293,16 @@ __device__ void phase_dominance(const V2& a, int s) {
             dead[hb] = true;
         }
       }
+      int kills = 0;
       for (int h = 0; h < 2; ++h)
         if (q[h] >= 0 && dead[h]) {
           N.alive[q[h]] = 0;
           atomicSub(&N.g_alive[N.group[q[h]]], 1);
+          atomicSub(&a.kid_cnt[nxt][lx[h] >> 32], 1);  // see phase_kids
+          ++kills;
         }
+      for (int o = 16; o > 0; o >>= 1) kills += __shfl_xor_sync(0xffffffffu, kills, o);
+      if (lane == 0 && kills && s + 1 < a.S) atomicSub(&a.ctl->alive_now[nxt], kills);  // F_S: k_term1 counts
     }
     if (lane == 0) a.pcnt[p] = 0;
   }
@@ -1918,11 +1922,17 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         // (successor statuses and candidate ranges): they meet at the transitions
         cudaStream_t rs_ = fork ? side : st_;
         if (fork) {
+          if (st == 0) {  // later steps launch k_kids beside the previous k_dom
+            MGS_CUDA_OK(cudaEventRecord(ev_rank_fork, st_));
+            MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_rank_fork, 0));
+            k_kids<<<g_kids, kThreads, 0, side>>>(d_args, st);
+          }
           MGS_CUDA_OK(cudaEventRecord(ev_rank_fork, st_));
           MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_rank_fork, 0));
+        } else {
+          k_kids<<<g_kids, kThreads, 0, rs_>>>(d_args, st);
+          after("kids", st);
         }
-        k_kids<<<g_kids, kThreads, 0, rs_>>>(d_args, st);
-        after("kids", st);
         k_kid_scan<<<g_kscan, kThreads, 0, rs_>>>(d_args, st);
         after("kid_scan", st);
         k_kid_fill<<<g_kfill, kThreads, 0, rs_>>>(d_args, st);
@@ -1957,6 +1967,11 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         after("band", st);
         k_write<<<g_write, kThreads, 0, st_>>>(d_args, st);
         after("write", st);
+        if (fork && st + 1 < S) {
+          MGS_CUDA_OK(cudaEventRecord(ev_rank_fork, st_));
+          MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_rank_fork, 0));
+          k_kids<<<g_kids, kThreads, 0, side>>>(d_args, st + 1);
+        }
         k_dom<<<g_dom, kThreads, 0, st_>>>(d_args, st);
         after("dom", st);
       }
