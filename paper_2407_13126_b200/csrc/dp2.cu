@@ -1431,12 +1431,19 @@ __global__ void __launch_bounds__(kThreads) k_place(const V2* __restrict__ ap, i
   if (fits) phase_place(a, s);
 }
 
-__global__ void __launch_bounds__(kThreads) k_ranks_big(const V2* __restrict__ ap, int s) {
+__global__ void __launch_bounds__(kThreads) k_ranks_big(const V2* __restrict__ ap, int s, int with_small) {
   const V2& a = c_v2;
   extern __shared__ unsigned long long smem_u64[];
   if (failed(a)) return;
   phase_ranks_big(a, s, smem_u64);
-  phase_ranks_small(a, s);  // independent of the big buckets: same launch
+  if (with_small) phase_ranks_small(a, s);  // independent of the big buckets
+}
+
+// small buckets on their own (full occupancy) beside k_ranks_big in the graph
+__global__ void __launch_bounds__(kThreads) k_ranks_small(const V2* __restrict__ ap, int s) {
+  const V2& a = c_v2;
+  if (failed(a)) return;
+  phase_ranks_small(a, s);
 }
 
 __global__ void MGS_LB k_tables(const V2* __restrict__ ap, int s) {
@@ -1829,6 +1836,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   const dim3 g_units = wave(reinterpret_cast<const void*>(kunits), 0);
   const dim3 g_scans = wave(reinterpret_cast<const void*>(k_scans), 0);
   const dim3 g_place = wave(reinterpret_cast<const void*>(k_place), 0);
+  const dim3 g_rsmall = wave(reinterpret_cast<const void*>(k_ranks_small), 0);
   const dim3 g_kids = wave(reinterpret_cast<const void*>(k_kids), 0);
   const dim3 g_kscan = wave(reinterpret_cast<const void*>(k_kid_scan), 0);
   const dim3 g_kfill = wave(reinterpret_cast<const void*>(k_kid_fill), 0);
@@ -1865,6 +1873,8 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     static const bool fork_ok = std::getenv("MGS_NO_FORK") == nullptr;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_rank_fork = nullptr, ev_rank_join = nullptr;
+    cudaEvent_t ev_rs_fork = nullptr, ev_rs_join = nullptr;
+    cudaStream_t side2 = nullptr;
     auto enqueue = [&](cudaStream_t st_, bool timed) {
       const bool fork = fork_ok && !timed && side != nullptr;
       auto mark = [&]() {
@@ -1937,16 +1947,27 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         after("kid_scan", st);
         k_kid_fill<<<g_kfill, kThreads, 0, rs_>>>(d_args, st);
         after("kid_fill", st);
-        k_ranks_big<<<g_rbig, kThreads, smem_rank, rs_>>>(d_args, st);
-        after("ranks", st);
-        if (fork) MGS_CUDA_OK(cudaEventRecord(ev_rank_join, side));
+        if (fork) {
+          MGS_CUDA_OK(cudaEventRecord(ev_rs_fork, side));
+          MGS_CUDA_OK(cudaStreamWaitEvent(side2, ev_rs_fork, 0));
+          k_ranks_small<<<g_rsmall, kThreads, 0, side2>>>(d_args, st);
+          MGS_CUDA_OK(cudaEventRecord(ev_rs_join, side2));
+          k_ranks_big<<<g_rbig, kThreads, smem_rank, side>>>(d_args, st, 0);
+          MGS_CUDA_OK(cudaEventRecord(ev_rank_join, side));
+        } else {
+          k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(d_args, st, 1);
+          after("ranks", st);
+        }
         kunits<<<g_units, kThreads, 0, st_>>>(d_args, st);
         after("units", st);
         k_scans<<<g_scans, kThreads, 0, st_>>>(d_args, st);
         after("scans", st);
         k_place<<<g_place, kThreads, 0, st_>>>(d_args, st);
         after("place", st);
-        if (fork) MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rank_join, 0));
+        if (fork) {
+          MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rank_join, 0));
+          MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rs_join, 0));
+        }
         if (fork) {  // graph: small-group transitions run beside tables -> big-group transitions
           MGS_CUDA_OK(cudaEventRecord(ev_fork, st_));
           MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_fork, 0));
@@ -1980,7 +2001,8 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
       k_term3<<<g_term, kThreads, 0, st_>>>(d_args);
       k_backtrack2<<<g_one, 32, 0, st_>>>(d_args);
     };
-    c.kernel_launches += static_cast<unsigned long long>(kK) * S + 4;
+    // graph replays split the ranks into two kernels (k_ranks_big + k_ranks_small)
+    c.kernel_launches += static_cast<unsigned long long>(kK + (!debug && fork_ok ? 1 : 0)) * S + 4;
     if (debug) {
       const auto host_t0 = std::chrono::steady_clock::now();
       enqueue(c.stream, true);
@@ -2013,6 +2035,9 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
         MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_rank_fork, cudaEventDisableTiming));
         MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_rank_join, cudaEventDisableTiming));
+        MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_rs_fork, cudaEventDisableTiming));
+        MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_rs_join, cudaEventDisableTiming));
+        MGS_CUDA_OK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
         MGS_CUDA_OK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
         enqueue(cap, false);
         MGS_CUDA_OK(cudaStreamEndCapture(cap, &graph));
@@ -2020,6 +2045,10 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         MGS_CUDA_OK(cudaEventDestroy(ev_join));
         MGS_CUDA_OK(cudaEventDestroy(ev_rank_fork));
         MGS_CUDA_OK(cudaEventDestroy(ev_rank_join));
+        MGS_CUDA_OK(cudaEventDestroy(ev_rs_fork));
+        MGS_CUDA_OK(cudaEventDestroy(ev_rs_join));
+        MGS_CUDA_OK(cudaStreamDestroy(side2));
+        side2 = nullptr;
         MGS_CUDA_OK(cudaStreamDestroy(side));
         side = nullptr;
         cudaGraphExec_t exec;
