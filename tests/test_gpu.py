@@ -472,3 +472,27 @@ def test_replay_requests_multi_window(gpu):
                 for w in range(sc.window_count):
                     tot += float(got[0, 0, k, w, m]["valid"])
                 assert bits(tot) == job[4]
+
+
+def test_launch_modes_agree(golden_dir):
+    """The captured graph (parallel branches per step), a single-chain graph
+    (MGS_NO_FORK) and eager launches (MGS_DEBUG_STEPS) give the same plans,
+    objective bits and counters, equal to the reference goldens."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    cases = [(stem, path, g) for stem, path, g in golden_dir["c1"] if int(stem.split("_")[1][1:]) <= 60][:2]
+    assert cases
+    script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "solve_variant.py")
+    results = {}
+    for name, extra in (("graph", {}), ("chain", {"MGS_NO_FORK": "1"}), ("eager", {"MGS_DEBUG_STEPS": "1"})):
+        env = dict(os.environ, **extra)
+        r = subprocess.run([sys.executable, script] + [str(p) for _, p, _ in cases], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, (name, r.stderr[-2000:])
+        results[name] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert results["graph"] == results["chain"] == results["eager"]
+    for stem, path, g in cases:
+        assert results["graph"][os.path.basename(str(path))]["obj"] == g["dp"]["obj"], stem
