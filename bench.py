@@ -267,7 +267,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(prob_e2e.S * (4 + 4 + 8) + 8),
                 "decision_latency_ms": 1e3 * e2e_s / args.steps},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": "per-window DP graph (13 phase kernels x S steps in two parallel branches, one graph launch)",
+        "roofline": {"bound": "hbm", "kernel": "per-window DP graph (14 phase kernels x S steps in parallel branches, one graph launch)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None,
                      "traffic": traffic.get("bytes_per_window") if traffic else None,
