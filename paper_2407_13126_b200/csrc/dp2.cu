@@ -574,14 +574,13 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
 // it kills off both counters (atomics on both sides, so the two kernels may
 // run in either order or concurrently: in the graph this one runs beside
 // k_dom, straight after k_write).
-__device__ void phase_kids(const V2& a, int s, long long* s_red) {
+__device__ void phase_kids(const V2& a, int s) {
   const int cur = s & 1;
   const FrontierV2& F = a.f[cur];
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const int n = s == 0 ? a.ctl->n_store[0] : a.ctl->sc[(s - 1) & 1].out_states;  // k_dom may not have published n_store yet
   for (int i = gtid; i < n; i += gstride) atomicAdd(&a.kid_cnt[cur][F.lex[i] >> 32], 1);
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.ctl->alive_now[cur], n);
-  (void)s_red;
 }
 
 // S3: placement
@@ -1403,9 +1402,8 @@ __global__ void __launch_bounds__(kThreads) k_kid_scan(const V2* __restrict__ ap
 
 __global__ void __launch_bounds__(kThreads) k_kids(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  __shared__ long long s_red[32];
   if (failed(a)) return;
-  phase_kids(a, s, s_red);
+  phase_kids(a, s);
 }
 
 __global__ void __launch_bounds__(kThreads) k_kid_fill(const V2* __restrict__ ap, int s) {
