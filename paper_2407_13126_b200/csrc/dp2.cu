@@ -1032,22 +1032,25 @@ __device__ void phase_trans_small(const V2& a, int s) {
 // S6: merge + band + output
 __device__ __forceinline__ void write_state(const V2& a, int s, int nxt, int q, int gidx, uint32_t key, int k) {
   const FrontierV2& N = a.f[nxt];
+  // every load (and the bucket atomic) is issued before the first store: the
+  // compiler cannot move loads across stores it cannot prove disjoint
   const int p = a.c_pid[k];
   const uint64_t lx = a.c_lex[k];
+  const double v = a.c_value[k];
+  const int parent = a.c_parent[k];
+  const long long h = a.hist_base[s + 1] + q;
+  const uint32_t ids = static_cast<uint32_t>(a.sp.pl_ids[p]);
+  const int slot = a.dominance_ok ? atomicAdd(&a.pcnt[p], 1) : 64;
   N.status[q] = key;
-  N.ids[q] = static_cast<uint32_t>(a.sp.pl_ids[p]);
+  N.ids[q] = ids;
   N.pid[q] = p;
-  N.value[q] = a.c_value[k];
+  N.value[q] = v;
   N.lex[q] = lx;
   N.alive[q] = 1;
   N.group[q] = gidx;
-  const long long h = a.hist_base[s + 1] + q;
-  a.h_parent[h] = a.c_parent[k];
+  a.h_parent[h] = parent;
   a.h_oi[h] = static_cast<int32_t>(lx & 0xffffffffu);
-  if (a.dominance_ok) {
-    const int slot = atomicAdd(&a.pcnt[p], 1);
-    if (slot < 64) a.pbucket[p * 64 + slot] = q;
-  }
+  if (slot < 64) a.pbucket[p * 64 + slot] = q;
 }
 
 // S6a: equal-key merge (multi-unit statuses) + band + survivor count per status
