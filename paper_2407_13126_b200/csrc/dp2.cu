@@ -590,12 +590,15 @@ __device__ void phase_place(const V2& a, int s) {
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const int NU = sc.n_units;
   for (int u = gtid; u < NU; u += gstride) {
+    // loads and atomics before the first store (no load may wait behind a store)
     const int id = a.u_ns[u];
     const int L = a.sig_len[a.u_sig[u]];
-    a.u_cbase[u] = a.ns_cbase[id] + atomicAdd(&a.ns_ccur[id], L);
-    a.ns_units[a.ns_ubase[id] + atomicAdd(&a.ns_ucur[id], 1)] = u;
     const int nsm = a.u_chs[u], nbg = a.u_chb[u];
     const int sb = a.u_sbase[u], bb = a.u_bbase[u];
+    const int cbase = a.ns_cbase[id], ubase = a.ns_ubase[id];
+    const int cpos = atomicAdd(&a.ns_ccur[id], L), upos = atomicAdd(&a.ns_ucur[id], 1);
+    a.u_cbase[u] = cbase + cpos;
+    a.ns_units[ubase + upos] = u;
     for (int c = 0; c < nsm; ++c) {
       a.it_s_unit[sb + c] = u;
       a.it_s_chunk[sb + c] = c;
@@ -628,12 +631,14 @@ __device__ void phase_kid_fill(const V2& a, int s) {
     bool big_first = false;
     int pr = 0;
     if (i < n && F.alive[i]) {
-      pr = static_cast<int>(F.lex[i] >> 32);
+      const uint64_t lx = F.lex[i];
+      pr = static_cast<int>(lx >> 32);
+      const int base = a.kid_base[pr], cnt = a.kid_cnt[cur][pr];  // loads before the stores
       const int q = atomicAdd(&a.kid_cur[cur][pr], 1);
-      const int slot = a.kid_base[pr] + q;
-      a.kid_items[slot] = ((F.lex[i] & 0xffffffffull) << 32) | static_cast<uint32_t>(i);
+      const int slot = base + q;
+      a.kid_items[slot] = ((lx & 0xffffffffull) << 32) | static_cast<uint32_t>(i);
       a.kid_pr[slot] = pr;
-      big_first = q == 0 && a.kid_cnt[cur][pr] > kBucketSmall;
+      big_first = q == 0 && cnt > kBucketSmall;
     }
     const unsigned bal = __ballot_sync(0xffffffffu, big_first);
     if (bal) {
