@@ -806,18 +806,46 @@ __device__ void phase_tables(const V2& a, int s) {
     }
     __syncthreads();
     unsigned long long bv = 0, brx = ~0ull;
-    for (int j = threadIdx.x; j < gn; j += kThreads) {  // claim placements, max value per entry, group best
-      if (!F.alive[gs + j]) continue;
-      const int pj = F.pid[gs + j];
-      const unsigned long long v = vbits(F.value[gs + j]);
-      const unsigned long long rx = (static_cast<unsigned long long>(F.rank[gs + j]) << 32) | static_cast<uint32_t>(j);
-      if (brx == ~0ull || v > bv || (v == bv && rx < brx)) {
-        bv = v;
-        brx = rx;
+    // software-pipelined: the next state's loads are issued before this
+    // state's stores / atomics (which loads could not be moved across)
+    int j = threadIdx.x;
+    bool al = false;
+    int pj = 0;
+    double vd = 0.0;
+    uint32_t rk = 0;
+    if (j < gn) {
+      al = F.alive[gs + j];
+      pj = F.pid[gs + j];
+      vd = F.value[gs + j];
+      rk = F.rank[gs + j];
+    }
+    for (; j < gn; j += kThreads) {  // claim placements, max value per entry, group best
+      const int jn = j + kThreads;
+      bool al_n = false;
+      int pj_n = 0;
+      double vd_n = 0.0;
+      uint32_t rk_n = 0;
+      if (jn < gn) {
+        al_n = F.alive[gs + jn];
+        pj_n = F.pid[gs + jn];
+        vd_n = F.value[gs + jn];
+        rk_n = F.rank[gs + jn];
       }
-      ex[pj] = static_cast<uint32_t>(j) + 1u;
-      for (int sub = 1; sub < nsub - 1; ++sub)
-        atomicMax(&vb[a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj]], v);
+      if (al) {
+        const unsigned long long v = vbits(vd);
+        const unsigned long long rx = (static_cast<unsigned long long>(rk) << 32) | static_cast<uint32_t>(j);
+        if (brx == ~0ull || v > bv || (v == bv && rx < brx)) {
+          bv = v;
+          brx = rx;
+        }
+        ex[pj] = static_cast<uint32_t>(j) + 1u;
+        for (int sub = 1; sub < nsub - 1; ++sub)
+          atomicMax(&vb[a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj]], v);
+      }
+      al = al_n;
+      pj = pj_n;
+      vd = vd_n;
+      rk = rk_n;
     }
     for (int o = 16; o > 0; o >>= 1) {
       const unsigned long long ov = __shfl_down_sync(0xffffffffu, bv, o);
