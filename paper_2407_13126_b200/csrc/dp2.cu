@@ -869,16 +869,17 @@ __device__ void phase_tables(const V2& a, int s) {
       a.tab_hdr[2 * b] = bv;
       a.tab_hdr[2 * b + 1] = brx;
     }
-    if (nsub > 2)
-      for (int j = threadIdx.x; j < gn; j += kThreads) {  // min (rank, idx) among the max
+    if (nsub > 2)  // min (rank, idx) among the max; M <= 2 here, so the partial subsets are 1 and 2
+      for (int j = threadIdx.x; j < gn; j += kThreads) {
         if (!F.alive[gs + j]) continue;
         const int pj = F.pid[gs + j];
         const unsigned long long v = vbits(F.value[gs + j]);
         const unsigned long long rx = (static_cast<unsigned long long>(F.rank[gs + j]) << 32) | static_cast<uint32_t>(j);
-        for (int sub = 1; sub < nsub - 1; ++sub) {
-          const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj];
-          if (vb[e] == v) atomicMin(&rxs[e], rx);
-        }
+        const int e1 = a.sp.proj_base[1] + a.sp.proj_id[1 * P1 + pj];
+        const int e2 = a.sp.proj_base[2] + a.sp.proj_id[2 * P1 + pj];
+        const unsigned long long m1 = vb[e1], m2 = vb[e2];  // both loads before either atomic
+        if (m1 == v) atomicMin(&rxs[e1], rx);
+        if (m2 == v) atomicMin(&rxs[e2], rx);
       }
     __syncthreads();
   }
