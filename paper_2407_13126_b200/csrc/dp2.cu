@@ -1134,25 +1134,51 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
                 else hi = mid;
               }
             }
-            for (int t = lo + threadIdx.x; t < n; t += kThreads) {
-              const int p = a.sp.cand_pid[b + t];
+            // software-pipelined: the next candidate's loads are issued
+            // before this one's atomics / stores
+            int t = lo + threadIdx.x;
+            int p = 0;
+            bool ok = false;
+            double v = 0.0;
+            unsigned long long lx = 0;
+            if (t < n) {
+              p = a.sp.cand_pid[b + t];
+              ok = a.c_ok[cbu + t];
+              v = a.c_value[cbu + t];
+              if (pass > 0) lx = a.c_lex[cbu + t];
+            }
+            for (; t < n; t += kThreads) {
               if (p >= w0 + win) break;
+              const int tn = t + kThreads;
+              int p_n = 0;
+              bool ok_n = false;
+              double v_n = 0.0;
+              unsigned long long lx_n = 0;
+              if (tn < n) {
+                p_n = a.sp.cand_pid[b + tn];
+                ok_n = a.c_ok[cbu + tn];
+                v_n = a.c_value[cbu + tn];
+                if (pass > 0) lx_n = a.c_lex[cbu + tn];
+              }
               const int k = cbu + t;
-              if (!a.c_ok[k]) {
+              if (!ok) {
                 if (pass == 2) a.c_live[k] = 0;
-                continue;
-              }
-              const double v = a.c_value[k];
-              const unsigned long long vb = vbits(v);
-              if (pass == 0) {
-                atomicMax(&mvb[p - w0], vb);
-              } else if (pass == 1) {
-                if (mvb[p - w0] == vb) atomicMin(&mlx[p - w0], a.c_lex[k]);
               } else {
-                const bool keep = mvb[p - w0] == vb && mlx[p - w0] == a.c_lex[k] && v >= thresh;
-                a.c_live[k] = keep ? 1 : 0;
-                mine += keep;
+                const unsigned long long vb = vbits(v);
+                if (pass == 0) {
+                  atomicMax(&mvb[p - w0], vb);
+                } else if (pass == 1) {
+                  if (mvb[p - w0] == vb) atomicMin(&mlx[p - w0], lx);
+                } else {
+                  const bool keep = mvb[p - w0] == vb && mlx[p - w0] == lx && v >= thresh;
+                  a.c_live[k] = keep ? 1 : 0;
+                  mine += keep;
+                }
               }
+              p = p_n;
+              ok = ok_n;
+              v = v_n;
+              lx = lx_n;
             }
           }
           __syncthreads();
