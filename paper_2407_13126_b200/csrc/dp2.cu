@@ -579,7 +579,15 @@ __device__ void phase_kids(const V2& a, int s) {
   const FrontierV2& F = a.f[cur];
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const int n = s == 0 ? a.ctl->n_store[0] : a.ctl->sc[(s - 1) & 1].out_states;  // k_dom may not have published n_store yet
-  for (int i = gtid; i < n; i += gstride) atomicAdd(&a.kid_cnt[cur][F.lex[i] >> 32], 1);
+  int i = gtid;
+  for (; i + 3 * gstride < n; i += 4 * gstride) {  // four loads in flight before the atomics
+    uint64_t l[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) l[u] = F.lex[i + u * gstride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) atomicAdd(&a.kid_cnt[cur][l[u] >> 32], 1);
+  }
+  for (; i < n; i += gstride) atomicAdd(&a.kid_cnt[cur][F.lex[i] >> 32], 1);
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.ctl->alive_now[cur], n);
 }
 
@@ -626,12 +634,19 @@ __device__ void phase_kid_fill(const V2& a, int s) {
   const FrontierV2& F = a.f[cur];
   const int n = a.ctl->n_store[cur];
   const int lane = threadIdx.x & 31;
-  for (int i0 = gtid - lane; i0 < n; i0 += gstride) {  // warp-uniform trip count
+  // software-pipelined: the next state's alive flag and lex are loaded ahead
+  int i0 = gtid - lane;
+  bool al = i0 + lane < n && F.alive[i0 + lane];
+  uint64_t lx_c = al ? F.lex[i0 + lane] : 0;
+  for (; i0 < n; i0 += gstride) {  // warp-uniform trip count
     const int i = i0 + lane;
+    const int in = i + gstride;
+    const bool al_n = in < n && F.alive[in];
+    const uint64_t lx_n = al_n ? F.lex[in] : 0;
     bool big_first = false;
     int pr = 0;
-    if (i < n && F.alive[i]) {
-      const uint64_t lx = F.lex[i];
+    if (al) {
+      const uint64_t lx = lx_c;
       pr = static_cast<int>(lx >> 32);
       const int base = a.kid_base[pr], cnt = a.kid_cnt[cur][pr];  // loads before the stores
       const int q = atomicAdd(&a.kid_cur[cur][pr], 1);
@@ -647,6 +662,8 @@ __device__ void phase_kid_fill(const V2& a, int s) {
       b0 = __shfl_sync(0xffffffffu, b0, 0);
       if (big_first) a.big_bucket[b0 + __popc(bal & ((1u << lane) - 1u))] = pr;
     }
+    al = al_n;
+    lx_c = lx_n;
   }
 }
 
@@ -696,17 +713,36 @@ __device__ void phase_ranks_small(const V2& a, int s) {
   const FrontierV2& F = a.f[cur];
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const int n = sc.kids;  // live states of F_s = filled slots
-  for (int i = gtid; i < n; i += gstride) {
-    const int pr = a.kid_pr[i];
-    const int c = a.kid_cnt[cur][pr];
-    if (c > kBucketSmall) continue;
-    const unsigned long long me = a.kid_items[i];
-    int rank = a.kid_base[pr];
-    if (c > 1) {
-      const int base = rank;
-      for (int k = 0; k < c; ++k) rank += a.kid_items[base + k] < me;
+  // software-pipelined: slot i + gstride is loaded before slot i's rank is stored
+  int i = gtid;
+  int pr = 0, c = 0, base = 0;
+  unsigned long long me = 0;
+  if (i < n) {
+    pr = a.kid_pr[i];
+    me = a.kid_items[i];
+    c = a.kid_cnt[cur][pr];
+    base = a.kid_base[pr];
+  }
+  for (; i < n; i += gstride) {
+    const int in = i + gstride;
+    int pr_n = 0, c_n = 0, base_n = 0;
+    unsigned long long me_n = 0;
+    if (in < n) {
+      pr_n = a.kid_pr[in];
+      me_n = a.kid_items[in];
+      c_n = a.kid_cnt[cur][pr_n];
+      base_n = a.kid_base[pr_n];
     }
-    F.rank[static_cast<uint32_t>(me)] = rank;
+    if (c <= kBucketSmall) {
+      int rank = base;
+      if (c > 1)
+        for (int k = 0; k < c; ++k) rank += a.kid_items[base + k] < me;
+      F.rank[static_cast<uint32_t>(me)] = rank;
+    }
+    pr = pr_n;
+    me = me_n;
+    c = c_n;
+    base = base_n;
   }
 }
 
