@@ -15,6 +15,11 @@ Outputs (all small, committed):
         windows (about two minutes of reference CPU time each).
   tests/golden/kat/*  hand-written known-answer scenarios whose expected values
         come from the reference's own tests (eval_test.cpp, solver_test.cpp).
+  tests/golden/multi_m<M>_<seed>.json, tests/golden/multi/*  M = 3..4 windows
+        solved by "reference + 1-line fix" (oracle/_ref/migref_patched: only the
+        packed-status widening at solvers.hpp:359,401,414), with brute force
+        where |O|^S is small, plus the unmodified reference's answer
+        (infeasible.joint, the truncation bug).
 """
 from __future__ import annotations
 
@@ -33,6 +38,7 @@ from paper_2407_13126_b200 import workloads as W  # noqa: E402
 
 GOLD = os.path.join(ROOT, "tests", "golden")
 MIGREF = os.path.join(HERE, "_ref", "migref")
+MIGREF_PATCHED = os.path.join(HERE, "_ref", "migref_patched")
 
 # (seed, count, allow_accuracy_drop): the seeds of the reference's solver /
 # baseline suites (solver_test.cpp:110-178, baseline_test.cpp:139-180) plus
@@ -41,9 +47,50 @@ RANDOM_SEEDS = [(20250101, 25, True), (424242, 10, True), (777, 4, True), (1312,
                 (31337, 20, True), (1, 25, True), (2, 25, False), (3, 25, True)]
 
 
-def ref_solve(path, *extra):
-    out = subprocess.run([MIGREF, "solve", path] + list(extra), check=True, capture_output=True, text=True)
+def ref_solve(path, *extra, binary=MIGREF):
+    out = subprocess.run([binary, "solve", path] + list(extra), check=True, capture_output=True, text=True)
     return json.loads(out.stdout)
+
+
+# M = 3..4 corpora: "reference + 1-line fix" (oracle/Makefile ref-patched), the
+# only reference build that can solve them. Each entry:
+# (M, seed, count, S_lo, S_hi, brute-force estimate cap or None for DP only).
+MULTI_SEEDS = [(3, 31, 24, 3, 4, 2e6), (3, 32, 12, 5, 8, None), (4, 41, 12, 4, 6, None)]
+# C2-shaped windows (workloads.c2_spec, shortened): (tenants, S, vol_per_gpc, seed)
+MULTI_C2 = [(3, 20, 6, 200003), (4, 12, 2, 200004), (4, 12, 3, 200004)]
+
+
+def make_multi():
+    for M, seed, count, s_lo, s_hi, cap in MULTI_SEEDS:
+        with tempfile.TemporaryDirectory() as td:
+            cmd = [MIGREF_PATCHED, "gen-multi", str(seed), str(count), td, str(M), str(s_lo), str(s_hi),
+                   "%g" % (cap or 1e300)]
+            paths = subprocess.run(cmd, check=True, capture_output=True, text=True).stdout.split()
+            bundle = {}
+            for p in paths:
+                stem = os.path.basename(p)[:-4]
+                files = {ext: open(os.path.join(td, stem + "." + ext)).read() for ext in ("scn", "catalog", "csv")}
+                extra = ["--chain"] + (["--bf"] if cap else [])
+                files["golden"] = ref_solve(p, *extra, binary=MIGREF_PATCHED)
+                files["golden"]["unpatched"] = ref_solve(p)  # the shipped reference: infeasible.joint
+                bundle[stem] = files
+        out = os.path.join(GOLD, "multi_m%d_%d.json" % (M, seed))
+        with open(out, "w") as f:
+            json.dump(bundle, f, indent=0, sort_keys=True)
+        print(out, len(bundle))
+    d = os.path.join(GOLD, "multi")
+    os.makedirs(d, exist_ok=True)
+    golden = {}
+    for M, S, vol, seed in MULTI_C2:
+        stem = "c2_m%d_S%d_v%d_%d" % (M, S, vol, seed)
+        spec = W.c2_spec(seed, steps=S, windows=1, tenants=M, vol_per_gpc=vol)
+        spec.catalog_path = os.path.join(GOLD, "lattice_a100.catalog")
+        scn = W.write_scenario(spec, d, stem)
+        golden[stem] = ref_solve(scn, binary=MIGREF_PATCHED)
+        golden[stem]["unpatched"] = ref_solve(scn)
+        print(stem, json.dumps(golden[stem])[:200])
+    with open(os.path.join(d, "multi_golden.json"), "w") as f:
+        json.dump(golden, f, indent=0, sort_keys=True)
 
 
 def make_random():
@@ -169,7 +216,7 @@ def make_kat():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1-full", action="store_true")
-    ap.add_argument("--only", choices=["random", "c1", "kat"])
+    ap.add_argument("--only", choices=["random", "c1", "kat", "multi"])
     a = ap.parse_args()
     if not os.path.exists(MIGREF):
         sys.exit("build the reference first: make -C oracle ref")
@@ -179,3 +226,5 @@ if __name__ == "__main__":
         make_random()
     if a.only in (None, "c1"):
         make_c1(a.c1_full)
+    if a.only in (None, "multi"):
+        make_multi()

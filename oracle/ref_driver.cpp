@@ -34,6 +34,14 @@
 //       (tests/test_util.hpp:104-181), written to files with
 //       write_scenario_files (workload.hpp:422) so other implementations
 //       read identical inputs.
+//   migref gen-multi <seed> <count> <outdir> <M> <S_lo> <S_hi> <est_cap>
+//       the same generator shape (test_util.hpp:104-181: mt19937, rng() % n,
+//       finalize_scenario, precheck, |O|^S estimate, solvability through
+//       solve_dp) widened to M = 3..4 tenants on A100 configurations with
+//       enough slots to anchor every tenant. Only meaningful when built
+//       against the patched headers (migref_patched, see oracle/Makefile):
+//       the unmodified solve_dp rejects every M >= 3 window
+//       (solvers.hpp:359,401,414 narrow the packed status to int).
 //
 // The shared-library build exports migref_solve_file() for bench.py.
 #include <chrono>
@@ -324,6 +332,110 @@ int cmd_gen_random(int argc, char** argv) {
   return 0;
 }
 
+// Multi-tenant sibling of testutil::random_oracle_scenario (test_util.hpp:
+// 104-181). RT tables are sparse (random subsets of sizes) so the option space
+// stays small enough for the brute-force cross-check.
+Scenario random_multi_scenario(std::mt19937& rng, int M, int S_lo, int S_hi, double est_cap) {
+  static const std::vector<std::string> pool = {
+      "config 4_2_1 4@0 2@4 1@6\n",         "config 4_1_1_1 4@0 1@4 1@5 1@6\n",
+      "config 3_2_2 2@0 2@2 3@4\n",         "config 3_2_1_1 2@0 1@2 1@3 3@4\n",
+      "config 3_1_1_1_1 1@0 1@1 1@2 1@3 3@4\n", "config 2_2_2_1 2@0 2@2 2@4 1@6\n",
+      "config 2_2_1_1_1 2@0 2@2 1@4 1@5 1@6\n",
+  };
+  auto pick_real = [&](double lo, double hi) {
+    return lo + (hi - lo) * (static_cast<double>(rng() % 10000) / 10000.0);
+  };
+  for (int attempt = 0; attempt < 2000; ++attempt) {
+    int S = S_lo + static_cast<int>(rng() % static_cast<unsigned>(S_hi - S_lo + 1));
+    // M >= 4 needs five slots (four anchored tenants + one retraining): draw
+    // from the pool's tail (3_1_1_1_1, 2_2_2_1, 2_2_1_1_1)
+    const int lo = M >= 4 ? 4 : 0;
+    int nconfigs = 1 + static_cast<int>(rng() % (M >= 4 ? 2 : 3));
+    std::set<int> chosen;
+    while (static_cast<int>(chosen.size()) < nconfigs)
+      chosen.insert(lo + static_cast<int>(rng() % static_cast<unsigned>(pool.size() - lo)));
+    std::string text;
+    for (int i : chosen) text += pool[i];
+    Catalog cat = load_catalog_text(text);
+    std::vector<ModelEntry> models;
+    for (int m = 0; m < M; ++m) {
+      ModelEntry e;
+      e.profile.name = "t" + std::to_string(m);
+      e.profile.gflops = pick_real(1.0, 20.0);
+      e.profile.min_deploy_gpcs = M >= 4 ? 1 : 1 + static_cast<int>(rng() % 2);
+      e.profile.latency_full = 0.01;
+      e.profile.reconfig_overhead = std::vector<double>{0.0, 0.3, 0.7, 1.0}[rng() % 4];
+      double cap = 4.0 + rng() % 8;
+      for (int k = 1; k <= 7; ++k) {
+        e.profile.capability[k] = cap;
+        cap += rng() % 10;
+      }
+      // sparse nonincreasing RT table: few retraining sizes keep |O| small
+      long long rt1 = 1 + static_cast<long long>(rng() % static_cast<unsigned>(S));
+      long long drop = rng() % 2;
+      for (int k = 1; k <= 7; ++k)
+        if (rng() % 3 == 0) e.retraining.rt_table[k] = std::max<long long>(1, rt1 - drop * (k - 1));
+      if (e.retraining.rt_table.empty() || (M >= 4 && !e.retraining.rt_table.count(1)))
+        e.retraining.rt_table[1] = std::max<long long>(rt1, e.retraining.rt_table.empty() ? 1 : e.retraining.rt_table.begin()->second);
+      double pre = pick_real(0.2, 0.9);
+      double post = rng() % 4 == 0 ? pick_real(0.1, pre) : pick_real(pre, 1.0);
+      e.retraining.accuracy_pre = {pre};
+      e.retraining.accuracy_post = {post};
+      models.push_back(std::move(e));
+    }
+    InferenceTrace trace;
+    for (int m = 0; m < M; ++m) {
+      std::vector<long long> counts;
+      bool zero = rng() % 12 == 0;
+      for (int s = 0; s < S; ++s) counts.push_back(zero ? 0 : rng() % 30);
+      trace.counts.push_back(std::move(counts));
+    }
+    Scenario sc;
+    try {
+      sc = finalize_scenario(std::move(cat), std::move(models), std::move(trace), S, 1, 1.0);
+    } catch (const Error& e) {
+      if (std::getenv("MIGREF_GEN_DEBUG")) std::fprintf(stderr, "finalize: %s\n", e.what());
+      continue;
+    }
+    PlanContext ctx{&sc, 0, std::nullopt};
+    if (!precheck_scenario(ctx).empty()) {
+      if (std::getenv("MIGREF_GEN_DEBUG")) std::fprintf(stderr, "precheck\n");
+      continue;
+    }
+    auto space = engine::Space::build(ctx);
+    if (std::pow(static_cast<double>(space.options.size()), S) > est_cap) {
+      if (std::getenv("MIGREF_GEN_DEBUG")) std::fprintf(stderr, "estimate %zu^%d\n", space.options.size(), S);
+      continue;
+    }
+    try {
+      ArrivalForecast fc = window_forecast(sc, 0);
+      (void)solve_dp(ctx, fc);
+    } catch (const Error& e) {
+      if (std::getenv("MIGREF_GEN_DEBUG")) std::fprintf(stderr, "solve: %s\n", e.code().c_str());
+      continue;
+    }
+    return sc;
+  }
+  throw std::runtime_error("random_multi_scenario: no scenario found");
+}
+
+int cmd_gen_multi(int argc, char** argv) {
+  if (argc < 9) return 2;
+  unsigned seed = static_cast<unsigned>(std::strtoul(argv[2], nullptr, 10));
+  int count = std::atoi(argv[3]);
+  std::string dir = argv[4];
+  int M = std::atoi(argv[5]), S_lo = std::atoi(argv[6]), S_hi = std::atoi(argv[7]);
+  double est_cap = std::atof(argv[8]);
+  std::mt19937 rng(seed);
+  for (int i = 0; i < count; ++i) {
+    Scenario sc = random_multi_scenario(rng, M, S_lo, S_hi, est_cap);
+    std::string stem = "m" + std::to_string(M) + "_" + std::to_string(seed) + "_" + std::to_string(i);
+    write_scenario_files(sc, dir, stem);
+    std::printf("%s/%s.scn\n", dir.c_str(), stem.c_str());
+  }
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -361,6 +473,7 @@ int main(int argc, char** argv) {
   std::string cmd = argv[1];
   if (cmd == "solve") return cmd_solve(argc, argv);
   if (cmd == "gen-random") return cmd_gen_random(argc, argv);
+  if (cmd == "gen-multi") return cmd_gen_multi(argc, argv);
   if (cmd == "replay") return cmd_replay(argc, argv);
   if (cmd == "preinit") return cmd_preinit(argc, argv);
   if (cmd == "drive") return cmd_drive(argc, argv);

@@ -129,13 +129,15 @@ def c1_spec(seed: int, steps: int = 200, data_volume: int = 3000, psi: float = 0
     return spec
 
 
-def c2_spec(seed: int, steps: int = 200, windows: int = 3, tenants: int = 4) -> ScenarioSpec:
+def c2_spec(seed: int, steps: int = 200, windows: int = 3, tenants: int = 4, vol_per_gpc: int = 80,
+            psi: float = 0.5) -> ScenarioSpec:
     """Config 2 / 4 generator: ResNet-50 / MobileNetV2 / ViT-B / BERT-base with
     c = 40/120/12/10 req/s/GPC, data_volume = 80c (RT = ceil(240/k)), psi 0.5,
-    explicit per-window accuracy lists, 2-state MMPP arrivals."""
+    explicit per-window accuracy lists, 2-state MMPP arrivals. Shorter windows
+    (parity fixtures) scale the data volume with `vol_per_gpc`."""
     table = [("resnet50", 40.0, 0.55, 0.85, 4.09), ("mobilenetv2", 120.0, 0.70, 0.80, 0.32),
              ("vitb", 12.0, 0.60, 0.88, 17.56), ("bertbase", 10.0, 0.50, 0.83, 22.2)][:tenants]
-    ts = [Tenant(n, c, [pre] * windows, [post] * windows, data_volume=int(80 * c), gflops=g)
+    ts = [Tenant(n, c, [pre] * windows, [post] * windows, data_volume=int(vol_per_gpc * c), gflops=g, psi=psi)
           for (n, c, pre, post, g) in table]
     spec = ScenarioSpec(ts, steps, windows)
     spec.counts = mmpp_trace([t.per_gpc for t in ts], steps * windows, seed)
