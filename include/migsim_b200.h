@@ -23,6 +23,10 @@
  *   mgs_preinit        plan_preinit + apply_preinit    preinit.hpp:41-114
  *   mgs_goodput_table_batch  solve_dp's ub_suffix table  solvers.hpp:258-280
  *                      for a batch of traces sharing one window's tables
+ *   mgs_check_feasible_batch check_feasible            evaluate.hpp:55-146
+ *   mgs_evaluate_views_batch evaluate_plan (any allocation, verify optional)
+ *                                                      evaluate.hpp:25-47,153-210
+ *   mgs_run_fluid      run_fluid (+ build_series)      simulator.hpp:72-131,171-203
  */
 #ifndef MIGSIM_B200_H
 #define MIGSIM_B200_H
@@ -144,6 +148,33 @@ typedef struct {
   double overhead_seconds;
 } mgs_job_metrics;
 
+/* check_feasible violation families (evaluate.hpp:82-144); the host wrapper
+ * formats the reference's message from code/step/model/detail. */
+typedef enum {
+  MGS_VIOL_DEPLOYMENT_FLOOR = 1,        /* "deployment-floor": detail[0] = GPC-sum check satisfied, detail[1] = L */
+  MGS_VIOL_RETRAINING_NOT_LAUNCHED = 2, /* "retraining-not-launched" (step -1) */
+  MGS_VIOL_RETRAINING_INTERRUPTED = 3,  /* "retraining-interrupted": detail[0] = run contiguous (size changed) */
+  MGS_VIOL_RETRAINING_SIZE = 4,         /* "retraining-size": detail[0] = k */
+  MGS_VIOL_RETRAINING_INCOMPLETE = 5,   /* "retraining-incomplete": detail = run length, RT, k */
+  MGS_VIOL_RETRAINING_OVERRUN = 6       /* "retraining-overrun": detail = run length, RT, k */
+} mgs_violation_family;
+
+typedef struct {
+  int32_t code;    /* mgs_violation_family */
+  int32_t step;    /* Violation::second (-1 for not-launched) */
+  int32_t model;   /* tenant index */
+  int32_t detail[3];
+} mgs_plan_violation;
+
+/* One evaluate_plan breakdown entry (plan_types.hpp:38-45). */
+typedef struct {
+  double throughput;     /* SLO-attained requests of the step */
+  double overhead_loss;  /* loss_frac * raw capability */
+  double goodput;        /* throughput * accuracy */
+  int32_t completion;    /* retraining finished strictly before the step */
+  int32_t pad;
+} mgs_score_entry;
+
 typedef struct mgs_ctx mgs_ctx;
 
 MGS_API int mgs_open(int device, mgs_ctx** out);
@@ -254,6 +285,42 @@ MGS_API int mgs_goodput_table_batch(mgs_ctx* ctx, const mgs_problem* p, const in
 MGS_API int mgs_goodput_table_batch_device(mgs_ctx* ctx, const mgs_problem* p, const int32_t* d_arrivals,
                                            int32_t n_traces, double* d_best, double* d_ub_suffix, int32_t* n_pareto,
                                            mgs_error* err);
+
+/* Plans as general per-step allocations (any sequence resolve_step reads,
+ * evaluate.hpp:25-47): step_config[i*S+s] = configuration index (lattice
+ * order); slot_tasks[(i*S+s)*MGS_MAX_SLOTS + k] = task bits of slot k of that
+ * configuration: bit 2m = inference task of tenant m, bit 2m+1 = its
+ * retraining task (several bits = a shared instance). String-level checks
+ * (unknown ids, second-index, validate_allocation) belong to the caller.
+ *
+ * check_feasible's constraint families for n_plans plans: up to cap records
+ * per plan at out[i*cap...] in the reference's order, n_out[i] = total count
+ * (0 = feasible). */
+MGS_API int mgs_check_feasible_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* step_config,
+                                     const uint8_t* slot_tasks, int32_t n_plans, mgs_plan_violation* out, int32_t cap,
+                                     int32_t* n_out, mgs_error* err);
+
+/* evaluate_plan of n_plans general plans x n_traces traces (arrivals
+ * [t][M][S]); psi_override (optional) [i][s][m] replaces the profile psi where
+ * it is not NaN (OverheadOverrides). total[i*n_traces+t]; entries (optional)
+ * [i][t][s][m]. verify != 0 runs check_feasible first: status[i] (required
+ * then) = MGS_ERR_PLAN_INFEASIBLE and first[i] (optional) = the first
+ * violation for infeasible plans, whose totals are left 0. */
+MGS_API int mgs_evaluate_views_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* step_config,
+                                     const uint8_t* slot_tasks, int32_t n_plans, const double* psi_override,
+                                     const int64_t* arrivals, int32_t n_traces, int32_t verify, double* total,
+                                     mgs_score_entry* entries, int32_t* status, mgs_plan_violation* first,
+                                     mgs_error* err);
+
+/* run_fluid: fluid-mode replay of `windows` consecutive windows of n_plans
+ * general plans (step_config / slot_tasks [i][w][s], psi_override
+ * [i][w][s][m] or NULL) against n_traces traces (arrivals [t][M][windows*S]);
+ * acc_pre/acc_post [w*M+m] (NULL with windows == 1: p's tables).
+ * out[((i*n_traces + t)*windows + w)*M + m] = per-window JobMetrics. */
+MGS_API int mgs_run_fluid(mgs_ctx* ctx, const mgs_problem* p, int32_t windows, const double* acc_pre,
+                          const double* acc_post, double step_seconds, const int32_t* step_config,
+                          const uint8_t* slot_tasks, int32_t n_plans, const double* psi_override,
+                          const int64_t* arrivals, int32_t n_traces, mgs_job_metrics* out, mgs_error* err);
 
 #ifdef __cplusplus
 }

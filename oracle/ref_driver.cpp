@@ -21,7 +21,7 @@
 //       plan_preinit + apply_preinit (preinit.hpp:41-114) of the window-0
 //       solve_dp plan: overrides, evaluate_plan total with them,
 //       overhead_summary, and run_requests of the EffectivePlan.
-//   migref drive <scenario.scn> <predictor>
+//   migref drive <scenario.scn> <predictor> [max_windows]
 //       the per-window planning loop from the reference's
 //       pieces: predict_arrivals (oracle for window 0) -> solve_dp with the
 //       carried final_ranges -> evaluate_plan on forecast and actual counts.
@@ -251,7 +251,8 @@ int cmd_drive(int argc, char** argv) {
     const int S = sc.window_size, M = static_cast<int>(sc.models.size());
     std::optional<std::map<TaskId, std::set<SlotRange>>> initial;
     std::string o = "{\"windows\":[";
-    for (int w = 0; w < sc.window_count; ++w) {
+    const int W = argc > 4 ? std::min(sc.window_count, std::atoi(argv[4])) : sc.window_count;
+    for (int w = 0; w < W; ++w) {
       ArrivalForecast actual = window_forecast(sc, w);
       ArrivalForecast fc;
       if (spec.kind == PredictorKind::Oracle || w == 0) {

@@ -15,7 +15,7 @@ from .capi import LIB_DIR, LIB_PATH, PKG_DIR
 
 ROOT = os.path.dirname(PKG_DIR)
 CSRC = os.path.join(PKG_DIR, "csrc")
-SOURCES = ["space.cu", "goodput.cu", "dp.cu", "dp2.cu", "bruteforce.cu", "table.cu", "wb.cu", "replay.cu", "preinit.cu", "scan.cu", "capi.cu"]
+SOURCES = ["space.cu", "goodput.cu", "dp.cu", "dp2.cu", "bruteforce.cu", "table.cu", "wb.cu", "replay.cu", "preinit.cu", "feasible.cu", "scan.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

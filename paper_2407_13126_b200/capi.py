@@ -72,6 +72,19 @@ class mgs_job_metrics(C.Structure):
                 ("reconfigurations", C.c_int32), ("overhead_seconds", C.c_double)]
 
 
+class mgs_plan_violation(C.Structure):
+    _fields_ = [("code", C.c_int32), ("step", C.c_int32), ("model", C.c_int32), ("detail", C.c_int32 * 3)]
+
+
+class mgs_score_entry(C.Structure):
+    _fields_ = [("throughput", C.c_double), ("overhead_loss", C.c_double), ("goodput", C.c_double),
+                ("completion", C.c_int32), ("pad", C.c_int32)]
+
+
+VIOLATION_FAMILIES = {1: "deployment-floor", 2: "retraining-not-launched", 3: "retraining-interrupted",
+                      4: "retraining-size", 5: "retraining-incomplete", 6: "retraining-overrun"}
+
+
 class mgs_stats(C.Structure):
     _fields_ = [("options", C.c_uint64), ("candidates", C.c_uint64), ("transitions_ref", C.c_uint64),
                 ("transitions", C.c_uint64), ("frontier_total", C.c_uint64), ("frontier_peak", C.c_uint64),
@@ -149,6 +162,14 @@ def load():
                                         P(C.c_double), C.c_double, P(C.c_int32),
                                         C.c_int32, P(C.c_uint8), P(C.c_int64), C.c_int32, P(C.c_uint64), C.c_int32,
                                         P(mgs_job_metrics), P(mgs_error)]
+    lib.mgs_check_feasible_batch.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_int32), P(C.c_uint8), C.c_int32,
+                                             P(mgs_plan_violation), C.c_int32, P(C.c_int32), P(mgs_error)]
+    lib.mgs_evaluate_views_batch.argtypes = [C.c_void_p, P(mgs_problem), P(C.c_int32), P(C.c_uint8), C.c_int32,
+                                             P(C.c_double), P(C.c_int64), C.c_int32, C.c_int32, P(C.c_double),
+                                             P(mgs_score_entry), P(C.c_int32), P(mgs_plan_violation), P(mgs_error)]
+    lib.mgs_run_fluid.argtypes = [C.c_void_p, P(mgs_problem), C.c_int32, P(C.c_double), P(C.c_double), C.c_double,
+                                  P(C.c_int32), P(C.c_uint8), C.c_int32, P(C.c_double), P(C.c_int64), C.c_int32,
+                                  P(mgs_job_metrics), P(mgs_error)]
     _LIB = lib
     return lib
 
@@ -156,7 +177,8 @@ def load():
 EXPORTED_SYMBOLS = ["mgs_open", "mgs_close", "mgs_status_code", "mgs_version", "mgs_set_stream", "mgs_enumerate",
                     "mgs_goodput_table", "mgs_solve_window", "mgs_solve_batch", "mgs_evaluate_batch",
                     "mgs_precheck", "mgs_bruteforce", "mgs_goodput_table_batch", "mgs_goodput_table_batch_device",
-                    "mgs_window_boundary", "mgs_replay_requests", "mgs_preinit"]
+                    "mgs_window_boundary", "mgs_replay_requests", "mgs_preinit", "mgs_check_feasible_batch",
+                    "mgs_evaluate_views_batch", "mgs_run_fluid"]
 
 
 def empty_error():

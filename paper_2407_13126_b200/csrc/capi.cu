@@ -111,6 +111,26 @@ void copy_plan_labels(Ctx& c, const mgs::DevSpace& sp, const std::vector<int32_t
   }
 }
 
+// the chosen plan's options, configurations, labels and objective packed for
+// one device->host copy: [S] int32 options | [S] int32 configs | [S][8] labels | total
+__global__ void k_gather_plan(const int32_t* opt_config, const int8_t* opt_labels, const int32_t* plan,
+                              const double* total, int S, uint8_t* out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < S) {
+    const int o = plan[s];
+    reinterpret_cast<int32_t*>(out)[s] = o;
+    reinterpret_cast<int32_t*>(out)[S + s] = opt_config[o];
+    for (int k = 0; k < MGS_MAX_SLOTS; ++k)
+      out[static_cast<size_t>(S) * 8 + static_cast<size_t>(s) * MGS_MAX_SLOTS + k] =
+          static_cast<uint8_t>(opt_labels[static_cast<size_t>(o) * MGS_MAX_SLOTS + k]);
+  }
+  if (s == 0) {
+    const double v = *total;
+    uint8_t* dst = out + static_cast<size_t>(S) * (8 + MGS_MAX_SLOTS);
+    for (int b = 0; b < 8; ++b) dst[b] = reinterpret_cast<const uint8_t*>(&v)[b];
+  }
+}
+
 void solve_one(Ctx& c, const mgs_problem& p, int32_t* out_option, int32_t* out_config, int8_t* out_labels,
                double* out_objective, mgs_stats* stats) {
   MGS_CUDA_OK(cudaEventRecord(c.ev0, c.stream));
@@ -137,28 +157,33 @@ void solve_one(Ctx& c, const mgs_problem& p, int32_t* out_option, int32_t* out_c
   } else {
     mgs::solve_dp(c, p, pr, sp, d_recv, d_ub, d_inc, out);
   }
-  // objective = evaluate_plan(...).total of the chosen plan, on the device
+  // objective = evaluate_plan(...).total of the chosen plan and the plan's
+  // configurations / labels, gathered on the device; one read-back of
+  // S*(4+4+8)+8 bytes for the whole solve
   c.phase(7);
   int32_t* d_plan = c.buf<int32_t>("plan_eval", S);
+  if (out.d_options) {
+    MGS_CUDA_OK(cudaMemcpyAsync(d_plan, out.d_options, S * 4, cudaMemcpyDeviceToDevice, c.stream));
+  } else {
+    MGS_CUDA_OK(cudaMemcpyAsync(d_plan, out.options.data(), S * 4, cudaMemcpyHostToDevice, c.stream));
+  }
   double* d_total = c.buf<double>("plan_total", 1);
-  MGS_CUDA_OK(cudaMemcpyAsync(d_plan, out.options.data(), S * 4, cudaMemcpyHostToDevice, c.stream));
   int64_t* d_arr = c.buf<int64_t>("forecast_i64", static_cast<size_t>(M) * S);
   mgs::evaluate_batch(c, pr, sp, d_plan, 1, d_arr, 1, d_total, nullptr, nullptr);
+  const size_t rb = static_cast<size_t>(S) * (4 + 4 + MGS_MAX_SLOTS) + 8;
+  uint8_t* d_rb = c.buf<uint8_t>("plan_readback", rb);
+  k_gather_plan<<<mgs::ceil_div(S, 128), 128, 0, c.stream>>>(sp.opt_config, sp.opt_labels, d_plan, d_total, S, d_rb);
+  ++c.kernel_launches;
+  uint8_t* h_rb = c.pinned.get<uint8_t>(rb);
+  MGS_CUDA_OK(cudaMemcpyAsync(h_rb, d_rb, rb, cudaMemcpyDeviceToHost, c.stream));
+  MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+  out.options.assign(reinterpret_cast<const int32_t*>(h_rb), reinterpret_cast<const int32_t*>(h_rb) + S);
+  const int32_t* h_cfg = reinterpret_cast<const int32_t*>(h_rb) + S;
+  const int8_t* h_lab = reinterpret_cast<const int8_t*>(h_rb + static_cast<size_t>(S) * 8);
   double total = 0.0;
-  MGS_CUDA_OK(cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, c.stream));
-  if (out_config || out_labels) {
-    std::vector<int32_t> cfg(sp.n_opt);
-    std::vector<int8_t> lab(static_cast<size_t>(sp.n_opt) * MGS_MAX_SLOTS);
-    MGS_CUDA_OK(cudaMemcpyAsync(cfg.data(), sp.opt_config, sp.n_opt * 4, cudaMemcpyDeviceToHost, c.stream));
-    MGS_CUDA_OK(cudaMemcpyAsync(lab.data(), sp.opt_labels, lab.size(), cudaMemcpyDeviceToHost, c.stream));
-    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
-    for (int s = 0; s < S; ++s) {
-      const int o = out.options[s];
-      if (out_config) out_config[s] = cfg[o];
-      if (out_labels)
-        for (int k = 0; k < MGS_MAX_SLOTS; ++k) out_labels[s * MGS_MAX_SLOTS + k] = lab[static_cast<size_t>(o) * MGS_MAX_SLOTS + k];
-    }
-  }
+  std::memcpy(&total, h_rb + static_cast<size_t>(S) * (8 + MGS_MAX_SLOTS), 8);
+  if (out_config) std::memcpy(out_config, h_cfg, static_cast<size_t>(S) * 4);
+  if (out_labels) std::memcpy(out_labels, h_lab, static_cast<size_t>(S) * MGS_MAX_SLOTS);
   c.phase(-1);
   MGS_CUDA_OK(cudaEventRecord(c.ev1, c.stream));
   MGS_CUDA_OK(cudaEventSynchronize(c.ev1));
@@ -640,6 +665,129 @@ int mgs_goodput_table_batch_device(mgs_ctx* ctx, const mgs_problem* p, const int
     Ctx& c = ctx->c;
     MGS_CUDA_OK(cudaSetDevice(c.device));
     table_batch(c, *p, d_arrivals, n_traces, d_best, d_ub_suffix, n_pareto);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// general per-step allocations (feasible.cu)
+int mgs_check_feasible_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* step_config, const uint8_t* slot_tasks,
+                             int32_t n_plans, mgs_plan_violation* out, int32_t cap, int32_t* n_out, mgs_error* err) {
+  if (!ctx || !p || n_plans < 0 || cap < 0) return MGS_ERR_ARGUMENT;
+  if (n_plans > 0 && (!step_config || !slot_tasks || !n_out || (cap > 0 && !out))) return MGS_ERR_ARGUMENT;
+  return guarded(err, [&] {
+    Ctx& c = ctx->c;
+    MGS_CUDA_OK(cudaSetDevice(c.device));
+    mgs::Prepared pr = prepare_problem(*p);  // input.scenario / input.catalog as Tables::build
+    if (n_plans == 0) return;
+    const int S = pr.t.S;
+    const mgs::ViewSet v = mgs::upload_views(c, p->lattice, pr, step_config, slot_tasks, static_cast<long long>(n_plans) * S);
+    const int cap1 = cap > 0 ? cap : 1;
+    mgs_plan_violation* d_out = c.buf<mgs_plan_violation>("cf_out", static_cast<size_t>(n_plans) * cap1);
+    int32_t* d_n = c.buf<int32_t>("cf_n", n_plans);
+    mgs::check_views(c, pr, v, n_plans, d_out, cap1, d_n);
+    if (cap > 0)
+      MGS_CUDA_OK(cudaMemcpyAsync(out, d_out, static_cast<size_t>(n_plans) * cap * sizeof(mgs_plan_violation),
+                                  cudaMemcpyDeviceToHost, c.stream));
+    MGS_CUDA_OK(cudaMemcpyAsync(n_out, d_n, static_cast<size_t>(n_plans) * 4, cudaMemcpyDeviceToHost, c.stream));
+    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int mgs_evaluate_views_batch(mgs_ctx* ctx, const mgs_problem* p, const int32_t* step_config, const uint8_t* slot_tasks,
+                             int32_t n_plans, const double* psi_override, const int64_t* arrivals, int32_t n_traces,
+                             int32_t verify, double* total, mgs_score_entry* entries, int32_t* status,
+                             mgs_plan_violation* first, mgs_error* err) {
+  if (!ctx || !p || n_plans < 0 || n_traces < 0) return MGS_ERR_ARGUMENT;
+  if (n_plans > 0 && (!step_config || !slot_tasks || (verify && !status))) return MGS_ERR_ARGUMENT;
+  if (static_cast<long long>(n_plans) * n_traces > 0 && (!arrivals || !total)) return MGS_ERR_ARGUMENT;
+  return guarded(err, [&] {
+    Ctx& c = ctx->c;
+    MGS_CUDA_OK(cudaSetDevice(c.device));
+    mgs::Prepared pr = prepare_problem(*p);
+    if (n_plans == 0) return;
+    const int M = pr.t.M, S = pr.t.S;
+    const mgs::ViewSet v = mgs::upload_views(c, p->lattice, pr, step_config, slot_tasks, static_cast<long long>(n_plans) * S);
+    std::vector<int32_t> nv;
+    std::vector<mgs_plan_violation> fv;
+    if (verify) {  // evaluate_plan(verify_feasibility = true): check_feasible first (evaluate.hpp:157-162)
+      mgs_plan_violation* d_out = c.buf<mgs_plan_violation>("ev_cf_out", n_plans);
+      int32_t* d_n = c.buf<int32_t>("ev_cf_n", n_plans);
+      mgs::check_views(c, pr, v, n_plans, d_out, 1, d_n);
+      nv.resize(n_plans);
+      fv.resize(n_plans);
+      MGS_CUDA_OK(cudaMemcpyAsync(nv.data(), d_n, static_cast<size_t>(n_plans) * 4, cudaMemcpyDeviceToHost, c.stream));
+      MGS_CUDA_OK(cudaMemcpyAsync(fv.data(), d_out, static_cast<size_t>(n_plans) * sizeof(mgs_plan_violation),
+                                  cudaMemcpyDeviceToHost, c.stream));
+    }
+    const long long n = static_cast<long long>(n_plans) * n_traces;
+    double* d_total = c.buf<double>("ev_total", std::max(1ll, n));
+    mgs_score_entry* d_ent = entries ? c.buf<mgs_score_entry>("ev_entries", std::max(1ll, n) * S * M) : nullptr;
+    double* d_psi = nullptr;
+    if (psi_override) {
+      d_psi = c.buf<double>("ev_psi", static_cast<size_t>(n_plans) * S * M);
+      MGS_CUDA_OK(cudaMemcpyAsync(d_psi, psi_override, static_cast<size_t>(n_plans) * S * M * 8, cudaMemcpyHostToDevice,
+                                  c.stream));
+    }
+    if (n > 0) {
+      int64_t* d_arr = c.buf<int64_t>("ev_arr", static_cast<size_t>(n_traces) * M * S);
+      MGS_CUDA_OK(cudaMemcpyAsync(d_arr, arrivals, static_cast<size_t>(n_traces) * M * S * 8, cudaMemcpyHostToDevice,
+                                  c.stream));
+      mgs::evaluate_views(c, pr, v, n_plans, d_psi, d_arr, n_traces, d_total, d_ent);
+      MGS_CUDA_OK(cudaMemcpyAsync(total, d_total, n * 8, cudaMemcpyDeviceToHost, c.stream));
+      if (entries)
+        MGS_CUDA_OK(cudaMemcpyAsync(entries, d_ent, static_cast<size_t>(n) * S * M * sizeof(mgs_score_entry),
+                                    cudaMemcpyDeviceToHost, c.stream));
+    }
+    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+    if (verify)
+      for (int i = 0; i < n_plans; ++i) {
+        status[i] = nv[i] ? MGS_ERR_PLAN_INFEASIBLE : MGS_OK;
+        if (first) first[i] = nv[i] ? fv[i] : mgs_plan_violation{};
+        if (nv[i])
+          for (int t = 0; t < n_traces; ++t) total[static_cast<size_t>(i) * n_traces + t] = 0.0;
+      }
+  });
+}
+
+int mgs_run_fluid(mgs_ctx* ctx, const mgs_problem* p, int32_t windows, const double* acc_pre, const double* acc_post,
+                  double step_seconds, const int32_t* step_config, const uint8_t* slot_tasks, int32_t n_plans,
+                  const double* psi_override, const int64_t* arrivals, int32_t n_traces, mgs_job_metrics* out,
+                  mgs_error* err) {
+  if (!ctx || !p || windows < 1 || n_plans < 0 || n_traces < 0) return MGS_ERR_ARGUMENT;
+  if ((acc_pre == nullptr) != (acc_post == nullptr) || (windows > 1 && !acc_pre)) return MGS_ERR_ARGUMENT;
+  const long long runs = static_cast<long long>(n_plans) * n_traces;
+  if (n_plans > 0 && (!step_config || !slot_tasks)) return MGS_ERR_ARGUMENT;
+  if (runs > 0 && (!arrivals || !out)) return MGS_ERR_ARGUMENT;
+  return guarded(err, [&] {
+    Ctx& c = ctx->c;
+    MGS_CUDA_OK(cudaSetDevice(c.device));
+    mgs::Prepared pr = prepare_problem(*p);
+    const int M = pr.t.M, S = pr.t.S, W = windows;
+    const size_t G = static_cast<size_t>(W) * S;
+    if (n_plans == 0) return;
+    const mgs::ViewSet v = mgs::upload_views(c, p->lattice, pr, step_config, slot_tasks, static_cast<long long>(n_plans) * G);
+    if (runs == 0) return;
+    std::vector<double> acc(static_cast<size_t>(W) * 2 * M);  // [W][pre|post][M]
+    for (int w = 0; w < W; ++w)
+      for (int m = 0; m < M; ++m) {
+        acc[(w * 2 + 0) * M + m] = acc_pre ? acc_pre[w * M + m] : p->tables.acc_pre[m];
+        acc[(w * 2 + 1) * M + m] = acc_post ? acc_post[w * M + m] : p->tables.acc_post[m];
+      }
+    double* d_acc = c.buf<double>("fl_acc", acc.size());
+    int64_t* d_arr = c.buf<int64_t>("fl_arr", static_cast<size_t>(n_traces) * M * G);
+    mgs_job_metrics* d_out = c.buf<mgs_job_metrics>("fl_out", static_cast<size_t>(runs) * W * M);
+    double* d_psi = nullptr;
+    if (psi_override) {
+      d_psi = c.buf<double>("fl_psi", static_cast<size_t>(n_plans) * G * M);
+      MGS_CUDA_OK(cudaMemcpyAsync(d_psi, psi_override, static_cast<size_t>(n_plans) * G * M * 8, cudaMemcpyHostToDevice,
+                                  c.stream));
+    }
+    MGS_CUDA_OK(cudaMemcpyAsync(d_acc, acc.data(), acc.size() * 8, cudaMemcpyHostToDevice, c.stream));
+    MGS_CUDA_OK(cudaMemcpyAsync(d_arr, arrivals, static_cast<size_t>(n_traces) * M * G * 8, cudaMemcpyHostToDevice, c.stream));
+    mgs::fluid_views(c, pr, W, v, n_plans, d_psi, d_acc, d_arr, n_traces, step_seconds, d_out);
+    MGS_CUDA_OK(cudaMemcpyAsync(out, d_out, static_cast<size_t>(runs) * W * M * sizeof(mgs_job_metrics),
+                                cudaMemcpyDeviceToHost, c.stream));
+    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));  // keeps `acc` alive until its copy has run
   });
 }
 

@@ -174,6 +174,7 @@ struct HostTables {
   long long rt[KM][8];
   int floor_[KM];
   double loss[KM];
+  double psi_raw[KM];  // profile psi in steps (overrides / spill replace it, not the loss fraction)
   double pre[KM], post[KM];
   long long min_rt[KM];
 };

@@ -216,6 +216,19 @@ void replay_requests(Ctx& c, const Prepared& pr, const DevSpace& sp, int W, cons
 // preinit.cu: plan_preinit + apply_preinit overrides [n_plans][S][M], fired [n_plans][S]
 void preinit_overrides(Ctx& c, const Prepared& pr, const DevSpace& sp, const mgs_lattice& lat, const int32_t* d_plans,
                        int n_plans, uint8_t* d_overrides, uint32_t* d_fired);
+// feasible.cu: plans as general per-step allocations (config + per-slot task bits)
+struct ViewSet {
+  void* views;  // device [n_steps] resolved steps
+  long long n;
+};
+ViewSet upload_views(Ctx& c, const mgs_lattice& lat, const Prepared& pr, const int32_t* config, const uint8_t* tasks,
+                     long long n_steps);
+void check_views(Ctx& c, const Prepared& pr, const ViewSet& v, int n_plans, mgs_plan_violation* d_out, int cap,
+                 int32_t* d_n);
+void evaluate_views(Ctx& c, const Prepared& pr, const ViewSet& v, int n_plans, const double* d_psi,
+                    const int64_t* d_arr, int n_traces, double* d_total, mgs_score_entry* d_entries);
+void fluid_views(Ctx& c, const Prepared& pr, int W, const ViewSet& v, int n_plans, const double* d_psi,
+                 const double* d_acc, const int64_t* d_arr, int n_traces, double step_seconds, mgs_job_metrics* d_out);
 // table.cu: batched ub table (Pareto placements prepared once per window shape)
 int table_prepare(Ctx& c, const Prepared& pr, const DevSpace& sp, double** wcp_out);
 void table_run(Ctx& c, const Prepared& pr, const double* wcp, int np, const int32_t* d_arr, int n_traces,
@@ -225,7 +238,8 @@ void goodput_reductions(Ctx& c, const Prepared& pr, const DevSpace& sp, const do
                         double* d_incumbent, int32_t* d_greedy);
 // dp.cu
 struct SolveOut {
-  std::vector<int32_t> options;
+  std::vector<int32_t> options;        // host copy (batched / multi-launch paths)
+  const int32_t* d_options = nullptr;  // device copy of the chosen options (device-resident engine)
   mgs_stats stats{};
 };
 void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& sp, const double* d_recv,
@@ -241,6 +255,7 @@ struct V2Lane {
   const double* ub = nullptr;
   const double* incumbent = nullptr;
   std::string prefix;  // the lane's buffer-name prefix
+  bool host_options = true;  // copy the chosen options to out.options (else only out.d_options)
   SolveOut out;
   int status = 0;      // mgs_status of this lane
   std::string msg;

@@ -113,7 +113,7 @@ struct V2 {
   int S;
   int has_initial;
   int dominance_ok;
-  double band;
+  const double* band;  // device scalar (k_band_value), so a solve needs no host round trip for it
   uint64_t budget;
   const double* recv;
   const double* ub;
@@ -167,6 +167,7 @@ struct V2 {
   int sc_big_ctas;               // CTAs of k_trans that may take big-group items
   int oi_bits;                   // bits of an option index (radix sort width)
   int merge_win;                 // placement window of the CTA merge table
+  int rank_words;                // 32-bit words of the option-index bitmap of k_ranks_big (0: does not fit)
   long long* dbg;                // [S][kDbg] per-step counters (debug dump)
   unsigned long long* dbg_time;  // barrier timestamps (debug)
 };
@@ -695,7 +696,44 @@ __device__ void phase_ranks_big(const V2& a, int s, unsigned long long* sm64) {
         if (i < c) F.rank[static_cast<uint32_t>(keys[k])] = base + i;
       }
       __syncthreads();
-    } else {  // beyond one CTA's sort: counting (rare, correct)
+    } else if (a.rank_words > 0) {
+      // beyond one CTA's sort (the root's children at step 1): the siblings'
+      // option indices are distinct, so a bitmap over option indices in shared
+      // memory and its word prefix popcounts give every rank in O(c + |O|/32)
+      uint32_t* bits = reinterpret_cast<uint32_t*>(sm64);
+      uint32_t* pre = bits + a.rank_words;
+      const int W = a.rank_words;
+      for (int w = threadIdx.x; w < W; w += kThreads) bits[w] = 0u;
+      __syncthreads();
+      for (int i = threadIdx.x; i < c; i += kThreads) {
+        const uint32_t oi = static_cast<uint32_t>(a.kid_items[base + i] >> 32);
+        atomicOr(&bits[oi >> 5], 1u << (oi & 31));
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {  // one warp: exclusive scan of the word popcounts
+        int run = 0;
+        for (int w0 = 0; w0 < W; w0 += 32) {
+          const int w = w0 + threadIdx.x;
+          const int v = w < W ? __popc(bits[w]) : 0;
+          int x = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (threadIdx.x >= o) x += y;
+          }
+          if (w < W) pre[w] = run + x - v;
+          run += __shfl_sync(0xffffffffu, x, 31);
+        }
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < c; i += kThreads) {
+        const unsigned long long me = a.kid_items[base + i];
+        const uint32_t oi = static_cast<uint32_t>(me >> 32);
+        const int pos = pre[oi >> 5] + __popc(bits[oi >> 5] & ((1u << (oi & 31)) - 1u));
+        F.rank[static_cast<uint32_t>(me)] = base + pos;
+      }
+      __syncthreads();
+    } else {  // counting (correct; only when the bitmap does not fit)
       for (int i = threadIdx.x; i < c; i += kThreads) {
         const unsigned long long me = a.kid_items[base + i];
         int pos = 0;
@@ -1137,7 +1175,7 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
   for (int w = blockIdx.x; w < nbig; w += gridDim.x) {
     const int id = a.ns_big[w];
     const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id], ub = a.ns_ubase[id], uc = a.ns_ucnt[id];
-    const double thresh = dsub(__longlong_as_double(static_cast<long long>(a.ns_vmax[id])), a.band);
+    const double thresh = dsub(__longlong_as_double(static_cast<long long>(a.ns_vmax[id])), *a.band);
     if (threadIdx.x == 0) s_cnt = 0;
     int mine = 0;
     if (uc == 1) {
@@ -1307,7 +1345,7 @@ __device__ void phase_write(const V2& a, int s) {
   for (int i = wid; i < nsm; i += nw) {
     const int id = a.ns_small[i];
     const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
-    const double thresh = dsub(__longlong_as_double(static_cast<long long>(a.ns_vmax[id])), a.band);
+    const double thresh = dsub(__longlong_as_double(static_cast<long long>(a.ns_vmax[id])), *a.band);
     int total = 0;
     for (int k0 = cb; k0 < cb + cc; k0 += 32) {
       const int k = k0 + lane;
@@ -1732,6 +1770,30 @@ __global__ void k_init_root(const V2* __restrict__ ap) {
   a.hist_base[1] = 0;
 }
 
+// band (solvers.hpp:258-267): 1e-9 + sum_m loss_m * cap_max_m * acc_max_m,
+// cap_max over the options' capabilities = over the placements'. One CTA.
+__global__ void k_band_value(const double* pl_cap, int P, HostTables t, double* band) {
+  __shared__ double s_max[KM][32];
+  double mx[KM] = {0.0, 0.0, 0.0, 0.0};
+  for (int q = threadIdx.x; q < P; q += blockDim.x)
+    for (int m = 0; m < t.M; ++m) mx[m] = fmax(mx[m], pl_cap[q * KM + m]);
+  for (int m = 0; m < KM; ++m) {
+    for (int o = 16; o > 0; o >>= 1) mx[m] = fmax(mx[m], __shfl_xor_sync(0xffffffffu, mx[m], o));
+    if ((threadIdx.x & 31) == 0) s_max[m][threadIdx.x >> 5] = mx[m];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 1e-9;
+    for (int m = 0; m < t.M; ++m) {
+      double cm = 0.0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) cm = fmax(cm, s_max[m][w]);
+      const double acc_max = t.pre[m] > t.post[m] ? t.pre[m] : t.post[m];
+      b = dadd(b, dmul(dmul(t.loss[m], cm), acc_max));
+    }
+    *band = b;
+  }
+}
+
 __global__ void k_sig_len(const int32_t* sig_off, int n_sig, int32_t* sig_len) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_sig; i += gridDim.x * blockDim.x)
     sig_len[i] = sig_off[i + 1] - sig_off[i];
@@ -1755,8 +1817,15 @@ bool solve_dp_v2_supported(const Prepared& pr, const DevSpace& sp) {
 
 namespace {
 
+// words of k_ranks_big's option-index bitmap (plus as many prefix counts);
+// 0 when the two arrays would not fit in shared memory
+int rank_words_of(long long n_opt) {
+  const long long w = (n_opt + 31) / 32;
+  return w * 8 <= 160 * 1024 ? static_cast<int>(w) : 0;
+}
+
 // Device buffers + scalars of one lane for the current capacities.
-V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, double band, int dominance_ok, int merge_win, int grid_term) {
+V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, int dominance_ok, int merge_win, int grid_term) {
   const DevSpace& sp = *L.sp;
   const HostTables& t = L.pr->t;
   const int S = t.S;
@@ -1768,7 +1837,12 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, double band, int dominan
   a.S = S;
   a.has_initial = L.pr->has_initial;
   a.dominance_ok = dominance_ok;
-  a.band = band;
+  {
+    double* d_band = c.buf<double>("v2_band", 1);
+    k_band_value<<<1, 256, 0, c.stream>>>(sp.pl_cap, sp.P, t, d_band);
+    ++c.kernel_launches;
+    a.band = d_band;
+  }
   a.budget = L.p->state_budget;
   a.recv = L.recv;
   a.ub = L.ub;
@@ -1874,6 +1948,7 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, double band, int dominan
   a.merge_win = merge_win;
   a.oi_bits = 1;
   while ((1ll << a.oi_bits) < sp.n_opt) ++a.oi_bits;
+  a.rank_words = rank_words_of(sp.n_opt);
   c.prefix = saved_prefix;
   return a;
 }
@@ -1887,32 +1962,21 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   for (const auto& L : lanes)
     if (L.pr->t.M != M || L.pr->t.S != S) throw PlanFail{MGS_ERR_ARGUMENT, "batched windows must share S and M"};
 
-  // per-lane scalars: band (solvers.hpp:258-267), dominance validity, tables' smem
-  std::vector<double> band(K);
+  // per-lane scalars: dominance validity, tables' smem (the band is computed
+  // on the device, k_band_value)
   std::vector<int> dom_ok(K), merge_win(K);
   size_t smem_merge = 0;
   for (int l = 0; l < K; ++l) {
     const HostTables& t = lanes[l].pr->t;
     const DevSpace& sp = *lanes[l].sp;
-    double acc_max[KM] = {0, 0, 0, 0};
     bool dominance_ok = true;
-    for (int m = 0; m < M; ++m) {
-      acc_max[m] = std::max(t.pre[m], t.post[m]);
-      dominance_ok = dominance_ok && t.post[m] >= t.pre[m];
-    }
-    std::vector<double> pc(static_cast<size_t>(sp.P) * KM);
-    MGS_CUDA_OK(cudaMemcpyAsync(pc.data(), sp.pl_cap, pc.size() * 8, cudaMemcpyDeviceToHost, c.stream));
-    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
-    double cap_max[KM] = {0, 0, 0, 0};
-    for (int q = 0; q < sp.P; ++q)
-      for (int m = 0; m < M; ++m) cap_max[m] = std::max(cap_max[m], pc[q * KM + m]);
-    band[l] = 1e-9;
-    for (int m = 0; m < M; ++m) band[l] += t.loss[m] * cap_max[m] * acc_max[m];
+    for (int m = 0; m < M; ++m) dominance_ok = dominance_ok && t.post[m] >= t.pre[m];
     dom_ok[l] = dominance_ok ? 1 : 0;
     merge_win[l] = std::min(sp.P1, 8192);  // whole placement range in one window when it fits
     smem_merge = std::max(smem_merge, static_cast<size_t>(2 * merge_win[l]) * 8);
   }
-  const size_t smem_rank = sizeof(typename cub::BlockRadixSort<unsigned long long, kThreads, kSortItems>::TempStorage);
+  size_t smem_rank = sizeof(typename cub::BlockRadixSort<unsigned long long, kThreads, kSortItems>::TempStorage);
+  for (int l = 0; l < K; ++l) smem_rank = std::max(smem_rank, static_cast<size_t>(rank_words_of(lanes[l].sp->n_opt)) * 8);
   auto ktbig = M == 1 ? k_trans_big<1> : k_trans_big<2>;
   auto ktsmall = M == 1 ? k_trans_small<1> : k_trans_small<2>;
   auto kunits = M == 1 ? k_units<1> : k_units<2>;
@@ -1952,7 +2016,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
                  g_tbig.x, g_tsmall.x, g_band.x, g_write.x, g_dom.x);
   for (int attempt = 0; attempt < 10; ++attempt) {
     std::vector<V2> args(K);
-    for (int l = 0; l < K; ++l) args[l] = lane_args(c, lanes[l], caps, band[l], dom_ok[l], merge_win[l], g_term.x);
+    for (int l = 0; l < K; ++l) args[l] = lane_args(c, lanes[l], caps, dom_ok[l], merge_win[l], g_term.x);
     V2* d_args = c.buf<V2>("v2_args", kMaxLanes);
     MGS_CUDA_OK(cudaMemcpyAsync(d_args, args.data(), sizeof(V2) * K, cudaMemcpyHostToDevice, c.stream));
     k_init_root<<<g_one, 32, 0, c.stream>>>(d_args);
@@ -1972,7 +2036,17 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_rank_fork = nullptr, ev_rank_join = nullptr;
     cudaEvent_t ev_rs_fork = nullptr, ev_rs_join = nullptr;
     cudaStream_t side2 = nullptr;
+    // MGS_STEP_TIMES (graph mode): an event node after every step, read back
+    // after the replay (per-step device time of the captured graph)
+    static std::vector<cudaEvent_t> step_ev;
+    static const bool step_times = std::getenv("MGS_STEP_TIMES") != nullptr;
+    if (step_times && !debug && static_cast<int>(step_ev.size()) < S + 1) {
+      for (auto e : step_ev) cudaEventDestroy(e);
+      step_ev.assign(S + 1, nullptr);
+      for (auto& e : step_ev) MGS_CUDA_OK(cudaEventCreate(&e));
+    }
     auto enqueue = [&](cudaStream_t st_, bool timed) {
+      if (!timed && !step_ev.empty()) MGS_CUDA_OK(cudaEventRecordWithFlags(step_ev[0], st_, cudaEventRecordExternal));
       const bool fork = fork_ok && !timed && side != nullptr;
       auto mark = [&]() {
         if (!timed) return;
@@ -2092,6 +2166,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         }
         k_dom<<<g_dom, kThreads, 0, st_>>>(d_args, st);
         after("dom", st);
+        if (!timed && !step_ev.empty()) MGS_CUDA_OK(cudaEventRecordWithFlags(step_ev[st + 1], st_, cudaEventRecordExternal));
       }
       k_term1<<<g_term, kThreads, 0, st_>>>(d_args);
       k_term2<<<g_term, kThreads, 0, st_>>>(d_args);
@@ -2107,10 +2182,17 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
       MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
       std::fprintf(stderr, "v2 host enqueue ms %.2f (eager, with events, %d lanes)\n", host_ms, K);
       double acc[kK] = {0};
+      std::vector<double> per_step(S, 0.0);
       for (size_t i = 1; i < evs.size(); ++i) {
         float ms = 0.f;
         MGS_CUDA_OK(cudaEventElapsedTime(&ms, evs[i - 1], evs[i]));
         acc[(i - 1) % kK] += ms;
+        if ((i - 1) / kK < static_cast<size_t>(S)) per_step[(i - 1) / kK] += ms;
+      }
+      if (std::getenv("MGS_STEP_TIMES")) {  // per-step device time (eager, serialised): floor + slope fit
+        std::fprintf(stderr, "v2 step_us");
+        for (int s = 0; s < S; ++s) std::fprintf(stderr, " %.1f", 1e3 * per_step[s]);
+        std::fprintf(stderr, "\n");
       }
       for (auto e : evs) cudaEventDestroy(e);
       std::fprintf(stderr, "v2 caps: fcap %d gcap %d ucap %d itcap %d ccap %d hbits %d hcap %lld\n", caps.fcap, caps.gcap,
@@ -2120,8 +2202,8 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
       std::fprintf(stderr, "\n");
     } else {
       char key[256];
-      std::snprintf(key, sizeof key, "v2:%d:%d:%d:%zu:%zu:%p", K, S, M, smem_merge, smem_rank,
-                    static_cast<void*>(d_args));
+      std::snprintf(key, sizeof key, "v2:%d:%d:%d:%zu:%zu:%p:%d", K, S, M, smem_merge, smem_rank,
+                    static_cast<void*>(d_args), step_ev.empty() ? 0 : 1);
       auto it = c.graphs.find(key);
       if (it == c.graphs.end()) {
         cudaStream_t cap;
@@ -2159,6 +2241,16 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         it = c.graphs.emplace(key, exec).first;
       }
       MGS_CUDA_OK(cudaGraphLaunch(it->second, c.stream));
+      if (!step_ev.empty()) {
+        MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+        std::fprintf(stderr, "v2 graph step_us");
+        for (int st = 0; st < S; ++st) {
+          float ms = 0.f;
+          MGS_CUDA_OK(cudaEventElapsedTime(&ms, step_ev[st], step_ev[st + 1]));
+          std::fprintf(stderr, " %.1f", 1e3 * ms);
+        }
+        std::fprintf(stderr, "\n");
+      }
     }
     MGS_CUDA_OK(cudaGetLastError());
     std::vector<Ctl> h(K);
@@ -2217,8 +2309,11 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         L.msg = "persistent DP: error " + std::to_string(hc.err_code);
         continue;
       }
-      L.out.options.resize(S);
-      MGS_CUDA_OK(cudaMemcpyAsync(L.out.options.data(), args[l].chosen, S * 4, cudaMemcpyDeviceToHost, c.stream));
+      L.out.d_options = args[l].chosen;
+      if (L.host_options) {
+        L.out.options.resize(S);
+        MGS_CUDA_OK(cudaMemcpyAsync(L.out.options.data(), args[l].chosen, S * 4, cudaMemcpyDeviceToHost, c.stream));
+      }
       L.out.stats.options = L.sp->n_opt;
       L.out.stats.candidates = L.sp->n_cand;
       L.out.stats.transitions_ref = hc.tr_ref;
@@ -2227,7 +2322,9 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
       L.out.stats.frontier_peak = hc.fpeak;
       L.out.stats.transition_bytes = hc.tbytes;
     }
-    MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+    bool any_host = false;
+    for (const auto& L : lanes) any_host = any_host || L.host_options;
+    if (any_host) MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
     return;
   }
   throw PlanFail{MGS_ERR_CUDA, "persistent DP: capacity growth did not converge"};
@@ -2244,9 +2341,10 @@ void solve_dp_v2(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpac
   L.ub = d_ub;
   L.incumbent = d_incumbent;
   L.prefix = c.prefix;
+  L.host_options = false;  // the caller reads the plan back together with its labels and objective
   solve_dp_v2_lanes(c, lanes);
   if (L.status != MGS_OK) throw PlanFail{L.status, L.msg, L.err_step, L.err_count};
-  out.options = std::move(L.out.options);
+  out.d_options = L.out.d_options;
   out.stats = L.out.stats;
 }
 

@@ -63,6 +63,7 @@ Prepared prepare_tables(const mgs_lattice& lat, const mgs_tables& tab) {
     }
     t.floor_[m] = tab.floor_gpcs[m];
     t.loss[m] = tab.psi[m] < 1.0 ? tab.psi[m] : 1.0;  // reconfig_loss_fraction, plan_types.hpp:68
+    t.psi_raw[m] = tab.psi[m];
     t.pre[m] = tab.acc_pre[m];
     t.post[m] = tab.acc_post[m];
     t.min_rt[m] = -1;  // space.hpp:79-83

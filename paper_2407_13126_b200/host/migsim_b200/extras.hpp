@@ -8,6 +8,10 @@
 //   b200::apply_preinit(ctx, seq)              == apply_preinit(ctx, seq, plan_preinit(cat, seq))
 //                                                                         preinit.hpp:41-114
 //   b200::run_requests(sc, plans, seed)        == run_requests           simulator.hpp:209-275
+//   b200::run_fluid(sc, plans)                 == run_fluid              simulator.hpp:171-203
+//                                                 (any allocation resolve_step reads)
+//   b200::check_feasible / b200::evaluate_plan == check_feasible / evaluate_plan
+//                                                 (evaluate_device.hpp) evaluate.hpp:55-210
 //   b200::evaluate_totals(ctx, seqs, traces, overrides)
 //                                              == evaluate_plan(...).total for plans x traces
 //                                                 (verify_feasibility = false)  evaluate.hpp:153-210
@@ -19,7 +23,9 @@
 
 #include "migsim/preinit.hpp"
 #include "migsim/simulator.hpp"
-#include "migsim/solvers.hpp"  // the drop-in: b200::context, b200::Problem, to_sequence
+#include "migsim/solvers.hpp"  // precheck_scenario (the drop-in's or the reference's)
+#include "migsim_b200/device.hpp"
+#include "migsim_b200/evaluate_device.hpp"
 
 namespace migsim::b200 {
 
@@ -180,6 +186,64 @@ inline std::vector<double> evaluate_totals(const PlanContext& ctx, const std::ve
                                     static_cast<int32_t>(traces.size()), totals.data(), nullptr, &err);
   if (st != MGS_OK) rethrow(st, err);
   return totals;
+}
+
+// run_fluid (simulator.hpp:171-203, build_series :72-131) on the device: the
+// plans are read as general allocations (PlanSteps), overrides as doubles.
+inline Metrics run_fluid(const Scenario& sc, const std::vector<EffectivePlan>& plans) {
+  const int W = static_cast<int>(plans.size());
+  if (W != sc.window_count) fail("input.plan", "plan count != window count");
+  PlanContext ctx0{&sc, 0, std::nullopt};
+  Problem pb(ctx0, nullptr, 4000000, 1);
+  const int S = pb.t.steps, M = pb.t.models;
+  PlanSteps steps;
+  std::vector<double> psi;
+  for (int w = 0; w < W; ++w) {
+    const auto& seq = plans[w].seq;
+    if (static_cast<int>(seq.allocations.size()) != S) fail("input.plan", "plan length != window size");
+    for (const auto& a : seq.allocations) steps.add(pb.t, sc.catalog, a);
+    if (!plans[w].overrides.empty() && psi.empty())
+      psi.assign(static_cast<size_t>(W) * S * M, std::numeric_limits<double>::quiet_NaN());
+    for (const auto& [key, v] : plans[w].overrides)
+      if (key.first >= 0 && key.first < M && key.second >= 0 && key.second < S)
+        psi[(static_cast<size_t>(w) * S + key.second) * M + key.first] = v;
+  }
+  std::vector<int64_t> arrivals(static_cast<size_t>(M) * W * S);
+  for (int m = 0; m < M; ++m)
+    for (int g = 0; g < W * S; ++g) arrivals[static_cast<size_t>(m) * W * S + g] = sc.trace.counts[m][g];
+  std::vector<double> acc_pre(static_cast<size_t>(W) * M), acc_post(static_cast<size_t>(W) * M);
+  for (int w = 0; w < W; ++w)
+    for (int m = 0; m < M; ++m) {
+      acc_pre[w * M + m] = sc.models[m].retraining.accuracy_pre[w];
+      acc_post[w * M + m] = sc.models[m].retraining.accuracy_post[w];
+    }
+  std::vector<mgs_job_metrics> out(static_cast<size_t>(W) * M);
+  mgs_error err{};
+  const int st = mgs_run_fluid(context(), &pb.p, W, acc_pre.data(), acc_post.data(), sc.step_seconds,
+                               steps.config.data(), steps.tasks.data(), 1, psi.empty() ? nullptr : psi.data(),
+                               arrivals.data(), 1, out.data(), &err);
+  if (st != MGS_OK) rethrow(st, err);
+  std::vector<WindowMetrics> windows;
+  for (int w = 0; w < W; ++w) {
+    WindowMetrics wm;
+    wm.window = w;
+    for (int m = 0; m < M; ++m) {
+      const mgs_job_metrics& r = out[static_cast<size_t>(w) * M + m];
+      JobMetrics j;
+      j.model = sc.models[m].profile.name;
+      j.received = r.received;
+      j.served = r.served;
+      j.timely = r.timely;
+      j.correct = r.correct;
+      j.valid = r.valid;
+      j.reconfigurations = r.reconfigurations;
+      j.overhead_seconds = r.overhead_seconds;
+      detail_sim::finalize_fractions(j);
+      wm.jobs.push_back(j);
+    }
+    windows.push_back(std::move(wm));
+  }
+  return detail_sim::assemble(sc, windows);
 }
 
 }  // namespace migsim::b200

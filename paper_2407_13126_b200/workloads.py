@@ -142,3 +142,27 @@ def c2_spec(seed: int, steps: int = 200, windows: int = 3, tenants: int = 4, vol
     spec = ScenarioSpec(ts, steps, windows)
     spec.counts = mmpp_trace([t.per_gpc for t in ts], steps * windows, seed)
     return spec
+
+
+def c5_specs(windows: int = 9, steps: int = 200, n_gpus: int = 8, seed0: int = 500001) -> list:
+    """Config 5: 8 physical A100 MIG GPUs x 7 slices, 16 tenants, 1800 slots.
+
+    The reference models exactly one 7-slice device (catalog.hpp:59-61) and at
+    most 4 tenants (space.hpp:49-50), so the box is decomposed the way SURVEY.md
+    §8(d) prescribes: tenants 2k and 2k+1 are pinned to physical GPU k, and each
+    GPU is an independent config-1-style two-tenant problem (ResNet-18 pair,
+    cap 40k / 50k, data_volume 3000, Poisson lambda 120 / 150, psi 0.5) over
+    `windows` windows of `steps` slots with explicit per-window accuracy lists
+    (drift resets accuracy every window), seed 500001 + k.
+    Each subproblem is bit-exact against the reference; the cross-GPU tenant
+    placement is fixed here (an extension, parity unpinned)."""
+    out = []
+    for k in range(n_gpus):
+        tenants = [
+            Tenant("g%d_r18a" % k, 40.0, [0.60] * windows, [0.90] * windows, data_volume=3000),
+            Tenant("g%d_r18b" % k, 50.0, [0.62] * windows, [0.89] * windows, data_volume=3000),
+        ]
+        spec = ScenarioSpec(tenants, steps, windows)
+        spec.counts = poisson_trace((120.0, 150.0), steps * windows, seed0 + k)
+        out.append(spec)
+    return out

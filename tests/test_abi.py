@@ -54,9 +54,12 @@ def test_open_without_gpu_fails_loudly():
 @pytest.mark.skipif(not os.path.isdir(REF), reason="reference headers not mounted")
 def test_dropin_header_compiles_against_reference(tmp_path):
     src = tmp_path / "t.cpp"
-    src.write_text('#include "migsim/solvers.hpp"\n#include "migsim/baselines.hpp"\n'
+    src.write_text('#include "migsim/solvers.hpp"\n#include "migsim/baselines.hpp"\n#include "migsim/simulator.hpp"\n'
+                   '#include "migsim_b200/extras.hpp"\n'
+                   "static_assert(sizeof(migsim::b200::PlanSteps) > 0);\n"
                    "int main() { migsim::SolveOptions o; return o.workers - 1; }\n")
-    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "paper_2407_13126_b200", "host"),
+    host = os.path.join(ROOT, "paper_2407_13126_b200", "host")
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(host, "dropin"), "-I", host,
                         "-I", os.path.join(ROOT, "include"), "-I", REF + "/include", str(src)],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-3000:]
