@@ -114,16 +114,17 @@ class WindowPlan:
     initial: list | None      # the carried-over ranges this window was planned with
 
 
-def plan_scenarios(planner, scenarios, predictor="oracle"):
-    """Plans every window of every scenario; returns [[WindowPlan per window] per scenario].
-    Scenarios must share window_count; each window index is one batched solve."""
+def plan_scenarios(planner, scenarios, predictor="oracle", max_windows=None):
+    """Plans every window (or the first max_windows) of every scenario; returns
+    [[WindowPlan per window] per scenario]. Scenarios must share window_count;
+    each window index is one batched solve."""
     spec = parse_predictor(predictor)
     W = scenarios[0].window_count
     if any(sc.window_count != W for sc in scenarios):
         raise ValueError("batched scenarios must have the same window count")
     out = [[] for _ in scenarios]
     initial = [None] * len(scenarios)
-    for w in range(W):
+    for w in range(W if max_windows is None else min(W, max_windows)):
         probs, fcs = [], []
         for i, sc in enumerate(scenarios):
             S = sc.window_size

@@ -44,3 +44,28 @@ def combine_best(objective: float, rank: int, world: int, device="cpu"):
     if world > 1:
         dist.all_reduce(owner, op=dist.ReduceOp.MIN)
     return key_objective(best), int(owner.item())
+
+
+def gather_rows(rows, world: int, device="cpu"):
+    """All-gather of each rank's int64 rows (a list of equal-width lists; ranks may
+    hold different row counts). Returns the rows of every rank, rank-major. Over
+    NCCL this is two all_gathers on NVLink (counts, then the padded rows)."""
+    import torch
+    import torch.distributed as dist
+    width = len(rows[0]) if rows else 0
+    if world == 1:
+        return [list(map(int, r)) for r in rows]
+    meta = torch.tensor([len(rows), width], dtype=torch.int64, device=device)
+    metas = [torch.zeros_like(meta) for _ in range(world)]
+    dist.all_gather(metas, meta)
+    n_max = max(int(m[0]) for m in metas)
+    width = max(int(m[1]) for m in metas)
+    buf = torch.zeros((max(1, n_max), max(1, width)), dtype=torch.int64, device=device)
+    if rows:
+        buf[:len(rows), :len(rows[0])] = torch.tensor(rows, dtype=torch.int64, device=device)
+    bufs = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(bufs, buf)
+    out = []
+    for m, b in zip(metas, bufs):
+        out.extend(b[:int(m[0]), :width].tolist())
+    return out
