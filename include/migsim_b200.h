@@ -27,6 +27,9 @@
  *   mgs_evaluate_views_batch evaluate_plan (any allocation, verify optional)
  *                                                      evaluate.hpp:25-47,153-210
  *   mgs_run_fluid      run_fluid (+ build_series)      simulator.hpp:72-131,171-203
+ *   mgs_shard_*, mgs_solve_batch_sharded: one process per GPU over NCCL
+ *                      (no reference analogue: the reference is single-node,
+ *                      single-process)
  */
 #ifndef MIGSIM_B200_H
 #define MIGSIM_B200_H
@@ -321,6 +324,29 @@ MGS_API int mgs_run_fluid(mgs_ctx* ctx, const mgs_problem* p, int32_t windows, c
                           const double* acc_post, double step_seconds, const int32_t* step_config,
                           const uint8_t* slot_tasks, int32_t n_plans, const double* psi_override,
                           const int64_t* arrivals, int32_t n_traces, mgs_job_metrics* out, mgs_error* err);
+
+/* ---- multi-GPU sharding over NCCL (one process per GPU) ----------------
+ * NCCL is loaded at run time (libnccl.so.2). A context holds one
+ * communicator: create it with mgs_shard_init (rank 0 calls
+ * mgs_nccl_unique_id and shares the bytes with the other ranks out of band),
+ * or attach a caller-owned ncclComm_t with mgs_shard_attach. Collectives run
+ * on the context's stream. */
+#define MGS_NCCL_ID_BYTES 128
+MGS_API int mgs_nccl_unique_id(uint8_t* id /* [MGS_NCCL_ID_BYTES] */);
+MGS_API int mgs_shard_init(mgs_ctx* ctx, int32_t world, int32_t rank, const uint8_t* id, mgs_error* err);
+MGS_API int mgs_shard_attach(mgs_ctx* ctx, void* nccl_comm, int32_t world, int32_t rank);
+/* recv[world*n] = every rank's n values, rank-major */
+MGS_API int mgs_shard_allgather_i64(mgs_ctx* ctx, const int64_t* send, int64_t n, int64_t* recv, mgs_error* err);
+/* per-shard best: *best = max objective over the ranks (objective >= 0),
+ * *owner = lowest rank holding it (all-reduce(max) of the order-preserving
+ * bits, then all-reduce(min) of the owner) */
+MGS_API int mgs_shard_best(mgs_ctx* ctx, double objective, double* best, int32_t* owner, mgs_error* err);
+/* mgs_solve_batch over the ranks: every rank passes all n windows; rank r
+ * solves [n*r/world, n*(r+1)/world) and the (status, objective, plan) rows are
+ * all-gathered, so every rank returns all n results. Without a communicator
+ * it solves all n windows locally. */
+MGS_API int mgs_solve_batch_sharded(mgs_ctx* ctx, const mgs_problem* problems, int32_t n, int32_t s_max,
+                                    int32_t* out_option, double* out_objective, int32_t* status, mgs_error* err);
 
 #ifdef __cplusplus
 }

@@ -21,7 +21,7 @@
 //       plan_preinit + apply_preinit (preinit.hpp:41-114) of the window-0
 //       solve_dp plan: overrides, evaluate_plan total with them,
 //       overhead_summary, and run_requests of the EffectivePlan.
-//   migref drive <scenario.scn> <predictor> [max_windows]
+//   migref drive <scenario.scn> <predictor> [max_windows] [lookback] [psi]
 //       the per-window planning loop from the reference's
 //       pieces: predict_arrivals (oracle for window 0) -> solve_dp with the
 //       carried final_ranges -> evaluate_plan on forecast and actual counts.
@@ -252,6 +252,10 @@ int cmd_drive(int argc, char** argv) {
     std::optional<std::map<TaskId, std::set<SlotRange>>> initial;
     std::string o = "{\"windows\":[";
     const int W = argc > 4 ? std::min(sc.window_count, std::atoi(argv[4])) : sc.window_count;
+    // sliding lookahead: the predictor sees only the last `lookback` windows
+    const int lookback = argc > 5 ? std::atoi(argv[5]) : (1 << 30);
+    if (argc > 6)  // reconfiguration-cost sweep point: every tenant's psi
+      for (auto& e : sc.models) e.profile.reconfig_overhead = std::atof(argv[6]);
     for (int w = 0; w < W; ++w) {
       ArrivalForecast actual = window_forecast(sc, w);
       ArrivalForecast fc;
@@ -259,8 +263,10 @@ int cmd_drive(int argc, char** argv) {
         fc = predict_arrivals(PredictorSpec{}, {}, S, S, &actual.counts);
       } else {
         std::vector<std::vector<long long>> history(M);
+        const int from = std::max(0, w - lookback);
         for (int m = 0; m < M; ++m)
-          history[m].assign(sc.trace.counts[m].begin(), sc.trace.counts[m].begin() + static_cast<long>(w) * S);
+          history[m].assign(sc.trace.counts[m].begin() + static_cast<long>(from) * S,
+                            sc.trace.counts[m].begin() + static_cast<long>(w) * S);
         fc = predict_arrivals(spec, history, S, S, &actual.counts);
       }
       PlanContext ctx{&sc, w, initial};

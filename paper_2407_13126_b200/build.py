@@ -15,7 +15,7 @@ from .capi import LIB_DIR, LIB_PATH, PKG_DIR
 
 ROOT = os.path.dirname(PKG_DIR)
 CSRC = os.path.join(PKG_DIR, "csrc")
-SOURCES = ["space.cu", "goodput.cu", "dp.cu", "dp2.cu", "bruteforce.cu", "table.cu", "wb.cu", "replay.cu", "preinit.cu", "feasible.cu", "scan.cu", "capi.cu"]
+SOURCES = ["space.cu", "goodput.cu", "dp.cu", "dp2.cu", "bruteforce.cu", "table.cu", "wb.cu", "replay.cu", "preinit.cu", "feasible.cu", "shard.cu", "scan.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [
@@ -52,7 +52,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             subprocess.run(cmd, check=True)
     if force or _stale(LIB_PATH, objs):
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB_PATH] + objs + \
-              ["-Xcompiler", "-fPIC", "-cudart", "static"]
+              ["-Xcompiler", "-fPIC", "-cudart", "static", "-ldl"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)

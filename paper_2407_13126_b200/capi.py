@@ -170,6 +170,13 @@ def load():
     lib.mgs_run_fluid.argtypes = [C.c_void_p, P(mgs_problem), C.c_int32, P(C.c_double), P(C.c_double), C.c_double,
                                   P(C.c_int32), P(C.c_uint8), C.c_int32, P(C.c_double), P(C.c_int64), C.c_int32,
                                   P(mgs_job_metrics), P(mgs_error)]
+    lib.mgs_nccl_unique_id.argtypes = [P(C.c_uint8)]
+    lib.mgs_shard_init.argtypes = [C.c_void_p, C.c_int32, C.c_int32, P(C.c_uint8), P(mgs_error)]
+    lib.mgs_shard_attach.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]
+    lib.mgs_shard_allgather_i64.argtypes = [C.c_void_p, P(C.c_int64), C.c_int64, P(C.c_int64), P(mgs_error)]
+    lib.mgs_shard_best.argtypes = [C.c_void_p, C.c_double, P(C.c_double), P(C.c_int32), P(mgs_error)]
+    lib.mgs_solve_batch_sharded.argtypes = [C.c_void_p, P(mgs_problem), C.c_int32, C.c_int32, P(C.c_int32),
+                                            P(C.c_double), P(C.c_int32), P(mgs_error)]
     _LIB = lib
     return lib
 
@@ -178,7 +185,8 @@ EXPORTED_SYMBOLS = ["mgs_open", "mgs_close", "mgs_status_code", "mgs_version", "
                     "mgs_goodput_table", "mgs_solve_window", "mgs_solve_batch", "mgs_evaluate_batch",
                     "mgs_precheck", "mgs_bruteforce", "mgs_goodput_table_batch", "mgs_goodput_table_batch_device",
                     "mgs_window_boundary", "mgs_replay_requests", "mgs_preinit", "mgs_check_feasible_batch",
-                    "mgs_evaluate_views_batch", "mgs_run_fluid"]
+                    "mgs_evaluate_views_batch", "mgs_run_fluid", "mgs_nccl_unique_id", "mgs_shard_init",
+                    "mgs_shard_attach", "mgs_shard_allgather_i64", "mgs_shard_best", "mgs_solve_batch_sharded"]
 
 
 def empty_error():

@@ -6,11 +6,10 @@
 #include <cstdio>
 #include <new>
 
+#include <functional>
+
 #include "ctx.cuh"
 
-struct mgs_ctx {
-  mgs::Ctx c;
-};
 
 namespace mgs {
 bool solve_dp_v2_supported(const Prepared& pr, const DevSpace& sp);
@@ -199,6 +198,9 @@ void solve_one(Ctx& c, const mgs_problem& p, int32_t* out_option, int32_t* out_c
 }
 
 }  // namespace
+
+// the same exception-to-status mapping for the other translation units (shard.cu)
+int mgs_guarded_call(mgs_error* err, const std::function<void()>& f) { return guarded(err, f); }
 
 extern "C" {
 
@@ -462,6 +464,12 @@ int mgs_solve_window(mgs_ctx* ctx, const mgs_problem* p, int32_t* out_option, in
 int mgs_solve_batch(mgs_ctx* ctx, const mgs_problem* problems, int32_t n, int32_t s_max, int32_t* out_option,
                     double* out_objective, int32_t* status, mgs_stats* stats, mgs_error* errs) {
   if (!ctx || (!problems && n > 0) || n < 0) return MGS_ERR_ARGUMENT;
+  // every window starts out failed: a call that stops early (CUDA error,
+  // capacity growth not converging) never leaves a status unwritten
+  for (int i = 0; i < n; ++i) {
+    if (status) status[i] = MGS_ERR_CUDA;
+    if (errs) fill_err(&errs[i], MGS_ERR_CUDA, "not solved: the batch call failed before this window");
+  }
   return guarded(nullptr, [&] {
     Ctx& c = ctx->c;
     MGS_CUDA_OK(cudaSetDevice(c.device));

@@ -129,6 +129,9 @@ struct PhaseTimer {
   }
 };
 
+struct Ctx;
+void shard_release(Ctx& c);  // shard.cu: destroys an owned NCCL communicator
+
 struct Ctx {
   int device = 0;
   int sm_count = 148;
@@ -176,7 +179,12 @@ struct Ctx {
   T* buf(const char* name, size_t n) {
     return bufs[prefix + name].get<T>(n);
   }
+  // multi-GPU sharding (shard.cu): this rank's NCCL communicator
+  void* nccl_comm = nullptr;
+  bool own_comm = false;
+  int world = 1, rank = 0;
   ~Ctx() {
+    shard_release(*this);
     for (auto& kv : bufs) kv.second.release();
     history.release();
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
@@ -187,6 +195,15 @@ struct Ctx {
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 };
+
+}  // namespace mgs
+
+// the opaque handle of the C ABI
+struct mgs_ctx {
+  mgs::Ctx c;
+};
+
+namespace mgs {
 
 // Host-side derived inputs of one window (engine::Tables + initial masks).
 struct Prepared {

@@ -195,6 +195,53 @@ class Planner:
             raise capi.PlannerError(st)
         return opts, obj, status, [s.as_dict() for s in stats], errs
 
+    # -- multi-GPU sharding over NCCL (C ABI, one process per GPU) --------------
+    def shard_init(self, world: int, rank: int, nccl_id: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        err = capi.empty_error()
+        st = self.lib.mgs_shard_init(self.h, world, rank, buf, C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+
+    def nccl_unique_id(self) -> bytes:
+        buf = (C.c_uint8 * 128)()
+        st = self.lib.mgs_nccl_unique_id(buf)
+        if st:
+            raise capi.PlannerError(st)
+        return bytes(buf)
+
+    def shard_allgather(self, values, world: int):
+        v = np.ascontiguousarray(values, np.int64)
+        out = np.zeros(v.size * world, np.int64)
+        err = capi.empty_error()
+        st = self.lib.mgs_shard_allgather_i64(self.h, capi.ptr(v, C.c_int64), v.size, capi.ptr(out, C.c_int64),
+                                              C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        return out.reshape(world, v.size)
+
+    def shard_best(self, objective: float):
+        best, owner = C.c_double(), C.c_int32()
+        err = capi.empty_error()
+        st = self.lib.mgs_shard_best(self.h, objective, C.byref(best), C.byref(owner), C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        return best.value, owner.value
+
+    def solve_batch_sharded(self, problems):
+        n = len(problems)
+        s_max = max(p.S for p in problems)
+        arr = (capi.mgs_problem * n)(*[p.c for p in problems])
+        opts = np.full((n, s_max), -1, np.int32)
+        obj = np.zeros(n, np.float64)
+        status = np.zeros(n, np.int32)
+        err = capi.empty_error()
+        st = self.lib.mgs_solve_batch_sharded(self.h, arr, n, s_max, capi.ptr(opts, C.c_int32),
+                                              capi.ptr(obj, C.c_double), capi.ptr(status, C.c_int32), C.byref(err))
+        if st:
+            raise capi.PlannerError(st, err)
+        return opts, obj, status
+
     # -- ub_suffix table for a batch of traces (configs 2/4) ---------------------
     def goodput_table_batch(self, problem: Problem, arrivals, with_best=False):
         """arrivals int32 [n][M][S] (host). Returns ub [n][S+1] (and best [n][S])

@@ -166,3 +166,33 @@ def c5_specs(windows: int = 9, steps: int = 200, n_gpus: int = 8, seed0: int = 5
         spec.counts = poisson_trace((120.0, 150.0), steps * windows, seed0 + k)
         out.append(spec)
     return out
+
+
+H100_LATTICE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "h100.catalog")
+C3_PSI_SWEEP = (0.0, 0.25, 0.5, 1.0, 6.0)
+
+
+def c3_specs(windows: int = 18, steps: int = 200, seed: int = 300000) -> list:
+    """Config 3: 6 tenants on the H100-80GB 7-slice lattice (data/h100.catalog),
+    3600 slots = 18 windows x 200, MMPP arrivals, reconfiguration-cost sweep.
+
+    The reference plans at most 4 tenants on one device (space.hpp:49-50), and
+    under the SURVEY.md §8(d) generator (RT = ceil(240/k), so a 1-GPC retraining
+    never fits a 200-slot window) six tenants cannot share one 7-slice GPU at
+    all: six inference slots leave one slice. The six tenants are therefore
+    planned as three two-tenant pairs, each on its own H100 lattice (pairs
+    ResNet-50 + MobileNetV2, ViT-B + BERT-base, Inception-v3 + ConvNeXt-base),
+    per-window decisions bit-exact against the reference; the 6-tenant joint
+    problem itself is unpinned. Each pair's trace is its own MMPP stream
+    (seed + pair index)."""
+    table = [("resnet50", 40.0, 0.55, 0.85, 4.09), ("mobilenetv2", 120.0, 0.70, 0.80, 0.32),
+             ("vitb", 12.0, 0.60, 0.88, 17.56), ("bertbase", 10.0, 0.50, 0.83, 22.2),
+             ("inceptionv3", 30.0, 0.65, 0.86, 5.7), ("convnextbase", 12.0, 0.58, 0.84, 15.4)]
+    out = []
+    for k in range(3):
+        ts = [Tenant(n, c, [pre] * windows, [post] * windows, data_volume=int(80 * c), gflops=g, psi=0.5)
+              for (n, c, pre, post, g) in table[2 * k:2 * k + 2]]
+        spec = ScenarioSpec(ts, steps, windows, catalog_path=H100_LATTICE)
+        spec.counts = mmpp_trace([t.per_gpc for t in ts], steps * windows, seed + k)
+        out.append(spec)
+    return out

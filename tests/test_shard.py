@@ -52,3 +52,29 @@ def test_combine_best_gloo_world2(objectives, expect):
     out = mgr.dict()
     mp.spawn(_worker, args=(2, _free_port(), objectives, out), nprocs=2, join=True)
     assert out[0] == expect and out[1] == expect
+
+
+@pytest.mark.gpu
+def test_nccl_shard_path_single_rank(golden_dir):
+    """The C-ABI NCCL path on one GPU (a real one-rank communicator): all-gather,
+    per-shard best, and the sharded batch solve equal the local batch solve."""
+    import numpy as np
+    from golden_util import bits
+    from paper_2407_13126_b200 import planner
+    from paper_2407_13126_b200 import scenario as SC
+    cases = golden_dir["random"][:6] + [c for c in golden_dir["c1"] if "S24" in c[0]]
+    probs = [SC.Problem(SC.load_scenario(path), 0) for _, path, _ in cases]
+    with planner.Planner(0) as pl:
+        pl.shard_init(1, 0, pl.nccl_unique_id())
+        got = pl.shard_allgather([1, -2, 3], 1)
+        assert got.tolist() == [[1, -2, 3]]
+        assert pl.shard_best(12.5) == (12.5, 0)
+        opts, obj, status = pl.solve_batch_sharded(probs)
+        ref_opts, ref_obj, ref_status, _, _ = pl.solve_batch(probs)
+    assert (status == ref_status).all() and (status == 0).all()
+    assert np.array_equal(opts, ref_opts)
+    assert [bits(x) for x in obj] == [bits(x) for x in ref_obj]
+    for (stem, _, g), o in zip(cases, obj):
+        want = g.get("dp", {}).get("obj")
+        if want:
+            assert bits(o) == want, stem
