@@ -1148,7 +1148,10 @@ __device__ __forceinline__ void write_state(const V2& a, int s, int nxt, int q, 
   const int parent = a.c_parent[k];
   const long long h = a.hist_base[s + 1] + q;
   const uint32_t ids = static_cast<uint32_t>(a.sp.pl_ids[p]);
-  const int slot = a.dominance_ok ? atomicAdd(&a.pcnt[p], 1) : 64;
+  // dominance buckets of more than 64 states are skipped (solvers.hpp:521), and a
+  // bucket count only grows within the step: once a (possibly stale) read shows
+  // more than 64, the bucket is dead and its atomic can be skipped
+  const int slot = a.dominance_ok && a.pcnt[p] <= 64 ? atomicAdd(&a.pcnt[p], 1) : 64;
   N.status[q] = key;
   N.ids[q] = ids;
   N.pid[q] = p;
