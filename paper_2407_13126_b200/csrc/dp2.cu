@@ -103,7 +103,8 @@ struct Ctl {
   unsigned long long tr_ref, tr, ftot, fpeak, tbytes;
   unsigned long long best_vb, best_lex;
   int best_idx;
-  int ranks_prev[2];  // [s&1]: live states of F_{s-1}, the parent-rank space of F_s
+  int ranks_prev[2];  // [s&1]: stored states of F_{s-1}, the parent-rank space of F_s
+  int dead[2];        // [x]: states of the frontier of parity x killed by dominance (k_dom)
   int scan_total[kNumScans];
 };
 
@@ -633,16 +634,19 @@ __device__ void phase_kid_fill(const V2& a, int s) {
   StepCounters& sc = a.ctl->sc[s & 1];
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const FrontierV2& F = a.f[cur];
-  const int n = a.ctl->n_store[cur];
+  // every stored state, live or dominated: ranks over the stored states order
+  // the live ones exactly like dense ranks over the live ones, and they do not
+  // wait for k_dom (this branch runs beside it)
+  const int n = s == 0 ? a.ctl->n_store[0] : a.ctl->sc[(s - 1) & 1].out_states;
   const int lane = threadIdx.x & 31;
-  // software-pipelined: the next state's alive flag and lex are loaded ahead
+  // software-pipelined: the next state's lex is loaded ahead
   int i0 = gtid - lane;
-  bool al = i0 + lane < n && F.alive[i0 + lane];
+  bool al = i0 + lane < n;
   uint64_t lx_c = al ? F.lex[i0 + lane] : 0;
   for (; i0 < n; i0 += gstride) {  // warp-uniform trip count
     const int i = i0 + lane;
     const int in = i + gstride;
-    const bool al_n = in < n && F.alive[in];
+    const bool al_n = in < n;
     const uint64_t lx_n = al_n ? F.lex[in] : 0;
     bool big_first = false;
     int pr = 0;
@@ -1138,14 +1142,12 @@ __device__ void phase_trans_small(const V2& a, int s) {
 
 // ---------------------------------------------------------------------------
 // S6: merge + band + output
-__device__ __forceinline__ void write_state(const V2& a, int s, int nxt, int q, int gidx, uint32_t key, int k) {
+// One survivor into F_{s+1} (state q of group gidx), from its candidate's
+// already-loaded fields. The two dependent lookups (placement ids, bucket
+// atomic) are issued before the first store.
+__device__ __forceinline__ void write_state_v(const V2& a, int s, int nxt, int q, int gidx, uint32_t key, int p,
+                                              uint64_t lx, double v, int parent) {
   const FrontierV2& N = a.f[nxt];
-  // every load (and the bucket atomic) is issued before the first store: the
-  // compiler cannot move loads across stores it cannot prove disjoint
-  const int p = a.c_pid[k];
-  const uint64_t lx = a.c_lex[k];
-  const double v = a.c_value[k];
-  const int parent = a.c_parent[k];
   const long long h = a.hist_base[s + 1] + q;
   const uint32_t ids = static_cast<uint32_t>(a.sp.pl_ids[p]);
   // dominance buckets of more than 64 states are skipped (solvers.hpp:521), and a
@@ -1162,6 +1164,16 @@ __device__ __forceinline__ void write_state(const V2& a, int s, int nxt, int q, 
   a.h_parent[h] = parent;
   a.h_oi[h] = static_cast<int32_t>(lx & 0xffffffffu);
   if (slot < 64) a.pbucket[p * 64 + slot] = q;
+}
+
+__device__ __forceinline__ void write_state(const V2& a, int s, int nxt, int q, int gidx, uint32_t key, int k) {
+  // every load is issued before the first store: the compiler cannot move
+  // loads across stores it cannot prove disjoint
+  const int p = a.c_pid[k];
+  const uint64_t lx = a.c_lex[k];
+  const double v = a.c_value[k];
+  const int parent = a.c_parent[k];
+  write_state_v(a, s, nxt, q, gidx, key, p, lx, v, parent);
 }
 
 // S6a: equal-key merge (multi-unit statuses) + band + survivor count per status
@@ -1342,42 +1354,98 @@ __device__ void phase_write(const V2& a, int s) {
     __syncthreads();
   }
   // small statuses (single unit, <= kBigNs candidates, so no merge): a warp
-  // each applies the band, claims its range with one atomic and writes
+  // each applies the band, claims its range with one atomic and writes. The
+  // next status's metadata is loaded while this one is processed, and a
+  // status of at most 32 candidates is done in one pass with every candidate
+  // field loaded up front.
   const int nsm = sc.n_small;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const double band = *a.band;
+  int id = 0, cb = 0, cc = 0;
+  unsigned long long vm = 0;
+  uint32_t hk = 0;
+  if (wid < nsm) {
+    id = a.ns_small[wid];
+    cb = a.ns_cbase[id];
+    cc = a.ns_ccnt[id];
+    vm = a.ns_vmax[id];
+    hk = a.hash[id];
+  }
   for (int i = wid; i < nsm; i += nw) {
-    const int id = a.ns_small[i];
-    const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
-    const double thresh = dsub(__longlong_as_double(static_cast<long long>(a.ns_vmax[id])), *a.band);
-    int total = 0;
-    for (int k0 = cb; k0 < cb + cc; k0 += 32) {
-      const int k = k0 + lane;
-      total += __popc(__ballot_sync(0xffffffffu, k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh));
-    }
-    if (total == 0) continue;  // uniform
-    int q0 = 0, gi = 0, ok = 0;
-    if (lane == 0) {
-      q0 = atomicAdd(&sc.out_states, total);
-      gi = atomicAdd(&sc.out_groups, 1);
-      ok = claim_fits(a, s, q0, total, gi) ? 1 : 0;
-    }
-    if (!__shfl_sync(0xffffffffu, ok, 0)) continue;
-    q0 = __shfl_sync(0xffffffffu, q0, 0);
-    gi = __shfl_sync(0xffffffffu, gi, 0);
-    const uint32_t key = a.hash[id] - 1u;
-    if (lane == 0) {
-      N.g_start[gi] = q0;
-      N.g_size[gi] = total;
-      N.g_status[gi] = key;
-      N.g_alive[gi] = total;
-    }
-    int run = 0;
-    for (int k0 = cb; k0 < cb + cc; k0 += 32) {
-      const int k = k0 + lane;
-      const bool keep = k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh;
+    const int in = i + nw;
+    int id_n = 0;
+    if (in < nsm) id_n = a.ns_small[in];
+    const double thresh = dsub(__longlong_as_double(static_cast<long long>(vm)), band);
+    const uint32_t key = hk - 1u;
+    if (cc <= 32) {
+      const int k = cb + lane;
+      const bool in_range = lane < cc;
+      const bool ok = in_range && a.c_ok[k];
+      const double v = in_range ? a.c_value[k] : 0.0;
+      const int p = in_range ? a.c_pid[k] : 0;
+      const uint64_t lx = in_range ? a.c_lex[k] : 0ull;
+      const int parent = in_range ? a.c_parent[k] : 0;
+      const bool keep = ok && v >= thresh;
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
-      run += __popc(bal);
+      const int total = __popc(bal);
+      if (total > 0) {  // uniform
+        int q0 = 0, gi = 0, fits = 0;
+        if (lane == 0) {
+          q0 = atomicAdd(&sc.out_states, total);
+          gi = atomicAdd(&sc.out_groups, 1);
+          fits = claim_fits(a, s, q0, total, gi) ? 1 : 0;
+        }
+        if (__shfl_sync(0xffffffffu, fits, 0)) {
+          q0 = __shfl_sync(0xffffffffu, q0, 0);
+          gi = __shfl_sync(0xffffffffu, gi, 0);
+          if (lane == 0) {
+            N.g_start[gi] = q0;
+            N.g_size[gi] = total;
+            N.g_status[gi] = key;
+            N.g_alive[gi] = total;
+          }
+          if (keep) write_state_v(a, s, nxt, q0 + __popc(bal & ((1u << lane) - 1u)), gi, key, p, lx, v, parent);
+        }
+      }
+    } else {
+      int total = 0;
+      for (int k0 = cb; k0 < cb + cc; k0 += 32) {
+        const int k = k0 + lane;
+        total += __popc(__ballot_sync(0xffffffffu, k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh));
+      }
+      if (total > 0) {  // uniform
+        int q0 = 0, gi = 0, fits = 0;
+        if (lane == 0) {
+          q0 = atomicAdd(&sc.out_states, total);
+          gi = atomicAdd(&sc.out_groups, 1);
+          fits = claim_fits(a, s, q0, total, gi) ? 1 : 0;
+        }
+        if (__shfl_sync(0xffffffffu, fits, 0)) {
+          q0 = __shfl_sync(0xffffffffu, q0, 0);
+          gi = __shfl_sync(0xffffffffu, gi, 0);
+          if (lane == 0) {
+            N.g_start[gi] = q0;
+            N.g_size[gi] = total;
+            N.g_status[gi] = key;
+            N.g_alive[gi] = total;
+          }
+          int run = 0;
+          for (int k0 = cb; k0 < cb + cc; k0 += 32) {
+            const int k = k0 + lane;
+            const bool keep = k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh;
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
+            run += __popc(bal);
+          }
+        }
+      }
+    }
+    if (in < nsm) {  // the next status's metadata (its id was loaded at the top)
+      id = id_n;
+      cb = a.ns_cbase[id];
+      cc = a.ns_ccnt[id];
+      vm = a.ns_vmax[id];
+      hk = a.hash[id];
     }
   }
 }
@@ -1437,11 +1505,13 @@ __device__ void phase_dominance(const V2& a, int s) {
         if (q[h] >= 0 && dead[h]) {
           N.alive[q[h]] = 0;
           atomicSub(&N.g_alive[N.group[q[h]]], 1);
-          atomicSub(&a.kid_cnt[nxt][lx[h] >> 32], 1);  // see phase_kids
           ++kills;
         }
       for (int o = 16; o > 0; o >>= 1) kills += __shfl_xor_sync(0xffffffffu, kills, o);
-      if (lane == 0 && kills && s + 1 < a.S) atomicSub(&a.ctl->alive_now[nxt], kills);  // F_S: k_term1 counts
+      if (lane == 0 && kills && s + 1 < a.S) {  // F_S: k_term1 counts
+        atomicSub(&a.ctl->alive_now[nxt], kills);
+        atomicAdd(&a.ctl->dead[nxt], kills);
+      }
     }
     if (lane == 0) a.pcnt[p] = 0;
   }
@@ -1456,6 +1526,20 @@ __global__ void MGS_LB k_units(const V2* __restrict__ ap, int s) {
   __shared__ int s_cnt[kBatch];
   __shared__ long long s_red[32];
   if (failed(a)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // frontier checks for F_s (solvers.hpp:348, :539-542): k_dom of the previous
+    // step (the last writer of F_s) has finished, so the live count is final
+    Ctl* ctl = a.ctl;
+    const int cur = s & 1;
+    const int alive_cur = ctl->n_store[cur] - ctl->dead[cur];
+    if (alive_cur == 0) raise_err(a, 0, MGS_ERR_INFEASIBLE_JOINT, s);
+    else if (s > 0 && static_cast<uint64_t>(alive_cur) > a.budget) raise_err(a, 0, MGS_ERR_STATE_BUDGET, s, alive_cur);
+    if (s > 0) {
+      ctl->ftot += alive_cur;
+      if (static_cast<unsigned long long>(alive_cur) > ctl->fpeak) ctl->fpeak = alive_cur;
+    }
+    ctl->ranks_prev[(s + 1) & 1] = ctl->n_store[cur];  // parent-rank space of F_{s+1}: stored F_s
+  }
   phase_units<M>(a, s, 0, s_cnt, s_red);
 }
 
@@ -1527,15 +1611,7 @@ __global__ void __launch_bounds__(kThreads) k_kid_scan(const V2* __restrict__ ap
   const int cur = s & 1;
   Ctl* ctl = a.ctl;
   StepCounters& sc = ctl->sc[s & 1];
-  const int alive_cur = ctl->alive_now[cur];
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // frontier checks for F_s (solvers.hpp:348, :539-542)
-    if (alive_cur == 0) raise_err(a, 0, MGS_ERR_INFEASIBLE_JOINT, s);
-    else if (s > 0 && static_cast<uint64_t>(alive_cur) > a.budget) raise_err(a, 0, MGS_ERR_STATE_BUDGET, s, alive_cur);
-    if (s > 0) {
-      ctl->ftot += alive_cur;
-      if (static_cast<unsigned long long>(alive_cur) > ctl->fpeak) ctl->fpeak = alive_cur;
-    }
-  }
+  (void)cur;
   const ScanJob jobs[1] = {{a.kid_cnt[cur], nullptr, a.kid_base, ctl->ranks_prev[s & 1], 0}};
   multi_scan(a, jobs, 1, 2 * (s + 1), &sc.ticket, ctl->scan_total);
 }
@@ -1607,6 +1683,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_trans_small(const V2* __restric
     const int nxt = (s + 1) & 1;
     a.ctl->sc[nxt] = StepCounters{};
     a.ctl->alive_now[nxt] = 0;
+    a.ctl->dead[nxt] = 0;
   }
 }
 
@@ -1663,7 +1740,6 @@ __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int
       d[4] = ctl->n_groups[nxt];
       d[5] = ctl->alive_now[cur];
     }
-    ctl->ranks_prev[nxt] = ctl->alive_now[cur];
   }
 }
 
@@ -2106,13 +2182,13 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         // (successor statuses and candidate ranges): they meet at the transitions
         cudaStream_t rs_ = fork ? side : st_;
         if (fork) {
-          if (st == 0) {  // later steps launch k_kids beside the previous k_dom
+          // later steps launch k_kids right after the previous k_write, beside
+          // k_dom: the rank branch (stored-state ranks) does not wait for dominance
+          if (st == 0) {
             MGS_CUDA_OK(cudaEventRecord(ev_rank_fork, st_));
             MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_rank_fork, 0));
             k_kids<<<g_kids, kThreads, 0, side>>>(d_args, st);
           }
-          MGS_CUDA_OK(cudaEventRecord(ev_rank_fork, st_));
-          MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_rank_fork, 0));
         } else {
           k_kids<<<g_kids, kThreads, 0, rs_>>>(d_args, st);
           after("kids", st);

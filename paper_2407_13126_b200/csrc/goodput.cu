@@ -249,12 +249,66 @@ __global__ void k_evaluate(DevSpace sp, HostTables t, const int32_t* plans, int 
   total[idx] = tot;
 }
 
+// Few (plan, trace) pairs (the solve's own objective): one CTA per pair. The
+// threads gather every (step, tenant) term in parallel -- option lookups,
+// change flags, completion, throughput, goodput -- into shared memory; one
+// thread then folds the goodputs in the reference's order (step-major,
+// tenant-minor), so the sequential part is S*M dependent adds, not S*M
+// dependent global loads.
+constexpr int kEvalOneThreads = 256;
+__global__ void __launch_bounds__(kEvalOneThreads) k_evaluate_one(DevSpace sp, HostTables t, const int32_t* plans,
+                                                                 int n_plans, const uint8_t* overrides,
+                                                                 const int64_t* arrivals, int n_traces,
+                                                                 int has_initial, uint4 init_lo, double* total,
+                                                                 double* thr_out) {
+  extern __shared__ double s_good[];  // [S*M]
+  __shared__ int s_finish[KM];
+  const int pair = blockIdx.x;
+  const int i = pair / n_traces, j = pair % n_traces;
+  const int S = t.S, M = t.M;
+  const int32_t* plan = plans + static_cast<size_t>(i) * S;
+  const int64_t* arr = arrivals + static_cast<size_t>(j) * M * S;
+  const uint32_t init[KM] = {init_lo.x, init_lo.y, init_lo.z, init_lo.w};
+  if (threadIdx.x < KM) s_finish[threadIdx.x] = 0;  // last retraining step + 1 (0: none)
+  __syncthreads();
+  for (int k = threadIdx.x; k < S * M; k += blockDim.x) {
+    const int s = k / M, m = k % M;
+    if (sp.opt_rsize[plan[s] * KM + m] > 0) atomicMax(&s_finish[m], s + 1);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < S * M; k += blockDim.x) {
+    const int s = k / M, m = k % M;
+    const int o = plan[s];
+    const uint32_t mask = sp.opt_mask[o * KM + m];
+    const bool changed = s == 0 ? (has_initial && mask != init[m]) : (mask != sp.opt_mask[plan[s - 1] * KM + m]);
+    const bool zero_psi = overrides && overrides[(static_cast<size_t>(i) * S + s) * M + m];
+    const double eff = eff_cap(sp.opt_cap[o * KM + m], changed && !zero_psi ? t.loss[m] : 0.0);
+    const double thr = thr_of(static_cast<double>(arr[m * S + s]), eff);
+    const bool done = s_finish[m] > 0 && s >= s_finish[m];  // Eq-12 (evaluate.hpp:174-179)
+    s_good[k] = dmul(thr, done ? t.post[m] : t.pre[m]);
+    if (thr_out) thr_out[(static_cast<size_t>(pair) * S + s) * M + m] = thr;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int k = 0; k < S * M; ++k) tot = dadd(tot, s_good[k]);
+    total[pair] = tot;
+  }
+}
+
 void evaluate_batch(Ctx& c, const Prepared& pr, const DevSpace& sp, const int32_t* d_plans, int n_plans,
                     const int64_t* d_arr, int n_traces, double* d_total, double* d_thr, const uint8_t* d_overrides) {
   const long long n = (long long)n_plans * n_traces;
   uint4 init{pr.init_mask[0], pr.init_mask[1], pr.init_mask[2], pr.init_mask[3]};
-  k_evaluate<<<ceil_div(n, 128), 128, 0, c.stream>>>(sp, pr.t, d_plans, n_plans, d_overrides, d_arr, n_traces, pr.has_initial,
-                                                     init, d_total, d_thr);
+  const size_t smem = static_cast<size_t>(pr.t.S) * pr.t.M * 8;
+  if (n <= c.sm_count && smem <= 48 * 1024) {
+    k_evaluate_one<<<static_cast<unsigned>(n), kEvalOneThreads, smem, c.stream>>>(
+        sp, pr.t, d_plans, n_plans, d_overrides, d_arr, n_traces, pr.has_initial, init, d_total, d_thr);
+  } else {
+    k_evaluate<<<ceil_div(n, 128), 128, 0, c.stream>>>(sp, pr.t, d_plans, n_plans, d_overrides, d_arr, n_traces,
+                                                       pr.has_initial, init, d_total, d_thr);
+  }
+  ++c.kernel_launches;
   MGS_CUDA_OK(cudaGetLastError());
 }
 
