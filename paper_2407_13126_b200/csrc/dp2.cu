@@ -1679,6 +1679,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_trans_small(const V2* __restric
   const V2& a = c_v2;
   if (failed(a)) return;
   phase_trans_small<M>(a, s);
+  {  // F_s's child counts were last read by the ranks: cleared here, off the critical path
+    const int cur = s & 1, rp = a.ctl->ranks_prev[s & 1];
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+    for (int i = gtid; i < rp; i += gstride) {
+      a.kid_cnt[cur][i] = 0;
+      a.kid_cur[cur][i] = 0;
+    }
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // counters of the next step
     const int nxt = (s + 1) & 1;
     a.ctl->sc[nxt] = StepCounters{};
@@ -1717,11 +1725,6 @@ __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int
     a.ns_ccnt[i] = 0;
     a.ns_ucur[i] = 0;
     a.ns_ccur[i] = 0;
-  }
-  const int rp = ctl->ranks_prev[s & 1];
-  for (int i = gtid; i < rp; i += gstride) {
-    a.kid_cnt[cur][i] = 0;
-    a.kid_cur[cur][i] = 0;
   }
   if (gtid == 0) {  // end-of-slot bookkeeping (every value read here is final)
     const int nxt = (s + 1) & 1;
@@ -2124,6 +2127,20 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
       step_ev.assign(S + 1, nullptr);
       for (auto& e : step_ev) MGS_CUDA_OK(cudaEventCreate(&e));
     }
+    // milestones inside each step (graph mode, MGS_STEP_TIMES): where the critical path runs
+    constexpr int kMile = 12;
+    static const char* kMileNames[kMile] = {"kids", "kid_scan", "kid_fill", "ranks_big", "ranks_small", "units",
+                                            "scans", "place", "trans_big", "trans_small", "band", "write"};
+    static std::vector<cudaEvent_t> mile_ev;
+    if (!step_ev.empty() && static_cast<int>(mile_ev.size()) < S * kMile) {
+      for (auto e : mile_ev) cudaEventDestroy(e);
+      mile_ev.assign(static_cast<size_t>(S) * kMile, nullptr);
+      for (auto& e : mile_ev) MGS_CUDA_OK(cudaEventCreate(&e));
+    }
+    auto mile = [&](int st, int k, cudaStream_t on) {
+      if (!mile_ev.empty()) MGS_CUDA_OK(cudaEventRecordWithFlags(mile_ev[static_cast<size_t>(st) * kMile + k], on,
+                                                                  cudaEventRecordExternal));
+    };
     auto enqueue = [&](cudaStream_t st_, bool timed) {
       if (!timed && !step_ev.empty()) MGS_CUDA_OK(cudaEventRecordWithFlags(step_ev[0], st_, cudaEventRecordExternal));
       const bool fork = fork_ok && !timed && side != nullptr;
@@ -2188,6 +2205,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
             MGS_CUDA_OK(cudaEventRecord(ev_rank_fork, st_));
             MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_rank_fork, 0));
             k_kids<<<g_kids, kThreads, 0, side>>>(d_args, st);
+            if (!timed) mile(st, 0, side);
           }
         } else {
           k_kids<<<g_kids, kThreads, 0, rs_>>>(d_args, st);
@@ -2195,14 +2213,18 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         }
         k_kid_scan<<<g_kscan, kThreads, 0, rs_>>>(d_args, st);
         after("kid_scan", st);
+        if (fork && !timed) mile(st, 1, rs_);
         k_kid_fill<<<g_kfill, kThreads, 0, rs_>>>(d_args, st);
         after("kid_fill", st);
+        if (fork && !timed) mile(st, 2, rs_);
         if (fork) {
           MGS_CUDA_OK(cudaEventRecord(ev_rs_fork, side));
           MGS_CUDA_OK(cudaStreamWaitEvent(side2, ev_rs_fork, 0));
           k_ranks_small<<<g_rsmall, kThreads, 0, side2>>>(d_args, st);
+          if (!timed) mile(st, 4, side2);
           MGS_CUDA_OK(cudaEventRecord(ev_rs_join, side2));
           k_ranks_big<<<g_rbig, kThreads, smem_rank, side>>>(d_args, st, 0);
+          if (!timed) mile(st, 3, side);
           MGS_CUDA_OK(cudaEventRecord(ev_rank_join, side));
         } else {
           k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(d_args, st, 1);
@@ -2210,10 +2232,13 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         }
         kunits<<<g_units, kThreads, 0, st_>>>(d_args, st);
         after("units", st);
+        if (fork && !timed) mile(st, 5, st_);
         k_scans<<<g_scans, kThreads, 0, st_>>>(d_args, st);
         after("scans", st);
+        if (fork && !timed) mile(st, 6, st_);
         k_place<<<g_place, kThreads, 0, st_>>>(d_args, st);
         after("place", st);
+        if (fork && !timed) mile(st, 7, st_);
         if (fork) {
           MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rank_join, 0));
           MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rs_join, 0));
@@ -2222,9 +2247,11 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
           MGS_CUDA_OK(cudaEventRecord(ev_fork, st_));
           MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_fork, 0));
           ktsmall<<<g_tsmall, kThreads, 0, side>>>(d_args, st);
+          if (!timed) mile(st, 9, side);
           MGS_CUDA_OK(cudaEventRecord(ev_join, side));
           k_tables<<<g_tables, kThreads, 0, st_>>>(d_args, st);
           ktbig<<<g_tbig, kThreads, 0, st_>>>(d_args, st);
+          if (!timed) mile(st, 8, st_);
           MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_join, 0));
         } else {
           k_tables<<<g_tables, kThreads, 0, st_>>>(d_args, st);
@@ -2236,12 +2263,15 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         }
         k_band<<<g_band, kThreads, smem_merge, st_>>>(d_args, st);
         after("band", st);
+        if (fork && !timed) mile(st, 10, st_);
         k_write<<<g_write, kThreads, 0, st_>>>(d_args, st);
         after("write", st);
+        if (fork && !timed) mile(st, 11, st_);
         if (fork && st + 1 < S) {
           MGS_CUDA_OK(cudaEventRecord(ev_rank_fork, st_));
           MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_rank_fork, 0));
           k_kids<<<g_kids, kThreads, 0, side>>>(d_args, st + 1);
+          if (!timed) mile(st + 1, 0, side);
         }
         k_dom<<<g_dom, kThreads, 0, st_>>>(d_args, st);
         after("dom", st);
@@ -2329,6 +2359,22 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
           std::fprintf(stderr, " %.1f", 1e3 * ms);
         }
         std::fprintf(stderr, "\n");
+        if (!mile_ev.empty() && fork_ok) {  // mean milestone time after the step's start (previous k_dom), us
+          std::fprintf(stderr, "v2 graph milestones_us (from step start):");
+          for (int k = 0; k < kMile; ++k) {
+            double acc = 0.0;
+            int n = 0;
+            for (int st = 1; st < S; ++st) {
+              float ms = 0.f;
+              if (cudaEventElapsedTime(&ms, step_ev[st], mile_ev[static_cast<size_t>(st) * kMile + k]) != cudaSuccess)
+                continue;
+              acc += 1e3 * ms;
+              ++n;
+            }
+            std::fprintf(stderr, " %s %.1f", kMileNames[k], n ? acc / n : 0.0);
+          }
+          std::fprintf(stderr, "\n");
+        }
       }
     }
     MGS_CUDA_OK(cudaGetLastError());
