@@ -292,7 +292,9 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "config-1 window: 2 ResNet-18 tenants, A100 7-slice lattice (12 configs, 9864 options), "
                                "S=200 x 1 s slots, Poisson lambda 120/150, psi 0.5",
-                   "seed": "100001+rank", "transitions_per_window": tr_window, "parallelism": "dp%d" % world,
+                   "seed": "100001+rank", "transitions_per_window": tr_window,
+                   "transitions_gpu_evaluated_per_window": stats[-1]["transitions"],
+                   "frontier_states_per_window": stats[-1]["frontier_total"], "parallelism": "dp%d" % world,
                    "collective": "per-step all-gather of (objective bits, plan checksum) over %s" % args.dist_backend,
                    "l2": "flushed between timed steps (256 MiB write)"},
         "per_rank": [{"rank": r[0], "device": r[1], "device_ms_per_step": r[2] / 1e3 / args.steps,

@@ -16,6 +16,14 @@
 //                                              == evaluate_plan(...).total for plans x traces
 //                                                 (verify_feasibility = false)  evaluate.hpp:153-210
 // Results are bit-identical to the reference functions (tests/dropin/extras_test.cpp).
+//
+// Plan representation: run_fluid, check_feasible and evaluate_plan read ANY
+// allocation sequence resolve_step can read (PlanSteps: configuration + per-slot
+// task bits). run_requests, apply_preinit and evaluate_totals map every step to
+// one of the planner's enumerated options (Space::build) and throw
+// plan.infeasible for a step that is not one (several inference slots of one
+// tenant, broken floors, shared instances): the planners' and baselines' plans
+// always are options.
 #pragma once
 
 #include <map>
