@@ -63,7 +63,7 @@ constexpr int kBucketSmall = 256;    // child buckets up to this size: thread pe
 constexpr int kSortItems = 16;       // big child buckets: CTA radix sort of up to 256*16 keys
 constexpr int kBatch = 512;          // groups / statuses per CTA allocation batch
 constexpr int kNumScans = 7;
-constexpr int kDbg = 10;  // per-step debug counters
+constexpr int kDbg = 14;  // per-step debug counters
 
 enum Err : int { kOk = 0, kOverflow = 100 };
 
@@ -1377,6 +1377,11 @@ __device__ void phase_write(const V2& a, int s) {
     if (in < nsm) id_n = a.ns_small[in];
     const double thresh = dsub(__longlong_as_double(static_cast<long long>(vm)), band);
     const uint32_t key = hk - 1u;
+    if (a.dbg && lane == 0) {  // [10] small statuses <= 32 candidates, [11] their candidates, [12] other small, [13] their candidates
+      unsigned long long* d = reinterpret_cast<unsigned long long*>(a.dbg + kDbg * s);
+      atomicAdd(d + (cc <= 32 ? 10 : 12), 1ull);
+      atomicAdd(d + (cc <= 32 ? 11 : 13), static_cast<unsigned long long>(cc));
+    }
     if (cc <= 32) {
       const int k = cb + lane;
       const bool in_range = lane < cc;
@@ -2411,8 +2416,8 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
           const long long* q = d.data() + kDbg * s;
           std::fprintf(stderr,
                        "v2 step %d units %lld ns %lld T %lld store %lld groups %lld alive_in %lld items_b %lld "
-                       "items_s %lld max_group %lld big_groups %lld\n",
-                       s, q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8], q[9]);
+                       "items_s %lld max_group %lld big_groups %lld small32 %lld/%lld small %lld/%lld\n",
+                       s, q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8], q[9], q[10], q[11], q[12], q[13]);
         }
       }
       L.status = MGS_OK;
