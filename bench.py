@@ -310,7 +310,7 @@ def run_ours(args):
                 "decision_latency_ms": 1e3 * e2e_s / args.steps,
                 "timing": "host wall clock around the C-ABI solve (pinned forecast in, plan out), max over ranks"},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": "per-window DP graph (14 phase kernels x S steps in parallel branches, one graph launch)",
+        "roofline": {"bound": "hbm", "kernel": "per-window DP graph (14 phase kernels x S steps in three graph branches, one graph launch)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None,
                      "traffic": traffic.get("bytes_per_window") if traffic else None,
@@ -338,7 +338,7 @@ def run_ours(args):
 
 def measured_traffic():
     """DRAM bytes per C1 window from the committed ncu metrics pass (profiles/)."""
-    path = os.path.join(ROOT, "profiles", "traffic_c1.json")
+    path = os.path.join(ROOT, "profiles", "r2", "traffic_c1.json")
     try:
         return json.load(open(path))
     except (OSError, ValueError):
