@@ -56,6 +56,8 @@ struct Codec {
   int S;
   int shift;
   __host__ __device__ explicit Codec(int s) : S(s), shift(s <= 8192 ? 13 : 0) {}
+  // sh = 0: the reference numbering (compact codes, < 256 for S <= 36)
+  __host__ __device__ Codec(int s, int sh) : S(s), shift(sh) {}
   __host__ __device__ static constexpr int done() { return 1; }
   __host__ __device__ int running(int k, long long rem) const {
     return shift ? 2 + (((k - 1) << shift) | static_cast<int>(rem - 1)) : 2 + (k - 1) * S + static_cast<int>(rem - 1);
@@ -144,6 +146,7 @@ struct DevSpace {
   int P1 = 0;          // P + 1 (the root's carried-over placement)
   int n_cand = 0;      // distinct (signature, placement) pairs
   int root_pid = 0;    // == P
+  int n_mask_ids[KM] = {0, 0, 0, 0};  // per tenant: mask ids in pl_ids (incl. the root's out-of-range id)
   // options (lex order)
   int32_t* opt_config = nullptr;
   int8_t* opt_labels = nullptr;   // [n_opt][MGS_MAX_SLOTS]

@@ -1,4 +1,4 @@
-// Device-resident DP engine (M <= 2): the whole per-window search of solve_dp
+// Device-resident DP engine (M <= 4): the whole per-window search of solve_dp
 // (solvers.hpp:242-579) as a stream of phase kernels with every count kept on
 // the device: no host round trips inside a window, no sorts, no hot
 // (same-address) global atomics.
@@ -169,6 +169,13 @@ struct V2 {
   int oi_bits;                   // bits of an option index (radix sort width)
   int merge_win;                 // placement window of the CTA merge table
   int rank_words;                // 32-bit words of the option-index bitmap of k_ranks_big (0: does not fit)
+  // Per-tenant fields of a packed status / placement-ids word: 16 bits at
+  // M <= 2; 8 bits at M = 3..4 (status codes in the reference numbering,
+  // < 256 for S <= 36; mask ids < 255, all-ones never matches)
+  int fw;                        // field width, bits
+  uint32_t fmask;
+  int codec_shift;
+  const uint32_t* ids32;         // [P1] placement ids packed fw bits per tenant
   long long* dbg;                // [S][kDbg] per-step counters (debug dump)
   unsigned long long* dbg_time;  // barrier timestamps (debug)
 };
@@ -426,16 +433,31 @@ __device__ int ns_slot(const V2& a, uint32_t key, int phi, int step, int* s_nnew
   return -1;
 }
 
+__device__ __forceinline__ int fld(const V2& a, uint32_t x, int m) {
+  return static_cast<int>((x >> (a.fw * m)) & a.fmask);
+}
+// the same with the width fixed by the tenant count (kernels templated on M)
+template <int M>
+__device__ __forceinline__ int fldm(uint32_t x, int m) {
+  constexpr int kW = M <= 2 ? 16 : 8;
+  return static_cast<int>((x >> (kW * m)) & ((1u << kW) - 1u));
+}
+template <int M>
+__device__ __forceinline__ uint32_t fput(int v, int m) {
+  constexpr int kW = M <= 2 ? 16 : 8;
+  return static_cast<uint32_t>(v) << (kW * m);
+}
+
 // per-tenant allowed retraining sizes of a status (allowed_sizes, solvers.hpp:79-97)
 template <int M>
 struct UnitSpace {
   int st[M], sizes[M][9], cnt[M], total;
   __device__ void init(const V2& a, uint32_t status, int s) {
-    const Codec codec{a.t.S};
+    const Codec codec{a.t.S, a.codec_shift};
     total = 1;
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      st[m] = static_cast<int>((status >> (16 * m)) & 0xffff);
+      st[m] = fldm<M>(status, m);
       cnt[m] = 0;
       if (Codec::is_running(st[m])) {
         sizes[m][cnt[m]++] = codec.run_size(st[m]);
@@ -451,7 +473,7 @@ struct UnitSpace {
   }
   // combination c -> (valid, signature, successor status) (solvers.hpp:388-402)
   __device__ bool combo(const V2& a, int c, int s, int* sig_out, uint32_t* ns_out) const {
-    const Codec codec{a.t.S};
+    const Codec codec{a.t.S, a.codec_shift};
     int rem = c, pick[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) {
@@ -467,7 +489,7 @@ struct UnitSpace {
     for (int m = 0; m < M; ++m) {
       const int adv = codec.advance(a.t.rt[m], st[m], sizes[m][pick[m]], s);
       ok = ok && adv >= 0 && !(adv == 0 && (a.t.min_rt[m] < 0 || s + 1 + a.t.min_rt[m] > a.t.S));
-      ns |= static_cast<uint32_t>(adv < 0 ? 0 : adv) << (16 * m);
+      ns |= fput<M>(adv < 0 ? 0 : adv, m);
     }
     *sig_out = sig;
     *ns_out = ns;
@@ -837,7 +859,7 @@ __device__ __forceinline__ unsigned long long emit_target(const V2& a, int s, in
   double v = F.value[pred];  // exact fold (solvers.hpp:451-458)
 #pragma unroll
   for (int m = 0; m < M; ++m) {
-    const bool changed = charge && ((pids >> (16 * m)) & 0xffff) != ((ids_p >> (16 * m)) & 0xffff);
+    const bool changed = charge && fldm<M>(pids, m) != fldm<M>(ids_p, m);
     const double eff = eff_cap(cap[m], changed ? t.loss[m] : 0.0);
     v = dadd(v, dmul(thr_of(a.recv[m * t.S + s], eff), acc[m]));
   }
@@ -854,7 +876,7 @@ template <int M>
 __device__ __forceinline__ void group_acc(const V2& a, uint32_t gstat, double* acc) {
 #pragma unroll
   for (int m = 0; m < M; ++m)
-    acc[m] = static_cast<int>((gstat >> (16 * m)) & 0xffff) == Codec::done() ? a.t.post[m] : a.t.pre[m];
+    acc[m] = fldm<M>(gstat, m) == Codec::done() ? a.t.post[m] : a.t.pre[m];
 }
 
 // Subset tables of every big group of F_s, built once per step (one CTA per
@@ -947,7 +969,7 @@ __device__ void phase_tables(const V2& a, int s) {
       a.tab_hdr[2 * b] = bv;
       a.tab_hdr[2 * b + 1] = brx;
     }
-    if (nsub > 2)  // min (rank, idx) among the max; M <= 2 here, so the partial subsets are 1 and 2
+    if (nsub == 4) {  // min (rank, idx) among the max; M = 2: the partial subsets are 1 and 2
       for (int j = threadIdx.x; j < gn; j += kThreads) {
         if (!F.alive[gs + j]) continue;
         const int pj = F.pid[gs + j];
@@ -959,6 +981,18 @@ __device__ void phase_tables(const V2& a, int s) {
         if (m1 == v) atomicMin(&rxs[e1], rx);
         if (m2 == v) atomicMin(&rxs[e2], rx);
       }
+    } else if (nsub > 4) {  // M = 3..4: every partial subset
+      for (int j = threadIdx.x; j < gn; j += kThreads) {
+        if (!F.alive[gs + j]) continue;
+        const int pj = F.pid[gs + j];
+        const unsigned long long v = vbits(F.value[gs + j]);
+        const unsigned long long rx = (static_cast<unsigned long long>(F.rank[gs + j]) << 32) | static_cast<uint32_t>(j);
+        for (int sub = 1; sub < nsub - 1; ++sub) {
+          const int e = a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj];
+          if (vb[e] == v) atomicMin(&rxs[e], rx);
+        }
+      }
+    }
     __syncthreads();
   }
 }
@@ -1018,7 +1052,7 @@ __device__ void phase_trans_big(const V2& a, int s) {
         }
       }
       const unsigned long long vb_t =
-          emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, static_cast<uint32_t>(a.sp.pl_ids[p]), bt, F);
+          emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, a.ids32[p], bt, F);
       vmax = vb_t > vmax ? vb_t : vmax;
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -1093,7 +1127,7 @@ __device__ void phase_trans_small(const V2& a, int s) {
     group_acc<M>(a, F.g_status[g], acc);
     const int p = a.sp.cand_pid[sb + ti];
     const int oi = a.sp.cand_oi[sb + ti];
-    const uint32_t ids_p = static_cast<uint32_t>(a.sp.pl_ids[p]);
+    const uint32_t ids_p = a.ids32[p];
     BestT<M> b;
 #pragma unroll
     for (int k = 1; k < (1 << M); ++k) {
@@ -1111,7 +1145,7 @@ __device__ void phase_trans_small(const V2& a, int s) {
       const uint32_t x = gids[j] ^ ids_p;
       int mt = 0;
 #pragma unroll
-      for (int m = 0; m < M; ++m) mt |= ((x >> (16 * m)) & 0xffff) == 0 ? (1 << m) : 0;
+      for (int m = 0; m < M; ++m) mt |= fldm<M>(x, m) == 0 ? (1 << m) : 0;
       if (mt == 0) continue;
       const double vj = gval[j];
       const uint32_t rj = grank[j];
@@ -1149,7 +1183,7 @@ __device__ __forceinline__ void write_state_v(const V2& a, int s, int nxt, int q
                                               uint64_t lx, double v, int parent) {
   const FrontierV2& N = a.f[nxt];
   const long long h = a.hist_base[s + 1] + q;
-  const uint32_t ids = static_cast<uint32_t>(a.sp.pl_ids[p]);
+  const uint32_t ids = a.ids32[p];
   // dominance buckets of more than 64 states are skipped (solvers.hpp:521), and a
   // bucket count only grows within the step: once a (possibly stale) read shows
   // more than 64, the bucket is dead and its atomic can be skipped
@@ -1463,19 +1497,22 @@ __device__ __forceinline__ bool dom_decoded(uint32_t x, uint32_t y) {
   return (x >> 24) == 2 && (y >> 24) == 2 && ((x ^ y) & 0x00ff0000u) == 0 && (x & 0xffffu) <= (y & 0xffffu);
 }
 
-// S7: status dominance within placement buckets (solvers.hpp:514-537)
+// S7: status dominance within placement buckets (solvers.hpp:514-537).
+// MK = 2 (M <= 2, 16-bit fields) or 4 (M = 3..4, 8-bit fields).
+template <int MK>
 __device__ void phase_dominance(const V2& a, int s) {
   const int nxt = (s + 1) & 1;
   const FrontierV2& N = a.f[nxt];
-  const Codec codec{a.t.S};
+  const Codec codec{a.t.S, a.codec_shift};
   const int lane = threadIdx.x & 31;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const int MT = a.t.M;
   for (int p = wid; p < a.sp.P1; p += nw) {
     const int n = a.pcnt[p];
     if (n >= 2 && n <= 64) {
       const int* bk = a.pbucket + p * 64;
       int q[2];
-      uint32_t dk[2][2];
+      uint32_t dk[2][MK];
       double v[2];
       uint64_t lx[2];
       for (int h = 0; h < 2; ++h) {
@@ -1484,8 +1521,9 @@ __device__ void phase_dominance(const V2& a, int s) {
         const uint32_t st = q[h] >= 0 ? N.status[q[h]] : 0;
         v[h] = q[h] >= 0 ? N.value[q[h]] : 0.0;
         lx[h] = q[h] >= 0 ? N.lex[q[h]] : 0;
-        for (int m = 0; m < 2; ++m) {  // decode once: kind (0 idle, 1 done, 2 running) | size | rem
-          const int code = m < a.t.M ? static_cast<int>((st >> (16 * m)) & 0xffff) : 0;
+#pragma unroll
+        for (int m = 0; m < MK; ++m) {  // decode once: kind (0 idle, 1 done, 2 running) | size | rem
+          const int code = m < MT ? fldm<MK>(st, m) : 0;
           dk[h][m] = code == Codec::done() ? (1u << 24)
                      : Codec::is_running(code) ? (2u << 24) | (static_cast<uint32_t>(codec.run_size(code)) << 16) |
                                                      static_cast<uint32_t>(codec.run_rem(code))
@@ -1497,11 +1535,18 @@ __device__ void phase_dominance(const V2& a, int s) {
         const int h = j >> 5, src = j & 31;
         const uint32_t d0 = __shfl_sync(0xffffffffu, dk[h][0], src);
         const uint32_t d1 = __shfl_sync(0xffffffffu, dk[h][1], src);
+        uint32_t d2 = 0, d3 = 0;
+        if constexpr (MK > 2) {
+          d2 = __shfl_sync(0xffffffffu, dk[h][2], src);
+          d3 = __shfl_sync(0xffffffffu, dk[h][3], src);
+        }
         const double va = __shfl_sync(0xffffffffu, v[h], src);
         const uint64_t la = __shfl_sync(0xffffffffu, lx[h], src);
         for (int hb = 0; hb < 2; ++hb) {
           if (q[hb] < 0 || lane + 32 * hb == j) continue;
-          if (dom_decoded(d0, dk[hb][0]) && dom_decoded(d1, dk[hb][1]) && better(va, la, v[hb], lx[hb]))
+          if (dom_decoded(d0, dk[hb][0]) && dom_decoded(d1, dk[hb][1]) &&
+              (MK <= 2 || (dom_decoded(d2, dk[hb][MK > 2 ? 2 : 0]) && dom_decoded(d3, dk[hb][MK > 2 ? 3 : 0]))) &&
+              better(va, la, v[hb], lx[hb]))
             dead[hb] = true;
         }
       }
@@ -1718,7 +1763,10 @@ __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int
   if (failed(a)) return;
   const int cur = s & 1;
   Ctl* ctl = a.ctl;
-  if (a.dominance_ok) phase_dominance(a, s);
+  if (a.dominance_ok) {
+    if (a.t.M <= 2) phase_dominance<2>(a, s);
+    else phase_dominance<4>(a, s);
+  }
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const int n_ns = ctl->sc[s & 1].n_ns;
   for (int k = gtid; k < n_ns; k += gstride) {  // S6 read the keys from the hash: clear the claimed slots
@@ -1752,9 +1800,9 @@ __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int
 }
 
 // terminal (solvers.hpp:552-565): live count of F_S, budget, best all-done state
-__device__ __forceinline__ uint32_t all_done_key(int M) {
+__device__ __forceinline__ uint32_t all_done_key(const V2& a, int M) {
   uint32_t k = 0;
-  for (int m = 0; m < M; ++m) k |= static_cast<uint32_t>(Codec::done()) << (16 * m);
+  for (int m = 0; m < M; ++m) k |= static_cast<uint32_t>(Codec::done()) << (a.fw * m);
   return k;
 }
 
@@ -1765,7 +1813,7 @@ __global__ void __launch_bounds__(kThreads) k_term1(const V2* __restrict__ ap) {
   const int fin = a.S & 1;
   const FrontierV2& F = a.f[fin];
   const int n = a.ctl->n_store[fin];
-  const uint32_t all_done = all_done_key(a.t.M);
+  const uint32_t all_done = all_done_key(a, a.t.M);
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   long long live = 0;
   unsigned long long mv = 0;
@@ -1790,7 +1838,7 @@ __global__ void __launch_bounds__(kThreads) k_term2(const V2* __restrict__ ap) {
   const int fin = a.S & 1;
   const FrontierV2& F = a.f[fin];
   const int n = a.ctl->n_store[fin];
-  const uint32_t all_done = all_done_key(a.t.M);
+  const uint32_t all_done = all_done_key(a, a.t.M);
   const int alive_fin = a.ctl->alive_now[fin];
   const unsigned long long bvb = a.ctl->best_vb;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
@@ -1811,7 +1859,7 @@ __global__ void __launch_bounds__(kThreads) k_term3(const V2* __restrict__ ap) {
   const int fin = a.S & 1;
   const FrontierV2& F = a.f[fin];
   const int n = a.ctl->n_store[fin];
-  const uint32_t all_done = all_done_key(a.t.M);
+  const uint32_t all_done = all_done_key(a, a.t.M);
   const unsigned long long bvb = a.ctl->best_vb, blx = a.ctl->best_lex;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   for (int i = gtid; i < n; i += gstride)
@@ -1835,7 +1883,7 @@ __global__ void k_init_root(const V2* __restrict__ ap) {
   const int root_pid = a.sp.root_pid;
   FrontierV2 F = a.f[0];
   F.status[0] = 0;
-  F.ids[0] = static_cast<uint32_t>(a.sp.pl_ids[root_pid]);
+  F.ids[0] = a.ids32[root_pid];
   F.pid[0] = root_pid;
   F.value[0] = 0.0;
   F.lex[0] = 0;
@@ -1881,6 +1929,15 @@ __global__ void k_band_value(const double* pl_cap, int P, HostTables t, double* 
   }
 }
 
+// placement ids (16 bits per tenant in pl_ids) repacked fw bits per tenant
+__global__ void k_ids32(const uint64_t* pl_ids, int n, int M, int fw, uint32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t v = 0;
+  for (int m = 0; m < M; ++m) v |= static_cast<uint32_t>((pl_ids[i] >> (16 * m)) & 0xffffu) << (fw * m);
+  out[i] = v;
+}
+
 __global__ void k_sig_len(const int32_t* sig_off, int n_sig, int32_t* sig_len) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_sig; i += gridDim.x * blockDim.x)
     sig_len[i] = sig_off[i + 1] - sig_off[i];
@@ -1894,10 +1951,14 @@ struct Caps {
 }  // namespace
 
 bool solve_dp_v2_supported(const Prepared& pr, const DevSpace& sp) {
-  if (pr.t.M > 2) return false;
   const char* e = std::getenv("MGS_DP_ENGINE");
   if (e && std::string(e) == "v1") return false;
-  (void)sp;
+  if (pr.t.M <= 2) return true;
+  // M = 3..4 in 8-bit fields: status codes in the reference numbering stay
+  // below 255 (2 + 7 * S - 1 < 255), mask ids below 255 (all-ones never matches)
+  if (7 * pr.t.S + 1 >= 255) return false;
+  for (int m = 0; m < pr.t.M; ++m)
+    if (sp.n_mask_ids[m] > 255) return false;
   return true;
 }
 
@@ -2036,6 +2097,15 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, int dominance_ok, int me
   a.oi_bits = 1;
   while ((1ll << a.oi_bits) < sp.n_opt) ++a.oi_bits;
   a.rank_words = rank_words_of(sp.n_opt);
+  a.fw = t.M <= 2 ? 16 : 8;
+  a.fmask = t.M <= 2 ? 0xffffu : 0xffu;
+  a.codec_shift = t.M <= 2 ? Codec(S).shift : 0;
+  {
+    uint32_t* ids32 = c.buf<uint32_t>("v2_ids32", sp.P1);
+    k_ids32<<<ceil_div(sp.P1, 256), 256, 0, c.stream>>>(sp.pl_ids, sp.P1, t.M, a.fw, ids32);
+    ++c.kernel_launches;
+    a.ids32 = ids32;
+  }
   c.prefix = saved_prefix;
   return a;
 }
@@ -2064,9 +2134,9 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   }
   size_t smem_rank = sizeof(typename cub::BlockRadixSort<unsigned long long, kThreads, kSortItems>::TempStorage);
   for (int l = 0; l < K; ++l) smem_rank = std::max(smem_rank, static_cast<size_t>(rank_words_of(lanes[l].sp->n_opt)) * 8);
-  auto ktbig = M == 1 ? k_trans_big<1> : k_trans_big<2>;
-  auto ktsmall = M == 1 ? k_trans_small<1> : k_trans_small<2>;
-  auto kunits = M == 1 ? k_units<1> : k_units<2>;
+  auto ktbig = M == 1 ? k_trans_big<1> : M == 2 ? k_trans_big<2> : M == 3 ? k_trans_big<3> : k_trans_big<4>;
+  auto ktsmall = M == 1 ? k_trans_small<1> : M == 2 ? k_trans_small<2> : M == 3 ? k_trans_small<3> : k_trans_small<4>;
+  auto kunits = M == 1 ? k_units<1> : M == 2 ? k_units<2> : M == 3 ? k_units<3> : k_units<4>;
   MGS_CUDA_OK(cudaFuncSetAttribute(k_ranks_big, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_rank)));
   MGS_CUDA_OK(cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_merge)));
   // One resident wave per kernel (SMs x max co-resident CTAs), shared by the

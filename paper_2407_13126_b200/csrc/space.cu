@@ -364,6 +364,7 @@ void build_space(Ctx& c, const mgs_lattice& lat, const Prepared& pr, DevSpace& s
     root |= static_cast<uint64_t>(id) << (16 * m);
   }
   MGS_CUDA_OK(cudaMemcpyAsync(sp.pl_ids + P, &root, 8, cudaMemcpyHostToDevice, c.stream));
+  for (int m = 0; m < M; ++m) sp.n_mask_ids[m] = static_cast<int>(host_vals[m].size()) + 1;
   sp.pl_cap = c.buf<double>("pl_cap", static_cast<size_t>(P + 1) * KM);
   MGS_CUDA_OK(cudaMemsetAsync(sp.pl_cap, 0, static_cast<size_t>(P + 1) * KM * 8, c.stream));
 
