@@ -154,3 +154,20 @@ def test_gpu_c2_shaped_windows(gpu, golden_dir):
         assert stats["options"] == g["options"]
         seen.add("solved")
     assert seen == {"solved", "planner.state-budget"}
+
+
+@pytest.mark.gpu
+def test_gpu_multi_launch_engine_fallback(gpu, golden_dir, monkeypatch):
+    """The multi-launch engine (csrc/dp.cu) stays the fallback for M = 3..4 windows
+    the graph engine's 8-bit fields cannot hold (S > 36): pinned on the same
+    goldens by forcing it (MGS_DP_ENGINE=v1)."""
+    monkeypatch.setenv("MGS_DP_ENGINE", "v1")
+    n = 0
+    for stem, path, g in golden_dir["multi"][:20]:
+        want = g["dp"]
+        if "error" in want:
+            continue
+        enc, obj, thr, _ = _gpu_solve(gpu, path, None)
+        _check(want, enc, obj, thr)
+        n += 1
+    assert n >= 10
