@@ -41,7 +41,7 @@ def test_c5_subproblems_match_reference():
         pytest.skip("c5 goldens not generated (oracle/make_c5_goldens.py)")
     g = json.load(open(path))
     stems = sorted(g["golden"])
-    assert len(stems) >= 2
+    assert len(stems) == 8  # every MIG-GPU subproblem of the box
     scs = [SC.load_scenario(os.path.join(D, stem + ".scn")) for stem in stems]
     with planner.Planner(0) as pl:
         plans = driver.plan_scenarios(pl, scs, "oracle", max_windows=g["max_windows"])
