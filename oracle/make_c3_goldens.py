@@ -21,7 +21,8 @@ from paper_2407_13126_b200 import workloads as W  # noqa: E402
 OUT = os.path.join(ROOT, "tests", "golden", "c3")
 # (pair, predictor, windows, lookback, psi): the sweep's extremes, both history
 # predictors, and a lookahead that slides (window 2 sees only window 1)
-CASES = [(0, "ewma:0.3", 3, 1, 0.5), (1, "persistence", 2, 1, 6.0), (2, "oracle", 2, 1, 0.0)]
+CASES = [(0, "ewma:0.3", 3, 1, 0.5), (1, "persistence", 2, 1, 6.0), (2, "oracle", 2, 1, 0.0),
+         (0, "persistence", 2, 1, 1.0), (1, "ewma:0.5", 3, 2, 0.25), (2, "ewma:0.3", 3, 1, 6.0)]
 
 
 def main():

@@ -23,7 +23,7 @@ def raw(path):
     rows = list(csv.reader(io.TextIOWrapper(gzip.open(path))))
     hdr, units, data = rows[0], rows[1], rows[2:]
     stall = [i for i, h in enumerate(hdr) if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued")]
-    print("%-28s " % "kernel" + " ".join("%8s" % l for _, l in RAW) + "  top stalls (pc samples)")
+    print("%-28s " % "kernel" + " ".join("%8s" % l for _, l in RAW) + "     GB/s  top stalls (pc samples)")
     for r in data:
         name = r[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
         vals = []
@@ -48,10 +48,14 @@ def raw(path):
                 vals.append("%8.1f" % x)
             except ValueError:
                 vals.append("%8s" % v[:8])
+        try:  # achieved DRAM bandwidth of the capture (cold caches): (read + write) / duration
+            gbs = "%9.1f" % ((float(vals[1]) + float(vals[2])) * 1e6 / (float(vals[0]) * 1e-6) / 1e9)
+        except (ValueError, ZeroDivisionError):
+            gbs = "%9s" % "-"
         tot = sum(float(r[i] or 0) for i in stall) or 1.0
         top = sorted(((float(r[i] or 0), hdr[i].replace("smsp__pcsamp_warps_issue_stalled_", "")) for i in stall),
                      reverse=True)[:3]
-        print("%-28s " % name[:28] + " ".join(vals) + "  " + " ".join("%s %.0f%%" % (n, 100 * v / tot) for v, n in top))
+        print("%-28s " % name[:28] + " ".join(vals) + gbs + "  " + " ".join("%s %.0f%%" % (n, 100 * v / tot) for v, n in top))
 
 
 def launches(path):
