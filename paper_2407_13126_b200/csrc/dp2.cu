@@ -207,6 +207,10 @@ __device__ void raise_err(const V2& a, int phi, int code, int step = 0, unsigned
 
 // every phase kernel returns immediately once any error was raised
 __device__ __forceinline__ bool failed(const V2& a) { return ld_volatile(&a.ctl->err_code) != 0; }
+// The entry check of a kernel, uniform over the block: a flag raised while the
+// block starts (by another block, or another kernel) must not let some of its
+// threads leave while the others reach a barrier or a full-warp collective.
+__device__ __forceinline__ bool block_failed(const V2& a) { return __syncthreads_or(failed(a) ? 1 : 0) != 0; }
 
 // ---------------------------------------------------------------------------
 // block reductions / scans (kThreads threads)
@@ -1575,7 +1579,7 @@ __global__ void MGS_LB k_units(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   __shared__ int s_cnt[kBatch];
   __shared__ long long s_red[32];
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     // frontier checks for F_s (solvers.hpp:348, :539-542): k_dom of the previous
     // step (the last writer of F_s) has finished, so the live count is final
@@ -1616,7 +1620,7 @@ __device__ __forceinline__ int warp_alloc(int* cursor, int n) {
 // lex ranks of F_s).
 __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   const int cur = s & 1;
   Ctl* ctl = a.ctl;
   StepCounters& sc = ctl->sc[s & 1];
@@ -1657,7 +1661,7 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
 // parent-rank order (the one order-bearing scan: the dense lex ranks)
 __global__ void __launch_bounds__(kThreads) k_kid_scan(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   const int cur = s & 1;
   Ctl* ctl = a.ctl;
   StepCounters& sc = ctl->sc[s & 1];
@@ -1668,20 +1672,20 @@ __global__ void __launch_bounds__(kThreads) k_kid_scan(const V2* __restrict__ ap
 
 __global__ void __launch_bounds__(kThreads) k_kids(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   phase_kids(a, s);
 }
 
 __global__ void __launch_bounds__(kThreads) k_kid_fill(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->sc[s & 1].kids = a.ctl->scan_total[0];
   phase_kid_fill(a, s);
 }
 
 __global__ void __launch_bounds__(kThreads) k_place(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   Ctl* ctl = a.ctl;
   StepCounters& sc = ctl->sc[s & 1];
   const int T_ = sc.T;
@@ -1698,7 +1702,7 @@ __global__ void __launch_bounds__(kThreads) k_place(const V2* __restrict__ ap, i
 __global__ void __launch_bounds__(kThreads) k_ranks_big(const V2* __restrict__ ap, int s, int with_small) {
   const V2& a = c_v2;
   extern __shared__ unsigned long long smem_u64[];
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   phase_ranks_big(a, s, smem_u64);
   if (with_small) phase_ranks_small(a, s);  // independent of the big buckets
 }
@@ -1706,20 +1710,20 @@ __global__ void __launch_bounds__(kThreads) k_ranks_big(const V2* __restrict__ a
 // small buckets on their own (full occupancy) beside k_ranks_big in the graph
 __global__ void __launch_bounds__(kThreads) k_ranks_small(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   phase_ranks_small(a, s);
 }
 
 __global__ void MGS_LB k_tables(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   phase_tables(a, s);
 }
 
 template <int M>
 __global__ void __launch_bounds__(kThreads, 4) k_trans_big(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   if (static_cast<int>(blockIdx.x) >= a.ctl->sc[s & 1].items_b) return;  // no item for this CTA
   phase_trans_big<M>(a, s);
 }
@@ -1727,7 +1731,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_trans_big(const V2* __restrict_
 template <int M>
 __global__ void __launch_bounds__(kThreads, 4) k_trans_small(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   phase_trans_small<M>(a, s);
   {  // F_s's child counts were last read by the ranks: cleared here, off the critical path
     const int cur = s & 1, rp = a.ctl->ranks_prev[s & 1];
@@ -1748,19 +1752,19 @@ __global__ void __launch_bounds__(kThreads, 4) k_trans_small(const V2* __restric
 __global__ void __launch_bounds__(kThreads) k_band(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   extern __shared__ unsigned long long smem_u64[];
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   phase_band(a, s, smem_u64, smem_u64 + a.merge_win);
 }
 
 __global__ void MGS_LB k_write(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   phase_write(a, s);
 }
 
 __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   const int cur = s & 1;
   Ctl* ctl = a.ctl;
   if (a.dominance_ok) {
@@ -1809,7 +1813,7 @@ __device__ __forceinline__ uint32_t all_done_key(const V2& a, int M) {
 __global__ void __launch_bounds__(kThreads) k_term1(const V2* __restrict__ ap) {
   const V2& a = c_v2;
   __shared__ long long s_red[32];
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   const int fin = a.S & 1;
   const FrontierV2& F = a.f[fin];
   const int n = a.ctl->n_store[fin];
@@ -1834,7 +1838,7 @@ __global__ void __launch_bounds__(kThreads) k_term1(const V2* __restrict__ ap) {
 
 __global__ void __launch_bounds__(kThreads) k_term2(const V2* __restrict__ ap) {
   const V2& a = c_v2;
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   const int fin = a.S & 1;
   const FrontierV2& F = a.f[fin];
   const int n = a.ctl->n_store[fin];
@@ -1855,7 +1859,7 @@ __global__ void __launch_bounds__(kThreads) k_term2(const V2* __restrict__ ap) {
 
 __global__ void __launch_bounds__(kThreads) k_term3(const V2* __restrict__ ap) {
   const V2& a = c_v2;
-  if (failed(a)) return;
+  if (block_failed(a)) return;
   const int fin = a.S & 1;
   const FrontierV2& F = a.f[fin];
   const int n = a.ctl->n_store[fin];
@@ -1868,7 +1872,7 @@ __global__ void __launch_bounds__(kThreads) k_term3(const V2* __restrict__ ap) {
 
 __global__ void k_backtrack2(const V2* __restrict__ ap) {
   const V2& a = c_v2;  // parent walk (solvers.hpp:567-574)
-  if (failed(a) || threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (block_failed(a) || threadIdx.x != 0 || blockIdx.x != 0) return;
   int idx = a.ctl->best_idx;
   for (int s = a.S - 1; s >= 0; --s) {
     const long long h = a.hist_base[s + 1] + idx;
@@ -2292,10 +2296,11 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         k_kid_fill<<<g_kfill, kThreads, 0, rs_>>>(d_args, st);
         after("kid_fill", st);
         if (fork && !timed) mile(st, 2, rs_);
+        static const bool ser_rs = std::getenv("MGS_SER_RS") != nullptr;  // concurrency probe
         if (fork) {
           MGS_CUDA_OK(cudaEventRecord(ev_rs_fork, side));
           MGS_CUDA_OK(cudaStreamWaitEvent(side2, ev_rs_fork, 0));
-          k_ranks_small<<<g_rsmall, kThreads, 0, side2>>>(d_args, st);
+          k_ranks_small<<<g_rsmall, kThreads, 0, ser_rs ? side : side2>>>(d_args, st);
           if (!timed) mile(st, 4, side2);
           MGS_CUDA_OK(cudaEventRecord(ev_rs_join, side2));
           k_ranks_big<<<g_rbig, kThreads, smem_rank, side>>>(d_args, st, 0);
@@ -2304,6 +2309,11 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         } else {
           k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(d_args, st, 1);
           after("ranks", st);
+        }
+        static const bool ser_rank = std::getenv("MGS_SER_RANK") != nullptr;  // concurrency probe
+        if (fork && ser_rank) {
+          MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rank_join, 0));
+          MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rs_join, 0));
         }
         kunits<<<g_units, kThreads, 0, st_>>>(d_args, st);
         after("units", st);
@@ -2318,7 +2328,12 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
           MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rank_join, 0));
           MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rs_join, 0));
         }
-        if (fork) {  // graph: small-group transitions run beside tables -> big-group transitions
+        static const bool ser_trans = std::getenv("MGS_SER_TRANS") != nullptr;  // concurrency probe
+        if (fork && ser_trans) {
+          k_tables<<<g_tables, kThreads, 0, st_>>>(d_args, st);
+          ktbig<<<g_tbig, kThreads, 0, st_>>>(d_args, st);
+          ktsmall<<<g_tsmall, kThreads, 0, st_>>>(d_args, st);
+        } else if (fork) {  // graph: small-group transitions run beside tables -> big-group transitions
           MGS_CUDA_OK(cudaEventRecord(ev_fork, st_));
           MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_fork, 0));
           ktsmall<<<g_tsmall, kThreads, 0, side>>>(d_args, st);

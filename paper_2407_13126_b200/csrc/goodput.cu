@@ -183,6 +183,141 @@ __global__ void __launch_bounds__(1024) k_greedy(DevSpace sp, HostTables t, Recv
   cluster.sync();  // no CTA exits while another may still read its shared memory
 }
 
+// The same walk on ONE CTA when the candidates and placements fit in shared
+// memory (the usual case: thousands of candidates at M <= 2): everything the
+// walk reads is staged once, the feasible signatures are flagged once per
+// step, and a step costs one first-max over shared memory and two barriers.
+constexpr int kGreedyOneThreads = 1024;
+
+__global__ void __launch_bounds__(kGreedyOneThreads) k_greedy_one(DevSpace sp, HostTables t, Recv recv,
+                                                                  int has_initial, double* incumbent,
+                                                                  int32_t* greedy) {
+  extern __shared__ unsigned char smem[];
+  const int M = t.M, nc = sp.n_cand, P1 = sp.P1;
+  double* s_cap = reinterpret_cast<double*>(smem);                         // [P1][M]
+  uint64_t* s_pids = reinterpret_cast<uint64_t*>(s_cap + static_cast<size_t>(P1) * M);  // [P1]
+  int32_t* s_oi = reinterpret_cast<int32_t*>(s_pids + P1);                 // [nc]
+  int32_t* s_sp = s_oi + nc;                                               // [nc] sig << 20 | pid
+  __shared__ double w_v[32];
+  __shared__ int w_oi[32], w_ci[32];
+  __shared__ uint8_t s_sig_ok[1 << (3 * KM)];
+  __shared__ int s_state[KM];
+  __shared__ uint64_t s_ids;
+  __shared__ double s_value;
+  __shared__ int s_alive, s_best;
+  const Codec codec{t.S};
+  for (int i = threadIdx.x; i < P1; i += blockDim.x) {
+    for (int m = 0; m < M; ++m) s_cap[i * M + m] = sp.pl_cap[i * KM + m];
+    s_pids[i] = sp.pl_ids[i];
+  }
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    s_oi[i] = sp.cand_oi[i];
+    s_sp[i] = (sp.cand_sig[i] << 20) | sp.cand_pid[i];
+  }
+  if (threadIdx.x == 0) {
+    for (int m = 0; m < KM; ++m) s_state[m] = 0;
+    s_ids = sp.pl_ids[sp.root_pid];
+    s_value = 0.0;
+    s_alive = 1;
+  }
+  __syncthreads();
+  const int n_sig = 1 << (3 * M);
+  for (int s = 0; s < t.S; ++s) {
+    const bool charge = s > 0 || has_initial;
+    for (int g = threadIdx.x; g < n_sig; g += blockDim.x) {  // status feasibility per signature
+      bool ok = true;
+      for (int m = 0; m < M && ok; ++m) {
+        const int ns = codec.advance(t.rt[m], s_state[m], (g >> (3 * m)) & 7, s);
+        ok = ns >= 0 && !(ns == 0 && (t.min_rt[m] < 0 || s + 1 + t.min_rt[m] > t.S));
+      }
+      s_sig_ok[g] = ok ? 1 : 0;
+    }
+    __syncthreads();
+    const double value = s_value;
+    const uint64_t cur_ids = s_ids;
+    double acc[KM], rv[KM];
+    for (int m = 0; m < M; ++m) {
+      acc[m] = s_state[m] == Codec::done() ? t.post[m] : t.pre[m];
+      rv[m] = recv(m, s);
+    }
+    double bv = -DBL_MAX;
+    int boi = INT_MAX, bci = -1;
+    for (int ci = threadIdx.x; ci < nc; ci += blockDim.x) {
+      const int spv = s_sp[ci];
+      if (!s_sig_ok[spv >> 20]) continue;
+      const int p = spv & 0xfffff;
+      const uint64_t ids = s_pids[p];
+      double v = value;
+      for (int m = 0; m < M; ++m) {
+        const bool changed = charge && field16(cur_ids, m) != field16(ids, m);
+        const double eff = eff_cap(s_cap[p * M + m], changed ? t.loss[m] : 0.0);
+        v = dadd(v, dmul(thr_of(rv[m], eff), acc[m]));
+      }
+      const int oi = s_oi[ci];
+      if (g_better(v, oi, ci, bv, boi, bci)) {
+        bv = v;
+        boi = oi;
+        bci = ci;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_down_sync(0xffffffffu, bv, o);
+      const int ooi = __shfl_down_sync(0xffffffffu, boi, o);
+      const int oci = __shfl_down_sync(0xffffffffu, bci, o);
+      if (g_better(ov, ooi, oci, bv, boi, bci)) {
+        bv = ov;
+        boi = ooi;
+        bci = oci;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      w_v[threadIdx.x >> 5] = bv;
+      w_oi[threadIdx.x >> 5] = boi;
+      w_ci[threadIdx.x >> 5] = bci;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // first-max over the warps, one warp
+      const int nw = static_cast<int>(blockDim.x >> 5);
+      double v = threadIdx.x < nw ? w_v[threadIdx.x] : -DBL_MAX;
+      int oi = threadIdx.x < nw ? w_oi[threadIdx.x] : INT_MAX, ci = threadIdx.x < nw ? w_ci[threadIdx.x] : -1;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_down_sync(0xffffffffu, v, o);
+        const int ooi = __shfl_down_sync(0xffffffffu, oi, o);
+        const int oci = __shfl_down_sync(0xffffffffu, ci, o);
+        if (g_better(ov, ooi, oci, v, oi, ci)) {
+          v = ov;
+          oi = ooi;
+          ci = oci;
+        }
+      }
+      if (threadIdx.x == 0) {
+        if (ci < 0) {
+          s_alive = 0;
+          greedy[s] = -1;
+        } else {
+          greedy[s] = oi;
+          s_value = v;
+          s_best = ci;
+          const int sig = s_sp[ci] >> 20;
+          for (int m = 0; m < M; ++m) s_state[m] = codec.advance(t.rt[m], s_state[m], (sig >> (3 * m)) & 7, s);
+          s_ids = s_pids[s_sp[ci] & 0xfffff];
+        }
+      }
+    }
+    __syncthreads();
+    if (!s_alive) break;
+  }
+  if (threadIdx.x == 0) {
+    bool all_done = s_alive != 0;
+    for (int m = 0; m < M; ++m) all_done = all_done && s_state[m] == Codec::done();
+    *incumbent = all_done ? s_value : -INFINITY;
+  }
+}
+
+size_t greedy_one_smem(const DevSpace& sp, int M) {
+  return static_cast<size_t>(sp.P1) * (M * 8 + 8) + static_cast<size_t>(sp.n_cand) * 8;
+}
+
 }  // namespace
 
 void goodput_reductions(Ctx& c, const Prepared& pr, const DevSpace& sp, const double* d_recv, double* d_ub,
@@ -194,6 +329,18 @@ void goodput_reductions(Ctx& c, const Prepared& pr, const DevSpace& sp, const do
   ++c.kernel_launches;
   k_ub_suffix<<<1, 32, 0, c.stream>>>(best, t.S, d_ub);
   ++c.kernel_launches;
+  const size_t smem = greedy_one_smem(sp, t.M);
+  if (smem <= 200 * 1024 && sp.P1 < (1 << 20) && t.M <= 2) {  // placement index in 20 bits, signature above
+    static size_t configured = 0;
+    if (smem > configured) {
+      MGS_CUDA_OK(cudaFuncSetAttribute(k_greedy_one, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      configured = smem;
+    }
+    k_greedy_one<<<1, kGreedyOneThreads, smem, c.stream>>>(sp, t, recv, pr.has_initial, d_incumbent, d_greedy);
+    ++c.kernel_launches;
+    MGS_CUDA_OK(cudaGetLastError());
+    return;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(kGreedyCluster);
   cfg.blockDim = dim3(1024);

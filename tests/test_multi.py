@@ -145,7 +145,7 @@ def test_gpu_c2_shaped_windows(gpu, golden_dir):
         if "error" in g:
             with pytest.raises(capi.PlannerError) as e:
                 _gpu_solve(gpu, path)
-            assert e.value.code == g["error"], stem
+            assert e.value.code == g["error"], (stem, e.value.message)
             assert e.value.message == g["message"], stem
             seen.add(g["error"])
             continue
@@ -171,3 +171,24 @@ def test_gpu_multi_launch_engine_fallback(gpu, golden_dir, monkeypatch):
         _check(want, enc, obj, thr)
         n += 1
     assert n >= 10
+
+
+@pytest.mark.gpu
+def test_gpu_budget_error_mid_kernel_is_clean(golden_dir):
+    """Regression: planner.state-budget is raised by one block of k_units while
+    the other blocks (and the rank branch beside it) are starting. Every kernel's
+    entry check is block-uniform (__syncthreads_or), so no block can lose some of
+    its threads before a barrier or a full-warp collective. Before the fix this
+    sequence (a 4-lane C1 batch, then the M = 4 budget window in a fresh context)
+    faulted with an illegal address in about half the runs."""
+    c1 = {stem: path for stem, path, g in golden_dir["c1"]}
+    probs = [SC.Problem(SC.load_scenario(c1[s]), 0) for s in ("c1_S200_100001", "c1_S200_100002") * 2]
+    with planner.Planner(0) as pl:
+        assert (pl.solve_batch(probs)[2] == 0).all()
+    budget = dict((stem, (path, g)) for stem, path, g in golden_dir["multi_c2"])["c2_m4_S12_v2_200004"]
+    with planner.Planner(0) as pl:
+        for _ in range(4):
+            with pytest.raises(capi.PlannerError) as e:
+                _gpu_solve(pl, budget[0])
+            assert e.value.code == "planner.state-budget" and e.value.message == budget[1]["message"]
+        enc, obj, thr, _ = _gpu_solve(pl, c1["c1_S200_100001"])  # the context is still healthy
