@@ -260,6 +260,8 @@ def run_ours(args):
         legs["goodput_table"] = table_leg(pl, work, stream, args.table, rank, world, coll_dev)
     if args.c5:
         legs["config5"] = c5_leg(pl, rank, world, coll_dev)
+    if args.table > 0:
+        legs["config4_dp"] = c4_dp_leg(pl, rank, world, coll_dev)
     if world == 1 and not args.no_cpu_baseline:
         legs["same_config"] = same_config_leg(pl)
     if rank != 0:
@@ -451,6 +453,36 @@ def table_leg(pl, work, stream, n_traces, rank, world, coll_dev, reps=5):
                          "unit": "GB/s", "frac": algo / (t_ms / 1e3) / 1e9 / peak, "algorithmic_bytes": algo,
                          "peak_kind": peak_kind},
             "ub0": float(ub_h[0, 0]) if mine else None}
+
+
+def c4_dp_leg(pl, rank, world, coll_dev, n=8):
+    """Config 4's DP at the size the reference can pin: the
+    M = 2 / S = 200 variant of the C4 generator (first two tenants of traces
+    400000 + rank*n + k), n windows per rank solved as one lane batch."""
+    import tempfile
+    import torch
+    from paper_2407_13126_b200 import scenario as SC
+    from paper_2407_13126_b200 import shard
+    from paper_2407_13126_b200 import workloads as W
+    d = tempfile.mkdtemp(prefix="mgs_c4dp_")
+    seeds = [400000 + rank * n + k for k in range(n)]
+    probs = [SC.Problem(SC.load_scenario(W.write_scenario(W.c2_spec(sd, steps=200, windows=1, tenants=2), d,
+                                                          "c4_%d" % sd)), 0) for sd in seeds]
+    pl.solve_batch(probs)  # warm: capacity + graph for this lane count
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    t0 = time.perf_counter()
+    opts, obj, status, stats, errs = pl.solve_batch(probs)
+    dt = max_over_ranks(time.perf_counter() - t0, world, coll_dev)
+    rows = shard.gather_rows([[sd, shard.objective_key(float(obj[k])), int(status[k])] for k, sd in enumerate(seeds)],
+                             world, coll_dev)
+    tr = sum(st["transitions_ref"] for st in stats) * world
+    return {"workload": "config 4 DP variant: first two tenants of C4 traces, S=200, %d windows per rank as lanes" % n,
+            "value": tr / dt, "unit": UNIT, "ms_per_window": 1e3 * dt / n, "windows": len(rows),
+            "ok": sum(1 for r in rows if r[2] == 0), "scaling": "weak",
+            "timing": "host wall clock around mgs_solve_batch, max over ranks"}
 
 
 def c5_leg(pl, rank, world, coll_dev):
