@@ -383,7 +383,7 @@ def batch_leg(pl, work, rank, world, n, coll_dev):
     rows = [[100001 + rank * n + k, shard.objective_key(float(obj[k])), int(status[k])] for k in range(n)]
     rows = shard.gather_rows(rows, world, device=coll_dev)
     tr = sum(s["transitions_ref"] for s in stats) * world  # equal work per rank (same window shape)
-    lanes = int(os.environ.get("MGS_BATCH_LANES", "8"))
+    lanes = int(os.environ.get("MGS_BATCH_LANES", "16"))
     return {"workload": "%d config-1 windows per rank (%d total), %d lanes per launch" % (n, n * world, lanes),
             "value": tr / dt, "unit": UNIT, "ms_per_window": 1e3 * dt / n, "ok": sum(1 for r in rows if r[2] == 0),
             "windows": len(rows), "scaling": "weak",
