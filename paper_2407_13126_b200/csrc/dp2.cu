@@ -140,6 +140,11 @@ struct V2 {
   unsigned long long* tab_hdr;  // [tcap][2] empty subset: value bits, (rank << 32 | j)
   int32_t *ns_ucnt, *ns_ccnt, *ns_ubase, *ns_cbase, *ns_ucur, *ns_ccur, *ns_units, *ns_bigpos, *ns_smallpos;
   int32_t *ns_big, *ns_small;
+  // per successor status: bit 1 = a unit of a small group with <= kChunkS
+  // candidates (one k_trans_small item), bit 2 = any other unit. A status whose
+  // only unit is of the first kind is "fused": its k_trans_small item applies the
+  // band and writes the survivors itself, and k_band / k_write skip it
+  int32_t* ns_fflag;
   int32_t* ns_out;  // survivors per status
   unsigned long long* ns_vmax;  // vbits of the best bound-passing candidate value per status (band max)
   int32_t *it_s_unit, *it_s_chunk, *it_b_unit, *it_b_chunk;
@@ -574,6 +579,7 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
               a.u_chb[u] = small ? 0 : (L + kChunkB - 1) / kChunkB;
               atomicAdd(&a.ns_ucnt[id], 1);
               atomicAdd(&a.ns_ccnt[id], L);
+              atomicOr(&a.ns_fflag[id], small && L <= kChunkS ? 1 : 2);
               ref += a.sp.sig_nopt[sig];
             }
           }
@@ -649,6 +655,7 @@ __device__ void phase_place(const V2& a, int s) {
     const int id = a.ns_used[k];
     const int uc = a.ns_ucnt[id];
     if (uc == 0) continue;
+    if (uc == 1 && a.ns_fflag[id] == 1) continue;  // fused: finished by its k_trans_small item
     if (uc > 1 || a.ns_ccnt[id] > kBigNs) a.ns_big[a.ns_bigpos[id]] = id;
     else a.ns_small[a.ns_smallpos[id]] = id;
   }
@@ -823,10 +830,17 @@ struct BestT {
   int i[1 << M];
 };
 
+struct Cand {  // one transition's result held in registers (fused statuses)
+  double v;
+  uint64_t lex;
+  int parent;
+  bool ok;
+};
+
 template <int M>
 __device__ __forceinline__ unsigned long long emit_target(const V2& a, int s, int charge, int unit, int t_idx, int gs,
                                             const double* acc, int p, int oi, uint32_t ids_p, const BestT<M>& b,
-                                            const FrontierV2& F) {
+                                            const FrontierV2& F, Cand* c = nullptr) {
   const HostTables& t = a.t;
   double cap[M], bonus[M];
 #pragma unroll
@@ -853,9 +867,9 @@ __device__ __forceinline__ unsigned long long emit_target(const V2& a, int s, in
       cr = b.r[sub];
     }
   }
-  const int slot = a.u_cbase[unit] + t_idx;
   if (chosen < 0) {  // cannot happen: units come from groups with live states
-    a.c_ok[slot] = 0;
+    if (c) c->ok = false;
+    else a.c_ok[a.u_cbase[unit] + t_idx] = 0;
     return 0ull;
   }
   const int pred = gs + chosen;
@@ -868,11 +882,20 @@ __device__ __forceinline__ unsigned long long emit_target(const V2& a, int s, in
     v = dadd(v, dmul(thr_of(a.recv[m * t.S + s], eff), acc[m]));
   }
   const bool ok = !(dadd(v, a.ub[s + 1]) < *a.incumbent);  // solvers.hpp:459 (strict)
-  a.c_value[slot] = v;
-  a.c_lex[slot] = (static_cast<uint64_t>(F.rank[pred]) << 32) | static_cast<uint32_t>(oi);
-  a.c_parent[slot] = pred;
-  a.c_pid[slot] = p;
-  a.c_ok[slot] = ok ? 1 : 0;
+  const uint64_t lex = (static_cast<uint64_t>(F.rank[pred]) << 32) | static_cast<uint32_t>(oi);
+  if (c) {  // kept in registers: the caller finishes the status itself
+    c->v = v;
+    c->lex = lex;
+    c->parent = pred;
+    c->ok = ok;
+  } else {
+    const int slot = a.u_cbase[unit] + t_idx;
+    a.c_value[slot] = v;
+    a.c_lex[slot] = lex;
+    a.c_parent[slot] = pred;
+    a.c_pid[slot] = p;
+    a.c_ok[slot] = ok ? 1 : 0;
+  }
   return ok ? vbits(v) : 0ull;  // values are >= 0: vbits orders them
 }
 
@@ -1069,6 +1092,10 @@ __device__ void phase_trans_big(const V2& a, int s) {
 
 // Small groups: one warp per (unit, 32 targets) item; every lane owns a target
 // and scans the group's states (broadcast loads) keeping the best per subset.
+__device__ __forceinline__ bool claim_fits(const V2& a, int s, int q0, int total, int gi);
+__device__ __forceinline__ void write_state_v(const V2& a, int s, int nxt, int q, int gidx, uint32_t key, int p,
+                                              uint64_t lx, double v, int parent);
+
 template <int M>
 __device__ void phase_trans_small(const V2& a, int s) {
   const int cur = s & 1;
@@ -1087,12 +1114,17 @@ __device__ void phase_trans_small(const V2& a, int s) {
   uint32_t* gids = sh_ids[warp];
   uint32_t* grank = sh_rank[warp];
   double* gval = sh_val[warp];
+  const double band = *a.band;
   for (int item = wid; item < nis; item += nw) {
     const int unit = a.it_s_unit[item], chunk = a.it_s_chunk[item];
     const int g = a.u_group[unit], sig = a.u_sig[unit];
     const int gs = F.g_start[g], gn = F.g_size[g];
     const int sb = a.sp.sig_off[sig], L = a.sp.sig_off[sig + 1] - sb;
     const int ti = chunk * kChunkS + lane;
+    const int ns_id = a.u_ns[unit];
+    const bool fused = a.ns_ucnt[ns_id] == 1 && a.ns_fflag[ns_id] == 1;  // then L <= 32, chunk 0
+    Cand cand{0.0, 0ull, 0, false};
+    int cand_p = 0;
     // empty subset: the group's best state, one warp-cooperative pass
     double v0 = 0.0;
     uint32_t r0 = 0xffffffffu;
@@ -1132,6 +1164,7 @@ __device__ void phase_trans_small(const V2& a, int s) {
     const int p = a.sp.cand_pid[sb + ti];
     const int oi = a.sp.cand_oi[sb + ti];
     const uint32_t ids_p = a.ids32[p];
+    cand_p = p;
     BestT<M> b;
 #pragma unroll
     for (int k = 1; k < (1 << M); ++k) {
@@ -1168,13 +1201,44 @@ __device__ void phase_trans_small(const V2& a, int s) {
         }
       }
     }
-    vb_t = emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, ids_p, b, F);
+    vb_t = emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, ids_p, b, F, fused ? &cand : nullptr);
     }
     for (int o = 16; o > 0; o >>= 1) {
       const unsigned long long y = __shfl_xor_sync(0xffffffffu, vb_t, o);
       vb_t = y > vb_t ? y : vb_t;
     }
-    if (lane == 0 && vb_t) atomicMax(&a.ns_vmax[a.u_ns[unit]], vb_t);
+    if (!fused) {
+      if (lane == 0 && vb_t) atomicMax(&a.ns_vmax[a.u_ns[unit]], vb_t);
+      continue;
+    }
+    // fused status: this item holds all of its candidates (single unit, <= 32
+    // targets), so the band (solvers.hpp:499-511: the status's best bound-passing
+    // value minus band) and the output happen here, as k_write would do them
+    const double thresh = dsub(__longlong_as_double(static_cast<long long>(vb_t)), band);
+    const bool keep = ti < L && cand.ok && cand.v >= thresh;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    const int total = __popc(bal);
+    if (total == 0) continue;  // uniform
+    const int nxt = (s + 1) & 1;
+    int q0 = 0, gi = 0, fits = 0;
+    if (lane == 0) {
+      q0 = atomicAdd(&sc.out_states, total);
+      gi = atomicAdd(&sc.out_groups, 1);
+      fits = claim_fits(a, s, q0, total, gi) ? 1 : 0;
+    }
+    if (!__shfl_sync(0xffffffffu, fits, 0)) continue;
+    q0 = __shfl_sync(0xffffffffu, q0, 0);
+    gi = __shfl_sync(0xffffffffu, gi, 0);
+    const uint32_t key = a.hash[ns_id] - 1u;
+    if (lane == 0) {
+      const FrontierV2& N = a.f[nxt];
+      N.g_start[gi] = q0;
+      N.g_size[gi] = total;
+      N.g_status[gi] = key;
+      N.g_alive[gi] = total;
+    }
+    if (keep)
+      write_state_v(a, s, nxt, q0 + __popc(bal & ((1u << lane) - 1u)), gi, key, cand_p, cand.lex, cand.v, cand.parent);
   }
 }
 
@@ -1632,11 +1696,12 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
     const bool valid = k < n_ns;
     const int id = valid ? a.ns_used[k] : 0;
     const int cc = valid ? a.ns_ccnt[id] : 0, uc = valid ? a.ns_ucnt[id] : 0;
-    const bool big = valid && (uc > 1 || cc > kBigNs);
+    const bool fused = valid && uc == 1 && a.ns_fflag[id] == 1;
+    const bool big = valid && !fused && (uc > 1 || cc > kBigNs);
     const int cb = warp_alloc(&sc.T, cc);
     const int ub = warp_alloc(&sc.u_cursor, uc);
     const int bp = warp_alloc(&sc.n_big, big ? 1 : 0);
-    const int sp = warp_alloc(&sc.n_small, valid && !big ? 1 : 0);
+    const int sp = warp_alloc(&sc.n_small, valid && !big && !fused ? 1 : 0);
     if (valid) {
       a.ns_cbase[id] = cb;
       a.ns_ubase[id] = ub;
@@ -1782,6 +1847,7 @@ __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int
     a.ns_ccnt[i] = 0;
     a.ns_ucur[i] = 0;
     a.ns_ccur[i] = 0;
+    a.ns_fflag[i] = 0;
   }
   if (gtid == 0) {  // end-of-slot bookkeeping (every value read here is final)
     const int nxt = (s + 1) & 1;
@@ -2053,6 +2119,8 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, int dominance_ok, int me
   a.ns_out = c.buf<int32_t>("v2_nsout", H);
   a.ns_vmax = c.buf<unsigned long long>("v2_nsvmax", H);
   MGS_CUDA_OK(cudaMemsetAsync(a.ns_vmax, 0, H * 8, c.stream));
+  a.ns_fflag = c.buf<int32_t>("v2_nsfflag", H);
+  MGS_CUDA_OK(cudaMemsetAsync(a.ns_fflag, 0, H * 4, c.stream));
   a.ns_big = c.buf<int32_t>("v2_nsbig", H);
   a.ns_small = c.buf<int32_t>("v2_nssmall", H);
   a.ns_used = c.buf<int32_t>("v2_nsused", H);
