@@ -2369,11 +2369,10 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         k_kid_fill<<<g_kfill, kThreads, 0, rs_>>>(d_args, st);
         after("kid_fill", st);
         if (fork && !timed) mile(st, 2, rs_);
-        static const bool ser_rs = std::getenv("MGS_SER_RS") != nullptr;  // concurrency probe
         if (fork) {
           MGS_CUDA_OK(cudaEventRecord(ev_rs_fork, side));
           MGS_CUDA_OK(cudaStreamWaitEvent(side2, ev_rs_fork, 0));
-          k_ranks_small<<<g_rsmall, kThreads, 0, ser_rs ? side : side2>>>(d_args, st);
+          k_ranks_small<<<g_rsmall, kThreads, 0, side2>>>(d_args, st);
           if (!timed) mile(st, 4, side2);
           MGS_CUDA_OK(cudaEventRecord(ev_rs_join, side2));
           k_ranks_big<<<g_rbig, kThreads, smem_rank, side>>>(d_args, st, 0);
@@ -2382,11 +2381,6 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         } else {
           k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(d_args, st, 1);
           after("ranks", st);
-        }
-        static const bool ser_rank = std::getenv("MGS_SER_RANK") != nullptr;  // concurrency probe
-        if (fork && ser_rank) {
-          MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rank_join, 0));
-          MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rs_join, 0));
         }
         kunits<<<g_units, kThreads, 0, st_>>>(d_args, st);
         after("units", st);
@@ -2401,12 +2395,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
           MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rank_join, 0));
           MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rs_join, 0));
         }
-        static const bool ser_trans = std::getenv("MGS_SER_TRANS") != nullptr;  // concurrency probe
-        if (fork && ser_trans) {
-          k_tables<<<g_tables, kThreads, 0, st_>>>(d_args, st);
-          ktbig<<<g_tbig, kThreads, 0, st_>>>(d_args, st);
-          ktsmall<<<g_tsmall, kThreads, 0, st_>>>(d_args, st);
-        } else if (fork) {  // graph: small-group transitions run beside tables -> big-group transitions
+        if (fork) {  // graph: small-group transitions run beside tables -> big-group transitions
           MGS_CUDA_OK(cudaEventRecord(ev_fork, st_));
           MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_fork, 0));
           ktsmall<<<g_tsmall, kThreads, 0, side>>>(d_args, st);

@@ -24,9 +24,11 @@ gzip -f $OUT/launches_warm.csv
 timeout 1800 ncu --set full --import-source on --clock-control none -k "$DP" --launch-skip ${DP_SKIP:-1400} --launch-count 14 \
   -o $OUT/ncu_dp_step100 python scripts/solve_once.py $C1 1 > $OUT/ncu_dp.log 2>&1; echo "rc $?" >> $OUT/ncu_dp.log
 export_rep $OUT/ncu_dp_step100
-# 4. --set full of every kernel outside the step loop (first launch of each)
+# 4. --set full of every kernel outside the step loop (first launch of each); SKIP_OTHER=1 skips it
+if [ -z "$SKIP_OTHER" ]; then
 timeout 1800 ncu --set full --import-source on --clock-control none \
   -k 'regex:\bk_(?!(kids|kid_scan|kid_fill|ranks_small|ranks_big|units|scans|place|trans_small|tables|trans_big|band|write|dom)\b)' \
   --launch-count 80 -o $OUT/ncu_other python scripts/exercise_all.py > $OUT/ncu_other.log 2>&1; echo "rc $?" >> $OUT/ncu_other.log
 export_rep $OUT/ncu_other
+fi
 du -sh $OUT
