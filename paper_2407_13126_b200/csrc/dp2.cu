@@ -1565,59 +1565,78 @@ __device__ __forceinline__ bool dom_decoded(uint32_t x, uint32_t y) {
   return (x >> 24) == 2 && (y >> 24) == 2 && ((x ^ y) & 0x00ff0000u) == 0 && (x & 0xffffu) <= (y & 0xffffu);
 }
 
+// one state of a dominance bucket, decoded: per tenant kind (0 idle, 1 done,
+// 2 running) | size | remaining steps; value; lex key
+template <int MK>
+struct DomRec {
+  uint32_t d[MK];
+  double v;
+  uint64_t lx;
+};
+
+// x dominates y on every tenant (branch-free form of dom_decoded over MK fields)
+template <int MK>
+__device__ __forceinline__ bool dom_all(const uint32_t (&x)[MK], const uint32_t (&y)[MK]) {
+  bool ok = true;
+#pragma unroll
+  for (int m = 0; m < MK; ++m) ok &= dom_decoded(x[m], y[m]);
+  return ok;
+}
+
 // S7: status dominance within placement buckets (solvers.hpp:514-537).
-// MK = 2 (M <= 2, 16-bit fields) or 4 (M = 3..4, 8-bit fields).
+// MK = 2 (M <= 2, 16-bit fields) or 4 (M = 3..4, 8-bit fields). One warp per
+// bucket of 2..64 states: the bucket's decoded records are staged in the warp's
+// shared-memory slice, then every lane tests its one or two states against each
+// record in turn (broadcast loads; the second half only for buckets above 32).
 template <int MK>
 __device__ void phase_dominance(const V2& a, int s) {
+  __shared__ DomRec<MK> s_rec[kThreads / 32][64];
   const int nxt = (s + 1) & 1;
   const FrontierV2& N = a.f[nxt];
   const Codec codec{a.t.S, a.codec_shift};
   const int lane = threadIdx.x & 31;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  DomRec<MK>* R = s_rec[threadIdx.x >> 5];
   const int MT = a.t.M;
   for (int p = wid; p < a.sp.P1; p += nw) {
     const int n = a.pcnt[p];
     if (n >= 2 && n <= 64) {
       const int* bk = a.pbucket + p * 64;
       int q[2];
-      uint32_t dk[2][MK];
-      double v[2];
-      uint64_t lx[2];
+      DomRec<MK> me[2];
       for (int h = 0; h < 2; ++h) {
         const int j = lane + 32 * h;
         q[h] = j < n ? bk[j] : -1;
         const uint32_t st = q[h] >= 0 ? N.status[q[h]] : 0;
-        v[h] = q[h] >= 0 ? N.value[q[h]] : 0.0;
-        lx[h] = q[h] >= 0 ? N.lex[q[h]] : 0;
+        me[h].v = q[h] >= 0 ? N.value[q[h]] : 0.0;
+        me[h].lx = q[h] >= 0 ? N.lex[q[h]] : 0;
 #pragma unroll
-        for (int m = 0; m < MK; ++m) {  // decode once: kind (0 idle, 1 done, 2 running) | size | rem
+        for (int m = 0; m < MK; ++m) {  // decode once
           const int code = m < MT ? fldm<MK>(st, m) : 0;
-          dk[h][m] = code == Codec::done() ? (1u << 24)
-                     : Codec::is_running(code) ? (2u << 24) | (static_cast<uint32_t>(codec.run_size(code)) << 16) |
-                                                     static_cast<uint32_t>(codec.run_rem(code))
-                                               : 0u;
+          me[h].d[m] = code == Codec::done() ? (1u << 24)
+                       : Codec::is_running(code) ? (2u << 24) | (static_cast<uint32_t>(codec.run_size(code)) << 16) |
+                                                       static_cast<uint32_t>(codec.run_rem(code))
+                                                 : 0u;
         }
+        if (q[h] >= 0) R[j] = me[h];
       }
+      __syncwarp();
       bool dead[2] = {false, false};
-      for (int j = 0; j < n; ++j) {
-        const int h = j >> 5, src = j & 31;
-        const uint32_t d0 = __shfl_sync(0xffffffffu, dk[h][0], src);
-        const uint32_t d1 = __shfl_sync(0xffffffffu, dk[h][1], src);
-        uint32_t d2 = 0, d3 = 0;
-        if constexpr (MK > 2) {
-          d2 = __shfl_sync(0xffffffffu, dk[h][2], src);
-          d3 = __shfl_sync(0xffffffffu, dk[h][3], src);
+      if (n <= 32) {
+#pragma unroll 4
+        for (int j = 0; j < n; ++j) {
+          const DomRec<MK> r = R[j];
+          dead[0] |= (j != lane) & dom_all<MK>(r.d, me[0].d) & better(r.v, r.lx, me[0].v, me[0].lx);
         }
-        const double va = __shfl_sync(0xffffffffu, v[h], src);
-        const uint64_t la = __shfl_sync(0xffffffffu, lx[h], src);
-        for (int hb = 0; hb < 2; ++hb) {
-          if (q[hb] < 0 || lane + 32 * hb == j) continue;
-          if (dom_decoded(d0, dk[hb][0]) && dom_decoded(d1, dk[hb][1]) &&
-              (MK <= 2 || (dom_decoded(d2, dk[hb][MK > 2 ? 2 : 0]) && dom_decoded(d3, dk[hb][MK > 2 ? 3 : 0]))) &&
-              better(va, la, v[hb], lx[hb]))
-            dead[hb] = true;
+      } else {
+#pragma unroll 2
+        for (int j = 0; j < n; ++j) {
+          const DomRec<MK> r = R[j];
+          dead[0] |= (j != lane) & dom_all<MK>(r.d, me[0].d) & better(r.v, r.lx, me[0].v, me[0].lx);
+          dead[1] |= (j != lane + 32) & dom_all<MK>(r.d, me[1].d) & better(r.v, r.lx, me[1].v, me[1].lx);
         }
       }
+      __syncwarp();  // R is rewritten by the warp's next bucket
       int kills = 0;
       for (int h = 0; h < 2; ++h)
         if (q[h] >= 0 && dead[h]) {
