@@ -1623,13 +1623,13 @@ __device__ void phase_dominance(const V2& a, int s) {
       __syncwarp();
       bool dead[2] = {false, false};
       if (n <= 32) {
-#pragma unroll 4
+#pragma unroll 2
         for (int j = 0; j < n; ++j) {
           const DomRec<MK> r = R[j];
           dead[0] |= (j != lane) & dom_all<MK>(r.d, me[0].d) & better(r.v, r.lx, me[0].v, me[0].lx);
         }
       } else {
-#pragma unroll 2
+#pragma unroll 1
         for (int j = 0; j < n; ++j) {
           const DomRec<MK> r = R[j];
           dead[0] |= (j != lane) & dom_all<MK>(r.d, me[0].d) & better(r.v, r.lx, me[0].v, me[0].lx);
