@@ -125,7 +125,7 @@ struct V2 {
   int32_t* h_oi;
   long long hcap;
   long long* hist_base;  // [S+2]
-  int32_t *u_group, *u_sig, *u_ns, *u_chs, *u_chb, *u_cbase, *u_sbase, *u_bbase;
+  int32_t *u_group, *u_sig, *u_ns, *u_chs, *u_chb, *u_cbase, *u_upos;  // u_cbase: within the status's range
   int ucap;
   uint32_t* hash;  // key+1 per slot; the slot index is the successor-status id
   int hmask;
@@ -138,7 +138,7 @@ struct V2 {
   unsigned long long* tab_rx;   // [tcap][n_partial] (rank << 32 | j) of the best among the max
   uint32_t* tab_ex;         // [tcap][P1] j + 1 of the group's state at each placement (0 = none)
   unsigned long long* tab_hdr;  // [tcap][2] empty subset: value bits, (rank << 32 | j)
-  int32_t *ns_ucnt, *ns_ccnt, *ns_ubase, *ns_cbase, *ns_ucur, *ns_ccur, *ns_units, *ns_bigpos, *ns_smallpos;
+  int32_t *ns_ucnt, *ns_ccnt, *ns_ubase, *ns_cbase, *ns_units;
   int32_t *ns_big, *ns_small;
   // per successor status: bit 1 = a unit of a small group with <= kChunkS
   // candidates (one k_trans_small item), bit 2 = any other unit. A status whose
@@ -577,8 +577,10 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
               a.u_ns[u] = id;
               a.u_chs[u] = small ? (L + kChunkS - 1) / kChunkS : 0;
               a.u_chb[u] = small ? 0 : (L + kChunkB - 1) / kChunkB;
-              atomicAdd(&a.ns_ucnt[id], 1);
-              atomicAdd(&a.ns_ccnt[id], L);
+              // the unit's slot in its status's unit list and candidate range
+              // (k_scans places the status's range; order is irrelevant)
+              a.u_upos[u] = atomicAdd(&a.ns_ucnt[id], 1);
+              a.u_cbase[u] = atomicAdd(&a.ns_ccnt[id], L);
               atomicOr(&a.ns_fflag[id], small && L <= kChunkS ? 1 : 2);
               ref += a.sp.sig_nopt[sig];
             }
@@ -626,41 +628,6 @@ __device__ void phase_kids(const V2& a, int s) {
 }
 
 // S3: placement
-__device__ void phase_place(const V2& a, int s) {
-  const int cur = s & 1;
-  StepCounters& sc = a.ctl->sc[s & 1];
-  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
-  const int NU = sc.n_units;
-  for (int u = gtid; u < NU; u += gstride) {
-    // loads and atomics before the first store (no load may wait behind a store)
-    const int id = a.u_ns[u];
-    const int L = a.sig_len[a.u_sig[u]];
-    const int nsm = a.u_chs[u], nbg = a.u_chb[u];
-    const int sb = a.u_sbase[u], bb = a.u_bbase[u];
-    const int cbase = a.ns_cbase[id], ubase = a.ns_ubase[id];
-    const int cpos = atomicAdd(&a.ns_ccur[id], L), upos = atomicAdd(&a.ns_ucur[id], 1);
-    a.u_cbase[u] = cbase + cpos;
-    a.ns_units[ubase + upos] = u;
-    for (int c = 0; c < nsm; ++c) {
-      a.it_s_unit[sb + c] = u;
-      a.it_s_chunk[sb + c] = c;
-    }
-    for (int c = 0; c < nbg; ++c) {
-      a.it_b_unit[bb + c] = u;
-      a.it_b_chunk[bb + c] = c;
-    }
-  }
-  const int n_ns = sc.n_ns;
-  for (int k = gtid; k < n_ns; k += gstride) {
-    const int id = a.ns_used[k];
-    const int uc = a.ns_ucnt[id];
-    if (uc == 0) continue;
-    if (uc == 1 && a.ns_fflag[id] == 1) continue;  // fused: finished by its k_trans_small item
-    if (uc > 1 || a.ns_ccnt[id] > kBigNs) a.ns_big[a.ns_bigpos[id]] = id;
-    else a.ns_small[a.ns_smallpos[id]] = id;
-  }
-}
-
 // R3 (rank branch): children into their parent's slots
 __device__ void phase_kid_fill(const V2& a, int s) {
   const int cur = s & 1;
@@ -838,7 +805,7 @@ struct Cand {  // one transition's result held in registers (fused statuses)
 };
 
 template <int M>
-__device__ __forceinline__ unsigned long long emit_target(const V2& a, int s, int charge, int unit, int t_idx, int gs,
+__device__ __forceinline__ unsigned long long emit_target(const V2& a, int s, int charge, int cbu, int t_idx, int gs,
                                             const double* acc, int p, int oi, uint32_t ids_p, const BestT<M>& b,
                                             const FrontierV2& F, Cand* c = nullptr) {
   const HostTables& t = a.t;
@@ -869,7 +836,7 @@ __device__ __forceinline__ unsigned long long emit_target(const V2& a, int s, in
   }
   if (chosen < 0) {  // cannot happen: units come from groups with live states
     if (c) c->ok = false;
-    else a.c_ok[a.u_cbase[unit] + t_idx] = 0;
+    else a.c_ok[cbu + t_idx] = 0;
     return 0ull;
   }
   const int pred = gs + chosen;
@@ -889,7 +856,7 @@ __device__ __forceinline__ unsigned long long emit_target(const V2& a, int s, in
     c->parent = pred;
     c->ok = ok;
   } else {
-    const int slot = a.u_cbase[unit] + t_idx;
+    const int slot = cbu + t_idx;
     a.c_value[slot] = v;
     a.c_lex[slot] = lex;
     a.c_parent[slot] = pred;
@@ -1036,8 +1003,10 @@ __device__ void phase_trans_big(const V2& a, int s) {
   const int nib = sc.items_b;
   for (int item = blockIdx.x; item < nib; item += gridDim.x) {
     const int unit = a.it_b_unit[item], chunk = a.it_b_chunk[item];
-    const int g = a.u_group[unit], sig = a.u_sig[unit];
+    const int g = a.u_group[unit], sig = a.u_sig[unit], ns_id = a.u_ns[unit];
     const int gs = F.g_start[g];
+    const int cbu = a.ns_cbase[ns_id] + a.u_cbase[unit];
+    if (chunk == 0 && threadIdx.x == 0) a.ns_units[a.ns_ubase[ns_id] + a.u_upos[unit]] = unit;  // for k_band's merge
     const int b = a.g_tab[g];
     const unsigned long long* vb = a.tab_vb + static_cast<size_t>(b) * np;
     const unsigned long long* rxs = a.tab_rx + static_cast<size_t>(b) * np;
@@ -1079,7 +1048,7 @@ __device__ void phase_trans_big(const V2& a, int s) {
         }
       }
       const unsigned long long vb_t =
-          emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, a.ids32[p], bt, F);
+          emit_target<M>(a, s, charge, cbu, ti, gs, acc, p, oi, a.ids32[p], bt, F);
       vmax = vb_t > vmax ? vb_t : vmax;
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -1123,6 +1092,8 @@ __device__ void phase_trans_small(const V2& a, int s) {
     const int ti = chunk * kChunkS + lane;
     const int ns_id = a.u_ns[unit];
     const bool fused = a.ns_ucnt[ns_id] == 1 && a.ns_fflag[ns_id] == 1;  // then L <= 32, chunk 0
+    const int cbu = a.ns_cbase[ns_id] + a.u_cbase[unit];
+    if (chunk == 0 && lane == 0) a.ns_units[a.ns_ubase[ns_id] + a.u_upos[unit]] = unit;  // for k_band's merge
     Cand cand{0.0, 0ull, 0, false};
     int cand_p = 0;
     // empty subset: the group's best state, one warp-cooperative pass
@@ -1201,7 +1172,7 @@ __device__ void phase_trans_small(const V2& a, int s) {
         }
       }
     }
-    vb_t = emit_target<M>(a, s, charge, unit, ti, gs, acc, p, oi, ids_p, b, F, fused ? &cand : nullptr);
+    vb_t = emit_target<M>(a, s, charge, cbu, ti, gs, acc, p, oi, ids_p, b, F, fused ? &cand : nullptr);
     }
     for (int o = 16; o > 0; o >>= 1) {
       const unsigned long long y = __shfl_xor_sync(0xffffffffu, vb_t, o);
@@ -1315,7 +1286,7 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
             const int u = a.ns_units[ub + q];
             const int sig = a.u_sig[u];
             const int b = a.sp.sig_off[sig], n = a.sp.sig_off[sig + 1] - b;
-            const int cbu = a.u_cbase[u];
+            const int cbu = cb + a.u_cbase[u];
             int lo = 0;
             if (w0 > 0) {  // the unit's candidates are sorted by placement: clip to the window
               int hi = n;
@@ -1699,8 +1670,10 @@ __device__ __forceinline__ int warp_alloc(int* cursor, int n) {
 // S2: ranges for the step's successor statuses (candidates, units, big/small
 // status lists) and units (work items), reserved with warp-aggregated
 // atomics -- their order is arbitrary and nothing depends on it -- and the
-// one order-bearing scan: children offsets in parent-rank order (the dense
-// lex ranks of F_s).
+// lists written straight away: the status lists here, the work-item lists
+// here (bounded by their capacity; the consumers check the totals at entry),
+// each unit's candidate range and list slot by the transition kernels (from
+// its offsets within the status, taken by k_units).
 __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (block_failed(a)) return;
@@ -1724,21 +1697,36 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
     if (valid) {
       a.ns_cbase[id] = cb;
       a.ns_ubase[id] = ub;
-      a.ns_bigpos[id] = bp;
-      a.ns_smallpos[id] = sp;
+      if (big) a.ns_big[bp] = id;
+      else if (!fused) a.ns_small[sp] = id;  // fused: finished by its k_trans_small item
     }
   }
   const int nu = sc.n_units;
   for (int u0 = gtid - lane; u0 < nu; u0 += gstride) {
     const int u = u0 + lane;
     const bool valid = u < nu;
-    const int sb = warp_alloc(&sc.items_s, valid ? a.u_chs[u] : 0);
-    const int bb = warp_alloc(&sc.items_b, valid ? a.u_chb[u] : 0);
-    if (valid) {
-      a.u_sbase[u] = sb;
-      a.u_bbase[u] = bb;
-    }
+    const int nsm = valid ? a.u_chs[u] : 0, nbg = valid ? a.u_chb[u] : 0;
+    const int sb = warp_alloc(&sc.items_s, nsm);
+    const int bb = warp_alloc(&sc.items_b, nbg);
+    if (sb + nsm <= a.itcap)
+      for (int c = 0; c < nsm; ++c) {
+        a.it_s_unit[sb + c] = u;
+        a.it_s_chunk[sb + c] = c;
+      }
+    if (bb + nbg <= a.itcap)
+      for (int c = 0; c < nbg; ++c) {
+        a.it_b_unit[bb + c] = u;
+        a.it_b_chunk[bb + c] = c;
+      }
   }
+}
+
+// the step's candidate range and work-item lists fit their buffers (the totals
+// are final once k_scans is done); read by every block of the consumers, so
+// their early exit is block-uniform
+__device__ __forceinline__ bool lists_fit(const V2& a, int s) {
+  const StepCounters& sc = a.ctl->sc[s & 1];
+  return sc.T <= a.ccap && sc.items_s <= a.itcap && sc.items_b <= a.itcap;
 }
 
 // R2 (rank branch): frontier checks for F_s and the children offsets in
@@ -1767,22 +1755,6 @@ __global__ void __launch_bounds__(kThreads) k_kid_fill(const V2* __restrict__ ap
   phase_kid_fill(a, s);
 }
 
-__global__ void __launch_bounds__(kThreads) k_place(const V2* __restrict__ ap, int s) {
-  const V2& a = c_v2;
-  if (block_failed(a)) return;
-  Ctl* ctl = a.ctl;
-  StepCounters& sc = ctl->sc[s & 1];
-  const int T_ = sc.T;
-  const bool fits = T_ <= a.ccap && sc.items_s <= a.itcap && sc.items_b <= a.itcap;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    ctl->tr += static_cast<unsigned long long>(T_);
-    ctl->tbytes += static_cast<unsigned long long>(ctl->n_store[s & 1]) * 20ull + static_cast<unsigned long long>(T_) * 37ull;
-    if (T_ > a.ccap) raise_err(a, 0, kOverflow, s, 0, 7, T_);
-    if (sc.items_s > a.itcap || sc.items_b > a.itcap) raise_err(a, 0, kOverflow, s, 0, 8, max(sc.items_s, sc.items_b));
-  }
-  if (fits) phase_place(a, s);
-}
-
 __global__ void __launch_bounds__(kThreads) k_ranks_big(const V2* __restrict__ ap, int s, int with_small) {
   const V2& a = c_v2;
   extern __shared__ unsigned long long smem_u64[];
@@ -1801,13 +1773,23 @@ __global__ void __launch_bounds__(kThreads) k_ranks_small(const V2* __restrict__
 __global__ void MGS_LB k_tables(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (block_failed(a)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // overflow of k_scans' lists; transition counters
+    Ctl* ctl = a.ctl;
+    const StepCounters& sc = ctl->sc[s & 1];
+    const int T_ = sc.T;
+    ctl->tr += static_cast<unsigned long long>(T_);
+    ctl->tbytes += static_cast<unsigned long long>(ctl->n_store[s & 1]) * 20ull + static_cast<unsigned long long>(T_) * 37ull;
+    if (T_ > a.ccap) raise_err(a, 0, kOverflow, s, 0, 7, T_);
+    if (sc.items_s > a.itcap || sc.items_b > a.itcap) raise_err(a, 0, kOverflow, s, 0, 8, max(sc.items_s, sc.items_b));
+  }
+  if (!lists_fit(a, s)) return;
   phase_tables(a, s);
 }
 
 template <int M>
 __global__ void __launch_bounds__(kThreads, 4) k_trans_big(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (block_failed(a)) return;
+  if (block_failed(a) || !lists_fit(a, s)) return;
   if (static_cast<int>(blockIdx.x) >= a.ctl->sc[s & 1].items_b) return;  // no item for this CTA
   phase_trans_big<M>(a, s);
 }
@@ -1815,7 +1797,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_trans_big(const V2* __restrict_
 template <int M>
 __global__ void __launch_bounds__(kThreads, 4) k_trans_small(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (block_failed(a)) return;
+  if (block_failed(a) || !lists_fit(a, s)) return;  // k_tables raises the overflow
   phase_trans_small<M>(a, s);
   {  // F_s's child counts were last read by the ranks: cleared here, off the critical path
     const int cur = s & 1, rp = a.ctl->ranks_prev[s & 1];
@@ -1864,8 +1846,6 @@ __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int
     a.ns_vmax[i] = 0ull;
     a.ns_ucnt[i] = 0;
     a.ns_ccnt[i] = 0;
-    a.ns_ucur[i] = 0;
-    a.ns_ccur[i] = 0;
     a.ns_fflag[i] = 0;
   }
   if (gtid == 0) {  // end-of-slot bookkeeping (every value read here is final)
@@ -2121,8 +2101,7 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, int dominance_ok, int me
   a.u_chs = c.buf<int32_t>("v2_uchs", caps.ucap);
   a.u_chb = c.buf<int32_t>("v2_uchb", caps.ucap);
   a.u_cbase = c.buf<int32_t>("v2_ucbase", caps.ucap);
-  a.u_sbase = c.buf<int32_t>("v2_usbase", caps.ucap);
-  a.u_bbase = c.buf<int32_t>("v2_ubbase", caps.ucap);
+  a.u_upos = c.buf<int32_t>("v2_uupos", caps.ucap);
   a.ns_units = c.buf<int32_t>("v2_nsunits", caps.ucap);
   a.hmask = (1 << caps.hbits) - 1;
   const size_t H = static_cast<size_t>(a.hmask) + 1;
@@ -2131,10 +2110,6 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, int dominance_ok, int me
   a.ns_ccnt = c.buf<int32_t>("v2_nsccnt", H);
   a.ns_ubase = c.buf<int32_t>("v2_nsubase", H);
   a.ns_cbase = c.buf<int32_t>("v2_nscbase", H);
-  a.ns_ucur = c.buf<int32_t>("v2_nsucur", H);
-  a.ns_ccur = c.buf<int32_t>("v2_nsccur", H);
-  a.ns_bigpos = c.buf<int32_t>("v2_nsbigpos", H);
-  a.ns_smallpos = c.buf<int32_t>("v2_nssmallpos", H);
   a.ns_out = c.buf<int32_t>("v2_nsout", H);
   a.ns_vmax = c.buf<unsigned long long>("v2_nsvmax", H);
   MGS_CUDA_OK(cudaMemsetAsync(a.ns_vmax, 0, H * 8, c.stream));
@@ -2152,7 +2127,7 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, int dominance_ok, int me
   a.tab_ex = c.buf<uint32_t>("v2_tabex", static_cast<size_t>(caps.tcap) * sp.P1);
   a.tab_hdr = c.buf<unsigned long long>("v2_tabhdr", static_cast<size_t>(caps.tcap) * 2);
   for (void* z : {static_cast<void*>(a.hash), static_cast<void*>(a.ns_ucnt), static_cast<void*>(a.ns_ccnt),
-                  static_cast<void*>(a.ns_ucur), static_cast<void*>(a.ns_ccur), static_cast<void*>(a.ns_out)})
+                  static_cast<void*>(a.ns_out)})
     MGS_CUDA_OK(cudaMemsetAsync(z, 0, H * 4, c.stream));
   a.itcap = caps.itcap;
   a.it_s_unit = c.buf<int32_t>("v2_itsu", caps.itcap);
@@ -2249,7 +2224,6 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   const dim3 g_one(1, static_cast<unsigned>(K));
   const dim3 g_units = wave(reinterpret_cast<const void*>(kunits), 0);
   const dim3 g_scans = wave(reinterpret_cast<const void*>(k_scans), 0);
-  const dim3 g_place = wave(reinterpret_cast<const void*>(k_place), 0);
   const dim3 g_rsmall = wave(reinterpret_cast<const void*>(k_ranks_small), 0);
   const dim3 g_kids = wave(reinterpret_cast<const void*>(k_kids), 0);
   const dim3 g_kscan = wave(reinterpret_cast<const void*>(k_kid_scan), 0);
@@ -2265,7 +2239,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr || std::getenv("MGS_TRACE") != nullptr;
   if (std::getenv("MGS_TRACE"))
     std::fprintf(stderr, "trace v2 setup: lanes %d S %d M %d smem trans %zu rank %zu merge %zu grid.x %u %u %u %u %u %u %u %u %u %u\n",
-                 K, S, M, size_t(0), smem_rank, smem_merge, g_units.x, g_scans.x, g_place.x, g_rbig.x, 0u,
+                 K, S, M, size_t(0), smem_rank, smem_merge, g_units.x, g_scans.x, 0u, g_rbig.x, 0u,
                  g_tbig.x, g_tsmall.x, g_band.x, g_write.x, g_dom.x);
   for (int attempt = 0; attempt < 10; ++attempt) {
     std::vector<V2> args(K);
@@ -2277,8 +2251,8 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     // The window's kernel sequence depends only on S, M, the lane count and
     // launch shapes (all problem data lives behind d_args), so it is captured
     // once into a CUDA graph and replayed; MGS_DEBUG_STEPS launches eagerly.
-    constexpr int kK = 13;
-    static const char* kNames[kK] = {"kids", "kid_scan", "kid_fill", "ranks", "units", "scans", "place", "tables",
+    constexpr int kK = 12;
+    static const char* kNames[kK] = {"kids", "kid_scan", "kid_fill", "ranks", "units", "scans", "tables",
                                      "trans_big", "trans_small", "band", "write", "dom"};
     std::vector<cudaEvent_t> evs;
     // trans_small depends only on the ranks, not on the subset tables (it
@@ -2301,7 +2275,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     // milestones inside each step (graph mode, MGS_STEP_TIMES): where the critical path runs
     constexpr int kMile = 12;
     static const char* kMileNames[kMile] = {"kids", "kid_scan", "kid_fill", "ranks_big", "ranks_small", "units",
-                                            "scans", "place", "trans_big", "trans_small", "band", "write"};
+                                            "scans", "-", "trans_big", "trans_small", "band", "write"};
     static std::vector<cudaEvent_t> mile_ev;
     if (!step_ev.empty() && static_cast<int>(mile_ev.size()) < S * kMile) {
       for (auto e : mile_ev) cudaEventDestroy(e);
@@ -2407,9 +2381,6 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         k_scans<<<g_scans, kThreads, 0, st_>>>(d_args, st);
         after("scans", st);
         if (fork && !timed) mile(st, 6, st_);
-        k_place<<<g_place, kThreads, 0, st_>>>(d_args, st);
-        after("place", st);
-        if (fork && !timed) mile(st, 7, st_);
         if (fork) {
           MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rank_join, 0));
           MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rs_join, 0));
