@@ -605,27 +605,6 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
   if (threadIdx.x == 0 && rs) atomicAdd(&a.ctl->tr_ref, static_cast<unsigned long long>(rs));
 }
 
-// R1 (rank branch): children per parent rank + live-state count of F_s.
-// Every stored state is counted; k_dom of the previous step takes the states
-// it kills off both counters (atomics on both sides, so the two kernels may
-// run in either order or concurrently: in the graph this one runs beside
-// k_dom, straight after k_write).
-__device__ void phase_kids(const V2& a, int s) {
-  const int cur = s & 1;
-  const FrontierV2& F = a.f[cur];
-  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
-  const int n = s == 0 ? a.ctl->n_store[0] : a.ctl->sc[(s - 1) & 1].out_states;  // k_dom may not have published n_store yet
-  int i = gtid;
-  for (; i + 3 * gstride < n; i += 4 * gstride) {  // four loads in flight before the atomics
-    uint64_t l[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) l[u] = F.lex[i + u * gstride];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) atomicAdd(&a.kid_cnt[cur][l[u] >> 32], 1);
-  }
-  for (; i < n; i += gstride) atomicAdd(&a.kid_cnt[cur][F.lex[i] >> 32], 1);
-  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.ctl->alive_now[cur], n);
-}
 
 // S3: placement
 // R3 (rank branch): children into their parent's slots
@@ -1227,6 +1206,10 @@ __device__ __forceinline__ void write_state_v(const V2& a, int s, int nxt, int q
   // bucket count only grows within the step: once a (possibly stale) read shows
   // more than 64, the bucket is dead and its atomic can be skipped
   const int slot = a.dominance_ok && a.pcnt[p] <= 64 ? atomicAdd(&a.pcnt[p], 1) : 64;
+  // R1 (rank branch) folded in: children per parent rank of F_s, for the dense
+  // ranks of F_{s+1}. Every stored state is counted (live or dominated: the
+  // ranks are over stored states); F_S is never ranked.
+  if (s + 1 < a.S) atomicAdd(&a.kid_cnt[nxt][static_cast<uint32_t>(lx >> 32)], 1);
   N.status[q] = key;
   N.ids[q] = ids;
   N.pid[q] = p;
@@ -1742,12 +1725,6 @@ __global__ void __launch_bounds__(kThreads) k_kid_scan(const V2* __restrict__ ap
   multi_scan(a, jobs, 1, 2 * (s + 1), &sc.ticket, ctl->scan_total);
 }
 
-__global__ void __launch_bounds__(kThreads) k_kids(const V2* __restrict__ ap, int s) {
-  const V2& a = c_v2;
-  if (block_failed(a)) return;
-  phase_kids(a, s);
-}
-
 __global__ void __launch_bounds__(kThreads) k_kid_fill(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (block_failed(a)) return;
@@ -1852,6 +1829,7 @@ __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int
     const int nxt = (s + 1) & 1;
     StepCounters& sc = ctl->sc[s & 1];
     ctl->n_store[nxt] = sc.out_states;   // F_{s+1} as allocated by k_write
+    if (s + 1 < a.S) atomicAdd(&ctl->alive_now[nxt], sc.out_states);  // k_dom's kills are subtracted beside it
     ctl->n_groups[nxt] = sc.out_groups;
     a.hist_base[s + 2] = a.hist_base[s + 1] + ctl->n_store[nxt];  // array has S+2 entries
     if (a.dbg) {
@@ -1970,6 +1948,8 @@ __global__ void k_init_root(const V2* __restrict__ ap) {
   c->best_lex = ~0ull;
   c->best_idx = -1;
   c->ranks_prev[0] = 1;
+  c->alive_now[0] = 1;
+  a.kid_cnt[0][0] = 1;  // the root's child count under its (rank 0) parent
   a.hist_base[0] = 0;
   a.hist_base[1] = 0;
 }
@@ -2225,7 +2205,6 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   const dim3 g_units = wave(reinterpret_cast<const void*>(kunits), 0);
   const dim3 g_scans = wave(reinterpret_cast<const void*>(k_scans), 0);
   const dim3 g_rsmall = wave(reinterpret_cast<const void*>(k_ranks_small), 0);
-  const dim3 g_kids = wave(reinterpret_cast<const void*>(k_kids), 0);
   const dim3 g_kscan = wave(reinterpret_cast<const void*>(k_kid_scan), 0);
   const dim3 g_kfill = wave(reinterpret_cast<const void*>(k_kid_fill), 0);
   const dim3 g_rbig = wave(reinterpret_cast<const void*>(k_ranks_big), smem_rank);
@@ -2251,8 +2230,8 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     // The window's kernel sequence depends only on S, M, the lane count and
     // launch shapes (all problem data lives behind d_args), so it is captured
     // once into a CUDA graph and replayed; MGS_DEBUG_STEPS launches eagerly.
-    constexpr int kK = 12;
-    static const char* kNames[kK] = {"kids", "kid_scan", "kid_fill", "ranks", "units", "scans", "tables",
+    constexpr int kK = 11;
+    static const char* kNames[kK] = {"kid_scan", "kid_fill", "ranks", "units", "scans", "tables",
                                      "trans_big", "trans_small", "band", "write", "dom"};
     std::vector<cudaEvent_t> evs;
     // trans_small depends only on the ranks, not on the subset tables (it
@@ -2274,7 +2253,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     }
     // milestones inside each step (graph mode, MGS_STEP_TIMES): where the critical path runs
     constexpr int kMile = 12;
-    static const char* kMileNames[kMile] = {"kids", "kid_scan", "kid_fill", "ranks_big", "ranks_small", "units",
+    static const char* kMileNames[kMile] = {"-", "kid_scan", "kid_fill", "ranks_big", "ranks_small", "units",
                                             "scans", "-", "trans_big", "trans_small", "band", "write"};
     static std::vector<cudaEvent_t> mile_ev;
     if (!step_ev.empty() && static_cast<int>(mile_ev.size()) < S * kMile) {
@@ -2343,18 +2322,12 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         // rank branch (F_s's dense lex ranks) beside the unit branch
         // (successor statuses and candidate ranges): they meet at the transitions
         cudaStream_t rs_ = fork ? side : st_;
-        if (fork) {
-          // later steps launch k_kids right after the previous k_write, beside
-          // k_dom: the rank branch (stored-state ranks) does not wait for dominance
-          if (st == 0) {
-            MGS_CUDA_OK(cudaEventRecord(ev_rank_fork, st_));
-            MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_rank_fork, 0));
-            k_kids<<<g_kids, kThreads, 0, side>>>(d_args, st);
-            if (!timed) mile(st, 0, side);
-          }
-        } else {
-          k_kids<<<g_kids, kThreads, 0, rs_>>>(d_args, st);
-          after("kids", st);
+        if (fork && st == 0) {
+          // later steps fork the rank branch right after the previous k_write
+          // (which counted the children), beside k_dom: the rank branch
+          // (stored-state ranks) does not wait for dominance
+          MGS_CUDA_OK(cudaEventRecord(ev_rank_fork, st_));
+          MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_rank_fork, 0));
         }
         k_kid_scan<<<g_kscan, kThreads, 0, rs_>>>(d_args, st);
         after("kid_scan", st);
@@ -2412,8 +2385,6 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         if (fork && st + 1 < S) {
           MGS_CUDA_OK(cudaEventRecord(ev_rank_fork, st_));
           MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_rank_fork, 0));
-          k_kids<<<g_kids, kThreads, 0, side>>>(d_args, st + 1);
-          if (!timed) mile(st + 1, 0, side);
         }
         k_dom<<<g_dom, kThreads, 0, st_>>>(d_args, st);
         after("dom", st);
