@@ -312,7 +312,7 @@ def run_ours(args):
                 "decision_latency_ms": 1e3 * e2e_s / args.steps,
                 "timing": "host wall clock around the C-ABI solve (pinned forecast in, plan out), max over ranks"},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": "per-window DP graph (14 phase kernels x S steps in three graph branches, one graph launch)",
+        "roofline": {"bound": "hbm", "kernel": "per-window DP graph (12 phase kernels x S steps in three graph branches, one graph launch)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None,
                      "traffic": traffic.get("bytes_per_window") if traffic else None,
