@@ -1251,7 +1251,9 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
     int mine = 0;
     if (uc == 1) {
       for (int k = cb + threadIdx.x; k < cb + cc; k += kThreads) {
-        const bool keep = a.c_ok[k] && a.c_value[k] >= thresh;
+        const uint8_t ok = a.c_ok[k];  // both loads issued together (no load behind a branch)
+        const double v = a.c_value[k];
+        const bool keep = ok && v >= thresh;
         a.c_live[k] = keep ? 1 : 0;
         mine += keep;
       }
@@ -1470,9 +1472,13 @@ __device__ void phase_write(const V2& a, int s) {
       }
     } else {
       int total = 0;
-      for (int k0 = cb; k0 < cb + cc; k0 += 32) {
-        const int k = k0 + lane;
-        total += __popc(__ballot_sync(0xffffffffu, k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh));
+      for (int k0 = cb; k0 < cb + cc; k0 += 64) {  // two chunks' loads in flight, none behind a branch
+        const int k1 = k0 + lane, k2 = k1 + 32;
+        const bool in1 = k1 < cb + cc, in2 = k2 < cb + cc;
+        const uint8_t o1 = in1 ? a.c_ok[k1] : 0, o2 = in2 ? a.c_ok[k2] : 0;
+        const double v1 = in1 ? a.c_value[k1] : 0.0, v2 = in2 ? a.c_value[k2] : 0.0;
+        total += __popc(__ballot_sync(0xffffffffu, o1 && v1 >= thresh)) +
+                 __popc(__ballot_sync(0xffffffffu, o2 && v2 >= thresh));
       }
       if (total > 0) {  // uniform
         int q0 = 0, gi = 0, fits = 0;
@@ -1493,7 +1499,10 @@ __device__ void phase_write(const V2& a, int s) {
           int run = 0;
           for (int k0 = cb; k0 < cb + cc; k0 += 32) {
             const int k = k0 + lane;
-            const bool keep = k < cb + cc && a.c_ok[k] && a.c_value[k] >= thresh;
+            const bool in = k < cb + cc;
+            const uint8_t ok = in ? a.c_ok[k] : 0;
+            const double v = in ? a.c_value[k] : 0.0;
+            const bool keep = ok && v >= thresh;
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
             if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
             run += __popc(bal);
@@ -1634,21 +1643,29 @@ __global__ void MGS_LB k_units(const V2* __restrict__ ap, int s) {
   phase_units<M>(a, s, 0, s_cnt, s_red);
 }
 
-// Warp-aggregated reservation of n (>= 0) slots from *cursor; every lane of
-// the warp must call it. Returns the lane's first slot.
-__device__ __forceinline__ int warp_alloc(int* cursor, int n) {
+// K independent warp-aggregated reservations at once: the K scans, then the K
+// atomics issued together, then the K broadcasts (one atomic round trip)
+template <int K>
+__device__ __forceinline__ void warp_alloc_n(int* const (&cursor)[K], const int (&n)[K], int (&first)[K]) {
   const int lane = threadIdx.x & 31;
-  int x = n;
+  int x[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) x[k] = n[k];
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int y = __shfl_up_sync(0xffffffffu, x[k], o);
+      if (lane >= o) x[k] += y;
+    }
   }
-  int base = 0;
-  if (lane == 31) base = atomicAdd(cursor, x);
-  base = __shfl_sync(0xffffffffu, base, 31);
-  return base + x - n;
+  int base[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) base[k] = lane == 31 ? atomicAdd(cursor[k], x[k]) : 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) first[k] = __shfl_sync(0xffffffffu, base[k], 31) + x[k] - n[k];
 }
+
 
 // S2: ranges for the step's successor statuses (candidates, units, big/small
 // status lists) and units (work items), reserved with warp-aggregated
@@ -1673,10 +1690,11 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
     const int cc = valid ? a.ns_ccnt[id] : 0, uc = valid ? a.ns_ucnt[id] : 0;
     const bool fused = valid && uc == 1 && a.ns_fflag[id] == 1;
     const bool big = valid && !fused && (uc > 1 || cc > kBigNs);
-    const int cb = warp_alloc(&sc.T, cc);
-    const int ub = warp_alloc(&sc.u_cursor, uc);
-    const int bp = warp_alloc(&sc.n_big, big ? 1 : 0);
-    const int sp = warp_alloc(&sc.n_small, valid && !big && !fused ? 1 : 0);
+    int* const cur4[4] = {&sc.T, &sc.u_cursor, &sc.n_big, &sc.n_small};
+    const int n4[4] = {cc, uc, big ? 1 : 0, valid && !big && !fused ? 1 : 0};
+    int f4[4];
+    warp_alloc_n<4>(cur4, n4, f4);
+    const int cb = f4[0], ub = f4[1], bp = f4[2], sp = f4[3];
     if (valid) {
       a.ns_cbase[id] = cb;
       a.ns_ubase[id] = ub;
@@ -1689,8 +1707,11 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
     const int u = u0 + lane;
     const bool valid = u < nu;
     const int nsm = valid ? a.u_chs[u] : 0, nbg = valid ? a.u_chb[u] : 0;
-    const int sb = warp_alloc(&sc.items_s, nsm);
-    const int bb = warp_alloc(&sc.items_b, nbg);
+    int* const cur2[2] = {&sc.items_s, &sc.items_b};
+    const int n2[2] = {nsm, nbg};
+    int f2[2];
+    warp_alloc_n<2>(cur2, n2, f2);
+    const int sb = f2[0], bb = f2[1];
     if (sb + nsm <= a.itcap)
       for (int c = 0; c < nsm; ++c) {
         a.it_s_unit[sb + c] = u;
