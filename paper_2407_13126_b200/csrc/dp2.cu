@@ -502,7 +502,8 @@ struct UnitSpace {
     }
     *sig_out = sig;
     *ns_out = ns;
-    return ok && a.sp.sig_nopt[sig] > 0;
+    const int nopt = a.sp.sig_nopt[sig];  // sig is in range whatever ok is: no load behind it
+    return ok && nopt > 0;
   }
 };
 
@@ -944,10 +945,13 @@ __device__ void phase_tables(const V2& a, int s) {
     }
     if (nsub == 4) {  // min (rank, idx) among the max; M = 2: the partial subsets are 1 and 2
       for (int j = threadIdx.x; j < gn; j += kThreads) {
-        if (!F.alive[gs + j]) continue;
+        const uint8_t al = F.alive[gs + j];  // every field load issued before the test
         const int pj = F.pid[gs + j];
-        const unsigned long long v = vbits(F.value[gs + j]);
-        const unsigned long long rx = (static_cast<unsigned long long>(F.rank[gs + j]) << 32) | static_cast<uint32_t>(j);
+        const double vd = F.value[gs + j];
+        const uint32_t rk = F.rank[gs + j];
+        if (!al) continue;
+        const unsigned long long v = vbits(vd);
+        const unsigned long long rx = (static_cast<unsigned long long>(rk) << 32) | static_cast<uint32_t>(j);
         const int e1 = a.sp.proj_base[1] + a.sp.proj_id[1 * P1 + pj];
         const int e2 = a.sp.proj_base[2] + a.sp.proj_id[2 * P1 + pj];
         const unsigned long long m1 = vb[e1], m2 = vb[e2];  // both loads before either atomic
@@ -1070,7 +1074,8 @@ __device__ void phase_trans_small(const V2& a, int s) {
     const int sb = a.sp.sig_off[sig], L = a.sp.sig_off[sig + 1] - sb;
     const int ti = chunk * kChunkS + lane;
     const int ns_id = a.u_ns[unit];
-    const bool fused = a.ns_ucnt[ns_id] == 1 && a.ns_fflag[ns_id] == 1;  // then L <= 32, chunk 0
+    const int ucnt = a.ns_ucnt[ns_id], fflag = a.ns_fflag[ns_id];  // both loads issued together
+    const bool fused = ucnt == 1 && fflag == 1;                     // then L <= 32, chunk 0
     const int cbu = a.ns_cbase[ns_id] + a.u_cbase[unit];
     if (chunk == 0 && lane == 0) a.ns_units[a.ns_ubase[ns_id] + a.u_upos[unit]] = unit;  // for k_band's merge
     Cand cand{0.0, 0ull, 0, false};
@@ -1084,9 +1089,10 @@ __device__ void phase_trans_small(const V2& a, int s) {
       const uint8_t al = F.alive[gs + j];
       const double vj = F.value[gs + j];
       const uint32_t rj = F.rank[gs + j];
+      const uint32_t idj = F.ids[gs + j];  // loaded with the others, not behind al
       // a dead state is staged with all-ones ids: no 16-bit field matches a
       // placement's (ids are indices < 0xffff, k_proj_keys' wildcard)
-      gids[j] = al ? F.ids[gs + j] : 0xffffffffu;
+      gids[j] = al ? idj : 0xffffffffu;
       grank[j] = rj;
       gval[j] = vj;
       if (!al) continue;
@@ -1688,7 +1694,8 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
     const bool valid = k < n_ns;
     const int id = valid ? a.ns_used[k] : 0;
     const int cc = valid ? a.ns_ccnt[id] : 0, uc = valid ? a.ns_ucnt[id] : 0;
-    const bool fused = valid && uc == 1 && a.ns_fflag[id] == 1;
+    const int fflag = valid ? a.ns_fflag[id] : 0;
+    const bool fused = valid && uc == 1 && fflag == 1;
     const bool big = valid && !fused && (uc > 1 || cc > kBigNs);
     int* const cur4[4] = {&sc.T, &sc.u_cursor, &sc.n_big, &sc.n_small};
     const int n4[4] = {cc, uc, big ? 1 : 0, valid && !big && !fused ? 1 : 0};
