@@ -76,6 +76,7 @@ struct FrontierV2 {
   uint32_t* rank;
   uint8_t* alive;
   int32_t* group;
+  int32_t* kpos;  // position among the parent's children (k_write's count atomic), for k_kid_fill
   int32_t* g_start;
   int32_t* g_size;
   uint32_t* g_status;
@@ -157,7 +158,6 @@ struct V2 {
   uint8_t* c_live;
   int ccap;
   int32_t* kid_cnt[2];
-  int32_t* kid_cur[2];
   int32_t* kid_base;
   uint64_t* kid_items;
   int32_t* kid_pr;
@@ -619,22 +619,24 @@ __device__ void phase_kid_fill(const V2& a, int s) {
   // wait for k_dom (this branch runs beside it)
   const int n = s == 0 ? a.ctl->n_store[0] : a.ctl->sc[(s - 1) & 1].out_states;
   const int lane = threadIdx.x & 31;
-  // software-pipelined: the next state's lex is loaded ahead
+  // software-pipelined: the next state's lex and sibling slot are loaded ahead
   int i0 = gtid - lane;
   bool al = i0 + lane < n;
   uint64_t lx_c = al ? F.lex[i0 + lane] : 0;
+  int kp_c = al ? F.kpos[i0 + lane] : 0;
   for (; i0 < n; i0 += gstride) {  // warp-uniform trip count
     const int i = i0 + lane;
     const int in = i + gstride;
     const bool al_n = in < n;
     const uint64_t lx_n = al_n ? F.lex[in] : 0;
+    const int kp_n = al_n ? F.kpos[in] : 0;
     bool big_first = false;
     int pr = 0;
     if (al) {
       const uint64_t lx = lx_c;
       pr = static_cast<int>(lx >> 32);
       const int base = a.kid_base[pr], cnt = a.kid_cnt[cur][pr];  // loads before the stores
-      const int q = atomicAdd(&a.kid_cur[cur][pr], 1);
+      const int q = kp_c;  // the state's slot among its siblings (k_write)
       const int slot = base + q;
       a.kid_items[slot] = ((lx & 0xffffffffull) << 32) | static_cast<uint32_t>(i);
       a.kid_pr[slot] = pr;
@@ -649,6 +651,7 @@ __device__ void phase_kid_fill(const V2& a, int s) {
     }
     al = al_n;
     lx_c = lx_n;
+    kp_c = kp_n;
   }
 }
 
@@ -1214,8 +1217,10 @@ __device__ __forceinline__ void write_state_v(const V2& a, int s, int nxt, int q
   const int slot = a.dominance_ok && a.pcnt[p] <= 64 ? atomicAdd(&a.pcnt[p], 1) : 64;
   // R1 (rank branch) folded in: children per parent rank of F_s, for the dense
   // ranks of F_{s+1}. Every stored state is counted (live or dominated: the
-  // ranks are over stored states); F_S is never ranked.
-  if (s + 1 < a.S) atomicAdd(&a.kid_cnt[nxt][static_cast<uint32_t>(lx >> 32)], 1);
+  // ranks are over stored states); F_S is never ranked. The returned count is
+  // the state's slot among its siblings (k_kid_fill needs no atomic); it is
+  // issued beside the bucket atomic, so it adds no round trip.
+  const int kpos = s + 1 < a.S ? atomicAdd(&a.kid_cnt[nxt][static_cast<uint32_t>(lx >> 32)], 1) : 0;
   N.status[q] = key;
   N.ids[q] = ids;
   N.pid[q] = p;
@@ -1223,6 +1228,7 @@ __device__ __forceinline__ void write_state_v(const V2& a, int s, int nxt, int q
   N.lex[q] = lx;
   N.alive[q] = 1;
   N.group[q] = gidx;
+  N.kpos[q] = kpos;
   a.h_parent[h] = parent;
   a.h_oi[h] = static_cast<int32_t>(lx & 0xffffffffu);
   if (slot < 64) a.pbucket[p * 64 + slot] = q;
@@ -1809,7 +1815,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_trans_small(const V2* __restric
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
     for (int i = gtid; i < rp; i += gstride) {
       a.kid_cnt[cur][i] = 0;
-      a.kid_cur[cur][i] = 0;
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // counters of the next step
@@ -1964,6 +1969,7 @@ __global__ void k_init_root(const V2* __restrict__ ap) {
   F.lex[0] = 0;
   F.alive[0] = 1;
   F.group[0] = 0;
+  F.kpos[0] = 0;
   F.rank[0] = 0;
   F.g_start[0] = 0;
   F.g_size[0] = 1;
@@ -2085,14 +2091,13 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, int dominance_ok, int me
     f.rank = c.buf<uint32_t>((tg + "rank").c_str(), caps.fcap);
     f.alive = c.buf<uint8_t>((tg + "alive").c_str(), caps.fcap);
     f.group = c.buf<int32_t>((tg + "group").c_str(), caps.fcap);
+    f.kpos = c.buf<int32_t>((tg + "kpos").c_str(), caps.fcap);
     f.g_start = c.buf<int32_t>((tg + "gstart").c_str(), caps.gcap);
     f.g_size = c.buf<int32_t>((tg + "gsize").c_str(), caps.gcap);
     f.g_status = c.buf<uint32_t>((tg + "gstatus").c_str(), caps.gcap);
     f.g_alive = c.buf<int32_t>((tg + "galive").c_str(), caps.gcap);
     a.kid_cnt[b] = c.buf<int32_t>((tg + "kidcnt").c_str(), caps.fcap);
-    a.kid_cur[b] = c.buf<int32_t>((tg + "kidcur").c_str(), caps.fcap);
     MGS_CUDA_OK(cudaMemsetAsync(a.kid_cnt[b], 0, static_cast<size_t>(caps.fcap) * 4, c.stream));
-    MGS_CUDA_OK(cudaMemsetAsync(a.kid_cur[b], 0, static_cast<size_t>(caps.fcap) * 4, c.stream));
   }
   a.kid_base = c.buf<int32_t>("v2_kidbase", caps.fcap + 1);
   a.kid_items = c.buf<uint64_t>("v2_kiditems", caps.fcap);
