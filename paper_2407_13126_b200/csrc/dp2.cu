@@ -1832,7 +1832,7 @@ __global__ void __launch_bounds__(kThreads) k_band(const V2* __restrict__ ap, in
   phase_band(a, s, smem_u64, smem_u64 + a.merge_win);
 }
 
-__global__ void MGS_LB k_write(const V2* __restrict__ ap, int s) {
+__global__ void __launch_bounds__(kThreads, 4) k_write(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (block_failed(a)) return;
   phase_write(a, s);
