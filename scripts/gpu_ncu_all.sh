@@ -21,7 +21,7 @@ timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byt
   --log-file $OUT/launches_warm.csv python scripts/solve_once.py $C1 1 > $OUT/launches_warm.log 2>&1; echo "rc $?" >> $OUT/launches_warm.log
 gzip -f $OUT/launches_warm.csv
 # 3. --set full of every DP phase kernel at the peak-frontier step (~100)
-timeout 1800 ncu --set full --import-source on --clock-control none -k "$DP" --launch-skip ${DP_SKIP:-1400} --launch-count 14 \
+timeout 1800 ncu --set full --import-source on --clock-control none -k "$DP" --launch-skip ${DP_SKIP:-1300} --launch-count 13 \
   -o $OUT/ncu_dp_step100 python scripts/solve_once.py $C1 1 > $OUT/ncu_dp.log 2>&1; echo "rc $?" >> $OUT/ncu_dp.log
 export_rep $OUT/ncu_dp_step100
 # 4. --set full of every kernel outside the step loop (first launch of each); SKIP_OTHER=1 skips it
