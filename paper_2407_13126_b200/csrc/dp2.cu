@@ -88,8 +88,20 @@ struct StepCounters {  // double buffered; zeroed one step ahead
   int u_cursor;  // unit-list allocation cursor (k_scans)
   int n_ns;  // successor statuses of the step = entries of the used-slot list
   int n_tab;  // big status groups of F_s whose subset tables k_tables builds
-  int out_states, out_groups;  // F_{s+1} allocation cursors (k_write, one atomic per CTA batch)
+  // F_{s+1} allocation cursor: states in the low 32 bits, groups in the high
+  // 32, so a status claims its range and its group with one atomic (every
+  // writing warp of the GPU hits this one address)
+  unsigned long long out_pack;
+  __host__ __device__ int out_states() const { return static_cast<int>(out_pack & 0xffffffffull); }
+  __host__ __device__ int out_groups() const { return static_cast<int>(out_pack >> 32); }
 };
+
+// claim `total` states and one group of F_{s+1}
+__device__ __forceinline__ void claim_out(StepCounters& sc, int total, int* q0, int* gi) {
+  const unsigned long long o = atomicAdd(&sc.out_pack, (1ull << 32) | static_cast<unsigned>(total));
+  *q0 = static_cast<int>(o & 0xffffffffull);
+  *gi = static_cast<int>(o >> 32);
+}
 
 struct Ctl {
   int err[2];
@@ -617,7 +629,7 @@ __device__ void phase_kid_fill(const V2& a, int s) {
   // every stored state, live or dominated: ranks over the stored states order
   // the live ones exactly like dense ranks over the live ones, and they do not
   // wait for k_dom (this branch runs beside it)
-  const int n = s == 0 ? a.ctl->n_store[0] : a.ctl->sc[(s - 1) & 1].out_states;
+  const int n = s == 0 ? a.ctl->n_store[0] : a.ctl->sc[(s - 1) & 1].out_states();
   const int lane = threadIdx.x & 31;
   // software-pipelined: the next state's lex and sibling slot are loaded ahead
   int i0 = gtid - lane;
@@ -1181,8 +1193,7 @@ __device__ void phase_trans_small(const V2& a, int s) {
     const int nxt = (s + 1) & 1;
     int q0 = 0, gi = 0, fits = 0;
     if (lane == 0) {
-      q0 = atomicAdd(&sc.out_states, total);
-      gi = atomicAdd(&sc.out_groups, 1);
+      claim_out(sc, total, &q0, &gi);
       fits = claim_fits(a, s, q0, total, gi) ? 1 : 0;
     }
     if (!__shfl_sync(0xffffffffu, fits, 0)) continue;
@@ -1391,8 +1402,7 @@ __device__ void phase_write(const V2& a, int s) {
     const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id];
     const uint32_t key = a.hash[id] - 1u;
     if (threadIdx.x == 0) {
-      s_q0 = atomicAdd(&sc.out_states, total);
-      s_gi = atomicAdd(&sc.out_groups, 1);
+      claim_out(sc, total, &s_q0, &s_gi);
       s_ok = claim_fits(a, s, s_q0, total, s_gi) ? 1 : 0;
       s_run = 0;
       if (a.dbg) {
@@ -1466,8 +1476,7 @@ __device__ void phase_write(const V2& a, int s) {
       if (total > 0) {  // uniform
         int q0 = 0, gi = 0, fits = 0;
         if (lane == 0) {
-          q0 = atomicAdd(&sc.out_states, total);
-          gi = atomicAdd(&sc.out_groups, 1);
+          claim_out(sc, total, &q0, &gi);
           fits = claim_fits(a, s, q0, total, gi) ? 1 : 0;
         }
         if (__shfl_sync(0xffffffffu, fits, 0)) {
@@ -1495,8 +1504,7 @@ __device__ void phase_write(const V2& a, int s) {
       if (total > 0) {  // uniform
         int q0 = 0, gi = 0, fits = 0;
         if (lane == 0) {
-          q0 = atomicAdd(&sc.out_states, total);
-          gi = atomicAdd(&sc.out_groups, 1);
+          claim_out(sc, total, &q0, &gi);
           fits = claim_fits(a, s, q0, total, gi) ? 1 : 0;
         }
         if (__shfl_sync(0xffffffffu, fits, 0)) {
@@ -1861,9 +1869,9 @@ __global__ void __launch_bounds__(kThreads) k_dom(const V2* __restrict__ ap, int
   if (gtid == 0) {  // end-of-slot bookkeeping (every value read here is final)
     const int nxt = (s + 1) & 1;
     StepCounters& sc = ctl->sc[s & 1];
-    ctl->n_store[nxt] = sc.out_states;   // F_{s+1} as allocated by k_write
-    if (s + 1 < a.S) atomicAdd(&ctl->alive_now[nxt], sc.out_states);  // k_dom's kills are subtracted beside it
-    ctl->n_groups[nxt] = sc.out_groups;
+    ctl->n_store[nxt] = sc.out_states();   // F_{s+1} as allocated by k_write
+    if (s + 1 < a.S) atomicAdd(&ctl->alive_now[nxt], sc.out_states());  // k_dom's kills are subtracted beside it
+    ctl->n_groups[nxt] = sc.out_groups();
     a.hist_base[s + 2] = a.hist_base[s + 1] + ctl->n_store[nxt];  // array has S+2 entries
     if (a.dbg) {
       long long* d = a.dbg + static_cast<long long>(kDbg) * s;
@@ -2347,7 +2355,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
                        " store %d/%d groups %d/%d alive %d/%d out %d/%d\n",
                        st, name, cudaGetErrorString(e), hc.err_code, q.n_units, q.T, q.items_s, q.items_b, q.n_big,
                        q.n_small, q.kids, hc.n_store[0], hc.n_store[1], hc.n_groups[0], hc.n_groups[1],
-                       hc.alive_now[0], hc.alive_now[1], q.out_states, q.out_groups);
+                       hc.alive_now[0], hc.alive_now[1], q.out_states(), q.out_groups());
         }
         mark();
       };
