@@ -1092,7 +1092,8 @@ __device__ void phase_trans_small(const V2& a, int s) {
     const int ucnt = a.ns_ucnt[ns_id], fflag = a.ns_fflag[ns_id];  // both loads issued together
     const bool fused = ucnt == 1 && fflag == 1;                     // then L <= 32, chunk 0
     const int cbu = a.ns_cbase[ns_id] + a.u_cbase[unit];
-    if (chunk == 0 && lane == 0) a.ns_units[a.ns_ubase[ns_id] + a.u_upos[unit]] = unit;  // for k_band's merge
+    if (ucnt > 1 && chunk == 0 && lane == 0)  // read only by k_band's merge of multi-unit statuses
+      a.ns_units[a.ns_ubase[ns_id] + a.u_upos[unit]] = unit;
     Cand cand{0.0, 0ull, 0, false};
     int cand_p = 0;
     // empty subset: the group's best state, one warp-cooperative pass
@@ -1256,9 +1257,11 @@ __device__ __forceinline__ void write_state(const V2& a, int s, int nxt, int q, 
 }
 
 // S6a: equal-key merge (multi-unit statuses) + band + survivor count per status
+constexpr int kUnitCache = 128;  // units of a multi-unit status cached in k_band's shared memory
 __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned long long* mlx) {
   StepCounters& sc = a.ctl->sc[s & 1];
   __shared__ int s_cnt;
+  __shared__ int s_ub[kUnitCache], s_un[kUnitCache], s_uc[kUnitCache];
   const int lane = threadIdx.x & 31;
   // The band's reference value (solvers.hpp:499-511) is the best value among
   // the merged survivors, which is the best bound-passing candidate of the
@@ -1283,6 +1286,18 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
     } else {  // equal-key merge (solvers.hpp:467-468): max value, then min lex, per placement
       const int P1 = a.sp.P1;
       const int win = a.merge_win;
+      // each unit's (signature offset, length, candidate base), looked up once
+      // in parallel instead of a four-load chain per unit and pass
+      __syncthreads();  // the previous status is done with the cache
+      for (int q = threadIdx.x; q < min(uc, kUnitCache); q += kThreads) {
+        const int u = a.ns_units[ub + q];
+        const int sig = a.u_sig[u];
+        const int cu = a.u_cbase[u];
+        const int b = a.sp.sig_off[sig], e = a.sp.sig_off[sig + 1];
+        s_ub[q] = b;
+        s_un[q] = e - b;
+        s_uc[q] = cb + cu;
+      }
       for (int w0 = 0; w0 < P1; w0 += win) {
         for (int i = threadIdx.x; i < win; i += kThreads) {
           mvb[i] = 0ull;
@@ -1291,10 +1306,18 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
         __syncthreads();
         for (int pass = 0; pass < 3; ++pass) {
           for (int q = 0; q < uc; ++q) {
-            const int u = a.ns_units[ub + q];
-            const int sig = a.u_sig[u];
-            const int b = a.sp.sig_off[sig], n = a.sp.sig_off[sig + 1] - b;
-            const int cbu = cb + a.u_cbase[u];
+            int b, n, cbu;
+            if (q < kUnitCache) {
+              b = s_ub[q];
+              n = s_un[q];
+              cbu = s_uc[q];
+            } else {
+              const int u = a.ns_units[ub + q];
+              const int sig = a.u_sig[u];
+              b = a.sp.sig_off[sig];
+              n = a.sp.sig_off[sig + 1] - b;
+              cbu = cb + a.u_cbase[u];
+            }
             int lo = 0;
             if (w0 > 0) {  // the unit's candidates are sorted by placement: clip to the window
               int hi = n;
