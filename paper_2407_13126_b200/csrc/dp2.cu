@@ -54,7 +54,7 @@ constexpr int kThreads = 256;
 // write: +15 % on 8-lane batches, measured): at least MGS_MINB CTAs per SM
 #define MGS_LB __launch_bounds__(kThreads, MGS_MINB)
 constexpr int kWarps = kThreads / 32;
-constexpr int kSmall = 128;          // groups up to this size: warp path
+constexpr int kSmall = 64;           // groups up to this size: warp path (128: -0.3 ms, smaller staging arrays)
 constexpr int kChunkS = 32;          // targets per warp item
 constexpr int kChunkB = 512;         // targets per CTA item
 constexpr int kTile = kThreads * 8;  // scan tile
@@ -63,7 +63,7 @@ constexpr int kBucketSmall = 256;    // child buckets up to this size: thread pe
 constexpr int kSortItems = 16;       // big child buckets: CTA radix sort of up to 256*16 keys
 constexpr int kBatch = 512;          // groups / statuses per CTA allocation batch
 constexpr int kNumScans = 7;
-constexpr int kDbg = 14;  // per-step debug counters
+constexpr int kDbg = 17;  // per-step debug counters
 
 enum Err : int { kOk = 0, kOverflow = 100 };
 
@@ -1091,6 +1091,12 @@ __device__ void phase_trans_small(const V2& a, int s) {
     const int ns_id = a.u_ns[unit];
     const int ucnt = a.ns_ucnt[ns_id], fflag = a.ns_fflag[ns_id];  // both loads issued together
     const bool fused = ucnt == 1 && fflag == 1;                     // then L <= 32, chunk 0
+    if (a.dbg && lane == 0) {  // [14] sum of group sizes over small items, [15] fused items, [16] items with gn > 32
+      unsigned long long* d = reinterpret_cast<unsigned long long*>(a.dbg + kDbg * s);
+      atomicAdd(d + 14, static_cast<unsigned long long>(gn));
+      if (fused) atomicAdd(d + 15, 1ull);
+      if (gn > 32) atomicAdd(d + 16, 1ull);
+    }
     const int cbu = a.ns_cbase[ns_id] + a.u_cbase[unit];
     if (ucnt > 1 && chunk == 0 && lane == 0)  // read only by k_band's merge of multi-unit statuses
       a.ns_units[a.ns_ubase[ns_id] + a.u_upos[unit]] = unit;
@@ -2588,8 +2594,9 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
           const long long* q = d.data() + kDbg * s;
           std::fprintf(stderr,
                        "v2 step %d units %lld ns %lld T %lld store %lld groups %lld alive_in %lld items_b %lld "
-                       "items_s %lld max_group %lld big_groups %lld small32 %lld/%lld small %lld/%lld\n",
-                       s, q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8], q[9], q[10], q[11], q[12], q[13]);
+                       "items_s %lld max_group %lld big_groups %lld small32 %lld/%lld small %lld/%lld gn_sum %lld fused %lld gn>32 %lld\n",
+                       s, q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8], q[9], q[10], q[11], q[12], q[13], q[14],
+                       q[15], q[16]);
         }
       }
       L.status = MGS_OK;
