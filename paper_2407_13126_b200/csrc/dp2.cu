@@ -2284,13 +2284,17 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
   const dim3 g_band = wave(reinterpret_cast<const void*>(k_band), smem_merge);
   const dim3 g_write = wave(reinterpret_cast<const void*>(k_write), 0);
   const dim3 g_dom = wave(reinterpret_cast<const void*>(k_dom), 0);
-  static thread_local Caps caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 8192, 128ll << 20};
+  // initial capacities (grown on overflow, kept per host thread); MGS_V2_SMALL_CAPS
+  // starts tiny so every overflow / regrow path runs (test_gpu.py::test_capacity_regrow)
+  static thread_local Caps caps = std::getenv("MGS_V2_SMALL_CAPS")
+                                      ? Caps{1 << 12, 1 << 10, 1 << 10, 1 << 9, 1 << 13, 11, 8, 1ll << 18}
+                                      : Caps{1 << 20, 1 << 18, 1 << 18, 1 << 18, 1 << 22, 16, 8192, 128ll << 20};
   const bool debug = std::getenv("MGS_DEBUG_STEPS") != nullptr || std::getenv("MGS_TRACE") != nullptr;
   if (std::getenv("MGS_TRACE"))
     std::fprintf(stderr, "trace v2 setup: lanes %d S %d M %d smem trans %zu rank %zu merge %zu grid.x %u %u %u %u %u %u %u %u %u %u\n",
                  K, S, M, size_t(0), smem_rank, smem_merge, g_units.x, g_scans.x, 0u, g_rbig.x, 0u,
                  g_tbig.x, g_tsmall.x, g_band.x, g_write.x, g_dom.x);
-  for (int attempt = 0; attempt < 10; ++attempt) {
+  for (int attempt = 0; attempt < 40; ++attempt) {  // each attempt stops at the first overflow
     std::vector<V2> args(K);
     for (int l = 0; l < K; ++l) args[l] = lane_args(c, lanes[l], caps, dom_ok[l], merge_win[l], g_term.x);
     V2* d_args = c.buf<V2>("v2_args", kMaxLanes);
@@ -2565,6 +2569,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     for (int l = 0; l < K; ++l)
       MGS_CUDA_OK(cudaMemcpyAsync(&h[l], args[l].ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c.stream));
     MGS_CUDA_OK(cudaStreamSynchronize(c.stream));
+    // a failing step's need is a lower bound for the later steps: 4x it
     bool grow = false;
     for (int l = 0; l < K; ++l) {
       if (h[l].err_code != kOverflow) continue;
@@ -2572,14 +2577,14 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
       const long long need = h[l].need;
       if (debug) std::fprintf(stderr, "v2 capacity growth: what %d need %lld at step %d\n", h[l].need_what, need, h[l].err_step);
       switch (h[l].need_what) {
-        case 2: caps.hbits += 1; break;
-        case 3: caps.ucap = static_cast<int>(std::max<long long>(need * 2, caps.ucap * 2ll)); break;
-        case 4: caps.fcap = static_cast<int>(std::max<long long>(need * 2, caps.fcap * 2ll)); break;
-        case 5: caps.gcap = static_cast<int>(std::max<long long>(need * 2, caps.gcap * 2ll)); break;
-        case 6: caps.hcap = std::max<long long>(need * 2, caps.hcap * 2); break;
-        case 7: caps.ccap = static_cast<int>(std::max<long long>(need * 2, caps.ccap * 2ll)); break;
-        case 8: caps.itcap = static_cast<int>(std::max<long long>(need * 2, caps.itcap * 2ll)); break;
-        case 9: caps.tcap = static_cast<int>(std::max<long long>(need * 2, caps.tcap * 2ll)); break;
+        case 2: caps.hbits += 2; break;  // table too full: 4x the slots
+        case 3: caps.ucap = static_cast<int>(std::max<long long>(need * 4, caps.ucap * 2ll)); break;
+        case 4: caps.fcap = static_cast<int>(std::max<long long>(need * 4, caps.fcap * 2ll)); break;
+        case 5: caps.gcap = static_cast<int>(std::max<long long>(need * 4, caps.gcap * 2ll)); break;
+        case 6: caps.hcap = std::max<long long>(need * 4, caps.hcap * 2); break;
+        case 7: caps.ccap = static_cast<int>(std::max<long long>(need * 4, caps.ccap * 2ll)); break;
+        case 8: caps.itcap = static_cast<int>(std::max<long long>(need * 4, caps.itcap * 2ll)); break;
+        case 9: caps.tcap = static_cast<int>(std::max<long long>(need * 4, caps.tcap * 2ll)); break;
         default: throw PlanFail{MGS_ERR_CUDA, "persistent DP: unknown capacity overflow"};
       }
     }

@@ -496,3 +496,34 @@ def test_launch_modes_agree(golden_dir):
     assert results["graph"] == results["chain"] == results["eager"]
     for stem, path, g in cases:
         assert results["graph"][os.path.basename(str(path))]["obj"] == g["dp"]["obj"], stem
+
+
+def test_capacity_regrow(golden_dir):
+    """Every device buffer of the graph engine starting tiny (MGS_V2_SMALL_CAPS):
+    each overflow is raised block-uniformly, the window is re-run with grown
+    capacities (frontier, groups, history, units, candidates, work items, subset
+    tables, successor hash), and plans, objective bits and counters come out
+    equal to the default run and to the reference goldens, single windows and
+    lane batches (M = 1..4)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    c1 = [(stem, path, g) for stem, path, g in golden_dir["c1"] if int(stem.split("_")[1][1:]) <= 60][:1]
+    rnd = golden_dir["random"][::16]
+    multi = [(stem, path, g) for stem, path, g in golden_dir["multi"] if "error" not in g["dp"]][:4]
+    cases = c1 + rnd + multi
+    script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "solve_variant.py")
+    results = {}
+    for name, extra in (("default", {}), ("small", {"MGS_V2_SMALL_CAPS": "1"})):
+        env = dict(os.environ, **extra)
+        r = subprocess.run([sys.executable, script, "--batch"] + [str(p) for _, p, _ in cases], env=env,
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, (name, r.stderr[-2000:])
+        results[name] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert results["default"] == results["small"]
+    for stem, path, g in cases:
+        name = os.path.basename(str(path))
+        assert results["small"][name]["obj"] == g["dp"]["obj"], stem
+        assert results["small"]["batch:" + name]["obj"] == g["dp"]["obj"], stem
