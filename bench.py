@@ -383,7 +383,7 @@ def batch_leg(pl, work, rank, world, n, coll_dev):
     rows = [[100001 + rank * n + k, shard.objective_key(float(obj[k])), int(status[k])] for k in range(n)]
     rows = shard.gather_rows(rows, world, device=coll_dev)
     tr = sum(s["transitions_ref"] for s in stats) * world  # equal work per rank (same window shape)
-    lanes = int(os.environ.get("MGS_BATCH_LANES", "16"))
+    lanes = min(n, int(os.environ.get("MGS_BATCH_LANES", "32")))
     return {"workload": "%d config-1 windows per rank (%d total), %d lanes per launch" % (n, n * world, lanes),
             "value": tr / dt, "unit": UNIT, "ms_per_window": 1e3 * dt / n, "ok": sum(1 for r in rows if r[2] == 0),
             "windows": len(rows), "scaling": "weak",
@@ -567,7 +567,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="collective backend for N>1 (gloo only for functional checks on fewer GPUs)")
-    ap.add_argument("--batch", type=int, default=16, help="windows in the batched-lanes throughput leg (0: skip)")
+    ap.add_argument("--batch", type=int, default=32, help="windows in the batched-lanes throughput leg (0: skip)")
     ap.add_argument("--table", type=int, default=4096, help="traces in the config-4 Goodput-table leg (0: skip)")
     ap.add_argument("--c5", type=int, default=1, help="run the config-5 leg (8 MIG GPUs x 16 tenants)")
     ap.add_argument("--s200", type=int, default=1, help="reference arm: also time one full S=200 window")

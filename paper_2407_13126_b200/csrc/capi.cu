@@ -476,7 +476,7 @@ int mgs_solve_batch(mgs_ctx* ctx, const mgs_problem* problems, int32_t n, int32_
     // Windows of equal shape (S, M <= 2) are solved together: up to
     // MGS_BATCH_LANES of them share every DP kernel launch (grid.y = lane).
     const char* env = std::getenv("MGS_BATCH_LANES");
-    const int max_lanes = std::max(1, std::min(mgs::kMaxLanes, env ? std::atoi(env) : 16));
+    const int max_lanes = std::max(1, std::min(mgs::kMaxLanes, env ? std::atoi(env) : 32));
     struct Prep {
       int i;
       mgs::Prepared pr;

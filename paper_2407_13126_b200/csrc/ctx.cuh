@@ -263,7 +263,7 @@ void solve_dp(Ctx& c, const mgs_problem& p, const Prepared& pr, const DevSpace& 
               const double* d_ub, const double* d_incumbent, SolveOut& out);
 // dp2.cu: the device-resident engine (M <= 2); several independent windows of
 // equal shape ("lanes") run in the same kernels (grid.y = lane).
-constexpr int kMaxLanes = 16;
+constexpr int kMaxLanes = 32;
 struct V2Lane {
   const mgs_problem* p = nullptr;
   const Prepared* pr = nullptr;

@@ -2263,10 +2263,11 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     static const int cap = std::getenv("MGS_GRID_CAP") ? std::atoi(std::getenv("MGS_GRID_CAP")) : 0;  // tuning probe
     if (cap > 0) occ = std::min(occ, cap);
     const int w = c.sm_count * std::max(1, occ);
-    // many lanes: two waves of CTAs shared by the lanes (16 lanes: 27.5 -> 26.0 ms
-    // per C1 window, profiles/r2/lanes_share_probe.log); MGS_LANE_SHARE overrides
+    // many lanes: waves of CTAs shared by the lanes (16 lanes, 2 waves: 27.5 -> 26.0
+    // ms per C1 window; 32 lanes, 3 waves: 22.8 vs 23.6 at 16 lanes,
+    // profiles/r2/lanes_share_probe.log); MGS_LANE_SHARE overrides
     static const int share_env = std::getenv("MGS_LANE_SHARE") ? std::atoi(std::getenv("MGS_LANE_SHARE")) : -1;
-    const int lane_share = share_env >= 0 ? share_env : (K >= 12 ? 2 : 0);
+    const int lane_share = share_env >= 0 ? share_env : (K >= 24 ? 3 : K >= 12 ? 2 : 0);
     if (lane_share > 0) return dim3(static_cast<unsigned>(std::max(1, w * lane_share / K)), static_cast<unsigned>(K));
     return dim3(static_cast<unsigned>(std::max(1, (w + K - 1) / K)), static_cast<unsigned>(K));
   };
