@@ -57,7 +57,8 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kSmall = 64;           // groups up to this size: warp path (128: -0.3 ms, smaller staging arrays)
 constexpr int kChunkS = 32;          // targets per warp item
 constexpr int kChunkB = 512;         // targets per CTA item
-constexpr int kTile = kThreads * 8;  // scan tile
+constexpr int kScanItems = 8;                 // elements per thread of a scan tile
+constexpr int kTile = kThreads * kScanItems;  // scan tile
 constexpr int kBigNs = 1024;         // single-unit statuses with more candidates use the CTA path
 constexpr int kBucketSmall = 256;    // child buckets up to this size: thread per slot
 constexpr int kSortItems = 16;       // big child buckets: CTA radix sort of up to 256*16 keys
@@ -297,13 +298,15 @@ __device__ __forceinline__ int scan_load(const ScanJob& J, int i) {
   return (J.mode == 1) == big ? 1 : 0;
 }
 
-__device__ int block_scan_tile(const ScanJob& J, int base, int* sm) {
+// block-wide exclusive scan of one tile (kScanItems per thread); the thread's
+// prefixes stay in v (written once the tile's offset is known); returns the
+// tile total
+__device__ int block_scan_tile(const ScanJob& J, int base, int* sm, int (&v)[kScanItems]) {
   const int tid = threadIdx.x;
-  int v[8];
   int sum = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    v[k] = scan_load(J, base + tid * 8 + k);
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = scan_load(J, base + tid * kScanItems + k);
     sum += v[k];
   }
   int x = sum;
@@ -328,15 +331,10 @@ __device__ int block_scan_tile(const ScanJob& J, int base, int* sm) {
   __syncthreads();
   int run = sm[32 + (tid >> 5)] + x - sum;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < kScanItems; ++k) {
     const int tmp = v[k];
     v[k] = run;
     run += tmp;
-  }
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int i = base + tid * 8 + k;
-    if (i < J.n) J.out[J.idx ? J.idx[i] : i] = v[k];
   }
   const int agg = sm[64];
   __syncthreads();
@@ -370,7 +368,8 @@ __device__ void multi_scan(const V2& a, const ScanJob* jobs, int njobs, int epoc
     while (t >= tbase[k + 1]) ++k;
     const int j = t - tbase[k];
     const ScanJob& J = jobs[k];
-    const int agg = block_scan_tile(J, j * kTile, sm);
+    int v[kScanItems];
+    const int agg = block_scan_tile(J, j * kTile, sm, v);
     if (threadIdx.x < 32) {  // warp-parallel decoupled look-back over windows of 32 predecessors
       const int lane = threadIdx.x;
       unsigned long long* st = a.scan_state + t;
@@ -412,8 +411,11 @@ __device__ void multi_scan(const V2& a, const ScanJob* jobs, int njobs, int epoc
     }
     __syncthreads();
     const int excl = s_excl;
-    if (excl)
-      for (int i = j * kTile + threadIdx.x; i < min(J.n, (j + 1) * kTile); i += kThreads) J.out[J.idx ? J.idx[i] : i] += excl;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {  // one write per element, offset included
+      const int i = j * kTile + threadIdx.x * kScanItems + k;
+      if (i < J.n) J.out[J.idx ? J.idx[i] : i] = v[k] + excl;
+    }
     __syncthreads();
   }
 }
