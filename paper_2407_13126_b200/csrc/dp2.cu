@@ -304,11 +304,22 @@ __device__ __forceinline__ int scan_load(const ScanJob& J, int i) {
 __device__ int block_scan_tile(const ScanJob& J, int base, int* sm, int (&v)[kScanItems]) {
   const int tid = threadIdx.x;
   int sum = 0;
+  if (J.mode == 0 && !J.idx && base + kTile <= J.n) {  // a full plain tile: 16-byte loads
+    const int4* p4 = reinterpret_cast<const int4*>(J.in + base + tid * kScanItems);
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    v[k] = scan_load(J, base + tid * kScanItems + k);
-    sum += v[k];
+    for (int k = 0; k < kScanItems / 4; ++k) {
+      const int4 q = p4[k];
+      v[4 * k] = q.x;
+      v[4 * k + 1] = q.y;
+      v[4 * k + 2] = q.z;
+      v[4 * k + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) v[k] = scan_load(J, base + tid * kScanItems + k);
   }
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) sum += v[k];
   int x = sum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -411,10 +422,18 @@ __device__ void multi_scan(const V2& a, const ScanJob* jobs, int njobs, int epoc
     }
     __syncthreads();
     const int excl = s_excl;
+    const int b0 = j * kTile + threadIdx.x * kScanItems;
+    if (!J.idx && (j + 1) * kTile <= J.n) {  // a full tile: 16-byte stores, offset included
+      int4* o4 = reinterpret_cast<int4*>(J.out + b0);
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {  // one write per element, offset included
-      const int i = j * kTile + threadIdx.x * kScanItems + k;
-      if (i < J.n) J.out[J.idx ? J.idx[i] : i] = v[k] + excl;
+      for (int k = 0; k < kScanItems / 4; ++k)
+        o4[k] = make_int4(v[4 * k] + excl, v[4 * k + 1] + excl, v[4 * k + 2] + excl, v[4 * k + 3] + excl);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kScanItems; ++k) {  // one write per element, offset included
+        const int i = b0 + k;
+        if (i < J.n) J.out[J.idx ? J.idx[i] : i] = v[k] + excl;
+      }
     }
     __syncthreads();
   }
