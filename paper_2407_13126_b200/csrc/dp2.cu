@@ -147,7 +147,6 @@ struct V2 {
   // per big group of F_s (> kSmall states): subset tables built once per step
   int tcap;                 // table slots
   int32_t* g_tab;           // [gcap] group -> slot (valid for big groups)
-  int32_t* tab_group;       // [tcap] slot -> group
   unsigned long long* tab_vb;   // [tcap][n_partial] max value bits per (subset, projection)
   unsigned long long* tab_rx;   // [tcap][n_partial] (rank << 32 | j) of the best among the max
   uint32_t* tab_ex;         // [tcap][P1] j + 1 of the group's state at each placement (0 = none)
@@ -583,16 +582,7 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
       // pass 2: write the units (same enumeration order)
       for (int g = bs + warp; g < be; g += kWarps) {
         if (F.g_alive[g] <= 0) continue;
-        const bool small = F.g_size[g] <= kSmall;
-        if (!small && lane == 0) {  // big group: one subset-table slot, built once by k_tables
-          const int slot = atomicAdd(&sc.n_tab, 1);
-          if (slot < a.tcap) {
-            a.g_tab[g] = slot;
-            a.tab_group[slot] = g;
-          } else {
-            raise_err(a, phi, kOverflow, s, 0, 9, slot + 1);
-          }
-        }
+        const bool small = F.g_size[g] <= kSmall;  // big groups: subset tables by k_tables
         UnitSpace<M> us;
         us.init(a, F.g_status[g], s);
         int run = base + s_cnt[g - bs];
@@ -901,10 +891,37 @@ __device__ void phase_tables(const V2& a, int s) {
   const int P1 = a.sp.P1, np = a.n_partial, M = a.t.M;
   const int nsub = 1 << M;
   __shared__ unsigned long long s_bv[kWarps], s_brx[kWarps];
+  __shared__ int s_list[kThreads], s_n, s_slot0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nt = min(sc.n_tab, a.tcap);
-  for (int b = blockIdx.x; b < nt; b += gridDim.x) {
-    const int g = a.tab_group[b];
+  // the CTA's own big groups: F_s's groups strided over the CTAs (big groups
+  // are written together, so their indices cluster), found with one parallel
+  // load per group (no dependency on k_units: this kernel runs on the rank
+  // branch beside the unit branch), then one slot reservation
+  const int G = a.ctl->n_groups[cur];
+  const int per = G > static_cast<int>(blockIdx.x) ? (G - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
+  for (int c0 = 0; c0 < per; c0 += kThreads) {
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  {
+    const int k = c0 + threadIdx.x;
+    const int g = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+    const bool in = k < per;
+    const int gsz = in ? F.g_size[g] : 0, gal = in ? F.g_alive[g] : 0;
+    if (in && gal > 0 && gsz > kSmall) s_list[atomicAdd(&s_n, 1)] = g;
+  }
+  __syncthreads();
+  const int nl = s_n;
+  if (nl == 0) continue;  // uniform
+  if (threadIdx.x == 0) s_slot0 = atomicAdd(&sc.n_tab, nl);
+  __syncthreads();
+  const int slot0 = s_slot0;
+  if (slot0 + nl > a.tcap) {  // uniform
+    if (threadIdx.x == 0) raise_err(a, 0, kOverflow, s, 0, 9, slot0 + nl);
+    return;
+  }
+  for (int li = 0; li < nl; ++li) {
+    const int g = s_list[li], b = slot0 + li;
+    if (threadIdx.x == 0) a.g_tab[g] = b;
     const int gs = F.g_start[g], gn = F.g_size[g];
     unsigned long long* vb = a.tab_vb + static_cast<size_t>(b) * np;
     unsigned long long* rxs = a.tab_rx + static_cast<size_t>(b) * np;
@@ -1007,6 +1024,7 @@ __device__ void phase_tables(const V2& a, int s) {
       }
     }
     __syncthreads();
+  }
   }
 }
 
@@ -1839,7 +1857,16 @@ __global__ void __launch_bounds__(kThreads) k_ranks_small(const V2* __restrict__
   phase_ranks_small(a, s);
 }
 
+// Depends on F_s's ranks and on k_dom(s-1) (alive flags) only: in the graph it
+// runs on the rank branch, beside k_units / k_scans
 __global__ void MGS_LB k_tables(const V2* __restrict__ ap, int s) {
+  const V2& a = c_v2;
+  if (block_failed(a)) return;
+  phase_tables(a, s);
+}
+
+template <int M>
+__global__ void __launch_bounds__(kThreads, 4) k_trans_big(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (block_failed(a)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // overflow of k_scans' lists; transition counters
@@ -1852,13 +1879,6 @@ __global__ void MGS_LB k_tables(const V2* __restrict__ ap, int s) {
     if (sc.items_s > a.itcap || sc.items_b > a.itcap) raise_err(a, 0, kOverflow, s, 0, 8, max(sc.items_s, sc.items_b));
   }
   if (!lists_fit(a, s)) return;
-  phase_tables(a, s);
-}
-
-template <int M>
-__global__ void __launch_bounds__(kThreads, 4) k_trans_big(const V2* __restrict__ ap, int s) {
-  const V2& a = c_v2;
-  if (block_failed(a) || !lists_fit(a, s)) return;
   if (static_cast<int>(blockIdx.x) >= a.ctl->sc[s & 1].items_b) return;  // no item for this CTA
   phase_trans_big<M>(a, s);
 }
@@ -1866,7 +1886,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_trans_big(const V2* __restrict_
 template <int M>
 __global__ void __launch_bounds__(kThreads, 4) k_trans_small(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
-  if (block_failed(a) || !lists_fit(a, s)) return;  // k_tables raises the overflow
+  if (block_failed(a) || !lists_fit(a, s)) return;  // k_trans_big raises the overflow
   phase_trans_small<M>(a, s);
   {  // F_s's child counts were last read by the ranks: cleared here, off the critical path
     const int cur = s & 1, rp = a.ctl->ranks_prev[s & 1];
@@ -2192,7 +2212,6 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, int dominance_ok, int me
   a.tcap = caps.tcap;
   const int n_partial_l = sp.proj_base[(1 << t.M) - 1];
   a.g_tab = c.buf<int32_t>("v2_gtab", caps.gcap);
-  a.tab_group = c.buf<int32_t>("v2_tabgroup", caps.tcap);
   a.tab_vb = c.buf<unsigned long long>("v2_tabvb", static_cast<size_t>(caps.tcap) * std::max(1, n_partial_l));
   a.tab_rx = c.buf<unsigned long long>("v2_tabrx", static_cast<size_t>(caps.tcap) * std::max(1, n_partial_l));
   a.tab_ex = c.buf<uint32_t>("v2_tabex", static_cast<size_t>(caps.tcap) * sp.P1);
@@ -2336,7 +2355,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     static const bool fork_ok = std::getenv("MGS_NO_FORK") == nullptr;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_rank_fork = nullptr, ev_rank_join = nullptr;
-    cudaEvent_t ev_rs_fork = nullptr, ev_rs_join = nullptr;
+    cudaEvent_t ev_rs_fork = nullptr, ev_rs_join = nullptr, ev_dom = nullptr, ev_tab = nullptr;
     cudaStream_t side2 = nullptr;
     // MGS_STEP_TIMES (graph mode): an event node after every step, read back
     // after the replay (per-step device time of the captured graph)
@@ -2350,7 +2369,7 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
     // milestones inside each step (graph mode, MGS_STEP_TIMES): where the critical path runs
     constexpr int kMile = 12;
     static const char* kMileNames[kMile] = {"-", "kid_scan", "kid_fill", "ranks_big", "ranks_small", "units",
-                                            "scans", "-", "trans_big", "trans_small", "band", "write"};
+                                            "scans", "tables", "trans_big", "trans_small", "band", "write"};
     static std::vector<cudaEvent_t> mile_ev;
     if (!step_ev.empty() && static_cast<int>(mile_ev.size()) < S * kMile) {
       for (auto e : mile_ev) cudaEventDestroy(e);
@@ -2432,6 +2451,11 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         after("kid_fill", st);
         if (fork && !timed) mile(st, 2, rs_);
         if (fork) {
+          // rank branch: ranks (big on side, small on side2), then the subset
+          // tables on side once k_dom(s-1) is done too (alive flags); the unit
+          // branch (units -> scans) runs beside it on the main stream. The
+          // small-group transitions (side2) need both branches, the big-group
+          // ones (main) the tables and the unit branch.
           MGS_CUDA_OK(cudaEventRecord(ev_rs_fork, side));
           MGS_CUDA_OK(cudaStreamWaitEvent(side2, ev_rs_fork, 0));
           k_ranks_small<<<g_rsmall, kThreads, 0, side2>>>(d_args, st);
@@ -2440,6 +2464,12 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
           k_ranks_big<<<g_rbig, kThreads, smem_rank, side>>>(d_args, st, 0);
           if (!timed) mile(st, 3, side);
           MGS_CUDA_OK(cudaEventRecord(ev_rank_join, side));
+          MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_rs_join, 0));
+          MGS_CUDA_OK(cudaEventRecord(ev_dom, st_));  // k_dom(s-1) (or the root) is done
+          MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_dom, 0));
+          k_tables<<<g_tables, kThreads, 0, side>>>(d_args, st);
+          if (!timed) mile(st, 7, side);
+          MGS_CUDA_OK(cudaEventRecord(ev_tab, side));
         } else {
           k_ranks_big<<<g_rbig, kThreads, smem_rank, st_>>>(d_args, st, 1);
           after("ranks", st);
@@ -2451,16 +2481,13 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         after("scans", st);
         if (fork && !timed) mile(st, 6, st_);
         if (fork) {
-          MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rank_join, 0));
-          MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_rs_join, 0));
-        }
-        if (fork) {  // graph: small-group transitions run beside tables -> big-group transitions
           MGS_CUDA_OK(cudaEventRecord(ev_fork, st_));
-          MGS_CUDA_OK(cudaStreamWaitEvent(side, ev_fork, 0));
-          ktsmall<<<g_tsmall, kThreads, 0, side>>>(d_args, st);
-          if (!timed) mile(st, 9, side);
-          MGS_CUDA_OK(cudaEventRecord(ev_join, side));
-          k_tables<<<g_tables, kThreads, 0, st_>>>(d_args, st);
+          MGS_CUDA_OK(cudaStreamWaitEvent(side2, ev_fork, 0));
+          MGS_CUDA_OK(cudaStreamWaitEvent(side2, ev_rank_join, 0));
+          ktsmall<<<g_tsmall, kThreads, 0, side2>>>(d_args, st);
+          if (!timed) mile(st, 9, side2);
+          MGS_CUDA_OK(cudaEventRecord(ev_join, side2));
+          MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_tab, 0));
           ktbig<<<g_tbig, kThreads, 0, st_>>>(d_args, st);
           if (!timed) mile(st, 8, st_);
           MGS_CUDA_OK(cudaStreamWaitEvent(st_, ev_join, 0));
@@ -2534,6 +2561,8 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_rank_join, cudaEventDisableTiming));
         MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_rs_fork, cudaEventDisableTiming));
         MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_rs_join, cudaEventDisableTiming));
+        MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_dom, cudaEventDisableTiming));
+        MGS_CUDA_OK(cudaEventCreateWithFlags(&ev_tab, cudaEventDisableTiming));
         MGS_CUDA_OK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
         MGS_CUDA_OK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
         enqueue(cap, false);
@@ -2544,6 +2573,8 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
         MGS_CUDA_OK(cudaEventDestroy(ev_rank_join));
         MGS_CUDA_OK(cudaEventDestroy(ev_rs_fork));
         MGS_CUDA_OK(cudaEventDestroy(ev_rs_join));
+        MGS_CUDA_OK(cudaEventDestroy(ev_dom));
+        MGS_CUDA_OK(cudaEventDestroy(ev_tab));
         MGS_CUDA_OK(cudaStreamDestroy(side2));
         side2 = nullptr;
         MGS_CUDA_OK(cudaStreamDestroy(side));
