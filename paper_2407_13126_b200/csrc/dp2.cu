@@ -2606,8 +2606,10 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
             int n = 0;
             for (int st = 1; st < S; ++st) {
               float ms = 0.f;
-              if (cudaEventElapsedTime(&ms, step_ev[st], mile_ev[static_cast<size_t>(st) * kMile + k]) != cudaSuccess)
+              if (cudaEventElapsedTime(&ms, step_ev[st], mile_ev[static_cast<size_t>(st) * kMile + k]) != cudaSuccess) {
+                (void)cudaGetLastError();  // a milestone this graph does not record
                 continue;
+              }
               acc += 1e3 * ms;
               ++n;
             }
