@@ -56,6 +56,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kSmall = 64;           // groups up to this size: warp path (128: -0.3 ms, smaller staging arrays)
 constexpr int kChunkS = 32;          // targets per warp item
+constexpr int kChunkH = 16;          // targets of a half item (two per warp)
 constexpr int kChunkB = 512;         // targets per CTA item
 constexpr int kScanItems = 8;                 // elements per thread of a scan tile
 constexpr int kTile = kThreads * kScanItems;  // scan tile
@@ -64,7 +65,7 @@ constexpr int kBucketSmall = 256;    // child buckets up to this size: thread pe
 constexpr int kSortItems = 16;       // big child buckets: CTA radix sort of up to 256*16 keys
 constexpr int kBatch = 512;          // groups / statuses per CTA allocation batch
 constexpr int kNumScans = 7;
-constexpr int kDbg = 17;  // per-step debug counters
+constexpr int kDbg = 19;  // per-step debug counters
 
 enum Err : int { kOk = 0, kOverflow = 100 };
 
@@ -86,6 +87,7 @@ struct FrontierV2 {
 
 struct StepCounters {  // double buffered; zeroed one step ahead
   int n_units, T, items_s, items_b, n_big, n_small, n_big_bucket, ticket, kids;
+  int items_h;  // half items: units of <= kChunkH targets over groups of <= kSmall / 2 states
   int u_cursor;  // unit-list allocation cursor (k_scans)
   int n_ns;  // successor statuses of the step = entries of the used-slot list
   int n_tab;  // big status groups of F_s whose subset tables k_tables builds
@@ -160,7 +162,7 @@ struct V2 {
   int32_t* ns_fflag;
   int32_t* ns_out;  // survivors per status
   unsigned long long* ns_vmax;  // vbits of the best bound-passing candidate value per status (band max)
-  int32_t *it_s_unit, *it_s_chunk, *it_b_unit, *it_b_chunk;
+  int32_t *it_s_unit, *it_s_chunk, *it_b_unit, *it_b_chunk, *it_h_unit;
   int itcap;
   double* c_value;
   uint64_t* c_lex;
@@ -599,7 +601,8 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
               a.u_group[u] = g;
               a.u_sig[u] = sig;
               a.u_ns[u] = id;
-              a.u_chs[u] = small ? (L + kChunkS - 1) / kChunkS : 0;
+              // -1: one half item (k_trans_small runs two per warp)
+              a.u_chs[u] = small ? (L <= kChunkH && F.g_size[g] <= kSmall / 2 ? -1 : (L + kChunkS - 1) / kChunkS) : 0;
               a.u_chb[u] = small ? 0 : (L + kChunkB - 1) / kChunkB;
               // the unit's slot in its status's unit list and candidate range
               // (k_scans places the status's range; order is irrelevant)
@@ -1102,51 +1105,65 @@ __device__ __forceinline__ bool claim_fits(const V2& a, int s, int q0, int total
 __device__ __forceinline__ void write_state_v(const V2& a, int s, int nxt, int q, int gidx, uint32_t key, int p,
                                               uint64_t lx, double v, int parent);
 
-template <int M>
-__device__ void phase_trans_small(const V2& a, int s) {
+// One warp task of k_trans_small: W = 32, one full item (32 targets of a
+// unit, it_s list); W = 16, two half items (it_h list: a unit of <= 16 targets
+// over a group of <= kSmall / 2 states), one per 16-lane half, with their own
+// staging, reductions and output.
+template <int M, int W>
+__device__ __forceinline__ void small_task(const V2& a, int s, int task, int nis, int nih, double band,
+                                           uint32_t* sh_ids, uint32_t* sh_rank, double* sh_val) {
   const int cur = s & 1;
   StepCounters& sc = a.ctl->sc[s & 1];
   const FrontierV2& F = a.f[cur];
   const int charge = (s > 0 || a.has_initial) ? 1 : 0;
   const int lane = threadIdx.x & 31;
-  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  const int nis = sc.items_s;
   constexpr int kFull = (1 << M) - 1;
-  // the item's group (<= kSmall states) staged once per warp in shared memory:
-  // every lane then scans it from there instead of re-reading global memory
-  __shared__ uint32_t sh_ids[kWarps][kSmall], sh_rank[kWarps][kSmall];
-  __shared__ double sh_val[kWarps][kSmall];
-  const int warp = threadIdx.x >> 5;
-  uint32_t* gids = sh_ids[warp];
-  uint32_t* grank = sh_rank[warp];
-  double* gval = sh_val[warp];
-  const double band = *a.band;
-  for (int item = wid; item < nis; item += nw) {
-    const int unit = a.it_s_unit[item], chunk = a.it_s_chunk[item];
+  constexpr bool half = W < 32;
+  {
+    const int sl = lane & (W - 1);    // lane within the item
+    const int hb = lane - sl;         // first lane of the item
+    int unit = 0, chunk = 0;
+    bool valid = true;
+    if (!half) {
+      unit = a.it_s_unit[task];
+      chunk = a.it_s_chunk[task];
+    } else {
+      const int hi = 2 * (task - nis) + (lane >> 4);
+      valid = hi < nih;
+      unit = valid ? a.it_h_unit[hi] : 0;
+    }
     const int g = a.u_group[unit], sig = a.u_sig[unit];
-    const int gs = F.g_start[g], gn = F.g_size[g];
-    const int sb = a.sp.sig_off[sig], L = a.sp.sig_off[sig + 1] - sb;
-    const int ti = chunk * kChunkS + lane;
+    const int gs = F.g_start[g], gn = valid ? F.g_size[g] : 0;
+    const int sb = a.sp.sig_off[sig], L = valid ? a.sp.sig_off[sig + 1] - sb : 0;
+    const int ti = chunk * kChunkS + sl;
     const int ns_id = a.u_ns[unit];
     const int ucnt = a.ns_ucnt[ns_id], fflag = a.ns_fflag[ns_id];  // both loads issued together
-    const bool fused = ucnt == 1 && fflag == 1;                     // then L <= 32, chunk 0
-    if (a.dbg && lane == 0) {  // [14] sum of group sizes over small items, [15] fused items, [16] items with gn > 32
+    const bool fused = valid && ucnt == 1 && fflag == 1;            // then L <= 32, chunk 0
+    if (a.dbg && sl == 0 && valid) {  // [14] group sizes, [15] fused, [16] gn > 32, [17] targets, [18] targets x gn
       unsigned long long* d = reinterpret_cast<unsigned long long*>(a.dbg + kDbg * s);
       atomicAdd(d + 14, static_cast<unsigned long long>(gn));
       if (fused) atomicAdd(d + 15, 1ull);
       if (gn > 32) atomicAdd(d + 16, 1ull);
+      const int act = min(32, L - chunk * kChunkS);
+      atomicAdd(d + 17, static_cast<unsigned long long>(act));
+      atomicAdd(d + 18, static_cast<unsigned long long>(act) * gn);
     }
     const int cbu = a.ns_cbase[ns_id] + a.u_cbase[unit];
-    if (ucnt > 1 && chunk == 0 && lane == 0)  // read only by k_band's merge of multi-unit statuses
+    if (valid && ucnt > 1 && chunk == 0 && sl == 0)  // read only by k_band's merge of multi-unit statuses
       a.ns_units[a.ns_ubase[ns_id] + a.u_upos[unit]] = unit;
     Cand cand{0.0, 0ull, 0, false};
     int cand_p = 0;
-    // empty subset: the group's best state, one warp-cooperative pass
+    // staging: a half item uses its half of the warp's arrays (gn <= kSmall / 2)
+    const int so = half ? (lane >> 4) * (kSmall / 2) : 0;
+    uint32_t* gids = sh_ids + so;
+    uint32_t* grank = sh_rank + so;
+    double* gval = sh_val + so;
+    // empty subset: the group's best state, one cooperative pass
     double v0 = 0.0;
     uint32_t r0 = 0xffffffffu;
     int i0 = -1;
-    __syncwarp();  // the previous item's scan is done with the staging arrays
-    for (int j = lane; j < gn; j += 32) {
+    __syncwarp();  // the previous task's scan is done with the staging arrays
+    for (int j = sl; j < gn; j += W) {
       const uint8_t al = F.alive[gs + j];
       const double vj = F.value[gs + j];
       const uint32_t rj = F.rank[gs + j];
@@ -1163,7 +1180,7 @@ __device__ void phase_trans_small(const V2& a, int s) {
         i0 = j;
       }
     }
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = W >> 1; o > 0; o >>= 1) {  // xor offsets < W stay inside the item's lanes
       const double ov = __shfl_xor_sync(0xffffffffu, v0, o);
       const uint32_t orr = __shfl_xor_sync(0xffffffffu, r0, o);
       const int oi = __shfl_xor_sync(0xffffffffu, i0, o);
@@ -1220,33 +1237,31 @@ __device__ void phase_trans_small(const V2& a, int s) {
     }
     vb_t = emit_target<M>(a, s, charge, cbu, ti, gs, acc, p, oi, ids_p, b, F, fused ? &cand : nullptr);
     }
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = W >> 1; o > 0; o >>= 1) {
       const unsigned long long y = __shfl_xor_sync(0xffffffffu, vb_t, o);
       vb_t = y > vb_t ? y : vb_t;
     }
-    if (!fused) {
-      if (lane == 0 && vb_t) atomicMax(&a.ns_vmax[a.u_ns[unit]], vb_t);
-      continue;
-    }
+    if (!fused && valid && sl == 0 && vb_t) atomicMax(&a.ns_vmax[ns_id], vb_t);
     // fused status: this item holds all of its candidates (single unit, <= 32
     // targets), so the band (solvers.hpp:499-511: the status's best bound-passing
     // value minus band) and the output happen here, as k_write would do them
     const double thresh = dsub(__longlong_as_double(static_cast<long long>(vb_t)), band);
-    const bool keep = ti < L && cand.ok && cand.v >= thresh;
-    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    const bool keep = fused && ti < L && cand.ok && cand.v >= thresh;
+    const unsigned imask = W == 32 ? 0xffffffffu : (0xffffu << hb);
+    const unsigned bal = __ballot_sync(0xffffffffu, keep) & imask;
     const int total = __popc(bal);
-    if (total == 0) continue;  // uniform
     const int nxt = (s + 1) & 1;
     int q0 = 0, gi = 0, fits = 0;
-    if (lane == 0) {
+    if (sl == 0 && total > 0) {
       claim_out(sc, total, &q0, &gi);
       fits = claim_fits(a, s, q0, total, gi) ? 1 : 0;
     }
-    if (!__shfl_sync(0xffffffffu, fits, 0)) continue;
-    q0 = __shfl_sync(0xffffffffu, q0, 0);
-    gi = __shfl_sync(0xffffffffu, gi, 0);
+    fits = __shfl_sync(0xffffffffu, fits, hb);
+    q0 = __shfl_sync(0xffffffffu, q0, hb);
+    gi = __shfl_sync(0xffffffffu, gi, hb);
+    if (!fits) return;  // per item (no warp-wide collective follows)
     const uint32_t key = a.hash[ns_id] - 1u;
-    if (lane == 0) {
+    if (sl == 0) {
       const FrontierV2& N = a.f[nxt];
       N.g_start[gi] = q0;
       N.g_size[gi] = total;
@@ -1255,6 +1270,24 @@ __device__ void phase_trans_small(const V2& a, int s) {
     }
     if (keep)
       write_state_v(a, s, nxt, q0 + __popc(bal & ((1u << lane) - 1u)), gi, key, cand_p, cand.lex, cand.v, cand.parent);
+  }
+}
+
+template <int M>
+__device__ void phase_trans_small(const V2& a, int s) {
+  const StepCounters& sc = a.ctl->sc[s & 1];
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const int nis = sc.items_s, nih = sc.items_h;
+  const int ntask = nis + (nih + 1) / 2;
+  // the item's group (<= kSmall states) staged once per warp in shared memory:
+  // every lane then scans it from there instead of re-reading global memory
+  __shared__ uint32_t sh_ids[kWarps][kSmall], sh_rank[kWarps][kSmall];
+  __shared__ double sh_val[kWarps][kSmall];
+  const int warp = threadIdx.x >> 5;
+  const double band = *a.band;
+  for (int task = wid; task < ntask; task += nw) {
+    if (task < nis) small_task<M, 32>(a, s, task, nis, nih, band, sh_ids[warp], sh_rank[warp], sh_val[warp]);
+    else small_task<M, 16>(a, s, task, nis, nih, band, sh_ids[warp], sh_rank[warp], sh_val[warp]);
   }
 }
 
@@ -1795,12 +1828,14 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
   for (int u0 = gtid - lane; u0 < nu; u0 += gstride) {
     const int u = u0 + lane;
     const bool valid = u < nu;
-    const int nsm = valid ? a.u_chs[u] : 0, nbg = valid ? a.u_chb[u] : 0;
-    int* const cur2[2] = {&sc.items_s, &sc.items_b};
-    const int n2[2] = {nsm, nbg};
-    int f2[2];
-    warp_alloc_n<2>(cur2, n2, f2);
-    const int sb = f2[0], bb = f2[1];
+    const int chs = valid ? a.u_chs[u] : 0, nbg = valid ? a.u_chb[u] : 0;
+    const int nsm = chs > 0 ? chs : 0, nh = chs < 0 ? 1 : 0;
+    int* const cur3[3] = {&sc.items_s, &sc.items_b, &sc.items_h};
+    const int n3[3] = {nsm, nbg, nh};
+    int f3[3];
+    warp_alloc_n<3>(cur3, n3, f3);
+    const int sb = f3[0], bb = f3[1], hb = f3[2];
+    if (nh && hb < a.itcap) a.it_h_unit[hb] = u;
     if (sb + nsm <= a.itcap)
       for (int c = 0; c < nsm; ++c) {
         a.it_s_unit[sb + c] = u;
@@ -1819,7 +1854,7 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
 // their early exit is block-uniform
 __device__ __forceinline__ bool lists_fit(const V2& a, int s) {
   const StepCounters& sc = a.ctl->sc[s & 1];
-  return sc.T <= a.ccap && sc.items_s <= a.itcap && sc.items_b <= a.itcap;
+  return sc.T <= a.ccap && sc.items_s <= a.itcap && sc.items_b <= a.itcap && sc.items_h <= a.itcap;
 }
 
 // R2 (rank branch): frontier checks for F_s and the children offsets in
@@ -1876,7 +1911,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_trans_big(const V2* __restrict_
     ctl->tr += static_cast<unsigned long long>(T_);
     ctl->tbytes += static_cast<unsigned long long>(ctl->n_store[s & 1]) * 20ull + static_cast<unsigned long long>(T_) * 37ull;
     if (T_ > a.ccap) raise_err(a, 0, kOverflow, s, 0, 7, T_);
-    if (sc.items_s > a.itcap || sc.items_b > a.itcap) raise_err(a, 0, kOverflow, s, 0, 8, max(sc.items_s, sc.items_b));
+    if (sc.items_s > a.itcap || sc.items_b > a.itcap || sc.items_h > a.itcap)
+      raise_err(a, 0, kOverflow, s, 0, 8, max(max(sc.items_s, sc.items_b), sc.items_h));
   }
   if (!lists_fit(a, s)) return;
   if (static_cast<int>(blockIdx.x) >= a.ctl->sc[s & 1].items_b) return;  // no item for this CTA
@@ -2222,6 +2258,7 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, int dominance_ok, int me
   a.itcap = caps.itcap;
   a.it_s_unit = c.buf<int32_t>("v2_itsu", caps.itcap);
   a.it_s_chunk = c.buf<int32_t>("v2_itsc", caps.itcap);
+  a.it_h_unit = c.buf<int32_t>("v2_itsh", caps.itcap);
   a.it_b_unit = c.buf<int32_t>("v2_itbu", caps.itcap);
   a.it_b_chunk = c.buf<int32_t>("v2_itbc", caps.itcap);
   a.ccap = caps.ccap;
@@ -2654,9 +2691,10 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
           const long long* q = d.data() + kDbg * s;
           std::fprintf(stderr,
                        "v2 step %d units %lld ns %lld T %lld store %lld groups %lld alive_in %lld items_b %lld "
-                       "items_s %lld max_group %lld big_groups %lld small32 %lld/%lld small %lld/%lld gn_sum %lld fused %lld gn>32 %lld\n",
+                       "items_s %lld max_group %lld big_groups %lld small32 %lld/%lld small %lld/%lld gn_sum %lld fused %lld gn>32 %lld"
+                       " small_targets %lld targets_x_gn %lld\n",
                        s, q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8], q[9], q[10], q[11], q[12], q[13], q[14],
-                       q[15], q[16]);
+                       q[15], q[16], q[17], q[18]);
         }
       }
       L.status = MGS_OK;
