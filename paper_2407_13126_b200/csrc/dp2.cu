@@ -57,6 +57,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kSmall = 64;           // groups up to this size: warp path (128: -0.3 ms, smaller staging arrays)
 constexpr int kChunkS = 32;          // targets per warp item
 constexpr int kChunkH = 16;          // targets of a half item (two per warp)
+constexpr int kChunkQ = 8;           // targets of a quarter item (four per warp)
 constexpr int kChunkB = 512;         // targets per CTA item
 constexpr int kScanItems = 8;                 // elements per thread of a scan tile
 constexpr int kTile = kThreads * kScanItems;  // scan tile
@@ -88,6 +89,7 @@ struct FrontierV2 {
 struct StepCounters {  // double buffered; zeroed one step ahead
   int n_units, T, items_s, items_b, n_big, n_small, n_big_bucket, ticket, kids;
   int items_h;  // half items: units of <= kChunkH targets over groups of <= kSmall / 2 states
+  int items_q;  // quarter items: units of <= kChunkQ targets over groups of <= kSmall / 4 states
   int u_cursor;  // unit-list allocation cursor (k_scans)
   int n_ns;  // successor statuses of the step = entries of the used-slot list
   int n_tab;  // big status groups of F_s whose subset tables k_tables builds
@@ -162,7 +164,7 @@ struct V2 {
   int32_t* ns_fflag;
   int32_t* ns_out;  // survivors per status
   unsigned long long* ns_vmax;  // vbits of the best bound-passing candidate value per status (band max)
-  int32_t *it_s_unit, *it_s_chunk, *it_b_unit, *it_b_chunk, *it_h_unit;
+  int32_t *it_s_unit, *it_s_chunk, *it_b_unit, *it_b_chunk, *it_h_unit, *it_q_unit;
   int itcap;
   double* c_value;
   uint64_t* c_lex;
@@ -601,8 +603,12 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
               a.u_group[u] = g;
               a.u_sig[u] = sig;
               a.u_ns[u] = id;
-              // -1: one half item (k_trans_small runs two per warp)
-              a.u_chs[u] = small ? (L <= kChunkH && F.g_size[g] <= kSmall / 2 ? -1 : (L + kChunkS - 1) / kChunkS) : 0;
+              // -1 / -2: one half / quarter item (k_trans_small runs two / four per warp)
+              const int gsz = F.g_size[g];
+              a.u_chs[u] = !small ? 0
+                           : L <= kChunkQ && gsz <= kSmall / 4 ? -2
+                           : L <= kChunkH && gsz <= kSmall / 2 ? -1
+                                                                : (L + kChunkS - 1) / kChunkS;
               a.u_chb[u] = small ? 0 : (L + kChunkB - 1) / kChunkB;
               // the unit's slot in its status's unit list and candidate range
               // (k_scans places the status's range; order is irrelevant)
@@ -1106,11 +1112,11 @@ __device__ __forceinline__ void write_state_v(const V2& a, int s, int nxt, int q
                                               uint64_t lx, double v, int parent);
 
 // One warp task of k_trans_small: W = 32, one full item (32 targets of a
-// unit, it_s list); W = 16, two half items (it_h list: a unit of <= 16 targets
-// over a group of <= kSmall / 2 states), one per 16-lane half, with their own
-// staging, reductions and output.
+// unit, it_s list); W = 16 / 8, two half / four quarter items (it_h / it_q
+// lists: a unit of <= 16 / 8 targets over a group of <= kSmall / 2 / kSmall / 4
+// states), one per W lanes, with their own staging, reductions and output.
 template <int M, int W>
-__device__ __forceinline__ void small_task(const V2& a, int s, int task, int nis, int nih, double band,
+__device__ __forceinline__ void small_task(const V2& a, int s, int task, const int32_t* list, int nlist, double band,
                                            uint32_t* sh_ids, uint32_t* sh_rank, double* sh_val) {
   const int cur = s & 1;
   StepCounters& sc = a.ctl->sc[s & 1];
@@ -1127,10 +1133,10 @@ __device__ __forceinline__ void small_task(const V2& a, int s, int task, int nis
     if (!half) {
       unit = a.it_s_unit[task];
       chunk = a.it_s_chunk[task];
-    } else {
-      const int hi = 2 * (task - nis) + (lane >> 4);
-      valid = hi < nih;
-      unit = valid ? a.it_h_unit[hi] : 0;
+    } else {  // task is relative to its list
+      const int hi = (32 / W) * task + lane / W;
+      valid = hi < nlist;
+      unit = valid ? list[hi] : 0;
     }
     const int g = a.u_group[unit], sig = a.u_sig[unit];
     const int gs = F.g_start[g], gn = valid ? F.g_size[g] : 0;
@@ -1153,8 +1159,8 @@ __device__ __forceinline__ void small_task(const V2& a, int s, int task, int nis
       a.ns_units[a.ns_ubase[ns_id] + a.u_upos[unit]] = unit;
     Cand cand{0.0, 0ull, 0, false};
     int cand_p = 0;
-    // staging: a half item uses its half of the warp's arrays (gn <= kSmall / 2)
-    const int so = half ? (lane >> 4) * (kSmall / 2) : 0;
+    // staging: a half / quarter item uses its part of the warp's arrays (gn <= kSmall * W / 32)
+    const int so = (lane / W) * (kSmall * W / 32);
     uint32_t* gids = sh_ids + so;
     uint32_t* grank = sh_rank + so;
     double* gval = sh_val + so;
@@ -1247,7 +1253,7 @@ __device__ __forceinline__ void small_task(const V2& a, int s, int task, int nis
     // value minus band) and the output happen here, as k_write would do them
     const double thresh = dsub(__longlong_as_double(static_cast<long long>(vb_t)), band);
     const bool keep = fused && ti < L && cand.ok && cand.v >= thresh;
-    const unsigned imask = W == 32 ? 0xffffffffu : (0xffffu << hb);
+    const unsigned imask = W == 32 ? 0xffffffffu : (((1u << W) - 1u) << hb);
     const unsigned bal = __ballot_sync(0xffffffffu, keep) & imask;
     const int total = __popc(bal);
     const int nxt = (s + 1) & 1;
@@ -1277,8 +1283,9 @@ template <int M>
 __device__ void phase_trans_small(const V2& a, int s) {
   const StepCounters& sc = a.ctl->sc[s & 1];
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  const int nis = sc.items_s, nih = sc.items_h;
-  const int ntask = nis + (nih + 1) / 2;
+  const int nis = sc.items_s, nih = sc.items_h, niq = sc.items_q;
+  const int nth = (nih + 1) / 2, ntq = (niq + 3) / 4;
+  const int ntask = nis + nth + ntq;
   // the item's group (<= kSmall states) staged once per warp in shared memory:
   // every lane then scans it from there instead of re-reading global memory
   __shared__ uint32_t sh_ids[kWarps][kSmall], sh_rank[kWarps][kSmall];
@@ -1286,8 +1293,11 @@ __device__ void phase_trans_small(const V2& a, int s) {
   const int warp = threadIdx.x >> 5;
   const double band = *a.band;
   for (int task = wid; task < ntask; task += nw) {
-    if (task < nis) small_task<M, 32>(a, s, task, nis, nih, band, sh_ids[warp], sh_rank[warp], sh_val[warp]);
-    else small_task<M, 16>(a, s, task, nis, nih, band, sh_ids[warp], sh_rank[warp], sh_val[warp]);
+    if (task < nis) small_task<M, 32>(a, s, task, nullptr, 0, band, sh_ids[warp], sh_rank[warp], sh_val[warp]);
+    else if (task < nis + nth)
+      small_task<M, 16>(a, s, task - nis, a.it_h_unit, nih, band, sh_ids[warp], sh_rank[warp], sh_val[warp]);
+    else
+      small_task<M, 8>(a, s, task - nis - nth, a.it_q_unit, niq, band, sh_ids[warp], sh_rank[warp], sh_val[warp]);
   }
 }
 
@@ -1829,13 +1839,14 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
     const int u = u0 + lane;
     const bool valid = u < nu;
     const int chs = valid ? a.u_chs[u] : 0, nbg = valid ? a.u_chb[u] : 0;
-    const int nsm = chs > 0 ? chs : 0, nh = chs < 0 ? 1 : 0;
-    int* const cur3[3] = {&sc.items_s, &sc.items_b, &sc.items_h};
-    const int n3[3] = {nsm, nbg, nh};
-    int f3[3];
-    warp_alloc_n<3>(cur3, n3, f3);
-    const int sb = f3[0], bb = f3[1], hb = f3[2];
+    const int nsm = chs > 0 ? chs : 0, nh = chs == -1 ? 1 : 0, nq = chs == -2 ? 1 : 0;
+    int* const cur4[4] = {&sc.items_s, &sc.items_b, &sc.items_h, &sc.items_q};
+    const int n4[4] = {nsm, nbg, nh, nq};
+    int f4[4];
+    warp_alloc_n<4>(cur4, n4, f4);
+    const int sb = f4[0], bb = f4[1], hb = f4[2], qb = f4[3];
     if (nh && hb < a.itcap) a.it_h_unit[hb] = u;
+    if (nq && qb < a.itcap) a.it_q_unit[qb] = u;
     if (sb + nsm <= a.itcap)
       for (int c = 0; c < nsm; ++c) {
         a.it_s_unit[sb + c] = u;
@@ -1854,7 +1865,8 @@ __global__ void __launch_bounds__(kThreads) k_scans(const V2* __restrict__ ap, i
 // their early exit is block-uniform
 __device__ __forceinline__ bool lists_fit(const V2& a, int s) {
   const StepCounters& sc = a.ctl->sc[s & 1];
-  return sc.T <= a.ccap && sc.items_s <= a.itcap && sc.items_b <= a.itcap && sc.items_h <= a.itcap;
+  return sc.T <= a.ccap && sc.items_s <= a.itcap && sc.items_b <= a.itcap && sc.items_h <= a.itcap &&
+         sc.items_q <= a.itcap;
 }
 
 // R2 (rank branch): frontier checks for F_s and the children offsets in
@@ -1911,8 +1923,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_trans_big(const V2* __restrict_
     ctl->tr += static_cast<unsigned long long>(T_);
     ctl->tbytes += static_cast<unsigned long long>(ctl->n_store[s & 1]) * 20ull + static_cast<unsigned long long>(T_) * 37ull;
     if (T_ > a.ccap) raise_err(a, 0, kOverflow, s, 0, 7, T_);
-    if (sc.items_s > a.itcap || sc.items_b > a.itcap || sc.items_h > a.itcap)
-      raise_err(a, 0, kOverflow, s, 0, 8, max(max(sc.items_s, sc.items_b), sc.items_h));
+    if (sc.items_s > a.itcap || sc.items_b > a.itcap || sc.items_h > a.itcap || sc.items_q > a.itcap)
+      raise_err(a, 0, kOverflow, s, 0, 8, max(max(sc.items_s, sc.items_b), max(sc.items_h, sc.items_q)));
   }
   if (!lists_fit(a, s)) return;
   if (static_cast<int>(blockIdx.x) >= a.ctl->sc[s & 1].items_b) return;  // no item for this CTA
@@ -2259,6 +2271,7 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, int dominance_ok, int me
   a.it_s_unit = c.buf<int32_t>("v2_itsu", caps.itcap);
   a.it_s_chunk = c.buf<int32_t>("v2_itsc", caps.itcap);
   a.it_h_unit = c.buf<int32_t>("v2_itsh", caps.itcap);
+  a.it_q_unit = c.buf<int32_t>("v2_itsq", caps.itcap);
   a.it_b_unit = c.buf<int32_t>("v2_itbu", caps.itcap);
   a.it_b_chunk = c.buf<int32_t>("v2_itbc", caps.itcap);
   a.ccap = caps.ccap;
