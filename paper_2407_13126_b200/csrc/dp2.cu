@@ -66,7 +66,7 @@ constexpr int kBucketSmall = 256;    // child buckets up to this size: thread pe
 constexpr int kSortItems = 16;       // big child buckets: CTA radix sort of up to 256*16 keys
 constexpr int kBatch = 512;          // groups / statuses per CTA allocation batch
 constexpr int kNumScans = 7;
-constexpr int kDbg = 22;  // per-step debug counters
+constexpr int kDbg = 19;  // per-step debug counters
 
 enum Err : int { kOk = 0, kOverflow = 100 };
 
@@ -789,11 +789,6 @@ __device__ void phase_ranks_small(const V2& a, int s) {
       me_n = a.kid_items[in];
       c_n = a.kid_cnt[cur][pr_n];
       base_n = a.kid_base[pr_n];
-    }
-    if (a.dbg && c > 1 && c <= kBucketSmall) {  // [19] / [20] rank loads (c per slot) for c <= 32 / > 32, [21] slots
-      unsigned long long* d = reinterpret_cast<unsigned long long*>(a.dbg + kDbg * s);
-      atomicAdd(d + (c <= 32 ? 19 : 20), static_cast<unsigned long long>(c));
-      atomicAdd(d + 21, 1ull);
     }
     if (c <= kBucketSmall) {
       int rank = base;
@@ -2710,9 +2705,9 @@ void solve_dp_v2_lanes(Ctx& c, std::vector<V2Lane>& lanes) {
           std::fprintf(stderr,
                        "v2 step %d units %lld ns %lld T %lld store %lld groups %lld alive_in %lld items_b %lld "
                        "items_s %lld max_group %lld big_groups %lld small32 %lld/%lld small %lld/%lld gn_sum %lld fused %lld gn>32 %lld"
-                       " small_targets %lld targets_x_gn %lld rank_loads_le32 %lld rank_loads_gt32 %lld rank_slots %lld\n",
+                       " small_targets %lld targets_x_gn %lld\n",
                        s, q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8], q[9], q[10], q[11], q[12], q[13], q[14],
-                       q[15], q[16], q[17], q[18], q[19], q[20], q[21]);
+                       q[15], q[16], q[17], q[18]);
         }
       }
       L.status = MGS_OK;
