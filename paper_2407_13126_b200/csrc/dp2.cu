@@ -65,6 +65,10 @@ constexpr int kBigNs = 1024;         // single-unit statuses with more candidate
 constexpr int kBucketSmall = 256;    // child buckets up to this size: thread per slot
 constexpr int kSortItems = 16;       // big child buckets: CTA radix sort of up to 256*16 keys
 constexpr int kBatch = 512;          // groups / statuses per CTA allocation batch
+#ifndef MGS_UNITS_T
+#define MGS_UNITS_T 48
+#endif
+constexpr int kUnitsThreadMin = MGS_UNITS_T;  // groups per CTA from which k_units takes a thread per group
 constexpr int kNumScans = 7;
 constexpr int kDbg = 19;  // per-step debug counters
 
@@ -638,6 +642,93 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
   if (threadIdx.x == 0 && rs) atomicAdd(&a.ctl->tr_ref, static_cast<unsigned long long>(rs));
 }
 
+
+// S1, thread per group (M <= 2: at most 9 x 9 size combinations, about one
+// valid unit per group on C1): one CTA-wide pass over 256 groups at a time --
+// count, block scan, one reservation, write -- instead of a warp walking its
+// groups one after another. The group's unit space stays in registers between
+// the count and the write.
+template <int M>
+__device__ void phase_units_thread(const V2& a, int s, int phi, int* s_cnt, long long* s_red) {
+  const int cur = s & 1;
+  StepCounters& sc = a.ctl->sc[s & 1];
+  const FrontierV2& F = a.f[cur];
+  const int G = a.ctl->n_groups[cur];
+  __shared__ int s_base, s_scan[80];
+  __shared__ int s_nnew, s_new[kNewCap];
+  if (threadIdx.x == 0) s_nnew = 0;
+  const int g0 = static_cast<int>(static_cast<long long>(G) * blockIdx.x / gridDim.x);
+  const int g1 = static_cast<int>(static_cast<long long>(G) * (blockIdx.x + 1) / gridDim.x);
+  long long ref = 0;
+  for (int bs = g0; bs < g1; bs += kThreads) {
+    const int g = bs + threadIdx.x;
+    const bool in = g < g1;
+    const int alive = in ? F.g_alive[g] : 0;  // the group's fields loaded together
+    const uint32_t gst = in ? F.g_status[g] : 0u;
+    const int gsz = in ? F.g_size[g] : 0;
+    UnitSpace<M> us;
+    us.total = 0;
+    int n = 0;
+    if (alive > 0) {
+      us.init(a, gst, s);
+      for (int c = 0; c < us.total; ++c) {
+        int sig;
+        uint32_t ns;
+        n += us.combo(a, c, s, &sig, &ns) ? 1 : 0;
+      }
+    }
+    s_cnt[threadIdx.x] = n;
+    __syncthreads();
+    const int total = block_scan_small(s_cnt, kThreads, s_scan);
+    if (threadIdx.x == 0) {
+      s_base = atomicAdd(&sc.n_units, total);
+      if (s_base + total > a.ucap) raise_err(a, phi, kOverflow, s, 0, 3, static_cast<long long>(s_base) + total);
+    }
+    __syncthreads();
+    const int base = s_base;
+    if (base + total <= a.ucap && n > 0) {
+      const bool small = gsz <= kSmall;  // big groups: subset tables by k_tables
+      int u = base + s_cnt[threadIdx.x];
+      for (int c = 0; c < us.total; ++c) {
+        int sig = 0;
+        uint32_t ns = 0;
+        if (!us.combo(a, c, s, &sig, &ns)) continue;
+        const int id = ns_slot(a, ns, phi, s, &s_nnew, s_new);
+        if (id >= 0) {
+          const int L = a.sig_len[sig];
+          a.u_group[u] = g;
+          a.u_sig[u] = sig;
+          a.u_ns[u] = id;
+          // -1 / -2: one half / quarter item (k_trans_small runs two / four per warp)
+          a.u_chs[u] = !small ? 0
+                       : L <= kChunkQ && gsz <= kSmall / 4 ? -2
+                       : L <= kChunkH && gsz <= kSmall / 2 ? -1
+                                                            : (L + kChunkS - 1) / kChunkS;
+          a.u_chb[u] = small ? 0 : (L + kChunkB - 1) / kChunkB;
+          // the unit's slot in its status's unit list and candidate range
+          // (k_scans places the status's range; order is irrelevant)
+          a.u_upos[u] = atomicAdd(&a.ns_ucnt[id], 1);
+          a.u_cbase[u] = atomicAdd(&a.ns_ccnt[id], L);
+          atomicOr(&a.ns_fflag[id], small && L <= kChunkS ? 1 : 2);
+          ref += a.sp.sig_nopt[sig];
+        }
+        ++u;
+      }
+    }
+    __syncthreads();
+    const int nn = min(s_nnew, kNewCap);
+    if (nn > 0) {  // uniform
+      if (threadIdx.x == 0) s_base = atomicAdd(&sc.n_ns, nn);
+      __syncthreads();
+      for (int i = threadIdx.x; i < nn; i += kThreads) a.ns_used[s_base + i] = s_new[i];
+      __syncthreads();
+      if (threadIdx.x == 0) s_nnew = 0;
+      __syncthreads();
+    }
+  }
+  const long long rs = block_sum(ref, s_red);
+  if (threadIdx.x == 0 && rs) atomicAdd(&a.ctl->tr_ref, static_cast<unsigned long long>(rs));
+}
 
 // S3: placement
 // R3 (rank branch): children into their parent's slots
@@ -1771,7 +1862,13 @@ __global__ void MGS_LB k_units(const V2* __restrict__ ap, int s) {
     }
     ctl->ranks_prev[(s + 1) & 1] = ctl->n_store[cur];  // parent-rank space of F_{s+1}: stored F_s
   }
-  phase_units<M>(a, s, 0, s_cnt, s_red);
+  // thread per group once a CTA has enough groups to fill its threads (lane
+  // batches: 20.7 vs 22.1 ms per C1 window at 16 lanes); a warp per group
+  // otherwise (one C1 window: 28 groups per CTA at the peak step, where the
+  // thread path leaves most threads idle and serialises the size combinations)
+  const int G = a.ctl->n_groups[s & 1];
+  if (M <= 2 && G >= kUnitsThreadMin * static_cast<int>(gridDim.x)) phase_units_thread<M>(a, s, 0, s_cnt, s_red);
+  else phase_units<M>(a, s, 0, s_cnt, s_red);
 }
 
 // K independent warp-aggregated reservations at once: the K scans, then the K
