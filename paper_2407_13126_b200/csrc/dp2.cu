@@ -500,7 +500,15 @@ __device__ __forceinline__ uint32_t fput(int v, int m) {
 // per-tenant allowed retraining sizes of a status (allowed_sizes, solvers.hpp:79-97)
 template <int M>
 struct UnitSpace {
-  int st[M], sizes[M][9], cnt[M], total;
+  // sizes of tenant m: 4-bit entries of sz[m] (<= 9 of them), so the
+  // runtime-indexed list stays in registers instead of local memory
+  int st[M], cnt[M], total;
+  unsigned long long sz[M];
+  __device__ __forceinline__ int size_at(int m, int i) const { return static_cast<int>((sz[m] >> (4 * i)) & 0xfull); }
+  __device__ __forceinline__ void push(int m, int k) {
+    sz[m] |= static_cast<unsigned long long>(k) << (4 * cnt[m]);
+    ++cnt[m];
+  }
   __device__ void init(const V2& a, uint32_t status, int s) {
     const Codec codec{a.t.S, a.codec_shift};
     total = 1;
@@ -508,14 +516,16 @@ struct UnitSpace {
     for (int m = 0; m < M; ++m) {
       st[m] = fldm<M>(status, m);
       cnt[m] = 0;
+      sz[m] = 0ull;
       if (Codec::is_running(st[m])) {
-        sizes[m][cnt[m]++] = codec.run_size(st[m]);
+        push(m, codec.run_size(st[m]));
       } else if (st[m] == Codec::done()) {
-        sizes[m][cnt[m]++] = 0;
+        push(m, 0);
       } else {
-        if (a.t.min_rt[m] >= 0 && s + 1 + a.t.min_rt[m] <= a.t.S) sizes[m][cnt[m]++] = 0;
+        if (a.t.min_rt[m] >= 0 && s + 1 + a.t.min_rt[m] <= a.t.S) push(m, 0);
+#pragma unroll
         for (int k = 1; k <= 7; ++k)
-          if (a.t.rt[m][k] >= 1 && s + a.t.rt[m][k] <= a.t.S) sizes[m][cnt[m]++] = k;
+          if (a.t.rt[m][k] >= 1 && s + a.t.rt[m][k] <= a.t.S) push(m, k);
       }
       total *= cnt[m];
     }
@@ -526,17 +536,24 @@ struct UnitSpace {
     int rem = c, pick[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      pick[m] = rem % cnt[m];
-      rem /= cnt[m];
+      if (m == M - 1) {  // c < total: what remains is the last pick
+        pick[m] = rem;
+      } else {
+        pick[m] = rem % cnt[m];
+        rem /= cnt[m];
+      }
     }
+    int sz_p[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) sz_p[m] = size_at(m, pick[m]);
     int sig = 0;
 #pragma unroll
-    for (int m = M - 1; m >= 0; --m) sig = sig * 8 + sizes[m][pick[m]];
+    for (int m = M - 1; m >= 0; --m) sig = sig * 8 + sz_p[m];
     bool ok = true;
     uint32_t ns = 0;
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      const int adv = codec.advance(a.t.rt[m], st[m], sizes[m][pick[m]], s);
+      const int adv = codec.advance(a.t.rt[m], st[m], sz_p[m], s);
       ok = ok && adv >= 0 && !(adv == 0 && (a.t.min_rt[m] < 0 || s + 1 + a.t.min_rt[m] > a.t.S));
       ns |= fput<M>(adv < 0 ? 0 : adv, m);
     }
