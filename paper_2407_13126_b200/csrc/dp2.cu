@@ -64,6 +64,10 @@ constexpr int kTile = kThreads * kScanItems;  // scan tile
 constexpr int kBigNs = 1024;         // single-unit statuses with more candidates use the CTA path
 constexpr int kBucketSmall = 256;    // child buckets up to this size: thread per slot
 constexpr int kSortItems = 16;       // big child buckets: CTA radix sort of up to 256*16 keys
+#ifndef MGS_BITMAP_PER_KEY
+#define MGS_BITMAP_PER_KEY 4
+#endif
+constexpr int kBitmapPerKey = MGS_BITMAP_PER_KEY;  // ... or the option bitmap when |O|/32 <= this x the bucket size
 constexpr int kBatch = 512;          // groups / statuses per CTA allocation batch
 #ifndef MGS_UNITS_T
 #define MGS_UNITS_T 48
@@ -809,7 +813,10 @@ __device__ void phase_ranks_big(const V2& a, int s, unsigned long long* sm64) {
   for (int b = blockIdx.x; b < nb; b += gridDim.x) {
     const int pr = a.big_bucket[b];
     const int base = a.kid_base[pr], c = a.kid_cnt[cur][pr];
-    if (c <= kThreads * kSortItems) {
+    // the option-index bitmap costs O(c + |O|/32) and the radix sort O(4096)
+    // per bucket: the bitmap whenever its words are few next to the bucket
+    const bool use_bits = a.rank_words > 0 && a.rank_words <= kBitmapPerKey * c;
+    if (!use_bits && c <= kThreads * kSortItems) {
       unsigned long long keys[kSortItems];
 #pragma unroll
       for (int k = 0; k < kSortItems; ++k) {
@@ -824,9 +831,9 @@ __device__ void phase_ranks_big(const V2& a, int s, unsigned long long* sm64) {
       }
       __syncthreads();
     } else if (a.rank_words > 0) {
-      // beyond one CTA's sort (the root's children at step 1): the siblings'
-      // option indices are distinct, so a bitmap over option indices in shared
-      // memory and its word prefix popcounts give every rank in O(c + |O|/32)
+      // the siblings' option indices are distinct, so a bitmap over option
+      // indices in shared memory and its word prefix popcounts give every rank
+      // in O(c + |O|/32) (also beyond one CTA's sort: the root's children)
       uint32_t* bits = reinterpret_cast<uint32_t*>(sm64);
       uint32_t* pre = bits + a.rank_words;
       const int W = a.rank_words;
