@@ -162,6 +162,10 @@ struct V2 {
   unsigned long long* tab_vb;   // [tcap][n_partial] max value bits per (subset, projection)
   unsigned long long* tab_rx;   // [tcap][n_partial] (rank << 32 | j) of the best among the max
   uint32_t* tab_ex;         // [tcap][P1] j + 1 of the group's state at each placement (0 = none)
+  // ex_bits > 0: entries are (step tag << ex_bits) | (j + 1) with tag = s + 1, so
+  // a slot's stale entries from earlier steps read as empty and the map needs no
+  // clearing (zeroed once per solve); 0: cleared per group and step as plain j + 1
+  int ex_bits;
   unsigned long long* tab_hdr;  // [tcap][2] empty subset: value bits, (rank << 32 | j)
   int32_t *ns_ucnt, *ns_ccnt, *ns_ubase, *ns_cbase, *ns_units;
   int32_t *ns_big, *ns_small;
@@ -1014,6 +1018,7 @@ __device__ void phase_tables(const V2& a, int s) {
   const FrontierV2& F = a.f[cur];
   const int P1 = a.sp.P1, np = a.n_partial, M = a.t.M;
   const int nsub = 1 << M;
+  const uint32_t ex_tag = a.ex_bits ? static_cast<uint32_t>(s + 1) << a.ex_bits : 0u;
   __shared__ unsigned long long s_bv[kWarps], s_brx[kWarps];
   __shared__ int s_list[kThreads], s_n, s_slot0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1050,7 +1055,8 @@ __device__ void phase_tables(const V2& a, int s) {
     unsigned long long* vb = a.tab_vb + static_cast<size_t>(b) * np;
     unsigned long long* rxs = a.tab_rx + static_cast<size_t>(b) * np;
     uint32_t* ex = a.tab_ex + static_cast<size_t>(b) * P1;
-    for (int i = threadIdx.x; i < P1; i += kThreads) ex[i] = 0u;
+    if (!a.ex_bits)
+      for (int i = threadIdx.x; i < P1; i += kThreads) ex[i] = 0u;
     for (int i = threadIdx.x; i < np; i += kThreads) {
       vb[i] = 0ull;
       rxs[i] = ~0ull;
@@ -1089,7 +1095,7 @@ __device__ void phase_tables(const V2& a, int s) {
           bv = v;
           brx = rx;
         }
-        ex[pj] = static_cast<uint32_t>(j) + 1u;
+        ex[pj] = ex_tag | (static_cast<uint32_t>(j) + 1u);
         for (int sub = 1; sub < nsub - 1; ++sub)
           atomicMax(&vb[a.sp.proj_base[sub] + a.sp.proj_id[sub * P1 + pj]], v);
       }
@@ -1195,7 +1201,8 @@ __device__ void phase_trans_big(const V2& a, int s) {
         bt.r[sub] = hit ? static_cast<uint32_t>(rx >> 32) : 0u;
       }
       {
-        const uint32_t w = ex[p];
+        const uint32_t w0 = ex[p];
+        const uint32_t w = a.ex_bits ? ((w0 >> a.ex_bits) == static_cast<uint32_t>(s + 1) ? w0 & ((1u << a.ex_bits) - 1u) : 0u) : w0;
         const int full = (1 << M) - 1;
         if (w) {
           const int j = static_cast<int>(w) - 1;
@@ -2384,6 +2391,13 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, int dominance_ok, int me
   a.tab_vb = c.buf<unsigned long long>("v2_tabvb", static_cast<size_t>(caps.tcap) * std::max(1, n_partial_l));
   a.tab_rx = c.buf<unsigned long long>("v2_tabrx", static_cast<size_t>(caps.tcap) * std::max(1, n_partial_l));
   a.tab_ex = c.buf<uint32_t>("v2_tabex", static_cast<size_t>(caps.tcap) * sp.P1);
+  {  // step-tagged placement maps when (S + 1) fits the bits j + 1 leaves
+    int jb = 1;
+    while ((1ll << jb) <= sp.P1) ++jb;
+    a.ex_bits = jb < 32 && (static_cast<long long>(S) + 1) < (1ll << (32 - jb)) && !std::getenv("MGS_EX_CLEAR") ? jb : 0;
+    if (a.ex_bits)
+      MGS_CUDA_OK(cudaMemsetAsync(a.tab_ex, 0, static_cast<size_t>(caps.tcap) * sp.P1 * sizeof(uint32_t), c.stream));
+  }
   a.tab_hdr = c.buf<unsigned long long>("v2_tabhdr", static_cast<size_t>(caps.tcap) * 2);
   for (void* z : {static_cast<void*>(a.hash), static_cast<void*>(a.ns_ucnt), static_cast<void*>(a.ns_ccnt),
                   static_cast<void*>(a.ns_out)})
