@@ -53,6 +53,9 @@ constexpr int kThreads = 256;
 // latency-bound phase kernels that gain from more resident warps (units, tables,
 // write: +15 % on 8-lane batches, measured): at least MGS_MINB CTAs per SM
 #define MGS_LB __launch_bounds__(kThreads, MGS_MINB)
+#ifndef MGS_TS_MINB
+#define MGS_TS_MINB 4  // k_trans_small: at least 4 CTAs per SM (64 registers)
+#endif
 constexpr int kWarps = kThreads / 32;
 constexpr int kSmall = 64;           // groups up to this size: warp path (128: -0.3 ms, smaller staging arrays)
 constexpr int kChunkS = 32;          // targets per warp item
@@ -2060,7 +2063,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_trans_big(const V2* __restrict_
 }
 
 template <int M>
-__global__ void __launch_bounds__(kThreads, 4) k_trans_small(const V2* __restrict__ ap, int s) {
+__global__ void __launch_bounds__(kThreads, MGS_TS_MINB) k_trans_small(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (block_failed(a) || !lists_fit(a, s)) return;  // k_trans_big raises the overflow
   phase_trans_small<M>(a, s);
