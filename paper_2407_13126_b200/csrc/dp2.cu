@@ -246,7 +246,16 @@ __device__ __forceinline__ bool failed(const V2& a) { return ld_volatile(&a.ctl-
 // The entry check of a kernel, uniform over the block: a flag raised while the
 // block starts (by another block, or another kernel) must not let some of its
 // threads leave while the others reach a barrier or a full-warp collective.
-__device__ __forceinline__ bool block_failed(const V2& a) { return __syncthreads_or(failed(a) ? 1 : 0) != 0; }
+// The control block's lines are prefetched into L1 beside the error-flag load,
+// so the step counters every phase kernel reads right after this check are L1
+// hits instead of a second L2 round trip (they were written by earlier kernels)
+__device__ __forceinline__ bool block_failed(const V2& a) {
+#ifndef MGS_NO_CTL_PREFETCH
+  if (threadIdx.x < (sizeof(Ctl) + 127) / 128)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(a.ctl) + 128 * threadIdx.x));
+#endif
+  return __syncthreads_or(failed(a) ? 1 : 0) != 0;
+}
 
 // ---------------------------------------------------------------------------
 // block reductions / scans (kThreads threads)
