@@ -246,16 +246,7 @@ __device__ __forceinline__ bool failed(const V2& a) { return ld_volatile(&a.ctl-
 // The entry check of a kernel, uniform over the block: a flag raised while the
 // block starts (by another block, or another kernel) must not let some of its
 // threads leave while the others reach a barrier or a full-warp collective.
-// The control block's lines are prefetched into L1 beside the error-flag load,
-// so the step counters every phase kernel reads right after this check are L1
-// hits instead of a second L2 round trip (they were written by earlier kernels)
-__device__ __forceinline__ bool block_failed(const V2& a) {
-#ifndef MGS_NO_CTL_PREFETCH
-  if (threadIdx.x < (sizeof(Ctl) + 127) / 128)
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(a.ctl) + 128 * threadIdx.x));
-#endif
-  return __syncthreads_or(failed(a) ? 1 : 0) != 0;
-}
+__device__ __forceinline__ bool block_failed(const V2& a) { return __syncthreads_or(failed(a) ? 1 : 0) != 0; }
 
 // ---------------------------------------------------------------------------
 // block reductions / scans (kThreads threads)
@@ -1088,6 +1079,12 @@ __device__ void phase_tables(const V2& a, int s) {
       vd = F.value[gs + j];
       rk = F.rank[gs + j];
     }
+    // a group of at most kThreads states is one iteration: the min pass below
+    // reuses these registers instead of loading the fields again
+    const bool al0 = al;
+    const int pj0 = pj;
+    const double vd0 = vd;
+    const uint32_t rk0 = rk;
     for (; j < gn; j += kThreads) {  // claim placements, max value per entry, group best
       const int jn = j + kThreads;
       bool al_n = false;
@@ -1139,11 +1136,12 @@ __device__ void phase_tables(const V2& a, int s) {
       a.tab_hdr[2 * b + 1] = brx;
     }
     if (nsub == 4) {  // min (rank, idx) among the max; M = 2: the partial subsets are 1 and 2
+      const bool one = gn <= kThreads;
       for (int j = threadIdx.x; j < gn; j += kThreads) {
-        const uint8_t al = F.alive[gs + j];  // every field load issued before the test
-        const int pj = F.pid[gs + j];
-        const double vd = F.value[gs + j];
-        const uint32_t rk = F.rank[gs + j];
+        const uint8_t al = one ? al0 : F.alive[gs + j];  // every field load issued before the test
+        const int pj = one ? pj0 : F.pid[gs + j];
+        const double vd = one ? vd0 : F.value[gs + j];
+        const uint32_t rk = one ? rk0 : F.rank[gs + j];
         if (!al) continue;
         const unsigned long long v = vbits(vd);
         const unsigned long long rx = (static_cast<unsigned long long>(rk) << 32) | static_cast<uint32_t>(j);
