@@ -169,6 +169,8 @@ struct V2 {
   // a slot's stale entries from earlier steps read as empty and the map needs no
   // clearing (zeroed once per solve); 0: cleared per group and step as plain j + 1
   int ex_bits;
+  int units_tmin;  // k_units: thread per group from this many groups per CTA (MGS_UNITS_THREAD_MIN)
+  int subitems;    // half / quarter k_trans_small items (MGS_NO_SUBITEMS=1: full items only)
   unsigned long long* tab_hdr;  // [tcap][2] empty subset: value bits, (rank << 32 | j)
   int32_t *ns_ucnt, *ns_ccnt, *ns_ubase, *ns_cbase, *ns_units;
   int32_t *ns_big, *ns_small;
@@ -638,8 +640,8 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
               // -1 / -2: one half / quarter item (k_trans_small runs two / four per warp)
               const int gsz = F.g_size[g];
               a.u_chs[u] = !small ? 0
-                           : L <= kChunkQ && gsz <= kSmall / 4 ? -2
-                           : L <= kChunkH && gsz <= kSmall / 2 ? -1
+                           : a.subitems && L <= kChunkQ && gsz <= kSmall / 4 ? -2
+                           : a.subitems && L <= kChunkH && gsz <= kSmall / 2 ? -1
                                                                 : (L + kChunkS - 1) / kChunkS;
               a.u_chb[u] = small ? 0 : (L + kChunkB - 1) / kChunkB;
               // the unit's slot in its status's unit list and candidate range
@@ -729,8 +731,8 @@ __device__ void phase_units_thread(const V2& a, int s, int phi, int* s_cnt, long
           a.u_ns[u] = id;
           // -1 / -2: one half / quarter item (k_trans_small runs two / four per warp)
           a.u_chs[u] = !small ? 0
-                       : L <= kChunkQ && gsz <= kSmall / 4 ? -2
-                       : L <= kChunkH && gsz <= kSmall / 2 ? -1
+                       : a.subitems && L <= kChunkQ && gsz <= kSmall / 4 ? -2
+                       : a.subitems && L <= kChunkH && gsz <= kSmall / 2 ? -1
                                                             : (L + kChunkS - 1) / kChunkS;
           a.u_chb[u] = small ? 0 : (L + kChunkB - 1) / kChunkB;
           // the unit's slot in its status's unit list and candidate range
@@ -1908,7 +1910,8 @@ __global__ void MGS_LB k_units(const V2* __restrict__ ap, int s) {
   // otherwise (one C1 window: 28 groups per CTA at the peak step, where the
   // thread path leaves most threads idle and serialises the size combinations)
   const int G = a.ctl->n_groups[s & 1];
-  if (M <= 2 && G >= kUnitsThreadMin * static_cast<int>(gridDim.x)) phase_units_thread<M>(a, s, 0, s_cnt, s_red);
+  if (M <= 2 && static_cast<long long>(G) >= static_cast<long long>(a.units_tmin) * gridDim.x)
+    phase_units_thread<M>(a, s, 0, s_cnt, s_red);
   else phase_units<M>(a, s, 0, s_cnt, s_red);
 }
 
@@ -2401,6 +2404,9 @@ V2 lane_args(Ctx& c, const V2Lane& L, const Caps& caps, int dominance_ok, int me
   a.tab_vb = c.buf<unsigned long long>("v2_tabvb", static_cast<size_t>(caps.tcap) * std::max(1, n_partial_l));
   a.tab_rx = c.buf<unsigned long long>("v2_tabrx", static_cast<size_t>(caps.tcap) * std::max(1, n_partial_l));
   a.tab_ex = c.buf<uint32_t>("v2_tabex", static_cast<size_t>(caps.tcap) * sp.P1);
+  // alternative kernel paths, selectable for the parity tests (test_gpu.py::test_kernel_paths_agree)
+  a.units_tmin = std::getenv("MGS_UNITS_THREAD_MIN") ? std::atoi(std::getenv("MGS_UNITS_THREAD_MIN")) : kUnitsThreadMin;
+  a.subitems = std::getenv("MGS_NO_SUBITEMS") ? 0 : 1;
   {  // step-tagged placement maps when (S + 1) fits the bits j + 1 leaves
     int jb = 1;
     while ((1ll << jb) <= sp.P1) ++jb;

@@ -498,6 +498,41 @@ def test_launch_modes_agree(golden_dir):
         assert results["graph"][os.path.basename(str(path))]["obj"] == g["dp"]["obj"], stem
 
 
+def test_kernel_paths_agree(golden_dir):
+    """Every alternative path of the graph engine gives the reference's plans and
+    objective bits, single windows and lane batches: k_units with a thread per
+    group everywhere (MGS_UNITS_THREAD_MIN=0) or a warp per group everywhere,
+    k_trans_small without half / quarter items (MGS_NO_SUBITEMS), and placement
+    maps cleared per group instead of step-tagged (MGS_EX_CLEAR). Includes both
+    full S = 200 C1 windows."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    c1 = list(golden_dir["c1"])
+    rnd = golden_dir["random"][::16]
+    multi = [(stem, path, g) for stem, path, g in golden_dir["multi"] if "error" not in g["dp"]][:4]
+    cases = c1 + rnd + multi
+    script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "solve_variant.py")
+    results = {}
+    variants = (("default", {}), ("units_thread", {"MGS_UNITS_THREAD_MIN": "0"}),
+                ("units_warp", {"MGS_UNITS_THREAD_MIN": "1000000000"}), ("full_items", {"MGS_NO_SUBITEMS": "1"}),
+                ("ex_clear", {"MGS_EX_CLEAR": "1"}))
+    for name, extra in variants:
+        env = dict(os.environ, **extra)
+        r = subprocess.run([sys.executable, script, "--batch"] + [str(p) for _, p, _ in cases], env=env,
+                           capture_output=True, text=True, timeout=1200)
+        assert r.returncode == 0, (name, r.stderr[-2000:])
+        results[name] = json.loads(r.stdout.strip().splitlines()[-1])
+    for name, _ in variants[1:]:
+        assert results[name] == results["default"], name
+    for stem, path, g in cases:
+        base = os.path.basename(str(path))
+        assert results["default"][base]["obj"] == g["dp"]["obj"], stem
+        assert results["default"]["batch:" + base]["obj"] == g["dp"]["obj"], stem
+
+
 def test_capacity_regrow(golden_dir):
     """Every device buffer of the graph engine starting tiny (MGS_V2_SMALL_CAPS):
     each overflow is raised block-uniformly, the window is re-run with grown
