@@ -1388,18 +1388,32 @@ __device__ __forceinline__ void small_task(const V2& a, int s, int task, const i
     const double thresh = dsub(__longlong_as_double(static_cast<long long>(vb_t)), band);
     const bool keep = fused && ti < L && cand.ok && cand.v >= thresh;
     const unsigned imask = W == 32 ? 0xffffffffu : (((1u << W) - 1u) << hb);
-    const unsigned bal = __ballot_sync(0xffffffffu, keep) & imask;
+    const unsigned ball = __ballot_sync(0xffffffffu, keep);  // every item of the task
+    const unsigned bal = ball & imask;
     const int total = __popc(bal);
     const int nxt = (s + 1) & 1;
-    int q0 = 0, gi = 0, fits = 0;
-    if (sl == 0 && total > 0) {
-      claim_out(sc, total, &q0, &gi);
-      fits = claim_fits(a, s, q0, total, gi) ? 1 : 0;
+    // one claim of F_{s+1} states and groups for the whole task (its 1, 2 or 4
+    // items): every lane derives each item's share from the ballot, lane 0
+    // issues the one atomic on the step's allocation cursor
+    int ngroups = 0, pre_groups = 0;
+#pragma unroll
+    for (int k = 0; k < 32 / W; ++k) {
+      const int ne = ((ball >> (k * W)) & (W == 32 ? 0xffffffffu : ((1u << W) - 1u))) != 0u ? 1 : 0;
+      ngroups += ne;
+      pre_groups += k < lane / W ? ne : 0;
     }
-    fits = __shfl_sync(0xffffffffu, fits, hb);
-    q0 = __shfl_sync(0xffffffffu, q0, hb);
-    gi = __shfl_sync(0xffffffffu, gi, hb);
-    if (!fits) return;  // per item (no warp-wide collective follows)
+    const int sum = __popc(ball);
+    unsigned long long o = 0ull;
+    int fits = 0;
+    if (lane == 0 && sum > 0) {
+      o = atomicAdd(&sc.out_pack, (static_cast<unsigned long long>(ngroups) << 32) | static_cast<unsigned>(sum));
+      fits = claim_fits(a, s, static_cast<int>(o & 0xffffffffull), sum, static_cast<int>(o >> 32) + ngroups - 1) ? 1 : 0;
+    }
+    fits = __shfl_sync(0xffffffffu, fits, 0);
+    o = __shfl_sync(0xffffffffu, o, 0);
+    if (!fits || total == 0) return;  // per item (no warp-wide collective follows)
+    const int q0 = static_cast<int>(o & 0xffffffffull) + __popc(ball & ((1u << hb) - 1u));
+    const int gi = static_cast<int>(o >> 32) + pre_groups;
     const uint32_t key = a.hash[ns_id] - 1u;
     if (sl == 0) {
       const FrontierV2& N = a.f[nxt];
