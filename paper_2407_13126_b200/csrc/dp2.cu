@@ -772,28 +772,37 @@ __device__ void phase_kid_fill(const V2& a, int s) {
   // wait for k_dom (this branch runs beside it)
   const int n = s == 0 ? a.ctl->n_store[0] : a.ctl->sc[(s - 1) & 1].out_states();
   const int lane = threadIdx.x & 31;
-  // software-pipelined: the next state's lex and sibling slot are loaded ahead
+  // software-pipelined, two deep: element i + 2 * stride's lex and sibling slot,
+  // and element i + stride's bucket base and count (its lex arrived one
+  // iteration earlier), are loaded before element i's stores
   int i0 = gtid - lane;
   bool al = i0 + lane < n;
   uint64_t lx_c = al ? F.lex[i0 + lane] : 0;
   int kp_c = al ? F.kpos[i0 + lane] : 0;
+  int base_c = al ? a.kid_base[static_cast<int>(lx_c >> 32)] : 0;
+  int cnt_c = al ? a.kid_cnt[cur][static_cast<int>(lx_c >> 32)] : 0;
+  bool al_n = i0 + lane + gstride < n;
+  uint64_t lx_n = al_n ? F.lex[i0 + lane + gstride] : 0;
+  int kp_n = al_n ? F.kpos[i0 + lane + gstride] : 0;
   for (; i0 < n; i0 += gstride) {  // warp-uniform trip count
     const int i = i0 + lane;
-    const int in = i + gstride;
-    const bool al_n = in < n;
-    const uint64_t lx_n = al_n ? F.lex[in] : 0;
-    const int kp_n = al_n ? F.kpos[in] : 0;
+    const int in2 = i + 2 * gstride;
+    const bool al_2 = in2 < n;
+    const uint64_t lx_2 = al_2 ? F.lex[in2] : 0;
+    const int kp_2 = al_2 ? F.kpos[in2] : 0;
+    const int pr_n = static_cast<int>(lx_n >> 32);
+    const int base_n = al_n ? a.kid_base[pr_n] : 0;
+    const int cnt_n = al_n ? a.kid_cnt[cur][pr_n] : 0;
     bool big_first = false;
     int pr = 0;
     if (al) {
       const uint64_t lx = lx_c;
       pr = static_cast<int>(lx >> 32);
-      const int base = a.kid_base[pr], cnt = a.kid_cnt[cur][pr];  // loads before the stores
       const int q = kp_c;  // the state's slot among its siblings (k_write)
-      const int slot = base + q;
+      const int slot = base_c + q;
       a.kid_items[slot] = ((lx & 0xffffffffull) << 32) | static_cast<uint32_t>(i);
       a.kid_pr[slot] = pr;
-      big_first = q == 0 && cnt > kBucketSmall;
+      big_first = q == 0 && cnt_c > kBucketSmall;
     }
     const unsigned bal = __ballot_sync(0xffffffffu, big_first);
     if (bal) {
@@ -805,6 +814,11 @@ __device__ void phase_kid_fill(const V2& a, int s) {
     al = al_n;
     lx_c = lx_n;
     kp_c = kp_n;
+    base_c = base_n;
+    cnt_c = cnt_n;
+    al_n = al_2;
+    lx_n = lx_2;
+    kp_n = kp_2;
   }
 }
 
@@ -894,23 +908,34 @@ __device__ void phase_ranks_small(const V2& a, int s) {
   const FrontierV2& F = a.f[cur];
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
   const int n = sc.kids;  // live states of F_s = filled slots
-  // software-pipelined: slot i + gstride is loaded before slot i's rank is stored
+  // software-pipelined, two deep: slot i + 2 * stride's parent and key, and
+  // slot i + stride's bucket count and base (its parent arrived one iteration
+  // earlier), are loaded before slot i's rank is stored
   int i = gtid;
-  int pr = 0, c = 0, base = 0;
+  int c = 0, base = 0;
   unsigned long long me = 0;
   if (i < n) {
-    pr = a.kid_pr[i];
+    const int pr = a.kid_pr[i];
     me = a.kid_items[i];
     c = a.kid_cnt[cur][pr];
     base = a.kid_base[pr];
   }
+  int pr_n = 0;
+  unsigned long long me_n = 0;
+  if (i + gstride < n) {
+    pr_n = a.kid_pr[i + gstride];
+    me_n = a.kid_items[i + gstride];
+  }
   for (; i < n; i += gstride) {
-    const int in = i + gstride;
-    int pr_n = 0, c_n = 0, base_n = 0;
-    unsigned long long me_n = 0;
+    const int in = i + gstride, in2 = i + 2 * gstride;
+    int pr_2 = 0;
+    unsigned long long me_2 = 0;
+    if (in2 < n) {
+      pr_2 = a.kid_pr[in2];
+      me_2 = a.kid_items[in2];
+    }
+    int c_n = 0, base_n = 0;
     if (in < n) {
-      pr_n = a.kid_pr[in];
-      me_n = a.kid_items[in];
       c_n = a.kid_cnt[cur][pr_n];
       base_n = a.kid_base[pr_n];
     }
@@ -920,10 +945,11 @@ __device__ void phase_ranks_small(const V2& a, int s) {
         for (int k = 0; k < c; ++k) rank += a.kid_items[base + k] < me;
       F.rank[static_cast<uint32_t>(me)] = rank;
     }
-    pr = pr_n;
     me = me_n;
     c = c_n;
     base = base_n;
+    pr_n = pr_2;
+    me_n = me_2;
   }
 }
 
