@@ -1825,16 +1825,19 @@ __device__ void phase_write(const V2& a, int s) {
   }
 }
 
-// decoded-status form of status_dominates (solvers.hpp:128-134): equal, or x
-// done, or both running on the same size with x's remaining steps <= y's
+// encoded-status form of status_dominates (solvers.hpp:128-134): a tenant's
+// status is (hi << 16 | lo) with idle = (0, 0), done = (0xffff, 0) and running =
+// (0x200 | size, remaining steps). x dominates y iff x == y, or x is done, or
+// both run the same size with x's remaining steps <= y's -- i.e. hi equal (or
+// x done) and lo(x) <= lo(y): done-vs-done, idle-vs-idle and equal running
+// codes pass; done y only by done x; idle and running never cross.
 __device__ __forceinline__ bool dom_decoded(uint32_t x, uint32_t y) {
-  if (x == y) return true;
-  if ((x >> 24) == 1) return true;
-  return (x >> 24) == 2 && (y >> 24) == 2 && ((x ^ y) & 0x00ff0000u) == 0 && (x & 0xffffu) <= (y & 0xffffu);
+  const uint32_t hx = x >> 16;
+  return (hx == (y >> 16) || hx == 0xffffu) && (x & 0xffffu) <= (y & 0xffffu);
 }
 
-// one state of a dominance bucket, decoded: per tenant kind (0 idle, 1 done,
-// 2 running) | size | remaining steps; value; lex key
+// one state of a dominance bucket: per tenant the encoded status (dom_decoded);
+// value; lex key
 template <int MK>
 struct DomRec {
   uint32_t d[MK];
@@ -1881,8 +1884,8 @@ __device__ void phase_dominance(const V2& a, int s) {
 #pragma unroll
         for (int m = 0; m < MK; ++m) {  // decode once
           const int code = m < MT ? fldm<MK>(st, m) : 0;
-          me[h].d[m] = code == Codec::done() ? (1u << 24)
-                       : Codec::is_running(code) ? (2u << 24) | (static_cast<uint32_t>(codec.run_size(code)) << 16) |
+          me[h].d[m] = code == Codec::done() ? 0xffff0000u
+                       : Codec::is_running(code) ? ((0x200u | static_cast<uint32_t>(codec.run_size(code))) << 16) |
                                                        static_cast<uint32_t>(codec.run_rem(code))
                                                  : 0u;
         }
