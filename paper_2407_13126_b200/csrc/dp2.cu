@@ -941,8 +941,11 @@ __device__ void phase_ranks_small(const V2& a, int s) {
     }
     if (c <= kBucketSmall) {
       int rank = base;
-      if (c > 1)
-        for (int k = 0; k < c; ++k) rank += a.kid_items[base + k] < me;
+      if (c > 1) {  // siblings' option indices (the keys' high words) are distinct: 32-bit compares
+        const uint32_t* hi = reinterpret_cast<const uint32_t*>(a.kid_items + base) + 1;
+        const uint32_t mo = static_cast<uint32_t>(me >> 32);
+        for (int k = 0; k < c; ++k) rank += hi[2 * k] < mo;
+      }
       F.rank[static_cast<uint32_t>(me)] = rank;
     }
     me = me_n;
