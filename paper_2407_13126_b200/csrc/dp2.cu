@@ -504,6 +504,17 @@ __device__ __forceinline__ int fldm(uint32_t x, int m) {
   constexpr int kW = M <= 2 ? 16 : 8;
   return static_cast<int>((x >> (kW * m)) & ((1u << kW) - 1u));
 }
+// some tenant field of x is zero (SWAR: a borrow reaches a field's top bit
+// only out of a zero field; unused high fields are padded non-zero)
+template <int M>
+__device__ __forceinline__ bool any_zero_field(uint32_t x) {
+  constexpr int kW = M <= 2 ? 16 : 8;
+  constexpr uint32_t ones = kW == 16 ? 0x00010001u : 0x01010101u;
+  constexpr uint32_t highs = kW == 16 ? 0x80008000u : 0x80808080u;
+  constexpr uint32_t pad = kW * M >= 32 ? 0u : ~((1u << (kW * M)) - 1u);
+  const uint32_t y = x | pad;
+  return ((y - ones) & ~y & highs) != 0u;
+}
 template <int M>
 __device__ __forceinline__ uint32_t fput(int v, int m) {
   constexpr int kW = M <= 2 ? 16 : 8;
@@ -1380,13 +1391,19 @@ __device__ __forceinline__ void small_task(const V2& a, int s, int task, const i
     b.r[0] = r0;
     // non-empty subsets: only states that agree with the target on the
     // subset's tenants can represent it (solvers.hpp:367-378)
-#pragma unroll 4
-    for (int j = 0; j < gn; ++j) {
+    // pass 1, branch-free: the states that agree with the target on some
+    // tenant (bit j; gn <= kSmall = 64); pass 2 visits only those, in
+    // ascending j (better() is a strict order: the visiting order is free)
+    unsigned long long mm = 0ull;
+#pragma unroll 8
+    for (int j = 0; j < gn; ++j) mm |= static_cast<unsigned long long>(any_zero_field<M>(gids[j] ^ ids_p)) << j;
+    while (mm) {
+      const int j = __ffsll(static_cast<long long>(mm)) - 1;
+      mm &= mm - 1ull;
       const uint32_t x = gids[j] ^ ids_p;
       int mt = 0;
 #pragma unroll
       for (int m = 0; m < M; ++m) mt |= fldm<M>(x, m) == 0 ? (1 << m) : 0;
-      if (mt == 0) continue;
       const double vj = gval[j];
       const uint32_t rj = grank[j];
       if (mt == kFull) {  // the full subset's key is the state's own placement: unique in the group
