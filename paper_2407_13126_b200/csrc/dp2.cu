@@ -1225,7 +1225,6 @@ __device__ void phase_trans_big(const V2& a, int s) {
     const int g = a.u_group[unit], sig = a.u_sig[unit], ns_id = a.u_ns[unit];
     const int gs = F.g_start[g];
     const int cbu = a.ns_cbase[ns_id] + a.u_cbase[unit];
-    if (chunk == 0 && threadIdx.x == 0) a.ns_units[a.ns_ubase[ns_id] + a.u_upos[unit]] = unit;  // for k_band's merge
     const int b = a.g_tab[g];
     const unsigned long long* vb = a.tab_vb + static_cast<size_t>(b) * np;
     const unsigned long long* rxs = a.tab_rx + static_cast<size_t>(b) * np;
@@ -1329,8 +1328,6 @@ __device__ __forceinline__ void small_task(const V2& a, int s, int task, const i
       atomicAdd(d + 18, static_cast<unsigned long long>(act) * gn);
     }
     const int cbu = a.ns_cbase[ns_id] + a.u_cbase[unit];
-    if (valid && ucnt > 1 && chunk == 0 && sl == 0)  // read only by k_band's merge of multi-unit statuses
-      a.ns_units[a.ns_ubase[ns_id] + a.u_upos[unit]] = unit;
     Cand cand{0.0, 0ull, 0, false};
     int cand_p = 0;
     // staging: a half / quarter item uses its part of the warp's arrays (gn <= kSmall * W / 32)
@@ -1539,11 +1536,9 @@ __device__ __forceinline__ void write_state(const V2& a, int s, int nxt, int q, 
 }
 
 // S6a: equal-key merge (multi-unit statuses) + band + survivor count per status
-constexpr int kUnitCache = 128;  // units of a multi-unit status cached in k_band's shared memory
 __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned long long* mlx) {
   StepCounters& sc = a.ctl->sc[s & 1];
   __shared__ int s_cnt;
-  __shared__ int s_ub[kUnitCache], s_un[kUnitCache], s_uc[kUnitCache];
   const int lane = threadIdx.x & 31;
   // The band's reference value (solvers.hpp:499-511) is the best value among
   // the merged survivors, which is the best bound-passing candidate of the
@@ -1553,7 +1548,7 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
   const int nbig = sc.n_big;
   for (int w = blockIdx.x; w < nbig; w += gridDim.x) {
     const int id = a.ns_big[w];
-    const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id], ub = a.ns_ubase[id], uc = a.ns_ucnt[id];
+    const int cb = a.ns_cbase[id], cc = a.ns_ccnt[id], uc = a.ns_ucnt[id];
     const double thresh = dsub(__longlong_as_double(static_cast<long long>(a.ns_vmax[id])), *a.band);
     if (threadIdx.x == 0) s_cnt = 0;
     int mine = 0;
@@ -1566,20 +1561,12 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
         mine += keep;
       }
     } else {  // equal-key merge (solvers.hpp:467-468): max value, then min lex, per placement
+      // flat over the status's candidate range (every unit's records are in it,
+      // each with its own placement id): the CTA's threads stride the whole
+      // range in each pass, no per-unit loop
       const int P1 = a.sp.P1;
       const int win = a.merge_win;
-      // each unit's (signature offset, length, candidate base), looked up once
-      // in parallel instead of a four-load chain per unit and pass
-      __syncthreads();  // the previous status is done with the cache
-      for (int q = threadIdx.x; q < min(uc, kUnitCache); q += kThreads) {
-        const int u = a.ns_units[ub + q];
-        const int sig = a.u_sig[u];
-        const int cu = a.u_cbase[u];
-        const int b = a.sp.sig_off[sig], e = a.sp.sig_off[sig + 1];
-        s_ub[q] = b;
-        s_un[q] = e - b;
-        s_uc[q] = cb + cu;
-      }
+      __syncthreads();  // the previous status is done with the merge table
       for (int w0 = 0; w0 < P1; w0 += win) {
         for (int i = threadIdx.x; i < win; i += kThreads) {
           mvb[i] = 0ull;
@@ -1587,74 +1574,50 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
         }
         __syncthreads();
         for (int pass = 0; pass < 3; ++pass) {
-          for (int q = 0; q < uc; ++q) {
-            int b, n, cbu;
-            if (q < kUnitCache) {
-              b = s_ub[q];
-              n = s_un[q];
-              cbu = s_uc[q];
-            } else {
-              const int u = a.ns_units[ub + q];
-              const int sig = a.u_sig[u];
-              b = a.sp.sig_off[sig];
-              n = a.sp.sig_off[sig + 1] - b;
-              cbu = cb + a.u_cbase[u];
+          // software-pipelined: the next candidate's loads are issued before
+          // this one's shared-memory atomics / stores
+          int k = cb + threadIdx.x;
+          int p = 0;
+          bool ok = false;
+          double v = 0.0;
+          unsigned long long lx = 0;
+          if (k < cb + cc) {
+            p = a.c_pid[k];
+            ok = a.c_ok[k];
+            v = a.c_value[k];
+            if (pass > 0) lx = a.c_lex[k];
+          }
+          for (; k < cb + cc; k += kThreads) {
+            const int kn = k + kThreads;
+            int p_n = 0;
+            bool ok_n = false;
+            double v_n = 0.0;
+            unsigned long long lx_n = 0;
+            if (kn < cb + cc) {
+              p_n = a.c_pid[kn];
+              ok_n = a.c_ok[kn];
+              v_n = a.c_value[kn];
+              if (pass > 0) lx_n = a.c_lex[kn];
             }
-            int lo = 0;
-            if (w0 > 0) {  // the unit's candidates are sorted by placement: clip to the window
-              int hi = n;
-              while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (a.sp.cand_pid[b + mid] < w0) lo = mid + 1;
-                else hi = mid;
-              }
-            }
-            // software-pipelined: the next candidate's loads are issued
-            // before this one's atomics / stores
-            int t = lo + threadIdx.x;
-            int p = 0;
-            bool ok = false;
-            double v = 0.0;
-            unsigned long long lx = 0;
-            if (t < n) {
-              p = a.sp.cand_pid[b + t];
-              ok = a.c_ok[cbu + t];
-              v = a.c_value[cbu + t];
-              if (pass > 0) lx = a.c_lex[cbu + t];
-            }
-            for (; t < n; t += kThreads) {
-              if (p >= w0 + win) break;
-              const int tn = t + kThreads;
-              int p_n = 0;
-              bool ok_n = false;
-              double v_n = 0.0;
-              unsigned long long lx_n = 0;
-              if (tn < n) {
-                p_n = a.sp.cand_pid[b + tn];
-                ok_n = a.c_ok[cbu + tn];
-                v_n = a.c_value[cbu + tn];
-                if (pass > 0) lx_n = a.c_lex[cbu + tn];
-              }
-              const int k = cbu + t;
-              if (!ok) {
-                if (pass == 2) a.c_live[k] = 0;
+            const bool inw = p >= w0 && p < w0 + win;
+            if (!ok) {
+              if (pass == 2 && w0 == 0) a.c_live[k] = 0;
+            } else if (inw) {
+              const unsigned long long vb = vbits(v);
+              if (pass == 0) {
+                atomicMax(&mvb[p - w0], vb);
+              } else if (pass == 1) {
+                if (mvb[p - w0] == vb) atomicMin(&mlx[p - w0], lx);
               } else {
-                const unsigned long long vb = vbits(v);
-                if (pass == 0) {
-                  atomicMax(&mvb[p - w0], vb);
-                } else if (pass == 1) {
-                  if (mvb[p - w0] == vb) atomicMin(&mlx[p - w0], lx);
-                } else {
-                  const bool keep = mvb[p - w0] == vb && mlx[p - w0] == lx && v >= thresh;
-                  a.c_live[k] = keep ? 1 : 0;
-                  mine += keep;
-                }
+                const bool keep = mvb[p - w0] == vb && mlx[p - w0] == lx && v >= thresh;
+                a.c_live[k] = keep ? 1 : 0;
+                mine += keep;
               }
-              p = p_n;
-              ok = ok_n;
-              v = v_n;
-              lx = lx_n;
             }
+            p = p_n;
+            ok = ok_n;
+            v = v_n;
+            lx = lx_n;
           }
           __syncthreads();
         }
