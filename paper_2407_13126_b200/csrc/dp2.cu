@@ -72,6 +72,9 @@ constexpr int kSortItems = 16;       // big child buckets: CTA radix sort of up 
 #endif
 constexpr int kBitmapPerKey = MGS_BITMAP_PER_KEY;  // ... or the option bitmap when |O|/32 <= this x the bucket size
 constexpr int kBatch = 512;          // groups / statuses per CTA allocation batch
+#ifndef MGS_UNITS_W
+#define MGS_UNITS_W 8  // lanes per status group in k_units' warp path (M <= 2)
+#endif
 #ifndef MGS_UNITS_T
 #define MGS_UNITS_T 48
 #endif
@@ -589,35 +592,47 @@ struct UnitSpace {
 };
 
 // S1
-template <int M>
+// W lanes per group (W = 32: a warp; W < 32: 32 / W groups per warp, for the
+// many groups with few size combinations). Loops run warp-uniformly: the
+// sub-groups' combination counts are maxed over the warp.
+template <int M, int W>
 __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* s_red) {
   const int cur = s & 1;
   StepCounters& sc = a.ctl->sc[s & 1];
   const FrontierV2& F = a.f[cur];
   const int G = a.ctl->n_groups[cur];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int GPW = 32 / W;  // groups per warp
+  const int sl = lane % W, sg = lane / W;
+  const unsigned smask = W == 32 ? 0xffffffffu : (((1u << W) - 1u) << (sg * W));
   __shared__ int s_base, s_scan[80];
   __shared__ int s_nnew, s_new[kNewCap];
   if (threadIdx.x == 0) s_nnew = 0;
   const int g0 = static_cast<int>(static_cast<long long>(G) * blockIdx.x / gridDim.x);
   const int g1 = static_cast<int>(static_cast<long long>(G) * (blockIdx.x + 1) / gridDim.x);
   long long ref = 0;
+  auto warp_max = [&](int x) {
+#pragma unroll
+    for (int o = 16; o >= W; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+    return x;
+  };
   for (int bs = g0; bs < g1; bs += kBatch) {
     const int be = min(g1, bs + kBatch);
     // pass 1: unit count per group
-    for (int g = bs + warp; g < be; g += kWarps) {
+    for (int gw = bs + warp * GPW; gw < be; gw += kWarps * GPW) {  // warp-uniform
+      const int g = gw + sg;
       int n = 0;
-      if (F.g_alive[g] > 0) {
-        UnitSpace<M> us;
-        us.init(a, F.g_status[g], s);
-        for (int c0 = 0; c0 < us.total; c0 += 32) {
-          int sig;
-          uint32_t ns;
-          const bool ok = c0 + lane < us.total && us.combo(a, c0 + lane, s, &sig, &ns);
-          n += __popc(__ballot_sync(0xffffffffu, ok));
-        }
+      UnitSpace<M> us;
+      us.total = 0;
+      if (g < be && F.g_alive[g] > 0) us.init(a, F.g_status[g], s);
+      const int tmax = warp_max(us.total);
+      for (int c0 = 0; c0 < tmax; c0 += W) {
+        int sig;
+        uint32_t ns;
+        const bool ok = c0 + sl < us.total && us.combo(a, c0 + sl, s, &sig, &ns);
+        n += __popc(__ballot_sync(0xffffffffu, ok) & smask);
       }
-      if (lane == 0) s_cnt[g - bs] = n;
+      if (g < be && sl == 0) s_cnt[g - bs] = n;
     }
     __syncthreads();
     const int total = block_scan_small(s_cnt, be - bs, s_scan);
@@ -629,17 +644,20 @@ __device__ void phase_units(const V2& a, int s, int phi, int* s_cnt, long long* 
     const int base = s_base;
     if (base + total <= a.ucap) {
       // pass 2: write the units (same enumeration order)
-      for (int g = bs + warp; g < be; g += kWarps) {
-        if (F.g_alive[g] <= 0) continue;
-        const bool small = F.g_size[g] <= kSmall;  // big groups: subset tables by k_tables
+      for (int gw = bs + warp * GPW; gw < be; gw += kWarps * GPW) {  // warp-uniform
+        const int g = gw + sg;
+        const bool gv = g < be && F.g_alive[g] > 0;
+        const bool small = gv && F.g_size[g] <= kSmall;  // big groups: subset tables by k_tables
         UnitSpace<M> us;
-        us.init(a, F.g_status[g], s);
-        int run = base + s_cnt[g - bs];
-        for (int c0 = 0; c0 < us.total; c0 += 32) {
+        us.total = 0;
+        if (gv) us.init(a, F.g_status[g], s);
+        int run = gv ? base + s_cnt[g - bs] : 0;
+        const int tmax = warp_max(us.total);
+        for (int c0 = 0; c0 < tmax; c0 += W) {
           int sig = 0;
           uint32_t ns = 0;
-          const bool ok = c0 + lane < us.total && us.combo(a, c0 + lane, s, &sig, &ns);
-          const unsigned bal = __ballot_sync(0xffffffffu, ok);
+          const bool ok = c0 + sl < us.total && us.combo(a, c0 + sl, s, &sig, &ns);
+          const unsigned bal = __ballot_sync(0xffffffffu, ok) & smask;
           if (ok) {
             const int u = run + __popc(bal & ((1u << lane) - 1u));
             const int id = ns_slot(a, ns, phi, s, &s_nnew, s_new);
@@ -1938,7 +1956,10 @@ __global__ void MGS_LB k_units(const V2* __restrict__ ap, int s) {
   const int G = a.ctl->n_groups[s & 1];
   if (M <= 2 && static_cast<long long>(G) >= static_cast<long long>(a.units_tmin) * gridDim.x)
     phase_units_thread<M>(a, s, 0, s_cnt, s_red);
-  else phase_units<M>(a, s, 0, s_cnt, s_red);
+  else if (M <= 2)
+    phase_units<M, MGS_UNITS_W>(a, s, 0, s_cnt, s_red);  // few combinations per group: sub-warps
+  else
+    phase_units<M, 32>(a, s, 0, s_cnt, s_red);
 }
 
 // K independent warp-aggregated reservations at once: the K scans, then the K
