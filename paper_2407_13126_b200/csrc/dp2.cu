@@ -1706,15 +1706,36 @@ __device__ void phase_write(const V2& a, int s) {
         N.g_status[gi] = key;
         N.g_alive[gi] = total;
       }
+      // software-pipelined: the warp's next chunk is loaded before this
+      // chunk's states are written
+      int k = cb + (threadIdx.x & ~31) + lane;
+      bool in = k < cb + cc;
+      bool lv = in && a.c_live[k];
+      double v = in ? a.c_value[k] : 0.0;
+      int p = in ? a.c_pid[k] : 0;
+      uint64_t lx = in ? a.c_lex[k] : 0ull;
+      int par = in ? a.c_parent[k] : 0;
       for (int k0 = cb + (threadIdx.x & ~31); k0 < cb + cc; k0 += kThreads) {
-        const int k = k0 + lane;
-        const bool keep = k < cb + cc && a.c_live[k];
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (bal == 0) continue;
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&s_run, __popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (keep) write_state(a, s, nxt, q0 + base + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
+        const int kn = k + kThreads;
+        const bool in_n = kn < cb + cc;
+        const bool lv_n = in_n && a.c_live[kn];
+        const double v_n = in_n ? a.c_value[kn] : 0.0;
+        const int p_n = in_n ? a.c_pid[kn] : 0;
+        const uint64_t lx_n = in_n ? a.c_lex[kn] : 0ull;
+        const int par_n = in_n ? a.c_parent[kn] : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, lv);
+        if (bal != 0) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(&s_run, __popc(bal));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (lv) write_state_v(a, s, nxt, q0 + base + __popc(bal & ((1u << lane) - 1u)), gi, key, p, lx, v, par);
+        }
+        k = kn;
+        lv = lv_n;
+        v = v_n;
+        p = p_n;
+        lx = lx_n;
+        par = par_n;
       }
     }
     __syncthreads();
@@ -1802,16 +1823,34 @@ __device__ void phase_write(const V2& a, int s) {
             N.g_status[gi] = key;
             N.g_alive[gi] = total;
           }
+          // software-pipelined: the next chunk's candidate fields are loaded
+          // before this chunk's states are written
           int run = 0;
+          int k = cb + lane;
+          bool in = k < cb + cc;
+          uint8_t ok = in ? a.c_ok[k] : 0;
+          double v = in ? a.c_value[k] : 0.0;
+          int p = in ? a.c_pid[k] : 0;
+          uint64_t lx = in ? a.c_lex[k] : 0ull;
+          int par = in ? a.c_parent[k] : 0;
           for (int k0 = cb; k0 < cb + cc; k0 += 32) {
-            const int k = k0 + lane;
-            const bool in = k < cb + cc;
-            const uint8_t ok = in ? a.c_ok[k] : 0;
-            const double v = in ? a.c_value[k] : 0.0;
+            const int kn = k + 32;
+            const bool in_n = kn < cb + cc;
+            const uint8_t ok_n = in_n ? a.c_ok[kn] : 0;
+            const double v_n = in_n ? a.c_value[kn] : 0.0;
+            const int p_n = in_n ? a.c_pid[kn] : 0;
+            const uint64_t lx_n = in_n ? a.c_lex[kn] : 0ull;
+            const int par_n = in_n ? a.c_parent[kn] : 0;
             const bool keep = ok && v >= thresh;
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
-            if (keep) write_state(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, k);
+            if (keep) write_state_v(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, p, lx, v, par);
             run += __popc(bal);
+            k = kn;
+            ok = ok_n;
+            v = v_n;
+            p = p_n;
+            lx = lx_n;
+            par = par_n;
           }
         }
       }
