@@ -1196,20 +1196,33 @@ __device__ void phase_tables(const V2& a, int s) {
       a.tab_hdr[2 * b + 1] = brx;
     }
     if (nsub == 4) {  // min (rank, idx) among the max; M = 2: the partial subsets are 1 and 2
-      const bool one = gn <= kThreads;
-      for (int j = threadIdx.x; j < gn; j += kThreads) {
-        const uint8_t al = one ? al0 : F.alive[gs + j];  // every field load issued before the test
-        const int pj = one ? pj0 : F.pid[gs + j];
-        const double vd = one ? vd0 : F.value[gs + j];
-        const uint32_t rk = one ? rk0 : F.rank[gs + j];
-        if (!al) continue;
-        const unsigned long long v = vbits(vd);
-        const unsigned long long rx = (static_cast<unsigned long long>(rk) << 32) | static_cast<uint32_t>(j);
-        const int e1 = a.sp.proj_base[1] + a.sp.proj_id[1 * P1 + pj];
-        const int e2 = a.sp.proj_base[2] + a.sp.proj_id[2 * P1 + pj];
-        const unsigned long long m1 = vb[e1], m2 = vb[e2];  // both loads before either atomic
-        if (m1 == v) atomicMin(&rxs[e1], rx);
-        if (m2 == v) atomicMin(&rxs[e2], rx);
+      // software-pipelined (the first iteration from pass 1's registers): the
+      // next state's fields are loaded before this state's atomics
+      int j = threadIdx.x;
+      bool al = al0;
+      int pj = pj0;
+      double vd = vd0;
+      uint32_t rk = rk0;
+      for (; j < gn; j += kThreads) {
+        const int jn = j + kThreads;
+        const bool in_n = jn < gn;
+        const bool al_n = in_n && F.alive[gs + jn];
+        const int pj_n = in_n ? F.pid[gs + jn] : 0;
+        const double vd_n = in_n ? F.value[gs + jn] : 0.0;
+        const uint32_t rk_n = in_n ? F.rank[gs + jn] : 0u;
+        if (al) {
+          const unsigned long long v = vbits(vd);
+          const unsigned long long rx = (static_cast<unsigned long long>(rk) << 32) | static_cast<uint32_t>(j);
+          const int e1 = a.sp.proj_base[1] + a.sp.proj_id[1 * P1 + pj];
+          const int e2 = a.sp.proj_base[2] + a.sp.proj_id[2 * P1 + pj];
+          const unsigned long long m1 = vb[e1], m2 = vb[e2];  // both loads before either atomic
+          if (m1 == v) atomicMin(&rxs[e1], rx);
+          if (m2 == v) atomicMin(&rxs[e2], rx);
+        }
+        al = al_n;
+        pj = pj_n;
+        vd = vd_n;
+        rk = rk_n;
       }
     } else if (nsub > 4) {  // M = 3..4: every partial subset
       for (int j = threadIdx.x; j < gn; j += kThreads) {
@@ -1571,12 +1584,19 @@ __device__ void phase_band(const V2& a, int s, unsigned long long* mvb, unsigned
     if (threadIdx.x == 0) s_cnt = 0;
     int mine = 0;
     if (uc == 1) {
-      for (int k = cb + threadIdx.x; k < cb + cc; k += kThreads) {
-        const uint8_t ok = a.c_ok[k];  // both loads issued together (no load behind a branch)
-        const double v = a.c_value[k];
+      // software-pipelined: the next candidate's loads before this one's store
+      int k = cb + threadIdx.x;
+      uint8_t ok = k < cb + cc ? a.c_ok[k] : 0;  // both loads issued together (no load behind a branch)
+      double v = k < cb + cc ? a.c_value[k] : 0.0;
+      for (; k < cb + cc; k += kThreads) {
+        const int kn = k + kThreads;
+        const uint8_t ok_n = kn < cb + cc ? a.c_ok[kn] : 0;
+        const double v_n = kn < cb + cc ? a.c_value[kn] : 0.0;
         const bool keep = ok && v >= thresh;
         a.c_live[k] = keep ? 1 : 0;
         mine += keep;
+        ok = ok_n;
+        v = v_n;
       }
     } else {  // equal-key merge (solvers.hpp:467-468): max value, then min lex, per placement
       // flat over the status's candidate range (every unit's records are in it,
