@@ -1266,9 +1266,15 @@ __device__ void phase_trans_big(const V2& a, int s) {
     const int sb = a.sp.sig_off[sig], L = a.sp.sig_off[sig + 1] - sb;
     const int t0 = chunk * kChunkB, t1 = min(L, t0 + kChunkB);
     unsigned long long vmax = 0ull;
+    // the next target's candidate is loaded before this target's stores
+    int p_n = t0 + threadIdx.x < t1 ? a.sp.cand_pid[sb + t0 + threadIdx.x] : 0;
+    int oi_n = t0 + threadIdx.x < t1 ? a.sp.cand_oi[sb + t0 + threadIdx.x] : 0;
     for (int ti = t0 + threadIdx.x; ti < t1; ti += kThreads) {
-      const int p = a.sp.cand_pid[sb + ti];
-      const int oi = a.sp.cand_oi[sb + ti];
+      const int p = p_n, oi = oi_n;
+      if (ti + kThreads < t1) {
+        p_n = a.sp.cand_pid[sb + ti + kThreads];
+        oi_n = a.sp.cand_oi[sb + ti + kThreads];
+      }
       BestT<M> bt;
       bt.i[0] = rx0 == ~0ull ? -1 : static_cast<int>(rx0 & 0xffffffffu);
       bt.v[0] = __longlong_as_double(static_cast<long long>(v0));
