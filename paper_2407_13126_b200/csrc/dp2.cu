@@ -378,11 +378,15 @@ __device__ int block_scan_tile(const ScanJob& J, int base, int* sm, int (&v)[kSc
 // Several exclusive scans in one pass: tiles are handed out by a ticket, so
 // every tile's predecessors are already owned by running CTAs (decoupled
 // look-back cannot deadlock in a cooperative launch).
-__device__ void multi_scan(const V2& a, const ScanJob* jobs, int njobs, int epoch, int* ticket, int* totals) {
+// NJ jobs, a compile-time count: the per-job tile tables stay in registers
+template <int NJ>
+__device__ __forceinline__ void multi_scan(const V2& a, const ScanJob (&jobs)[NJ], int epoch, int* ticket, int* totals) {
+  constexpr int njobs = NJ;
   __shared__ int sm[80];
   __shared__ int s_tile, s_excl;
-  int tiles[kNumScans], tbase[kNumScans + 1];
+  int tiles[NJ], tbase[NJ + 1];
   tbase[0] = 0;
+#pragma unroll
   for (int k = 0; k < njobs; ++k) {
     tiles[k] = (jobs[k].n + kTile - 1) / kTile;
     tbase[k + 1] = tbase[k] + tiles[k];
@@ -399,7 +403,8 @@ __device__ void multi_scan(const V2& a, const ScanJob* jobs, int njobs, int epoc
     __syncthreads();
     if (t >= total_tiles) break;
     int k = 0;
-    while (t >= tbase[k + 1]) ++k;
+#pragma unroll
+    for (int q = 1; q < NJ; ++q) k += t >= tbase[q] ? 1 : 0;
     const int j = t - tbase[k];
     const ScanJob& J = jobs[k];
     int v[kScanItems];
@@ -2132,7 +2137,7 @@ __global__ void __launch_bounds__(kThreads) k_kid_scan(const V2* __restrict__ ap
   StepCounters& sc = ctl->sc[s & 1];
   (void)cur;
   const ScanJob jobs[1] = {{a.kid_cnt[cur], nullptr, a.kid_base, ctl->ranks_prev[s & 1], 0}};
-  multi_scan(a, jobs, 1, 2 * (s + 1), &sc.ticket, ctl->scan_total);
+  multi_scan<1>(a, jobs, 2 * (s + 1), &sc.ticket, ctl->scan_total);
 }
 
 __global__ void __launch_bounds__(kThreads) k_kid_fill(const V2* __restrict__ ap, int s) {
