@@ -72,6 +72,9 @@ constexpr int kSortItems = 16;       // big child buckets: CTA radix sort of up 
 #endif
 constexpr int kBitmapPerKey = MGS_BITMAP_PER_KEY;  // ... or the option bitmap when |O|/32 <= this x the bucket size
 constexpr int kBatch = 512;          // groups / statuses per CTA allocation batch
+#ifndef MGS_RB_MINB
+#define MGS_RB_MINB 2  // k_ranks_big: 2 CTAs per SM (127 registers; 1: ranks 6.0 ms eager, 2: 4.6)
+#endif
 #ifndef MGS_UNITS_W
 #define MGS_UNITS_W 8  // lanes per status group in k_units' warp path (M <= 2)
 #endif
@@ -2147,7 +2150,7 @@ __global__ void __launch_bounds__(kThreads) k_kid_fill(const V2* __restrict__ ap
   phase_kid_fill(a, s);
 }
 
-__global__ void __launch_bounds__(kThreads) k_ranks_big(const V2* __restrict__ ap, int s, int with_small) {
+__global__ void __launch_bounds__(kThreads, MGS_RB_MINB) k_ranks_big(const V2* __restrict__ ap, int s, int with_small) {
   const V2& a = c_v2;
   extern __shared__ unsigned long long smem_u64[];
   if (block_failed(a)) return;
