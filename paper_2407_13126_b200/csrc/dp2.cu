@@ -1915,9 +1915,14 @@ __device__ __forceinline__ bool dom_decoded(uint32_t x, uint32_t y) {
 template <int MK>
 struct DomRec {
   uint32_t d[MK];
-  double v;
+  unsigned long long vb;  // value bits: values are >= 0, so the bits order like the values
   uint64_t lx;
 };
+
+// dp_better on value bits (integer compares, no FP64 pipe): values are >= 0
+__device__ __forceinline__ bool better_bits(unsigned long long va, uint64_t la, unsigned long long vb, uint64_t lb) {
+  return va > vb || (va == vb && la < lb);
+}
 
 // x dominates y on every tenant (branch-free form of dom_decoded over MK fields)
 template <int MK>
@@ -1953,7 +1958,7 @@ __device__ void phase_dominance(const V2& a, int s) {
         const int j = lane + 32 * h;
         q[h] = j < n ? bk[j] : -1;
         const uint32_t st = q[h] >= 0 ? N.status[q[h]] : 0;
-        me[h].v = q[h] >= 0 ? N.value[q[h]] : 0.0;
+        me[h].vb = q[h] >= 0 ? vbits(N.value[q[h]]) : 0ull;
         me[h].lx = q[h] >= 0 ? N.lex[q[h]] : 0;
 #pragma unroll
         for (int m = 0; m < MK; ++m) {  // decode once
@@ -1971,14 +1976,14 @@ __device__ void phase_dominance(const V2& a, int s) {
 #pragma unroll 2
         for (int j = 0; j < n; ++j) {
           const DomRec<MK> r = R[j];
-          dead[0] |= (j != lane) & dom_all<MK>(r.d, me[0].d) & better(r.v, r.lx, me[0].v, me[0].lx);
+          dead[0] |= (j != lane) & dom_all<MK>(r.d, me[0].d) & better_bits(r.vb, r.lx, me[0].vb, me[0].lx);
         }
       } else {
 #pragma unroll 1
         for (int j = 0; j < n; ++j) {
           const DomRec<MK> r = R[j];
-          dead[0] |= (j != lane) & dom_all<MK>(r.d, me[0].d) & better(r.v, r.lx, me[0].v, me[0].lx);
-          dead[1] |= (j != lane + 32) & dom_all<MK>(r.d, me[1].d) & better(r.v, r.lx, me[1].v, me[1].lx);
+          dead[0] |= (j != lane) & dom_all<MK>(r.d, me[0].d) & better_bits(r.vb, r.lx, me[0].vb, me[0].lx);
+          dead[1] |= (j != lane + 32) & dom_all<MK>(r.d, me[1].d) & better_bits(r.vb, r.lx, me[1].vb, me[1].lx);
         }
       }
       __syncwarp();  // R is rewritten by the warp's next bucket
