@@ -72,6 +72,9 @@ constexpr int kSortItems = 16;       // big child buckets: CTA radix sort of up 
 #endif
 constexpr int kBitmapPerKey = MGS_BITMAP_PER_KEY;  // ... or the option bitmap when |O|/32 <= this x the bucket size
 constexpr int kBatch = 512;          // groups / statuses per CTA allocation batch
+#ifndef MGS_TB_MINB
+#define MGS_TB_MINB 4  // k_trans_big: CTAs per SM the register budget must allow
+#endif
 #ifndef MGS_RB_MINB
 #define MGS_RB_MINB 2  // k_ranks_big: 2 CTAs per SM (127 registers; 1: ranks 6.0 ms eager, 2: 4.6)
 #endif
@@ -2179,7 +2182,7 @@ __global__ void MGS_LB k_tables(const V2* __restrict__ ap, int s) {
 }
 
 template <int M>
-__global__ void __launch_bounds__(kThreads, 4) k_trans_big(const V2* __restrict__ ap, int s) {
+__global__ void __launch_bounds__(kThreads, MGS_TB_MINB) k_trans_big(const V2* __restrict__ ap, int s) {
   const V2& a = c_v2;
   if (block_failed(a)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // overflow of k_scans' lists; transition counters
