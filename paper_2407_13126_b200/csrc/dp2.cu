@@ -1573,6 +1573,27 @@ __device__ __forceinline__ void write_state_v(const V2& a, int s, int nxt, int q
   if (slot < 64) a.pbucket[p * 64 + slot] = q;
 }
 
+// the same with the placement ids and a (possibly stale, see above) bucket
+// count already loaded by the caller, one chunk ahead
+__device__ __forceinline__ void write_state_w(const V2& a, int s, int nxt, int q, int gidx, uint32_t key, int p,
+                                              uint64_t lx, double v, int parent, uint32_t ids, int pcv) {
+  const FrontierV2& N = a.f[nxt];
+  const long long h = a.hist_base[s + 1] + q;
+  const int slot = a.dominance_ok && pcv <= 64 ? atomicAdd(&a.pcnt[p], 1) : 64;
+  const int kpos = s + 1 < a.S ? atomicAdd(&a.kid_cnt[nxt][static_cast<uint32_t>(lx >> 32)], 1) : 0;
+  N.status[q] = key;
+  N.ids[q] = ids;
+  N.pid[q] = p;
+  N.value[q] = v;
+  N.lex[q] = lx;
+  N.alive[q] = 1;
+  N.group[q] = gidx;
+  N.kpos[q] = kpos;
+  a.h_parent[h] = parent;
+  a.h_oi[h] = static_cast<int32_t>(lx & 0xffffffffu);
+  if (slot < 64) a.pbucket[p * 64 + slot] = q;
+}
+
 __device__ __forceinline__ void write_state(const V2& a, int s, int nxt, int q, int gidx, uint32_t key, int k) {
   // every load is issued before the first store: the compiler cannot move
   // loads across stores it cannot prove disjoint
@@ -1870,17 +1891,25 @@ __device__ void phase_write(const V2& a, int s) {
           int p = in ? a.c_pid[k] : 0;
           uint64_t lx = in ? a.c_lex[k] : 0ull;
           int par = in ? a.c_parent[k] : 0;
+          uint32_t ids = in ? a.ids32[p] : 0u;
+          int pcv = in ? a.pcnt[p] : 0;
+          int p_n = k + 32 < cb + cc ? a.c_pid[k + 32] : 0;
           for (int k0 = cb; k0 < cb + cc; k0 += 32) {
-            const int kn = k + 32;
+            // two deep: the next chunk's fields and placement lookups, the
+            // placement of the one after, all before this chunk's writes
+            const int kn = k + 32, k2 = k + 64;
             const bool in_n = kn < cb + cc;
             const uint8_t ok_n = in_n ? a.c_ok[kn] : 0;
             const double v_n = in_n ? a.c_value[kn] : 0.0;
-            const int p_n = in_n ? a.c_pid[kn] : 0;
             const uint64_t lx_n = in_n ? a.c_lex[kn] : 0ull;
             const int par_n = in_n ? a.c_parent[kn] : 0;
+            const uint32_t ids_n = in_n ? a.ids32[p_n] : 0u;
+            const int pcv_n = in_n ? a.pcnt[p_n] : 0;
+            const int p_2 = k2 < cb + cc ? a.c_pid[k2] : 0;
             const bool keep = ok && v >= thresh;
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
-            if (keep) write_state_v(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, p, lx, v, par);
+            if (keep)
+              write_state_w(a, s, nxt, q0 + run + __popc(bal & ((1u << lane) - 1u)), gi, key, p, lx, v, par, ids, pcv);
             run += __popc(bal);
             k = kn;
             ok = ok_n;
@@ -1888,6 +1917,9 @@ __device__ void phase_write(const V2& a, int s) {
             p = p_n;
             lx = lx_n;
             par = par_n;
+            ids = ids_n;
+            pcv = pcv_n;
+            p_n = p_2;
           }
         }
       }
