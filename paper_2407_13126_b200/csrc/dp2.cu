@@ -1773,20 +1773,27 @@ __device__ void phase_write(const V2& a, int s) {
       int p = in ? a.c_pid[k] : 0;
       uint64_t lx = in ? a.c_lex[k] : 0ull;
       int par = in ? a.c_parent[k] : 0;
+      uint32_t ids = in ? a.ids32[p] : 0u;
+      int pcv = in ? a.pcnt[p] : 0;
+      int p_n = k + kThreads < cb + cc ? a.c_pid[k + kThreads] : 0;
       for (int k0 = cb + (threadIdx.x & ~31); k0 < cb + cc; k0 += kThreads) {
-        const int kn = k + kThreads;
+        // two deep, as the small-status loop below
+        const int kn = k + kThreads, k2 = k + 2 * kThreads;
         const bool in_n = kn < cb + cc;
         const bool lv_n = in_n && a.c_live[kn];
         const double v_n = in_n ? a.c_value[kn] : 0.0;
-        const int p_n = in_n ? a.c_pid[kn] : 0;
         const uint64_t lx_n = in_n ? a.c_lex[kn] : 0ull;
         const int par_n = in_n ? a.c_parent[kn] : 0;
+        const uint32_t ids_n = in_n ? a.ids32[p_n] : 0u;
+        const int pcv_n = in_n ? a.pcnt[p_n] : 0;
+        const int p_2 = k2 < cb + cc ? a.c_pid[k2] : 0;
         const unsigned bal = __ballot_sync(0xffffffffu, lv);
         if (bal != 0) {
           int base = 0;
           if (lane == 0) base = atomicAdd(&s_run, __popc(bal));
           base = __shfl_sync(0xffffffffu, base, 0);
-          if (lv) write_state_v(a, s, nxt, q0 + base + __popc(bal & ((1u << lane) - 1u)), gi, key, p, lx, v, par);
+          if (lv)
+            write_state_w(a, s, nxt, q0 + base + __popc(bal & ((1u << lane) - 1u)), gi, key, p, lx, v, par, ids, pcv);
         }
         k = kn;
         lv = lv_n;
@@ -1794,6 +1801,9 @@ __device__ void phase_write(const V2& a, int s) {
         p = p_n;
         lx = lx_n;
         par = par_n;
+        ids = ids_n;
+        pcv = pcv_n;
+        p_n = p_2;
       }
     }
     __syncthreads();
