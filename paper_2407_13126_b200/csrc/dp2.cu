@@ -1331,6 +1331,8 @@ __device__ void phase_trans_big(const V2& a, int s) {
 __device__ __forceinline__ bool claim_fits(const V2& a, int s, int q0, int total, int gi);
 __device__ __forceinline__ void write_state_v(const V2& a, int s, int nxt, int q, int gidx, uint32_t key, int p,
                                               uint64_t lx, double v, int parent);
+__device__ __forceinline__ void write_state_w(const V2& a, int s, int nxt, int q, int gidx, uint32_t key, int p,
+                                              uint64_t lx, double v, int parent, uint32_t ids, int pcv);
 
 // One warp task of k_trans_small: W = 32, one full item (32 targets of a
 // unit, it_s list); W = 16 / 8, two half / four quarter items (it_h / it_q
@@ -1377,7 +1379,8 @@ __device__ __forceinline__ void small_task(const V2& a, int s, int task, const i
     }
     const int cbu = a.ns_cbase[ns_id] + a.u_cbase[unit];
     Cand cand{0.0, 0ull, 0, false};
-    int cand_p = 0;
+    int cand_p = 0, cand_pcv = 0;
+    uint32_t cand_ids = 0u;
     // staging: a half / quarter item uses its part of the warp's arrays (gn <= kSmall * W / 32)
     const int so = (lane / W) * (kSmall * W / 32);
     uint32_t* gids = sh_ids + so;
@@ -1424,6 +1427,8 @@ __device__ __forceinline__ void small_task(const V2& a, int s, int task, const i
     const int oi = a.sp.cand_oi[sb + ti];
     const uint32_t ids_p = a.ids32[p];
     cand_p = p;
+    cand_ids = ids_p;
+    cand_pcv = fused ? a.pcnt[p] : 0;  // (possibly stale) bucket count for the fused write
     BestT<M> b;
 #pragma unroll
     for (int k = 1; k < (1 << M); ++k) {
@@ -1514,7 +1519,8 @@ __device__ __forceinline__ void small_task(const V2& a, int s, int task, const i
       N.g_alive[gi] = total;
     }
     if (keep)
-      write_state_v(a, s, nxt, q0 + __popc(bal & ((1u << lane) - 1u)), gi, key, cand_p, cand.lex, cand.v, cand.parent);
+      write_state_w(a, s, nxt, q0 + __popc(bal & ((1u << lane) - 1u)), gi, key, cand_p, cand.lex, cand.v, cand.parent,
+                    cand_ids, cand_pcv);
   }
 }
 
