@@ -1094,7 +1094,7 @@ __device__ void phase_tables(const V2& a, int s) {
   const int nsub = 1 << M;
   const uint32_t ex_tag = a.ex_bits ? static_cast<uint32_t>(s + 1) << a.ex_bits : 0u;
   __shared__ unsigned long long s_bv[kWarps], s_brx[kWarps];
-  __shared__ int s_list[kThreads], s_n, s_slot0;
+  __shared__ int s_list[kThreads], s_lgs[kThreads], s_lgn[kThreads], s_n, s_slot0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // the CTA's own big groups: F_s's groups strided over the CTAs (big groups
   // are written together, so their indices cluster), found with one parallel
@@ -1109,8 +1109,13 @@ __device__ void phase_tables(const V2& a, int s) {
     const int k = c0 + threadIdx.x;
     const int g = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
     const bool in = k < per;
-    const int gsz = in ? F.g_size[g] : 0, gal = in ? F.g_alive[g] : 0;
-    if (in && gal > 0 && gsz > kSmall) s_list[atomicAdd(&s_n, 1)] = g;
+    const int gsz = in ? F.g_size[g] : 0, gal = in ? F.g_alive[g] : 0, gst = in ? F.g_start[g] : 0;
+    if (in && gal > 0 && gsz > kSmall) {  // the group's range kept beside it (no reload per group)
+      const int li = atomicAdd(&s_n, 1);
+      s_list[li] = g;
+      s_lgs[li] = gst;
+      s_lgn[li] = gsz;
+    }
   }
   __syncthreads();
   const int nl = s_n;
@@ -1125,7 +1130,7 @@ __device__ void phase_tables(const V2& a, int s) {
   for (int li = 0; li < nl; ++li) {
     const int g = s_list[li], b = slot0 + li;
     if (threadIdx.x == 0) a.g_tab[g] = b;
-    const int gs = F.g_start[g], gn = F.g_size[g];
+    const int gs = s_lgs[li], gn = s_lgn[li];
     unsigned long long* vb = a.tab_vb + static_cast<size_t>(b) * np;
     unsigned long long* rxs = a.tab_rx + static_cast<size_t>(b) * np;
     uint32_t* ex = a.tab_ex + static_cast<size_t>(b) * P1;
